@@ -1,0 +1,168 @@
+"""Stream-K decomposition and mapping of LeanTiles (§4.3, Alg. 2).  TEST INFRASTRUCTURE ONLY.
+
+Integer work; the C++ planner must reproduce it bit-exactly.
+
+* Linearisation: units (output tiles) in batch -> heads order, each unit's C_n
+  LeanTile iterations contiguous ("crossing the head and query boundary as it may").  For
+  the ragged packed layout the order is heads -> total context.  Reading C14: the
+  caller passes the per-unit C_n list already in memory order of its KV layout.
+* Eq. 2 / Alg. 2 §4-7: I = sum_u C_n(u), I_G = I / G.
+  Reading C8: the first r = I mod G CTAs take ceil(I/G), the rest floor(I/G)
+  (cta_start = g*floor(I/G) + min(g, r)).
+* Alg. 2 §8-18 + §41: each CTA walks its range segment by segment
+  (reading C10: while-loop, iter jumps to tile_iter_end).  host-block iff iter == tile_iter
+  (§17); finishing-block iff cta_end >= tile_iter_end (§18).
+* Alg. 2 §26 ``last_cta = tile_iter_end / C_n`` is garbled (it is a tile index);
+  reading C9: last_cta = owner(tile_iter_end - 1), the CTA holding the tile's last
+  iteration.  :func:`last_cta_literal` keeps the literal formula so a test can show it
+  drops a contributor on the paper's own Fig. 1 example.
+
+Two independent constructions are provided and tested against each other:
+:func:`stream_k_segments` (Alg. 2's per-CTA walk) and :func:`segments_from_owner_table`
+(brute force: the owner of every single global iteration, grouped into maximal runs).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Sequence, Tuple
+
+
+@dataclass(frozen=True)
+class Segment:
+    """One call of LeanTile() by one CTA: Alg. 2 §11-18 quantities for that call."""
+
+    cta: int           # g
+    unit: int          # tile_idx (output tile = work unit)
+    begin: int         # local_iter
+    end: int           # local_iter_end (exclusive)
+    host: bool         # iter == tile_iter                     (§17)
+    finishing: bool    # cta_end >= tile_iter_end              (§18)
+    last_cta: int      # owner(tile_iter_end - 1)              (§26, reading C9)
+
+    def row(self) -> Tuple[int, int, int, int, int, int, int]:
+        return (self.cta, self.unit, self.begin, self.end, int(self.host),
+                int(self.finishing), self.last_cta)
+
+
+def iters_per_cta(total_iters: int, grid: int) -> List[int]:
+    """Per-CTA iteration counts: Eq. 2 / Alg. 2 §7 with reading C8's remainder rule."""
+    if grid < 1:
+        raise ValueError("grid must be >= 1")
+    q, r = divmod(total_iters, grid)
+    return [q + 1 if g < r else q for g in range(grid)]
+
+
+def cta_range(total_iters: int, grid: int, g: int) -> Tuple[int, int]:
+    """Alg. 2 §9: [cta_start, cta_end) of CTA g."""
+    q, r = divmod(total_iters, grid)
+    start = g * q + min(g, r)
+    return start, start + (q + 1 if g < r else q)
+
+
+def owner(total_iters: int, grid: int, it: int) -> int:
+    """The CTA whose range contains global iteration ``it`` (closed form of reading C8)."""
+    q, r = divmod(total_iters, grid)
+    if it < r * (q + 1):
+        return it // (q + 1)
+    return r + (it - r * (q + 1)) // q
+
+
+def _offsets(c_n: Sequence[int]) -> List[int]:
+    off = [0]
+    for c in c_n:
+        if c < 1:
+            raise ValueError("every unit needs >= 1 LeanTile (reading C6)")
+        off.append(off[-1] + c)
+    return off
+
+
+def stream_k_segments(c_n: Sequence[int], grid: int) -> List[Segment]:
+    """Alg. 2 §8-18, §41 executed for every CTA in index order."""
+    off = _offsets(c_n)
+    total = off[-1]
+    segs: List[Segment] = []
+    unit = 0
+    for g in range(grid):                                   # fork CTA_g       (§8)
+        cta_start, cta_end = cta_range(total, grid, g)      #                  (§9)
+        it = cta_start
+        while it < cta_end:                                 # (§10, reading C10)
+            while off[unit + 1] <= it:                      # tile_idx         (§11)
+                unit += 1
+            tile_iter = off[unit]                           #                  (§12)
+            tile_iter_end = tile_iter + c_n[unit]           #                  (§13)
+            local_iter = it - tile_iter                     #                  (§14)
+            local_iter_end = min(tile_iter_end, cta_end) - tile_iter  #        (§15)
+            segs.append(Segment(
+                cta=g, unit=unit, begin=local_iter, end=local_iter_end,
+                host=(it == tile_iter),                     #                  (§17)
+                finishing=(cta_end >= tile_iter_end),       #                  (§18)
+                last_cta=owner(total, grid, tile_iter_end - 1)))   # (§26, reading C9)
+            it = tile_iter_end                              #                  (§41)
+    return segs
+
+
+def owner_table(total_iters: int, grid: int) -> List[int]:
+    """Brute force: hand out iterations CTA by CTA, counts from :func:`iters_per_cta`."""
+    table: List[int] = []
+    for g, n in enumerate(iters_per_cta(total_iters, grid)):
+        table.extend([g] * n)
+    assert len(table) == total_iters
+    return table
+
+
+def segments_from_owner_table(c_n: Sequence[int], grid: int) -> List[Segment]:
+    """Independent construction: maximal runs of equal (owner, unit) over all iterations."""
+    off = _offsets(c_n)
+    own = owner_table(off[-1], grid)
+    segs: List[Segment] = []
+    for u in range(len(c_n)):
+        first, last = off[u], off[u + 1] - 1
+        run_start = first
+        for it in range(first, last + 1):
+            if it == last or own[it + 1] != own[it]:
+                segs.append(Segment(
+                    cta=own[it], unit=u, begin=run_start - first, end=it + 1 - first,
+                    host=(run_start == first), finishing=(it == last),
+                    last_cta=own[last]))
+                run_start = it + 1
+    segs.sort(key=lambda s: (s.cta, s.unit))
+    return segs
+
+
+def last_cta_literal(c_n_uniform: int, unit: int) -> int:
+    """Alg. 2 §26 read literally: tile_iter_end / C_n (= unit + 1).  Kept only to test that
+    it is NOT the CTA index (reading C9)."""
+    tile_iter_end = (unit + 1) * c_n_uniform
+    return tile_iter_end // c_n_uniform
+
+
+def fixed_split_segments(c_n: Sequence[int], grid: int, split: int) -> List[Segment]:
+    """FlashDecoding's fixed-split decomposition: each unit's C_n
+    iterations cut into ``split`` near-equal chunks (first chunks take the extra iteration,
+    S:271), chunks dealt round-robin to the grid in launch order; host = chunk 0.
+    ``cta`` is the worker; a worker may hold several chunks (successive waves)."""
+    segs: List[Segment] = []
+    chunk_id = 0
+    for u, c in enumerate(c_n):
+        s = min(split, c)
+        q, r = divmod(c, s)
+        begin = 0
+        chunk_owner = []
+        for j in range(s):
+            n = q + 1 if j < r else q
+            chunk_owner.append((chunk_id % grid, begin, begin + n))
+            chunk_id += 1
+            begin += n
+        last_owner = chunk_owner[-1][0]
+        for j, (w, b0, b1) in enumerate(chunk_owner):
+            segs.append(Segment(cta=w, unit=u, begin=b0, end=b1, host=(j == 0),
+                                finishing=(j == s - 1), last_cta=last_owner))
+    return segs
+
+
+def quantization_efficiency(segs: Sequence[Segment], grid: int) -> float:
+    """I / (G * max per-worker iterations)."""
+    load = [0] * grid
+    for s in segs:
+        load[s.cta] += s.end - s.begin
+    return sum(load) / (grid * max(load))

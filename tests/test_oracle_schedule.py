@@ -1,0 +1,173 @@
+"""Pins for oracle.schedule (§4.3 / Eq. 2 / Alg. 2 §4-18, §26, §41).
+
+* the paper's Fig. 1 schedule (golden, P:42 + P:261 + P:412);
+* Eq. 2 arithmetic and the remainder rule (golden);
+* the literal Alg. 2 §26 formula drops a contributor on Fig. 1 (reading C9);
+* Alg. 2's per-CTA walk == brute-force owner enumeration, exhaustively on small cases;
+* structural invariants (coverage, balance <= 1, unique host, <= 1 partial per CTA, peers
+  contiguous, non-host = first segment, non-finishing host = last segment);
+* FA2 / FlashDecoding recovery and fixed-split quantization efficiency.
+"""
+import itertools
+import os
+
+import pytest
+
+import oracle
+from oracle.schedule import Segment
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _read_rows(name):
+    rows = []
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line)
+    return rows
+
+
+def test_fig1_golden():
+    rows = [tuple(int(x) for x in r.split()) for r in _read_rows("fig1_schedule.txt")]
+    segs = oracle.stream_k_segments([5, 5], 5)
+    assert [s.row() for s in segs] == rows
+    # SM0 and SM1 get 2 LeanTiles of h0, SM2 gets 1
+    h0 = {s.cta: s.end - s.begin for s in segs if s.unit == 0}
+    assert h0 == {0: 2, 1: 2, 2: 1}
+
+
+def _expand(rle):
+    out = []
+    for tok in rle.split():
+        n, v = tok.split("x")
+        out += [int(v)] * int(n)
+    return out
+
+
+def test_eq2_golden():
+    for row in _read_rows("eq2_arithmetic.txt"):
+        lhs, rhs = row.split("->")
+        kind, *args = lhs.split()
+        expect = _expand(rhs)
+        if kind == "eq2":
+            B, H, N, T, G = map(int, args)
+            c_n = [-(-N // T)] * (B * H)
+        elif kind == "ragged":
+            lens = [int(x) for x in args[0].split(",")]
+            h, T, G = int(args[1]), int(args[2]), int(args[3])
+            c_n = [-(-n // T) for _ in range(h) for n in lens]   # heads -> total context
+        else:
+            I, G = int(args[0]), int(args[1])
+            c_n = [I]
+        counts = oracle.iters_per_cta(sum(c_n), G)
+        assert counts == expect, row
+        segs = oracle.stream_k_segments(c_n, G)
+        per = [0] * G
+        for s in segs:
+            per[s.cta] += s.end - s.begin
+        assert per == expect
+    assert sum(oracle.iters_per_cta(1728, 216)) == 1728
+    assert oracle.quantization_efficiency(oracle.stream_k_segments([10], 4), 4) == pytest.approx(10 / 12)
+
+
+def test_literal_alg2_line26_drops_a_contributor():
+    # Alg. 2 §26 literally: last_cta = tile_iter_end / C_n.  On Fig. 1, head 0's host (CTA 0)
+    # would wait only on CTA 1 and miss CTA 2's partial (reading C9).
+    segs = oracle.stream_k_segments([5, 5], 5)
+    assert oracle.last_cta_literal(5, 0) == 1 and oracle.last_cta_literal(5, 1) == 2
+    true_last = {s.unit: s.last_cta for s in segs}
+    assert true_last == {0: 2, 1: 4}
+    contributors = {u: sorted({s.cta for s in segs if s.unit == u}) for u in (0, 1)}
+    assert contributors == {0: [0, 1, 2], 1: [2, 3, 4]}
+
+
+def _check_invariants(c_n, G, segs):
+    I = sum(c_n)
+    off = [0]
+    for c in c_n:
+        off.append(off[-1] + c)
+    # coverage / disjointness of global iterations
+    seen = []
+    for s in segs:
+        seen += list(range(off[s.unit] + s.begin, off[s.unit] + s.end))
+    assert sorted(seen) == list(range(I))
+    # balance <= 1
+    per = [0] * G
+    for s in segs:
+        per[s.cta] += s.end - s.begin
+    assert max(per) - min(per) <= 1
+    by_cta = {}
+    for s in segs:
+        by_cta.setdefault(s.cta, []).append(s)
+    for u in range(len(c_n)):
+        us = sorted([s for s in segs if s.unit == u], key=lambda s: s.begin)
+        hosts = [s for s in us if s.host]
+        assert len(hosts) == 1 and hosts[0].begin == 0            # unique host, owns iter 0
+        h = hosts[0]
+        ctas = [s.cta for s in us]
+        assert ctas == list(range(h.cta, h.cta + len(us)))          # contiguous peers
+        assert ctas[-1] == h.last_cta
+        assert (len(us) == 1) == h.finishing
+        for s in us[1:]:
+            assert by_cta[s.cta][0] == s                            # non-host = first segment
+        if not h.finishing:
+            assert by_cta[h.cta][-1] == h                           # waiting host = last segment
+    for g, ss in by_cta.items():
+        assert sum(1 for s in ss if not s.host) <= 1                # <= 1 partial per CTA
+
+
+def test_walk_equals_owner_enumeration_exhaustive():
+    n_cases = 0
+    for n_units in range(1, 5):
+        for c_n in itertools.product(range(1, 7), repeat=n_units):
+            I = sum(c_n)
+            for G in range(1, I + 1):
+                a = oracle.stream_k_segments(list(c_n), G)
+                b = oracle.segments_from_owner_table(list(c_n), G)
+                assert a == b, (c_n, G)
+                _check_invariants(c_n, G, a)
+                n_cases += 1
+    assert n_cases > 20000
+
+
+def test_owner_closed_form_and_idle_ctas():
+    for I in range(1, 60):
+        for G in range(1, 70):
+            table = oracle.owner_table(I, G)
+            assert [oracle.owner(I, G, i) for i in range(I)] == table
+            segs = oracle.stream_k_segments([I], G)
+            assert len({s.cta for s in segs}) == min(I, G)          # G > I: idle CTAs
+
+
+def test_fa2_and_flashdecoding_recovery():
+    # grid == #output tiles -> FA2 (one full tile per CTA)
+    c_n = [7, 7, 7, 7]
+    segs = oracle.stream_k_segments(c_n, 4)
+    assert [(s.cta, s.unit, s.begin, s.end, s.host, s.finishing) for s in segs] == \
+           [(u, u, 0, 7, True, True) for u in range(4)]
+    # grid == s * #tiles with s | C_n -> FlashDecoding's equal split
+    c_n = [6, 6, 6]
+    segs = oracle.stream_k_segments(c_n, 6)
+    assert [(s.unit, s.begin, s.end) for s in segs] == \
+           [(0, 0, 3), (0, 3, 6), (1, 0, 3), (1, 3, 6), (2, 0, 3), (2, 3, 6)]
+    fs = oracle.fixed_split_segments(c_n, 6, 2)
+    assert sorted((s.unit, s.begin, s.end) for s in fs) == sorted((s.unit, s.begin, s.end) for s in segs)
+
+
+def test_fixed_split_efficiency():
+    # S:232 / S:258: 56 tiles, grid 108, split 1 -> 56/108
+    fs = oracle.fixed_split_segments([4] * 56, 108, 1)
+    load = [0] * 108
+    for s in fs:
+        load[s.cta] += s.end - s.begin
+    assert sum(1 for x in load if x == 0) == 52
+    assert oracle.quantization_efficiency(fs, 108) == pytest.approx(56 / 108)
+    # 2 tiles of C_n=5, split 2 -> chunks 3 + 2
+    fs = oracle.fixed_split_segments([5, 5], 4, 2)
+    assert [(s.unit, s.end - s.begin) for s in fs] == [(0, 3), (0, 2), (1, 3), (1, 2)]
+    # stream-K is never less efficient than fixed-split
+    for c_n, G, s in [([5, 5], 4, 2), ([9] * 7, 16, 2), ([3, 17, 8], 5, 3)]:
+        assert oracle.quantization_efficiency(oracle.stream_k_segments(c_n, G), G) >= \
+            oracle.quantization_efficiency(oracle.fixed_split_segments(c_n, G, s), G)
