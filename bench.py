@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- LeanAttention decode on B200: latency and achieved HBM GB/s (BASELINE.json).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c1..c5]
+
+* N = 1 (default): BASELINE.json configs[1] (c2: batch 1, 32 heads, d 128, context 256k,
+  bf16 KV) on one B200 -- the north-star workload.  One step = one la_decode (the whole hot
+  path: stream-K LeanTiles + in-kernel fixup + finalize, one launch).
+* N > 1 (torchrun, one rank per GPU): configs[4] (c5: context 1M) sequence-sharded --
+  every rank decodes its contiguous 1/N of every head's context (la_decode_partial), NCCL
+  all-gathers the per-head (O_r, L_r) and la_combine folds them.  Total work is fixed:
+  "scaling": "strong".
+* --impl reference: the fp64 CPU oracle (oracle/), timed on this host's cores on a bounded
+  sample of the same workload (this tier has no runnable reference implementation).
+
+``value`` = algorithmic KV bytes (2 * H_kv * sum n * d * 2 B) / device time, GB/s, whole job.
+Inputs (4.3 GB at c2) are larger than the 126 MB L2, so no flush is needed between steps;
+configs whose KV fits in L2 are flushed (a 512 MB memset) before every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-attention latency (µs) and achieved HBM GB/s vs peak at 1/2/4/8 B200"
+WORKLOADS = {
+    "c1": "batch 1, 1 head, head_dim 64, context 4096, fp32 inputs",
+    "c2": "batch 1, 32 heads, head_dim 128, context 256k, bf16 KV cache, 1 B200",
+    "c3": "batch 8, 64 q-heads / 8 kv-heads (GQA), head_dim 128, context 64k, bf16",
+    "c4": "batch 16, 32 heads, head_dim 128, ragged context lengths 1k-128k per request",
+    "c5": "batch 1, 32 heads, head_dim 128, context 1M, KV sequence-sharded across N B200 with NCCL partial combine",
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, help="c1..c5 (default c2 at N=1, c5 at N>1)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-heads", type=int, default=32, help="heads in the oracle cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# --------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self._nv = None
+            self.error = str(e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h) \
+                    if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        if not self._nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "error", "")}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# --------------------------------------------------------------------------------------
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: copy, read+write bytes)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config: str):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    ent = d.get(config)
+    return None if ent is None else ent.get("dram_bytes_per_launch")
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return 1
+
+
+def oracle_sample(p, heads, tokens=None, device="cuda"):
+    """Host fp64 inputs for the oracle's bounded sample: the first `heads` units, optionally
+    only their first `tokens` keys.  Generated by synth (bit-identical on any device)."""
+    import synth
+    units = []
+    q_all = synth.gen_q(p, "cpu")
+    for u in range(heads):
+        b, h = divmod(u, p.heads_kv)
+        n = p.ctx_lens[b] if tokens is None else min(tokens, p.ctx_lens[b])
+        k = synth.gen_kv_unit(p, b, h, "k", device, 0, n).cpu()
+        v = synth.gen_kv_unit(p, b, h, "v", device, 0, n).cpu()
+        units.append((q_all[b, h * p.group:(h + 1) * p.group], k, v))
+    return units
+
+
+def run_oracle_sample(units, scale):
+    """The oracle as it stands on the sample (bf16 -> fp64 upcast included)."""
+    import numpy as np
+    import torch
+    import oracle
+    t0 = time.perf_counter()
+    for q, k, v in units:
+        oracle.decode_attention_unit(q.to(torch.float64).numpy(), k.to(torch.float64).numpy(),
+                                     v.to(torch.float64).numpy(), scale)
+    return time.perf_counter() - t0
+
+
+def sample_bytes(units, elem=2):
+    return sum(2 * k.numel() * elem for _, k, _ in units)
+
+
+# --------------------------------------------------------------------------------------
+def bench_reference(args):
+    """--impl reference: the oracle on this host's cores, same metric/unit/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import synth
+    cfg = args.config or ("c2" if args.gpus == 1 else "c5")
+    p = synth.config(cfg)
+    dev = "cuda" if _has_cuda() else "cpu"
+    # size the per-step sample so that (K + W) steps stay within ~120 s
+    probe = oracle_sample(p, 1, tokens=min(p.ctx_lens[0], 1 << 16), device=dev)
+    t_probe = run_oracle_sample(probe, p.scale)
+    per_token = t_probe / probe[0][1].shape[0]
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    tokens = int(max(1024, min(p.ctx_lens[0], budget / max(per_token, 1e-12))))
+    units = oracle_sample(p, 1, tokens=tokens, device=dev)
+    for _ in range(args.warmup):
+        run_oracle_sample(units, p.scale)
+    t = 0.0
+    for _ in range(args.steps):
+        t += run_oracle_sample(units, p.scale)
+    step_s = t / args.steps
+    gbs = sample_bytes(units) / step_s / 1e9
+    sample = f"1 of {p.batch * p.heads_kv} (b, h_kv) units of {cfg}, first {tokens} of {p.ctx_lens[0]} tokens"
+    line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak" if args.gpus == 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based generator, D1)",
+            "config": {"workload": f"{cfg}: {WORKLOADS[cfg]}", "sample": sample},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": blas_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _has_cuda():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+# --------------------------------------------------------------------------------------
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2405_10480_b200 as la
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = args.config or ("c2" if world == 1 else "c5")
+    p = synth.config(cfg)
+    bounds = synth.shard_bounds(p, rank, world)
+    lens = [b - a for a, b in bounds]
+
+    q = synth.gen_q(p, dev)
+    k = synth.fill_kv_cache(p, "k", dev, token_range=bounds)
+    v = synth.fill_kv_cache(p, "v", dev, token_range=bounds)
+    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout)
+    info = plan.info
+    total_kv = p.kv_bytes                       # whole job
+    local_kv = info.kv_bytes
+    stream = torch.cuda.current_stream(dev)
+    rows = p.batch * p.heads_q
+    out = torch.empty(p.batch, p.heads_q, p.head_dim, dtype=torch.float32, device=dev)
+    lse = torch.empty(p.batch, p.heads_q, dtype=torch.float32, device=dev)
+    if world > 1:
+        o_all = torch.empty(world, rows, p.head_dim, dtype=torch.float32, device=dev)
+        l_all = torch.empty(world, rows, dtype=torch.float32, device=dev)
+        fin_o = torch.empty(rows, p.head_dim, dtype=torch.float32, device=dev)
+        fin_l = torch.empty(rows, dtype=torch.float32, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if total_kv < 2 * L2_BYTES else None
+
+    def step(ev0=None, ev1=None):
+        if flush is not None:
+            flush.zero_()
+        if ev0 is not None:
+            ev0.record(stream)
+        if world == 1:
+            plan.decode(q, k, v, out, lse, stream=stream)
+        else:
+            plan.decode_partial(q, k, v, out, lse, stream=stream)
+        if ev1 is not None:
+            ev1.record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(o_all, out.view(rows, p.head_dim))
+            dist.all_gather_into_tensor(l_all, lse.view(rows))
+            la.la_combine(o_all, l_all, fin_o, fin_l, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = la.launch_count()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(ev0[i], ev1[i])
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = la.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1)) / args.steps
+    step_ms = total_ms / args.steps
+    if flush is not None:   # the flush is not part of the step: report the kernel time
+        step_ms = kern_ms if world == 1 else step_ms
+    if world > 1:
+        t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, kern_ms = t.tolist()
+
+    # ---- end to end through the C ABI with host buffers ---------------------------------
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        qh = q.cpu().pin_memory()
+        kh = k.cpu().pin_memory()
+        vh = v.cpu().pin_memory()
+        oh = torch.empty(p.batch, p.heads_q, p.head_dim, dtype=torch.float32).pin_memory()
+        lh = torch.empty(p.batch, p.heads_q, dtype=torch.float32).pin_memory()
+        plan.decode_host(qh, kh, vh, oh, lh, stream=stream)   # warm-up (allocates staging)
+        if world > 1:
+            oh_all = torch.empty(world, rows, p.head_dim, dtype=torch.float32, device=dev)
+            lh_all = torch.empty(world, rows, dtype=torch.float32, device=dev)
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            plan.decode_host(qh, kh, vh, oh, lh, stream=stream)
+            if world > 1:
+                o_dev = oh.to(dev, non_blocking=True).view(rows, p.head_dim)
+                l_dev = lh.to(dev, non_blocking=True).view(rows)
+                dist.all_gather_into_tensor(oh_all, o_dev)
+                dist.all_gather_into_tensor(lh_all, l_dev)
+                fo, fl = la.la_combine(oh_all, lh_all, stream=stream)
+                fo.cpu()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        e2e = {"value": total_kv / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(qh.numel() * qh.element_size() + 2 * kh.numel() * kh.element_size()),
+               "d2h_bytes_per_step": int(oh.numel() * 4 + lh.numel() * 4)}
+
+    # ---- oracle cpu_baseline (rank 0, N = 1 only) -----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        units = oracle_sample(p, min(args.cpu_heads, p.batch * p.heads_kv), device=dev)
+        secs = run_oracle_sample(units, p.scale)
+        cpu = {"value": sample_bytes(units, synth.DTYPE_BYTES[p.dtype]) / secs / 1e9, "unit": "GB/s",
+               "cores": blas_threads(), "kind": "oracle", "seconds": secs,
+               "sample": f"{len(units)} of {p.batch * p.heads_kv} (b, h_kv) units of {cfg} (full context each)"}
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        achieved = local_kv / (kern_ms * 1e-3) / 1e9   # dominant kernel, per launch
+        traffic = ncu_traffic(cfg)
+        line = {
+            "metric": METRIC, "value": total_kv / (step_ms * 1e-3) / 1e9, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "latency_us": step_ms * 1e3, "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based generator, distribution D1; DESIGN.md input recipe)",
+            "config": {"workload": f"{cfg}: {WORKLOADS[cfg]}", "batch": p.batch, "heads_q": p.heads_q,
+                       "heads_kv": p.heads_kv, "head_dim": p.head_dim,
+                       "context": p.ctx_lens[0] if len(set(p.ctx_lens)) == 1 else p.ctx_lens,
+                       "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
+                       "stage_tokens": info.stage_tokens,
+                       "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),
+                       "parallelism": "single GPU" if world == 1 else f"sequence-sharded x{world} + NCCL all-gather + la_combine"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "la_decode_mha<bf16,128>", "kernel_us": kern_ms * 1e3,
+                         "algorithmic_bytes_per_launch": local_kv},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,198 @@
+/*
+ * la.h -- C ABI of the B200-native LeanAttention decode library (libleanattn.so).
+ *
+ * LeanAttention (arXiv 2405.10480): exact decode-phase attention (query length 1, or one
+ * GQA query group per KV head) over a long KV cache, decomposed stream-K style.
+ * Citations: P:n = line n of the paper text, S:n = line n of SPEC.md,
+ * Alg1§k / Alg2§k = statement k of Algorithm 1 / 2, readings Cn = DESIGN.md §Readings.
+ *
+ * The operation (Eq. 1; Table 1 decode column): for every request b,
+ * query head h_q (KV head h_kv = h_q / g, g = heads_q / heads_kv, reading C3) and the
+ * n_b = ctx_lens[b] cached keys/values,
+ *     s_j = scale * <q[b,h_q,:], k[b,h_kv,j,:]>            j = 0 .. n_b - 1
+ *     O[b,h_q,:] = sum_j softmax(s)_j v[b,h_kv,j,:]         (fp32, reading C4)
+ *     L[b,h_q]   = ln sum_j e^{s_j}                          (Alg2§39, reading C2)
+ * computed by ONE persistent kernel launch: the flattened (unit x LeanTile) iteration
+ * space is cut into G equal contiguous ranges (Eq. 2, Alg2§4-9), each
+ * CTA runs Alg. 1 over its segments and boundary-straddling units are merged
+ * in-kernel by the owning ("host") CTA with the softmax re-scaling operator (§4.1
+ * P:286-294; Alg2§19-36), with no second launch.
+ *
+ * Conventions for every entry point:
+ *  - Return LA_OK or an error code; no C++ exception crosses the ABI.  A human-readable
+ *    message for the last error on the calling thread is available from la_last_error().
+ *  - Device pointers are plain CUDA device addresses owned by the CALLER (e.g. torch
+ *    tensors); the library never frees them.  `stream` is a cudaStream_t (NULL = legacy
+ *    default stream).  Kernels run asynchronously on `stream`; device-side faults surface
+ *    at the caller's next synchronisation.
+ *  - A plan owns all device memory it allocates (schedule tables, per-CTA partial slots
+ *    Op/mp/lp and flags, Alg2§20-23) until la_plan_destroy().  la_decode never allocates.
+ *  - Not thread-safe on one plan: two la_decode calls on the same plan must be ordered
+ *    on one stream (they share the partial slots and flags).
+ */
+#ifndef LEANATTN_LA_H
+#define LEANATTN_LA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LA_VERSION 1
+
+typedef enum {
+  LA_OK = 0,
+  LA_ERR_INVALID = 1,      /* bad argument: null/misaligned pointer, bad shape or size  */
+  LA_ERR_UNSUPPORTED = 2,  /* valid request this build does not implement (dtype, d, g)  */
+  LA_ERR_CUDA = 3,         /* a CUDA runtime call failed (message in la_last_error)     */
+  LA_ERR_NOMEM = 4,        /* device or host allocation failed                          */
+  LA_ERR_STATE = 5         /* e.g. la_decode on a host-only plan                         */
+} la_status;
+
+/* Storage type of Q, K and V ("FP16->32": 16-bit inputs, fp32 arithmetic). */
+typedef enum { LA_BF16 = 0, LA_FP16 = 1, LA_FP32 = 2 } la_dtype;
+
+/* KV cache layouts (reading C14 fixes the unit linearisation order). */
+typedef enum {
+  /* (B, H_kv, max_ctx, d) contiguous, request b valid on rows [0, ctx_lens[b]).
+     Units (b, h_kv) linearised batch -> heads. */
+  LA_KV_BHSD = 0,
+  /* The paper's unpadded ragged layout (H_kv, sum_b n_b, d), request b on rows
+     cu_seqlens[b] .. cu_seqlens[b+1] (cu_seqlens = prefix sum of ctx_lens, built by the
+     planner).  Units linearised heads -> total context. */
+  LA_KV_PACKED = 1
+} la_layout;
+
+/* Work decomposition.  STREAMK is the method; the other two are its
+   special cases / the baselines it is compared with, kept for the NEXT-1 comparison. */
+typedef enum {
+  LA_SCHED_STREAMK = 0,    /* Eq. 2 + Alg. 2: equal contiguous iteration ranges        */
+  LA_SCHED_SEQUENTIAL = 1  /* FA2: one CTA per unit, G = #units            */
+} la_schedule;
+
+typedef struct {
+  float scale;       /* softmax scale applied to every score before max/exp (reading C1);
+                        0 -> 1/sqrt(head_dim) (Eq. 1)                              */
+  int layout;        /* la_layout, default LA_KV_BHSD                                     */
+  int64_t max_ctx;   /* BHSD row stride of one (b, h_kv) slab in tokens; 0 -> max(ctx_lens) */
+  int grid;          /* G.  0 -> min(#co-resident CTAs = 148 x occupancy, I) (reading C15);
+                        > 0 forces G (tests), clamped to the co-resident maximum on device
+                        plans because hosts wait on peers (Alg2§28 needs co-residency)    */
+  int num_sms;       /* host-only plans: SM count assumed when grid == 0 (default 148)    */
+  int ctas_per_sm;   /* host-only plans: occupancy assumed when grid == 0 (default 1)     */
+  int host_only;     /* 1 -> plan the schedule only, no device state (inspection/tests)   */
+  int schedule;      /* la_schedule, default LA_SCHED_STREAMK                             */
+} la_plan_opts;
+
+typedef struct la_plan_s* la_plan_t;
+
+typedef struct {
+  int batch, heads_q, heads_kv, head_dim, group;
+  int dtype, layout, schedule;
+  int tile_n;              /* LeanTile tokens T_n                                 */
+  int stage_tokens;        /* tokens per shared-memory ring stage (<= tile_n)             */
+  int grid;                /* G                                                           */
+  int num_units;           /* output tiles = B * H_kv                                     */
+  int64_t total_iters;     /* I = sum_u ceil(n_u / T_n)  (Alg2§6, reading C15)           */
+  int64_t num_segments;    /* LeanTile() calls over all CTAs (rows of la_plan_export)     */
+  int64_t num_partials;    /* non-host segments = partial slots actually written          */
+  int64_t workspace_bytes; /* device bytes owned by the plan                              */
+  int64_t kv_bytes;        /* algorithmic K+V bytes one la_decode reads                   */
+  float scale;
+} la_plan_info;
+
+/* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */
+la_status la_plan_opts_init(la_plan_opts* opts);
+
+/*
+ * la_plan -- build the stream-K schedule for one decode step (host, synchronous).
+ *
+ * batch, heads_q, heads_kv >= 1, heads_q % heads_kv == 0 (reading C3); head_dim in
+ * {64, 128}; ctx_lens: HOST array of `batch` int32, each >= 1 (reading C6); tile_n: LeanTile
+ * tokens in {16, 32, 64, 128, 256, 512}, or 0 for the default (T_n giving 64 KiB of K+V per
+ * LeanTile -- 128 tokens at d=128 bf16, 256 at d=64, as the paper's sweep found, P:396 --
+ * halved while I < #SMs so small problems still fill the machine).
+ * dtype: storage type of q, k, v.  opts may be NULL (defaults).
+ *
+ * Implements Alg2§4-18: units in memory order, C_n(u) = ceil(n_u / T_n), I = sum C_n,
+ * per-CTA ranges by the remainder rule (reading C8), per unit the owning host CTA and the
+ * last contributing CTA (reading C9).  Device plans allocate and upload the tables, G
+ * partial slots of (g x d + 2) fp32 (Alg2§20-22) and G flags, and query the kernel's
+ * occupancy on the current device.  On success *out receives a plan to be released with
+ * la_plan_destroy.  Errors: LA_ERR_INVALID (shape/size), LA_ERR_UNSUPPORTED (head_dim,
+ * dtype or group this build lacks), LA_ERR_CUDA / LA_ERR_NOMEM (device setup).
+ */
+la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int32_t* ctx_lens,
+                  int tile_n, la_dtype dtype, const la_plan_opts* opts, la_plan_t* out);
+
+/* Scalar facts about a plan (host, synchronous). */
+la_status la_plan_info_get(la_plan_t plan, la_plan_info* info);
+
+/*
+ * la_plan_export -- dump the schedule, one row of 7 int32 per segment (= LeanTile call),
+ * in SPEC's dump order: cta, unit, local_begin, local_end, host, finishing,
+ * last_cta (Alg2§11-18, §26 with reading C9).  rows: HOST buffer of cap_rows * 7 int32 (may
+ * be NULL with cap_rows = 0 to query the count); *n_rows receives the total row count.
+ * LA_ERR_INVALID if cap_rows is non-zero but too small.
+ */
+la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t* n_rows);
+
+/*
+ * la_decode -- one decode-attention step on `stream` (asynchronous).
+ *
+ * q: device (B, H_q, d) of the plan's dtype, contiguous.  k_cache, v_cache: device, plan's
+ * layout and dtype, contiguous, 16-byte aligned.  out: device (B, H_q, d) fp32.  lse:
+ * device (B, H_q) fp32 natural-log logsumexp L, or NULL to skip it.  ctx_lens are the
+ * plan's (a serving loop re-plans when they change; planning is O(B*H_kv + G)).
+ * Errors: LA_ERR_INVALID (null or misaligned pointer), LA_ERR_STATE (host-only plan),
+ * LA_ERR_CUDA (launch failure).
+ */
+la_status la_decode(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache,
+                    float* out, float* lse, void* stream);
+
+/*
+ * la_decode_partial -- la_decode on one sequence shard of the KV cache (BASELINE.json
+ * north star, multi-GPU): identical computation, `lse` is mandatory because the shard's
+ * (O_r, L_r) is then combined across ranks with la_combine.
+ */
+la_status la_decode_partial(la_plan_t plan, const void* q, const void* k_shard,
+                            const void* v_shard, float* o_part, float* lse_part, void* stream);
+
+/*
+ * la_combine -- fold P normalised partials with the softmax re-scaling operator (§4.1,
+ * P:286-294, exact for any split by associativity P:264), in ascending part order:
+ *     L = ln sum_r e^{L_r},  O = sum_r e^{L_r - L} O_r
+ * o_parts: device [parts][rows][head_dim] fp32; lse_parts: device [parts][rows] fp32;
+ * out: device [rows][head_dim] fp32; lse: device [rows] fp32 or NULL.  head_dim in
+ * {64, 128}; parts >= 1; rows >= 1.  Asynchronous on `stream`.
+ */
+la_status la_combine(const float* o_parts, const float* lse_parts, int parts, int rows,
+                     int head_dim, float* out, float* lse, void* stream);
+
+/*
+ * la_decode_host -- la_decode through HOST buffers (end-to-end path): copies q, k, v
+ * (plan's layout; sizes from the plan) host->device into plan-owned staging buffers
+ * (allocated on first use, kept until la_plan_destroy), decodes, copies out (and lse if
+ * non-NULL) device->host, and synchronises `stream`.  Host buffers should be pinned for
+ * full PCIe/NVLink-C2C bandwidth.  kv_rows: total rows of one cache (B*H_kv*max_ctx for
+ * BHSD, H_kv*sum n for PACKED) -- checked against the plan.
+ */
+la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache,
+                         int64_t kv_rows, float* out, float* lse, void* stream);
+
+/* Release a plan and all device memory it owns.  NULL is a no-op. */
+void la_plan_destroy(la_plan_t plan);
+
+/* Kernel launches issued by this library since load (for the bench's gpu_launches). */
+int64_t la_launch_count(void);
+
+const char* la_status_string(la_status s);
+const char* la_last_error(void);
+int la_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEANATTN_LA_H */

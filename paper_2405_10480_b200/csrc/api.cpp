@@ -1,0 +1,393 @@
+// C-ABI layer of libleanattn.so (include/la.h): argument validation, plan ownership of
+// device state, launch configuration.  Every step of the decode path runs in the kernels
+// of kernels.cu; this file only plans (integer work) and marshals.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "la_internal.h"
+
+using la::DevUnit;
+
+struct la_plan_s {
+  la::Problem prob;
+  la::Schedule sched;
+  la::KernelInfo kinfo;
+  int stage_tokens = 0;
+  bool host_only = true;
+  bool needs_wait = false;   // any non-finishing host -> cooperative launch required
+  int device = -1;
+  // device state owned by the plan
+  void* d_tables = nullptr;
+  DevUnit* d_units = nullptr;
+  int32_t* d_cta_begin = nullptr;
+  int32_t* d_cta_first = nullptr;
+  float* d_part_o = nullptr;
+  float* d_part_ml = nullptr;
+  uint32_t* d_flags = nullptr;
+  uint32_t epoch = 0;
+  int64_t workspace = 0;
+  // la_decode_host staging
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+la_status fail(la_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+la_status cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();  // clear sticky-less errors
+  return LA_ERR_CUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int auto_tile_n(const la::Problem& p, int max_ctas) {
+  // 64 KiB of K+V per LeanTile: 128 tokens at d=128 and 256 at d=64 for 16-bit inputs,
+  // the sizes the paper's sweep found; halved while the problem has fewer
+  // LeanTiles than resident CTAs so small problems still spread over the machine.
+  const int row_bytes = p.head_dim * p.elem_bytes();
+  int t = 65536 / (2 * row_bytes);
+  t = std::max(32, std::min(512, t));
+  auto iters = [&](int tn) {
+    int64_t I = 0;
+    for (int32_t n : p.ctx_lens) I += (int64_t(n) + tn - 1) / tn;
+    return I * p.heads_kv;
+  };
+  while (t > 32 && iters(t) < max_ctas) t /= 2;
+  return t;
+}
+
+void release_device(la_plan_s* p) {
+  if (p->d_tables) cudaFree(p->d_tables);
+  if (p->d_stage) cudaFree(p->d_stage);
+  p->d_tables = nullptr;
+  p->d_stage = nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int la_version(void) { return LA_VERSION; }
+
+const char* la_last_error(void) { return g_err.c_str(); }
+
+const char* la_status_string(la_status s) {
+  switch (s) {
+    case LA_OK: return "LA_OK";
+    case LA_ERR_INVALID: return "LA_ERR_INVALID";
+    case LA_ERR_UNSUPPORTED: return "LA_ERR_UNSUPPORTED";
+    case LA_ERR_CUDA: return "LA_ERR_CUDA";
+    case LA_ERR_NOMEM: return "LA_ERR_NOMEM";
+    case LA_ERR_STATE: return "LA_ERR_STATE";
+  }
+  return "LA_ERR_UNKNOWN";
+}
+
+int64_t la_launch_count(void) { return la::launch_count(); }
+
+la_status la_plan_opts_init(la_plan_opts* o) {
+  if (!o) return fail(LA_ERR_INVALID, "opts is NULL");
+  std::memset(o, 0, sizeof(*o));
+  o->layout = LA_KV_BHSD;
+  o->num_sms = 148;
+  o->ctas_per_sm = 1;
+  o->schedule = LA_SCHED_STREAMK;
+  return LA_OK;
+}
+
+la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int32_t* ctx_lens,
+                  int tile_n, la_dtype dtype, const la_plan_opts* opts_in, la_plan_t* out) {
+  if (!out) return fail(LA_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  la_plan_opts opts;
+  la_plan_opts_init(&opts);
+  if (opts_in) opts = *opts_in;
+  if (batch < 1 || heads_q < 1 || heads_kv < 1) return fail(LA_ERR_INVALID, "batch/heads must be >= 1");
+  if (heads_q % heads_kv) return fail(LA_ERR_INVALID, "heads_q must be a multiple of heads_kv (reading C3)");
+  if (!ctx_lens) return fail(LA_ERR_INVALID, "ctx_lens is NULL");
+  if (head_dim != 64 && head_dim != 128) return fail(LA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (dtype != LA_BF16 && dtype != LA_FP16 && dtype != LA_FP32) return fail(LA_ERR_INVALID, "bad dtype");
+  if (opts.layout != LA_KV_BHSD && opts.layout != LA_KV_PACKED) return fail(LA_ERR_INVALID, "bad layout");
+  if (opts.schedule != LA_SCHED_STREAMK && opts.schedule != LA_SCHED_SEQUENTIAL)
+    return fail(LA_ERR_INVALID, "bad schedule");
+  if (tile_n != 0 && tile_n != 16 && tile_n != 32 && tile_n != 64 && tile_n != 128 && tile_n != 256 &&
+      tile_n != 512)
+    return fail(LA_ERR_INVALID, "tile_n must be 0 or one of 16..512 (powers of two)");
+  if (opts.grid < 0) return fail(LA_ERR_INVALID, "grid must be >= 0");
+
+  la::Problem p;
+  p.batch = batch;
+  p.heads_q = heads_q;
+  p.heads_kv = heads_kv;
+  p.head_dim = head_dim;
+  p.group = heads_q / heads_kv;
+  p.dtype = dtype;
+  p.layout = opts.layout;
+  p.schedule = opts.schedule;
+  p.ctx_lens.assign(ctx_lens, ctx_lens + batch);
+  int64_t maxn = 0, total = 0;
+  for (int32_t n : p.ctx_lens) {
+    if (n < 1) return fail(LA_ERR_INVALID, "every ctx_lens[b] must be >= 1 (reading C6)");
+    maxn = std::max<int64_t>(maxn, n);
+    total += n;
+  }
+  p.max_ctx = opts.max_ctx ? opts.max_ctx : maxn;
+  if (p.layout == LA_KV_BHSD && p.max_ctx < maxn) return fail(LA_ERR_INVALID, "max_ctx < max(ctx_lens)");
+  p.scale = opts.scale != 0.f ? opts.scale : float(1.0 / std::sqrt(double(head_dim)));
+  if (!(p.scale > 0.f) || !std::isfinite(p.scale)) return fail(LA_ERR_INVALID, "scale must be finite and > 0");
+
+  auto* plan = new (std::nothrow) la_plan_s();
+  if (!plan) return fail(LA_ERR_NOMEM, "host allocation failed");
+  plan->prob = p;
+  plan->host_only = opts.host_only != 0;
+
+  // ---- co-resident CTA budget (reading C15) -----------------------------------------
+  int max_ctas = 0;
+  if (plan->host_only) {
+    max_ctas = std::max(1, opts.num_sms) * std::max(1, opts.ctas_per_sm);
+  } else {
+    plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.group);
+    if (!plan->kinfo.supported) {
+      delete plan;
+      return fail(LA_ERR_UNSUPPORTED, "no decode kernel for this (dtype, head_dim, group) in this build");
+    }
+    cudaError_t e = cudaGetDevice(&plan->device);
+    if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaGetDevice"); }
+    int sms = 0, occ = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
+    if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaDeviceGetAttribute"); }
+    e = cudaFuncSetAttribute(plan->kinfo.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             plan->kinfo.smem_bytes);
+    if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaFuncSetAttribute"); }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plan->kinfo.fn, plan->kinfo.threads,
+                                                      plan->kinfo.smem_bytes);
+    if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor"); }
+    if (occ < 1) { delete plan; return fail(LA_ERR_UNSUPPORTED, "decode kernel does not fit on an SM"); }
+    max_ctas = sms * occ;
+  }
+
+  // ---- schedule (Alg2§4-18) -----------------------------------------------------------
+  const int tn = tile_n ? tile_n : auto_tile_n(p, max_ctas);
+  la::Schedule& s = plan->sched;
+  s.tile_n = tn;
+  la::build_units(p, tn, s.units, s.total_iters);
+  if (s.total_iters >= (int64_t(1) << 31)) { delete plan; return fail(LA_ERR_INVALID, "too many LeanTiles"); }
+  if (p.schedule == LA_SCHED_SEQUENTIAL) {
+    s.grid = int(s.units.size());
+    la::sequential_ranges(s.units, s.cta_begin);
+  } else {
+    int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
+    if (!plan->host_only) G = std::min(G, max_ctas);  // hosts wait on peers: co-residency
+    s.grid = std::max(1, G);
+    la::streamk_ranges(s.total_iters, s.grid, s.cta_begin);
+  }
+  la::finish_schedule(s);
+  for (const DevUnit& u : s.units)
+    if (u.last_cta != u.host_cta) plan->needs_wait = true;
+  if (!plan->host_only && p.schedule == LA_SCHED_SEQUENTIAL && plan->needs_wait) {
+    delete plan;
+    return fail(LA_ERR_INVALID, "internal: sequential schedule with peers");
+  }
+  if (!plan->host_only && plan->needs_wait && s.grid > max_ctas) {
+    delete plan;
+    return fail(LA_ERR_INVALID, "grid exceeds the co-resident CTA count");
+  }
+  plan->stage_tokens = plan->host_only ? std::min(tn, 64) : std::min(tn, plan->kinfo.stage_tokens_max);
+
+  // ---- device state -------------------------------------------------------------------
+  if (!plan->host_only) {
+    const int G = s.grid;
+    auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t b_units = align(s.units.size() * sizeof(DevUnit));
+    const size_t b_begin = align(size_t(G + 1) * sizeof(int32_t));
+    const size_t b_first = align(size_t(G) * sizeof(int32_t));
+    const size_t b_po = align(size_t(G) * p.group * head_dim * sizeof(float));
+    const size_t b_pml = align(size_t(G) * p.group * 2 * sizeof(float));
+    const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
+    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags;
+    cudaError_t e = cudaMalloc(&plan->d_tables, bytes);
+    if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaMalloc(plan tables)"); }
+    char* base = static_cast<char*>(plan->d_tables);
+    plan->d_units = reinterpret_cast<DevUnit*>(base);
+    plan->d_cta_begin = reinterpret_cast<int32_t*>(base + b_units);
+    plan->d_cta_first = reinterpret_cast<int32_t*>(base + b_units + b_begin);
+    plan->d_part_o = reinterpret_cast<float*>(base + b_units + b_begin + b_first);
+    plan->d_part_ml = reinterpret_cast<float*>(base + b_units + b_begin + b_first + b_po);
+    plan->d_flags = reinterpret_cast<uint32_t*>(base + b_units + b_begin + b_first + b_po + b_pml);
+    plan->workspace = int64_t(bytes);
+    e = cudaMemcpy(plan->d_units, s.units.data(), s.units.size() * sizeof(DevUnit), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(plan->d_cta_begin, s.cta_begin.data(), (G + 1) * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(plan->d_cta_first, s.cta_first_unit.data(), G * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(plan->d_flags, 0, G * sizeof(uint32_t));
+    if (e != cudaSuccess) {
+      release_device(plan);
+      delete plan;
+      return cuda_fail(e, "plan upload");
+    }
+  }
+  *out = plan;
+  return LA_OK;
+}
+
+la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
+  if (!plan || !info) return fail(LA_ERR_INVALID, "NULL argument");
+  const la::Problem& p = plan->prob;
+  const la::Schedule& s = plan->sched;
+  std::memset(info, 0, sizeof(*info));
+  info->batch = p.batch;
+  info->heads_q = p.heads_q;
+  info->heads_kv = p.heads_kv;
+  info->head_dim = p.head_dim;
+  info->group = p.group;
+  info->dtype = p.dtype;
+  info->layout = p.layout;
+  info->schedule = p.schedule;
+  info->tile_n = s.tile_n;
+  info->stage_tokens = plan->stage_tokens;
+  info->grid = s.grid;
+  info->num_units = int(s.units.size());
+  info->total_iters = s.total_iters;
+  info->num_segments = s.num_segments;
+  info->num_partials = s.num_partials;
+  info->workspace_bytes = plan->workspace;
+  int64_t tokens = 0;
+  for (int32_t n : p.ctx_lens) tokens += n;
+  info->kv_bytes = 2 * int64_t(p.heads_kv) * tokens * p.head_dim * p.elem_bytes();
+  info->scale = p.scale;
+  return LA_OK;
+}
+
+la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t* n_rows) {
+  if (!plan || !n_rows) return fail(LA_ERR_INVALID, "NULL argument");
+  std::vector<int32_t> r;
+  la::export_segments(plan->sched, r);
+  *n_rows = r.size() / 7;
+  if (cap_rows == 0) return LA_OK;
+  if (!rows || cap_rows < *n_rows) return fail(LA_ERR_INVALID, "rows buffer too small");
+  std::memcpy(rows, r.data(), r.size() * sizeof(int32_t));
+  return LA_OK;
+}
+
+static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const void* v, float* out,
+                             float* lse, void* stream) {
+  if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
+  if (plan->host_only) return fail(LA_ERR_STATE, "host-only plan cannot decode");
+  if (!q || !k || !v || !out) return fail(LA_ERR_INVALID, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out))
+    return fail(LA_ERR_INVALID, "tensor pointers must be 16-byte aligned");
+  la::DecodeArgs a{};
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.out = out;
+  a.lse = lse;
+  a.units = plan->d_units;
+  a.cta_begin = plan->d_cta_begin;
+  a.cta_first_unit = plan->d_cta_first;
+  a.part_o = plan->d_part_o;
+  a.part_ml = plan->d_part_ml;
+  a.flags = plan->d_flags;
+  if (++plan->epoch == 0) {  // epoch wrapped: flags may hold any old value -> reset
+    cudaMemsetAsync(plan->d_flags, 0, plan->sched.grid * sizeof(uint32_t), (cudaStream_t)stream);
+    plan->epoch = 1;
+  }
+  a.epoch = plan->epoch;
+  a.grid = plan->sched.grid;
+  a.tile_n = plan->sched.tile_n;
+  a.stage_tokens = plan->stage_tokens;
+  a.group = plan->prob.group;
+  a.scale_log2 = float(double(plan->prob.scale) * 1.4426950408889634);
+  std::string err;
+  if (la::launch_decode(plan->kinfo, a, plan->needs_wait, stream, err) != 0)
+    return fail(LA_ERR_CUDA, err);
+  return LA_OK;
+}
+
+la_status la_decode(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache, float* out,
+                    float* lse, void* stream) {
+  return decode_impl(plan, q, k_cache, v_cache, out, lse, stream);
+}
+
+la_status la_decode_partial(la_plan_t plan, const void* q, const void* k_shard, const void* v_shard,
+                            float* o_part, float* lse_part, void* stream) {
+  if (!lse_part) return fail(LA_ERR_INVALID, "la_decode_partial needs lse_part");
+  return decode_impl(plan, q, k_shard, v_shard, o_part, lse_part, stream);
+}
+
+la_status la_combine(const float* o_parts, const float* lse_parts, int parts, int rows, int head_dim,
+                     float* out, float* lse, void* stream) {
+  if (!o_parts || !lse_parts || !out) return fail(LA_ERR_INVALID, "NULL tensor pointer");
+  if (parts < 1 || rows < 1) return fail(LA_ERR_INVALID, "parts and rows must be >= 1");
+  if (head_dim != 64 && head_dim != 128) return fail(LA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  std::string err;
+  if (la::launch_combine(o_parts, lse_parts, parts, rows, head_dim, out, lse, stream, err) != 0)
+    return fail(LA_ERR_CUDA, err);
+  return LA_OK;
+}
+
+la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache,
+                         int64_t kv_rows, float* out, float* lse, void* stream) {
+  if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
+  if (plan->host_only) return fail(LA_ERR_STATE, "host-only plan cannot decode");
+  if (!q || !k_cache || !v_cache || !out) return fail(LA_ERR_INVALID, "NULL host pointer");
+  const la::Problem& p = plan->prob;
+  if (kv_rows != p.kv_rows()) return fail(LA_ERR_INVALID, "kv_rows does not match the plan");
+  const size_t eb = size_t(p.elem_bytes());
+  const size_t q_bytes = size_t(p.batch) * p.heads_q * p.head_dim * eb;
+  const size_t kv_bytes = size_t(kv_rows) * p.head_dim * eb;
+  const size_t o_bytes = size_t(p.batch) * p.heads_q * p.head_dim * sizeof(float);
+  const size_t l_bytes = size_t(p.batch) * p.heads_q * sizeof(float);
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t need = align(q_bytes) + 2 * align(kv_bytes) + align(o_bytes) + align(l_bytes);
+  if (plan->stage_bytes < need) {
+    if (plan->d_stage) cudaFree(plan->d_stage);
+    plan->d_stage = nullptr;
+    plan->stage_bytes = 0;
+    cudaError_t e = cudaMalloc(&plan->d_stage, need);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+    plan->stage_bytes = need;
+  }
+  char* base = static_cast<char*>(plan->d_stage);
+  void* dq = base;
+  void* dk = base + align(q_bytes);
+  void* dv = base + align(q_bytes) + align(kv_bytes);
+  float* dout = reinterpret_cast<float*>(base + align(q_bytes) + 2 * align(kv_bytes));
+  float* dlse = reinterpret_cast<float*>(base + align(q_bytes) + 2 * align(kv_bytes) + align(o_bytes));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(dq, q, q_bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dk, k_cache, kv_bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dv, v_cache, kv_bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  la_status s = decode_impl(plan, dq, dk, dv, dout, lse ? dlse : nullptr, stream);
+  if (s != LA_OK) return s;
+  e = cudaMemcpyAsync(out, dout, o_bytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && lse) e = cudaMemcpyAsync(lse, dlse, l_bytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H/sync");
+  return LA_OK;
+}
+
+void la_plan_destroy(la_plan_t plan) {
+  if (!plan) return;
+  release_device(plan);
+  delete plan;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+// Internal declarations shared by the planner, the C-ABI layer and the kernels.
+// Nothing here is visible through include/la.h.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "la.h"
+
+namespace la {
+
+// One work unit (= output tile): the T_m = g query heads of (b, h_kv) against
+// that KV head's n_b cached rows.  32 bytes, uploaded as-is to the device.
+struct DevUnit {
+  int64_t row0;        // first K/V row of the unit (a row = head_dim elements)
+  int32_t len;         // n_b
+  int32_t iter_begin;  // tile_iter of Alg2§12: global index of the unit's first LeanTile
+  int32_t iter_end;    // tile_iter_end of Alg2§13
+  int32_t q_row;       // row of the unit's first q-head in the (B*H_q) query/output rows
+  int32_t last_cta;    // owner(iter_end - 1): reading C9 of Alg2§26
+  int32_t host_cta;    // owner(iter_begin): the host block of P:412 / Alg2§17
+};
+static_assert(sizeof(DevUnit) == 32, "DevUnit layout");
+
+// Host-side schedule: Alg2§4-18 for every CTA.  Pure integer work, no CUDA.
+struct Schedule {
+  int tile_n = 0;
+  int grid = 0;
+  int64_t total_iters = 0;
+  std::vector<DevUnit> units;
+  std::vector<int32_t> cta_begin;       // G + 1 entries: CTA g owns [cta_begin[g], cta_begin[g+1])
+  std::vector<int32_t> cta_first_unit;  // G entries: unit containing cta_begin[g]
+  int64_t num_segments = 0;
+  int64_t num_partials = 0;
+};
+
+struct Problem {
+  int batch = 0, heads_q = 0, heads_kv = 0, head_dim = 0, group = 0;
+  int dtype = LA_BF16, layout = LA_KV_BHSD, schedule = LA_SCHED_STREAMK;
+  int64_t max_ctx = 0;
+  float scale = 0.f;
+  std::vector<int32_t> ctx_lens;
+  int64_t kv_rows() const;   // rows of one K (or V) cache in its layout
+  int elem_bytes() const { return dtype == LA_FP32 ? 4 : 2; }
+};
+
+// Build units in memory order (reading C14) with their row bases and C_n = ceil(n/T_n).
+void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int64_t& total_iters);
+// Eq. 2 / Alg2§7-9 with the remainder rule (reading C8); grid >= 1.
+void streamk_ranges(int64_t total_iters, int grid, std::vector<int32_t>& cta_begin);
+// Sequential (FA2): one CTA per unit.
+void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& cta_begin);
+// host_cta / last_cta per unit, first unit per CTA, segment & partial counts.
+void finish_schedule(Schedule& s);
+// Segment rows (7 int32 each, SPEC S:275 order) by the Alg2§10-18,§41 walk.
+void export_segments(const Schedule& s, std::vector<int32_t>& rows);
+
+// ---- device side (kernels.cu) -------------------------------------------------------
+struct DecodeArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  float* out;
+  float* lse;
+  const DevUnit* units;
+  const int32_t* cta_begin;
+  const int32_t* cta_first_unit;
+  float* part_o;      // [G][group][d]  Op of Alg2§20
+  float* part_ml;     // [G][group][2]  mp, lp of Alg2§21-22 (m in log2 units)
+  uint32_t* flags;    // [G]            flags of Alg2§23/§28, epoch-valued (reading C17)
+  uint32_t epoch;
+  int grid;
+  int tile_n;
+  int stage_tokens;
+  int group;
+  float scale_log2;   // scale * log2(e): scores live in the exp2 domain inside the kernel
+};
+
+// Kernel configuration for (dtype, head_dim, group): threads, dynamic smem, max stage tokens.
+struct KernelInfo {
+  bool supported = false;
+  int threads = 0;
+  int smem_bytes = 0;
+  int stage_tokens_max = 0;
+  const void* fn = nullptr;
+};
+KernelInfo decode_kernel_info(int dtype, int head_dim, int group);
+// Launch the decode kernel (cooperative when any CTA waits on a peer).
+int launch_decode(const KernelInfo& ki, const DecodeArgs& a, bool cooperative, void* stream,
+                  std::string& err);
+int launch_combine(const float* o_parts, const float* lse_parts, int parts, int rows,
+                   int head_dim, float* out, float* lse, void* stream, std::string& err);
+int64_t launch_count();
+
+}  // namespace la

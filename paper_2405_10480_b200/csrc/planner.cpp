@@ -1,0 +1,122 @@
+// Host planner: the stream-K decomposition and mapping of LeanTiles (§4.3, Alg. 2 §4-18).
+//
+// P:412  "Each CTAs range of LeanTile iterations is mapped contiguously into the batch size
+//         -> heads -> context length linearization, crossing the head and query boundary as
+//         it may ... each attention output tile is consolidated by the CTA that performed that
+//         output's first LeanTile (called as a host block)."
+// P:432  ragged: "mapped contiguously in a Heads -> TotalContextLength linearization".
+// Eq. 2 / Alg2§6-9: I = sum_u C_n(u), equal contiguous ranges per CTA.
+//
+// Integer work only; tests check it bit-exactly against the oracle's independent
+// enumeration (tests/test_planner.py).
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "la_internal.h"
+
+namespace la {
+
+int64_t Problem::kv_rows() const {
+  if (layout == LA_KV_BHSD) return int64_t(batch) * heads_kv * max_ctx;
+  int64_t total = 0;
+  for (int32_t n : ctx_lens) total += n;
+  return int64_t(heads_kv) * total;
+}
+
+void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int64_t& total_iters) {
+  units.clear();
+  units.reserve(size_t(p.batch) * p.heads_kv);
+  std::vector<int64_t> cu(p.batch + 1, 0);  // cu_seqlens
+  for (int b = 0; b < p.batch; ++b) cu[b + 1] = cu[b] + p.ctx_lens[b];
+  int64_t it = 0;
+  auto add = [&](int b, int h) {
+    DevUnit u{};
+    u.len = p.ctx_lens[b];
+    u.row0 = (p.layout == LA_KV_BHSD) ? (int64_t(b) * p.heads_kv + h) * p.max_ctx
+                                      : int64_t(h) * cu[p.batch] + cu[b];
+    u.q_row = b * p.heads_q + h * p.group;
+    u.iter_begin = int32_t(it);
+    it += (int64_t(u.len) + tile_n - 1) / tile_n;   // C_n = ceil(n_b / T_n)   (Alg2§5)
+    u.iter_end = int32_t(it);
+    u.last_cta = u.host_cta = -1;
+    units.push_back(u);
+  };
+  if (p.layout == LA_KV_BHSD) {
+    for (int b = 0; b < p.batch; ++b)           // batch -> heads -> context
+      for (int h = 0; h < p.heads_kv; ++h) add(b, h);
+  } else {
+    for (int h = 0; h < p.heads_kv; ++h)        // heads -> total context
+      for (int b = 0; b < p.batch; ++b) add(b, h);
+  }
+  total_iters = it;
+}
+
+void streamk_ranges(int64_t total_iters, int grid, std::vector<int32_t>& cta_begin) {
+  // Reading C8: the first r = I mod G CTAs take ceil(I/G), the others floor(I/G).
+  const int64_t q = total_iters / grid, r = total_iters % grid;
+  cta_begin.resize(size_t(grid) + 1);
+  for (int g = 0; g <= grid; ++g) cta_begin[g] = int32_t(g * q + std::min<int64_t>(g, r));
+}
+
+void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& cta_begin) {
+  cta_begin.resize(units.size() + 1);
+  for (size_t u = 0; u < units.size(); ++u) cta_begin[u] = units[u].iter_begin;
+  cta_begin[units.size()] = units.empty() ? 0 : units.back().iter_end;
+}
+
+static int owner_of(const std::vector<int32_t>& cta_begin, int64_t it) {
+  // The CTA g with cta_begin[g] <= it < cta_begin[g+1]; empty CTAs (G > I) are skipped
+  // because upper_bound lands past every CTA whose range starts at the same index.
+  auto pos = std::upper_bound(cta_begin.begin(), cta_begin.end(), int32_t(it));
+  return int(pos - cta_begin.begin()) - 1;
+}
+
+void finish_schedule(Schedule& s) {
+  const int G = s.grid;
+  for (DevUnit& u : s.units) {
+    u.host_cta = owner_of(s.cta_begin, u.iter_begin);     // host block (Alg2§17)
+    u.last_cta = owner_of(s.cta_begin, u.iter_end - 1);   // reading C9 of Alg2§26
+  }
+  s.cta_first_unit.assign(G, 0);
+  size_t unit = 0;
+  int64_t segs = 0, partials = 0;
+  for (int g = 0; g < G; ++g) {
+    const int64_t b = s.cta_begin[g], e = s.cta_begin[g + 1];
+    while (unit < s.units.size() && s.units[unit].iter_end <= b) ++unit;
+    s.cta_first_unit[g] = int32_t(std::min(unit, s.units.empty() ? 0 : s.units.size() - 1));
+    size_t u = unit;
+    for (int64_t it = b; it < e;) {                        // Alg2§10, §41 (reading C10)
+      while (s.units[u].iter_end <= it) ++u;
+      ++segs;
+      if (it != s.units[u].iter_begin) ++partials;         // non-host segment (Alg2§19)
+      it = s.units[u].iter_end;
+    }
+  }
+  s.num_segments = segs;
+  s.num_partials = partials;
+}
+
+void export_segments(const Schedule& s, std::vector<int32_t>& rows) {
+  rows.clear();
+  rows.reserve(size_t(s.num_segments) * 7);
+  for (int g = 0; g < s.grid; ++g) {
+    const int64_t cta_start = s.cta_begin[g], cta_end = s.cta_begin[g + 1];   // Alg2§9
+    size_t u = size_t(s.cta_first_unit[g]);
+    for (int64_t it = cta_start; it < cta_end;) {
+      while (s.units[u].iter_end <= it) ++u;                                   // tile_idx §11
+      const DevUnit& d = s.units[u];
+      const int64_t tile_iter = d.iter_begin, tile_iter_end = d.iter_end;      // §12-13
+      rows.push_back(g);
+      rows.push_back(int32_t(u));
+      rows.push_back(int32_t(it - tile_iter));                                 // local_iter §14
+      rows.push_back(int32_t(std::min(tile_iter_end, cta_end) - tile_iter));   // §15
+      rows.push_back(it == tile_iter ? 1 : 0);                                 // host §17
+      rows.push_back(cta_end >= tile_iter_end ? 1 : 0);                        // finishing §18
+      rows.push_back(d.last_cta);                                              // §26 (C9)
+      it = tile_iter_end;                                                      // §41
+    }
+  }
+}
+
+}  // namespace la

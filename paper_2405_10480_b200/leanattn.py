@@ -1,0 +1,225 @@
+"""Thin ctypes binding of libleanattn.so (include/la.h).  Argument marshalling only.
+
+Every step of the decode path runs in the library's CUDA kernels; this module converts
+torch tensors to raw pointers and the current CUDA stream to a ``cudaStream_t``.  There is
+no fallback: if the shared library is missing or a call fails, it raises.
+
+Names follow the C ABI: :func:`la_plan` -> :class:`Plan`, ``Plan.decode`` = ``la_decode``,
+``Plan.decode_partial`` = ``la_decode_partial``, :func:`la_combine`, ``Plan.export`` =
+``la_plan_export``, ``Plan.info`` = ``la_plan_info_get``, ``Plan.decode_host`` =
+``la_decode_host``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libleanattn.so")
+
+LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE = range(6)
+LA_BF16, LA_FP16, LA_FP32 = 0, 1, 2
+LA_KV_BHSD, LA_KV_PACKED = 0, 1
+LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL = 0, 1
+
+_DTYPE_CODES = {"bf16": LA_BF16, "fp16": LA_FP16, "fp32": LA_FP32}
+_LAYOUT_CODES = {"bhsd": LA_KV_BHSD, "packed": LA_KV_PACKED}
+_SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL}
+
+# Every symbol include/la.h declares (tests check the library exports all of them).
+EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
+           "la_decode_partial", "la_combine", "la_decode_host", "la_plan_destroy",
+           "la_launch_count", "la_status_string", "la_last_error", "la_version")
+
+
+class LaError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: status {status}: {msg}")
+        self.status = status
+
+
+class la_plan_opts(ctypes.Structure):
+    _fields_ = [("scale", ctypes.c_float), ("layout", ctypes.c_int), ("max_ctx", ctypes.c_int64),
+                ("grid", ctypes.c_int), ("num_sms", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
+                ("host_only", ctypes.c_int), ("schedule", ctypes.c_int)]
+
+
+class la_plan_info(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("batch", "heads_q", "heads_kv", "head_dim", "group", "dtype",
+                                            "layout", "schedule", "tile_n", "stage_tokens", "grid",
+                                            "num_units")] + \
+               [(n, ctypes.c_int64) for n in ("total_iters", "num_segments", "num_partials",
+                                              "workspace_bytes", "kv_bytes")] + \
+               [("scale", ctypes.c_float)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libleanattn.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                           f"g.build()'` (there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, f32p = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_float)
+    L.la_plan_opts_init.argtypes = [ctypes.POINTER(la_plan_opts)]
+    L.la_plan.argtypes = [i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int32), i32, i32,
+                          ctypes.POINTER(la_plan_opts), ctypes.POINTER(vp)]
+    L.la_plan_info_get.argtypes = [vp, ctypes.POINTER(la_plan_info)]
+    L.la_plan_export.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.c_size_t,
+                                 ctypes.POINTER(ctypes.c_size_t)]
+    L.la_decode.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.la_decode_partial.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.la_combine.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
+    L.la_decode_host.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
+    L.la_plan_destroy.argtypes = [vp]
+    L.la_plan_destroy.restype = None
+    L.la_launch_count.restype = i64
+    L.la_status_string.restype = ctypes.c_char_p
+    L.la_last_error.restype = ctypes.c_char_p
+    for name in ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
+                 "la_decode_partial", "la_combine", "la_decode_host"):
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int, where: str):
+    if status != LA_OK:
+        raise LaError(status, where, lib().la_last_error().decode())
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def launch_count() -> int:
+    return int(lib().la_launch_count())
+
+
+class Plan:
+    """``la_plan``: the stream-K schedule (and, unless host_only, its device state)."""
+
+    def __init__(self, batch: int, heads_q: int, heads_kv: int, head_dim: int, ctx_lens: Sequence[int],
+                 tile_n: int = 0, dtype: str = "bf16", scale: float = 0.0, layout: str = "bhsd",
+                 max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
+                 ctas_per_sm: int = 1, schedule: str = "streamk"):
+        L = lib()
+        opts = la_plan_opts()
+        _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
+        opts.scale = float(scale)
+        opts.layout = _LAYOUT_CODES[layout]
+        opts.max_ctx = int(max_ctx)
+        opts.grid = int(grid)
+        opts.num_sms = int(num_sms)
+        opts.ctas_per_sm = int(ctas_per_sm)
+        opts.host_only = 1 if host_only else 0
+        opts.schedule = _SCHED_CODES[schedule]
+        lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
+        h = ctypes.c_void_p()
+        self._h = None
+        _check(L.la_plan(int(batch), int(heads_q), int(heads_kv), int(head_dim), lens, int(tile_n),
+                         _DTYPE_CODES[dtype], ctypes.byref(opts), ctypes.byref(h)), "la_plan")
+        self._h = h
+        self.dtype = dtype
+        self.layout = layout
+        self.ctx_lens = [int(x) for x in ctx_lens]
+        self.info = self._info()
+
+    def _info(self) -> la_plan_info:
+        inf = la_plan_info()
+        _check(lib().la_plan_info_get(self._h, ctypes.byref(inf)), "la_plan_info_get")
+        return inf
+
+    def export(self) -> np.ndarray:
+        """``la_plan_export``: (n_segments, 7) int32 rows
+        (cta, unit, local_begin, local_end, host, finishing, last_cta)."""
+        n = ctypes.c_size_t()
+        _check(lib().la_plan_export(self._h, None, 0, ctypes.byref(n)), "la_plan_export")
+        buf = np.zeros((n.value, 7), dtype=np.int32)
+        _check(lib().la_plan_export(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n.value,
+                                    ctypes.byref(n)), "la_plan_export")
+        return buf
+
+    def _outputs(self, q, out, lse, need_lse):
+        import torch
+        B, H, D = self.info.batch, self.info.heads_q, self.info.head_dim
+        if out is None:
+            out = torch.empty(B, H, D, dtype=torch.float32, device=q.device)
+        if lse is None and need_lse:
+            lse = torch.empty(B, H, dtype=torch.float32, device=q.device)
+        return out, lse
+
+    def _check_inputs(self, q, k, v):
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous CUDA tensor")
+
+    def decode(self, q, k, v, out=None, lse=None, stream=None, want_lse: bool = True):
+        """``la_decode``; returns (out fp32 (B, H_q, d), lse fp32 (B, H_q) or None)."""
+        self._check_inputs(q, k, v)
+        out, lse = self._outputs(q, out, lse, want_lse)
+        _check(lib().la_decode(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _stream(stream)),
+               "la_decode")
+        return out, lse
+
+    def decode_partial(self, q, k_shard, v_shard, o_part=None, lse_part=None, stream=None):
+        """``la_decode_partial`` on one sequence shard; lse is always produced."""
+        self._check_inputs(q, k_shard, v_shard)
+        o_part, lse_part = self._outputs(q, o_part, lse_part, True)
+        _check(lib().la_decode_partial(self._h, _ptr(q), _ptr(k_shard), _ptr(v_shard), _ptr(o_part),
+                                       _ptr(lse_part), _stream(stream)), "la_decode_partial")
+        return o_part, lse_part
+
+    def decode_host(self, q, k, v, out, lse=None, stream=None):
+        """``la_decode_host``: host (ideally pinned) tensors in, host tensors out."""
+        rows = k.numel() // self.info.head_dim
+        _check(lib().la_decode_host(self._h, _ptr(q), _ptr(k), _ptr(v), int(rows), _ptr(out), _ptr(lse),
+                                    _stream(stream)), "la_decode_host")
+        return out, lse
+
+    def close(self):
+        if self._h is not None:
+            lib().la_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def la_plan(*args, **kw) -> Plan:
+    return Plan(*args, **kw)
+
+
+def la_combine(o_parts, lse_parts, out=None, lse=None, stream=None):
+    """``la_combine``: o_parts (P, rows..., d) fp32, lse_parts (P, rows...) fp32 (CUDA)."""
+    import torch
+    P = o_parts.shape[0]
+    d = o_parts.shape[-1]
+    rows = lse_parts[0].numel()
+    if out is None:
+        out = torch.empty(o_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
+    if lse is None:
+        lse = torch.empty(lse_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
+    if not (o_parts.is_contiguous() and lse_parts.is_contiguous()):
+        raise ValueError("o_parts / lse_parts must be contiguous")
+    _check(lib().la_combine(_ptr(o_parts), _ptr(lse_parts), int(P), int(rows), int(d), _ptr(out), _ptr(lse),
+                            _stream(stream)), "la_combine")
+    return out, lse

@@ -1,0 +1,156 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Sizes the oracle finishes in seconds that still span several LeanTiles, CTAs and ragged
+tails; the BASELINE.json configs at full size are checked on sampled units (oracle) and by
+closed forms that hold at any size (census input, q = 0 -> L = ln n)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from _helpers import cuda_inputs, gate, run_cuda, run_oracle, oracle_unit, census_expect
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2405_10480_b200 import build as b
+    b.build()
+    import paper_2405_10480_b200 as la
+    la.lib()
+
+
+@pytest.mark.parametrize("dist", ["D0", "D1", "D2", "D3", "D4"])
+def test_c1_fp32_d64(dist):
+    p = synth.config("c1", dist=dist)
+    O, L, plan = run_cuda(p)
+    O_ref, L_ref = run_oracle(p)
+    gate(O, L, O_ref, L_ref, what=f"c1/{dist}")
+    assert plan.info.grid > 1 and plan.info.num_partials > 0     # the fixup path is exercised
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("dist", ["D1", "D2", "D4"])
+def test_small_multi_tile_ragged(dtype, d, dist):
+    p = synth.Problem(2, 3, 3, d, [1000, 777], dtype=dtype, dist=dist, seed=11, max_ctx=1024)
+    O_ref, L_ref = run_oracle(p)
+    inputs = cuda_inputs(p)
+    for tile_n in (32, 128):
+        for grid in (1, 2, 3, 7, 64, 0):
+            O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid)
+            gate(O, L, O_ref, L_ref, what=f"{dtype}/d{d}/{dist}/T{tile_n}/G{grid}")
+
+
+def test_forced_grid_and_tile_invariance_and_determinism():
+    p = synth.Problem(1, 4, 4, 128, [5000], dtype="bf16", dist="D2", seed=12)
+    O_ref, L_ref = run_oracle(p)
+    inputs = cuda_inputs(p)
+    outs = []
+    for grid in (1, 2, 3, 5, 16, 37, 148, 0):
+        for tile_n in (16, 64, 256):
+            O, L, _ = run_cuda(p, inputs=inputs, grid=grid, tile_n=tile_n)
+            gate(O, L, O_ref, L_ref, what=f"G{grid}/T{tile_n}")
+            outs.append(O)
+    # bitwise determinism of a fixed plan (reading C16)
+    import paper_2405_10480_b200 as la
+    q, k, v = inputs
+    plan = la.Plan(1, 4, 4, 128, [5000], grid=37, tile_n=64)
+    ref = plan.decode(q, k, v)[0].clone()
+    for _ in range(10):
+        assert torch.equal(plan.decode(q, k, v)[0], ref)
+
+
+def test_census_and_zero_query_closed_forms():
+    # q = 0: every score is 0 -> O = census closed form, L = ln n exactly (coverage, C21)
+    p = synth.Problem(3, 2, 2, 128, [4096, 2048, 1000], dtype="bf16", dist="D3", seed=13, max_ctx=4096)
+    O, L, plan = run_cuda(p, tile_n=64, grid=0)
+    for b in range(3):
+        o_exp, l_exp = census_expect(p, b)
+        for h in range(2):
+            assert np.max(np.abs(O[b, h] - o_exp)) <= 1e-6
+            assert abs(L[b, h] - l_exp) <= 1e-5
+
+
+def test_packed_layout_equals_oracle():
+    p = synth.Problem(4, 2, 2, 128, [300, 1500, 64, 999], dtype="bf16", dist="D1", seed=14, layout="packed")
+    O_ref, L_ref = run_oracle(p)
+    for grid in (3, 0):
+        O, L, _ = run_cuda(p, tile_n=64, grid=grid)
+        gate(O, L, O_ref, L_ref, what=f"packed/G{grid}")
+
+
+def test_single_token_and_tiny_contexts():
+    p = synth.Problem(5, 1, 1, 128, [1, 2, 31, 32, 33], dtype="bf16", dist="D1", seed=15)
+    O_ref, L_ref = run_oracle(p)
+    for grid in (1, 2, 0):
+        O, L, _ = run_cuda(p, tile_n=16, grid=grid)
+        gate(O, L, O_ref, L_ref, what=f"tiny/G{grid}")
+
+
+def test_c2_full_size_sampled():
+    """North-star config (B=1, H=32, d=128, n=256k, bf16) in the bench's launch config."""
+    p = synth.config("c2")
+    inputs = cuda_inputs(p)
+    O, L, plan = run_cuda(p, inputs=inputs)
+    assert plan.info.grid == 148 and plan.info.tile_n == 128
+    for h in (0, 19):
+        O_ref, L_ref = oracle_unit(p, 0, h)
+        gate(O[0, h:h + 1], L[0, h:h + 1], O_ref, L_ref, what=f"c2 head {h}")
+    del inputs
+    torch.cuda.empty_cache()
+    # census at full size: closed form for every head
+    p3 = synth.config("c2", dist="D3")
+    O3, L3, _ = run_cuda(p3)
+    o_exp, l_exp = census_expect(p3, 0)
+    assert np.max(np.abs(O3[0] - o_exp[None, :])) <= 1e-5
+    assert np.max(np.abs(L3[0] - l_exp)) <= 1e-5
+
+
+def test_c4_ragged_full_size_sampled():
+    p = synth.config("c4")
+    O, L, plan = run_cuda(p)
+    assert plan.info.total_iters == 245056
+    for b, h in ((1, 3), (6, 0), (13, 31)):
+        O_ref, L_ref = oracle_unit(p, b, h)
+        gate(O[b, h:h + 1], L[b, h:h + 1], O_ref, L_ref, what=f"c4 b{b} h{h}")
+    torch.cuda.empty_cache()
+    p3 = synth.config("c4", dist="D3")
+    O3, L3, _ = run_cuda(p3)
+    for b in range(p3.batch):
+        o_exp, l_exp = census_expect(p3, b)
+        assert np.max(np.abs(O3[b] - o_exp[None, :])) <= 1e-5, b
+        assert np.max(np.abs(L3[b] - l_exp)) <= 1e-5, b
+    torch.cuda.empty_cache()
+
+
+def test_c4_packed_full_size_sampled():
+    p = synth.config("c4", layout="packed")
+    O, L, plan = run_cuda(p)
+    for b, h in ((1, 3), (9, 17)):
+        O_ref, L_ref = oracle_unit(p, b, h)
+        gate(O[b, h:h + 1], L[b, h:h + 1], O_ref, L_ref, what=f"c4 packed b{b} h{h}")
+    torch.cuda.empty_cache()
+
+
+def test_synth_device_host_bit_identity():
+    p = synth.config("c2")
+    a = synth.gen_kv_unit(p, 0, 7, "k", "cuda", 1000, 3000).cpu()
+    b = synth.gen_kv_unit(p, 0, 7, "k", "cpu", 1000, 3000)
+    assert torch.equal(a, b)
+    assert torch.equal(synth.gen_q(p, "cuda").cpu(), synth.gen_q(p, "cpu"))
+
+
+def test_decode_host_e2e_path():
+    p = synth.Problem(2, 4, 4, 128, [3000, 100], dtype="bf16", dist="D1", seed=16)
+    q, k, v = [t.cpu().pin_memory() for t in cuda_inputs(p, device="cpu")]
+    import paper_2405_10480_b200 as la
+    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, p.ctx_lens)
+    out = torch.empty(p.batch, p.heads_q, p.head_dim, dtype=torch.float32).pin_memory()
+    lse = torch.empty(p.batch, p.heads_q, dtype=torch.float32).pin_memory()
+    plan.decode_host(q, k, v, out, lse)
+    O_ref, L_ref = run_oracle(p)
+    gate(out.numpy(), lse.numpy(), O_ref, L_ref, what="decode_host")

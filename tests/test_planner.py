@@ -1,0 +1,126 @@
+"""C-ABI library (CPU side): it loads, exports every symbol include/la.h declares, and its
+host planner reproduces the oracle's stream-K enumeration BIT-EXACTLY (BASELINE.json:
+"The planner's tile-to-CTA schedule is integer work and must match a reference
+enumeration bit-exactly").  No compute calls -- host-only plans need no GPU."""
+import itertools
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.lean_attention import unit_order
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def la():
+    from paper_2405_10480_b200 import build as b
+    b.build()
+    import paper_2405_10480_b200 as pkg
+    pkg.lib()
+    return pkg
+
+
+def test_exports_every_declared_symbol(la):
+    header = open(os.path.join(ROOT, "include", "la.h")).read()
+    declared = set(re.findall(r"^\s*(?:la_status|void|int64_t|int|const char\*)\s+(la_\w+)\s*\(", header, re.M))
+    assert declared == set(la.EXPORTS)
+    nm = subprocess.run(["nm", "-D", "--defined-only", la.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (la_\w+)", nm))
+    assert declared <= exported, declared - exported
+    L = la.lib()
+    assert L.la_version() == 1
+    assert L.la_status_string(1) == b"LA_ERR_INVALID"
+
+
+def _oracle_rows(batch, heads_kv, lens, tile_n, grid, layout):
+    units = unit_order(batch, heads_kv, layout)
+    c_n = [-(-lens[b] // tile_n) for (b, _h) in units]
+    return np.array([s.row() for s in oracle.stream_k_segments(c_n, grid)], dtype=np.int32).reshape(-1, 7)
+
+
+def test_fig1_golden_through_the_abi(la):
+    p = la.Plan(1, 2, 2, 128, [5 * 128], tile_n=128, grid=5, host_only=True)
+    rows = p.export()
+    golden = [tuple(int(x) for x in l.split()) for l in open(os.path.join(ROOT, "tests", "golden", "fig1_schedule.txt"))
+              if l.strip() and not l.startswith("#")]
+    assert [tuple(r) for r in rows] == golden
+    assert p.info.total_iters == 10 and p.info.num_partials == 4 and p.info.grid == 5
+
+
+def test_exhaustive_small_bit_exact(la):
+    n = 0
+    for batch, heads, layout in itertools.product([1, 2, 3], [1, 2], ["bhsd", "packed"]):
+        for lens in itertools.product([1, 16, 17, 40, 64], repeat=batch):
+            I = sum(-(-x // 16) for x in lens) * heads
+            for G in sorted({1, 2, 3, I // 2 + 1, I, I + 2}):
+                p = la.Plan(batch, heads, heads, 64, list(lens), tile_n=16, grid=G, layout=layout, host_only=True)
+                got = p.export()
+                exp = _oracle_rows(batch, heads, list(lens), 16, G, layout)
+                assert np.array_equal(got, exp), (batch, heads, lens, G, layout)
+                assert p.info.total_iters == I
+                n += 1
+    assert n > 500
+
+
+def test_random_large_and_configs_bit_exact(la):
+    rng = np.random.default_rng(0)
+    for trial in range(30):
+        batch = int(rng.integers(1, 17))
+        heads = int(rng.integers(1, 33))
+        lens = [int(x) for x in rng.integers(1, 20000, size=batch)]
+        tile = int(rng.choice([32, 64, 128, 256]))
+        layout = ["bhsd", "packed"][trial % 2]
+        I = sum(-(-x // tile) for x in lens) * heads
+        G = int(rng.integers(1, min(I, 600) + 1))
+        p = la.Plan(batch, heads, heads, 128, lens, tile_n=tile, grid=G, layout=layout, host_only=True)
+        assert np.array_equal(p.export(), _oracle_rows(batch, heads, lens, tile, G, layout))
+    # BASELINE.json configs on a 148-SM B200 (1 CTA / SM)
+    import synth
+    expect_I = {"c2": 65536, "c3": 32768, "c4": 245056, "c5": 262144}
+    for name, I in expect_I.items():
+        pr = synth.config(name)
+        p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
+                    num_sms=148, ctas_per_sm=1, layout=pr.layout)
+        assert p.info.total_iters == I and p.info.grid == 148 and p.info.tile_n == 128
+        rows = p.export()
+        assert np.array_equal(rows, _oracle_rows(pr.batch, pr.heads_kv, pr.ctx_lens, 128, 148, pr.layout))
+        per = np.bincount(rows[:, 0], weights=rows[:, 3] - rows[:, 2])
+        assert per.max() - per.min() <= 1                      # Eq. 2 balance
+        # <= 1 partial per CTA (the plan allocates one slot per CTA)
+        assert np.bincount(rows[rows[:, 4] == 0][:, 0], minlength=148).max() <= 1
+    # c4 packed layout: heads -> total context
+    pr = synth.config("c4", layout="packed")
+    p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
+                layout="packed")
+    assert np.array_equal(p.export(), _oracle_rows(pr.batch, pr.heads_kv, pr.ctx_lens, 128, 148, "packed"))
+
+
+def test_auto_tile_and_sequential(la):
+    p = la.Plan(1, 32, 32, 128, [262144], host_only=True)
+    assert p.info.tile_n == 128 and p.info.grid == 148           # P:396 for d=128
+    p = la.Plan(1, 8, 8, 64, [1 << 16], host_only=True)
+    assert p.info.tile_n == 256                                  # P:396 for d=64
+    p = la.Plan(1, 1, 1, 64, [4096], dtype="fp32", host_only=True)
+    assert p.info.total_iters >= 64                              # small problem spread out
+    p = la.Plan(2, 3, 3, 128, [300, 1000], tile_n=64, host_only=True, schedule="sequential")
+    rows = p.export()
+    assert p.info.grid == 6 and len(rows) == 6
+    assert all(r[4] == 1 and r[5] == 1 and r[0] == r[1] for r in rows)   # FA2: one full unit per CTA
+
+
+@pytest.mark.parametrize("args,status", [
+    (dict(head_dim=96), 2), (dict(heads_q=3, heads_kv=2), 1), (dict(lens=[0]), 1),
+    (dict(tile_n=100), 1), (dict(batch=0, lens=[]), 1),
+])
+def test_validation(la, args, status):
+    kw = dict(batch=1, heads_q=2, heads_kv=2, head_dim=128, lens=[100], tile_n=0)
+    kw.update(args)
+    with pytest.raises(la.LaError) as e:
+        la.Plan(kw["batch"], kw["heads_q"], kw["heads_kv"], kw["head_dim"], kw["lens"], tile_n=kw["tile_n"],
+                host_only=True)
+    assert e.value.status == status
