@@ -1,19 +1,20 @@
 // sm_100a kernels of libleanattn.so.
 //
-//  la_decode_mha<T, D, NCW, NST>  -- LeanAttention decode, one persistent launch:
+//  la_decode_mha<T, D, NST, WPS>  -- LeanAttention decode, one persistent launch:
 //      stream-K segment walk (Alg2§10-18, §41) + LeanTile online softmax (Alg. 1) +
 //      in-kernel fixup through global partials and epoch flags (Alg2§19-36) + finalize
 //      (Alg2§38-39).  MHA (T_m = group = 1), CUDA-core fp32 arithmetic.
 //  la_combine_kernel<D>           -- sequence-shard combine of (O_r, L_r) (§4.1 operator).
 //
 // Design:
-//  * warp NCW (one elected lane) is the producer: it walks the CTA's iteration range and
+//  * the last warp (one elected lane) is the producer: it walks the CTA's iteration range and
 //    streams each stage (<= 64 tokens of K and V, contiguous in both layouts) HBM -> SMEM
 //    with two 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) into an NST-deep ring
 //    guarded by full/empty mbarriers; L2 evict-first (KV is read exactly once).
-//  * warps 0..NCW-1 consume stages round-robin; each warp keeps its own (m, l, O) state
-//    (§4.1 partial) and the warps are folded with the re-scaling operator once per
-//    segment, so there is no CTA-wide barrier per tile.
+//  * NCW = NST * WPS consumer warps: WPS warps own each ring slot and split its 32-key
+//    rounds; each warp keeps its own (m, l, O) state (§4.1 partial) and the warps are
+//    folded with the re-scaling operator once per segment, so there is no CTA-wide barrier
+//    per tile.
 //  * QK^T: a key is split over LPK = row_bytes/16 lanes (16 B = one LDS.128 each); every lane
 //    accumulates LPK keys' partial dot products with FHFMA (bf16/fp16 x bf16/fp16 + fp32,
 //    exact products, fp32 accumulate) and an XOR transpose-butterfly (LPK-1 shuffles, no
@@ -241,8 +242,9 @@ struct Chunk<float> {
 // ---------------------------------------------------------------------------------------
 // Compile-time configuration of the MHA kernel.
 // ---------------------------------------------------------------------------------------
-template <typename T, int D, int NCW, int NST>
+template <typename T, int D, int NST, int WPS>
 struct MhaCfg {
+  static constexpr int NCW = NST * WPS;                     // consumer warps (WPS per slot)
   static constexpr int ROWB = D * int(sizeof(T));          // bytes of one K (or V) row
   static constexpr int LPK = ROWB / 16;                     // lanes per key
   static constexpr int EPL = 16 / int(sizeof(T));           // elements per lane chunk
@@ -257,16 +259,16 @@ struct MhaCfg {
 };
 
 // One ring stage: ntok (<= STAGE_TOK) keys of one unit.  Updates this warp's (m, l, o).
-template <typename T, int D, int NCW, int NST>
-__device__ __forceinline__ void process_stage(const unsigned char* __restrict__ st, int ntok,
+template <typename T, int D, int NST, int WPS>
+__device__ __forceinline__ void process_stage(const unsigned char* __restrict__ st, int r0, int ntok,
                                               const typename Chunk<T>::Q& qf, float scale_log2, int kg,
                                               int li, float& m, float& l,
                                               float2 (&o)[Chunk<T>::EPL / 2]) {
-  using C = MhaCfg<T, D, NCW, NST>;
+  using C = MhaCfg<T, D, NST, WPS>;
   constexpr int LPK = C::LPK;
   const unsigned char* ks = st;
   const unsigned char* vs = st + C::STAGE_TOK * C::ROWB;
-  for (int r = 0; r < ntok; r += 32) {
+  for (int r = r0; r < ntok; r += 32 * WPS) {  // this warp's 32-key rounds of the stage
     const int kb = r + kg * LPK;  // first key of this lane group in the round
     // ---- S_f = Q_f K_f^T (Alg1§20): lane li accumulates key (jj ^ li), chunk li ----------
     float acc[LPK];
@@ -307,10 +309,11 @@ __device__ __forceinline__ void process_stage(const unsigned char* __restrict__ 
   }
 }
 
-template <typename T, int D, int NCW, int NST>
-__global__ void __launch_bounds__(MhaCfg<T, D, NCW, NST>::THREADS, 1)
+template <typename T, int D, int NST, int WPS>
+__global__ void __launch_bounds__(MhaCfg<T, D, NST, WPS>::THREADS, 1)
     la_decode_mha(const DecodeArgs a) {
-  using C = MhaCfg<T, D, NCW, NST>;
+  using C = MhaCfg<T, D, NST, WPS>;
+  constexpr int NCW = C::NCW;
   using E = Chunk<T>;
   constexpr int EPL = C::EPL;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -319,7 +322,8 @@ __global__ void __launch_bounds__(MhaCfg<T, D, NCW, NST>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(fold + 2 * C::FOLD_FLOATS);
   uint64_t* empty = full + NST;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0 so the compiler knows it is warp-uniform
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int g = blockIdx.x;
   const int it0 = a.cta_begin[g], it1 = a.cta_begin[g + 1];
   if (it0 >= it1) return;  // idle CTA (G > I); no barrier below involves it
@@ -331,7 +335,7 @@ __global__ void __launch_bounds__(MhaCfg<T, D, NCW, NST>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], WPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -376,7 +380,11 @@ __global__ void __launch_bounds__(MhaCfg<T, D, NCW, NST>::THREADS, 1)
   }
 
   // ================================= consumers ==========================================
+  // Consumer warp w owns ring slot w / WPS and takes rounds (w % WPS), (w % WPS) + WPS, ...
+  // of every stage landing in that slot.  Fixed slot ownership keeps each slot's consumers
+  // in stage order, so a wait on the slot's next phase can never alias the previous one.
   const int NCT = NCW * 32;
+  const int my_slot = warp / WPS, sub = warp % WPS;
   const int kg = lane / C::LPK, li = lane % C::LPK;
   const int t = threadIdx.x;  // 0 .. NCT-1
   int j = 0, seg = 0;
@@ -400,14 +408,13 @@ __global__ void __launch_bounds__(MhaCfg<T, D, NCW, NST>::THREADS, 1)
       const int t0 = (it - u.iter_begin) * a.tile_n;
       const int t1 = min(t0 + a.tile_n, u.len);
       for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
-        if (j % NCW == warp) {
+        if (j % NST == my_slot) {
           const int ntok = min(a.stage_tokens, t1 - s0);
-          const int slot = j % NST;
-          mbar_wait(&full[slot], (j / NST) & 1);
-          process_stage<T, D, NCW, NST>(ring + slot * C::STAGE_BYTES, ntok, qf, a.scale_log2, kg, li, m,
-                                        l, o);
+          mbar_wait(&full[my_slot], (j / NST) & 1);
+          process_stage<T, D, NST, WPS>(ring + my_slot * C::STAGE_BYTES, sub * 32, ntok, qf, a.scale_log2,
+                                        kg, li, m, l, o);
           __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);
+          if (lane == 0) mbar_arrive(&empty[my_slot]);
         }
         ++j;
       }
@@ -511,14 +518,14 @@ __global__ void __launch_bounds__(D) la_combine_kernel(const float* __restrict__
 
 template <typename T, int D>
 KernelInfo mha_info() {
-  constexpr int NCW = 8, NST = 6;
-  using C = MhaCfg<T, D, NCW, NST>;
+  constexpr int NST = 6, WPS = 2;
+  using C = MhaCfg<T, D, NST, WPS>;
   KernelInfo k;
   k.supported = true;
   k.threads = C::THREADS;
   k.smem_bytes = C::SMEM;
   k.stage_tokens_max = C::STAGE_TOK;
-  k.fn = reinterpret_cast<const void*>(&la_decode_mha<T, D, NCW, NST>);
+  k.fn = reinterpret_cast<const void*>(&la_decode_mha<T, D, NST, WPS>);
   return k;
 }
 
