@@ -84,6 +84,7 @@ typedef struct {
   int ctas_per_sm;   /* host-only plans: occupancy assumed when grid == 0 (default 1)     */
   int host_only;     /* 1 -> plan the schedule only, no device state (inspection/tests)   */
   int schedule;      /* la_schedule, default LA_SCHED_STREAMK                             */
+  int trace;         /* 1 -> every la_decode records a per-CTA timeline (la_plan_trace)     */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;
@@ -181,6 +182,17 @@ la_status la_combine(const float* o_parts, const float* lse_parts, int parts, in
  */
 la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache,
                          int64_t kv_rows, float* out, float* lse, void* stream);
+
+/*
+ * la_plan_trace -- per-CTA timeline of the most recent la_decode on a plan created with
+ * opts.trace = 1 (SURVEY §5 tracing; the E2 SM-balance analog of P:191).  Synchronises the
+ * device.  out: HOST buffer of cap_ctas * LA_TRACE_FIELDS uint64, one record per CTA:
+ * smid, t_start, t_publish (non-host partial signalled, Alg2§23; 0 if none), t_wait_begin,
+ * t_wait_end (host fold wait, Alg2§28; 0 if none), t_end -- %globaltimer nanoseconds.
+ * *n_ctas receives G.  LA_ERR_STATE if the plan has no trace buffer.
+ */
+#define LA_TRACE_FIELDS 6
+la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* n_ctas);
 
 /* Release a plan and all device memory it owns.  NULL is a no-op. */
 void la_plan_destroy(la_plan_t plan);

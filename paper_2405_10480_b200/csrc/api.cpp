@@ -31,6 +31,7 @@ struct la_plan_s {
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   uint32_t* d_flags = nullptr;
+  unsigned long long* d_trace = nullptr;
   uint32_t epoch = 0;
   int64_t workspace = 0;
   // la_decode_host staging
@@ -219,7 +220,8 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     const size_t b_po = align(size_t(G) * p.group * head_dim * sizeof(float));
     const size_t b_pml = align(size_t(G) * p.group * 2 * sizeof(float));
     const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
-    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags;
+    const size_t b_trace = opts.trace ? align(size_t(G) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
+    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_trace;
     cudaError_t e = cudaMalloc(&plan->d_tables, bytes);
     if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaMalloc(plan tables)"); }
     char* base = static_cast<char*>(plan->d_tables);
@@ -229,6 +231,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     plan->d_part_o = reinterpret_cast<float*>(base + b_units + b_begin + b_first);
     plan->d_part_ml = reinterpret_cast<float*>(base + b_units + b_begin + b_first + b_po);
     plan->d_flags = reinterpret_cast<uint32_t*>(base + b_units + b_begin + b_first + b_po + b_pml);
+    if (opts.trace)
+      plan->d_trace = reinterpret_cast<unsigned long long*>(base + b_units + b_begin + b_first + b_po + b_pml +
+                                                            b_flags);
     plan->workspace = int64_t(bytes);
     e = cudaMemcpy(plan->d_units, s.units.data(), s.units.size() * sizeof(DevUnit), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
@@ -236,6 +241,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     if (e == cudaSuccess)
       e = cudaMemcpy(plan->d_cta_first, s.cta_first_unit.data(), G * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(plan->d_flags, 0, G * sizeof(uint32_t));
+    if (e == cudaSuccess && plan->d_trace) e = cudaMemset(plan->d_trace, 0, b_trace);
     if (e != cudaSuccess) {
       release_device(plan);
       delete plan;
@@ -309,6 +315,7 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
     plan->epoch = 1;
   }
   a.epoch = plan->epoch;
+  a.trace = plan->d_trace;
   a.grid = plan->sched.grid;
   a.tile_n = plan->sched.tile_n;
   a.stage_tokens = plan->stage_tokens;
@@ -381,6 +388,20 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
   if (e == cudaSuccess && lse) e = cudaMemcpyAsync(lse, dlse, l_bytes, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "D2H/sync");
+  return LA_OK;
+}
+
+la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* n_ctas) {
+  if (!plan || !n_ctas) return fail(LA_ERR_INVALID, "NULL argument");
+  if (!plan->d_trace) return fail(LA_ERR_STATE, "plan was created without opts.trace");
+  const size_t G = size_t(plan->sched.grid);
+  *n_ctas = G;
+  if (cap_ctas == 0) return LA_OK;
+  if (!out || cap_ctas < G) return fail(LA_ERR_INVALID, "trace buffer too small");
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaMemcpy(out, plan->d_trace, G * LA_TRACE_FIELDS * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "la_plan_trace");
   return LA_OK;
 }
 

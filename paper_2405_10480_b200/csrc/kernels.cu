@@ -106,6 +106,21 @@ __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ float ld_cg(const float* p) { return __ldcg(p); }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+
+// LA_TRACE record fields (include/la.h la_plan_trace)
+enum { TR_SMID = 0, TR_START, TR_PUBLISH, TR_WAIT0, TR_WAIT1, TR_END, TR_FIELDS };
+
 __device__ __forceinline__ void consumer_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
@@ -327,6 +342,12 @@ __global__ void __launch_bounds__(MhaCfg<T, D, NST, WPS>::THREADS, 1)
   const int g = blockIdx.x;
   const int it0 = a.cta_begin[g], it1 = a.cta_begin[g + 1];
   if (it0 >= it1) return;  // idle CTA (G > I); no barrier below involves it
+  unsigned long long* tr = a.trace ? a.trace + size_t(g) * TR_FIELDS : nullptr;
+  if (tr && threadIdx.x == 0) {
+    tr[TR_SMID] = smid();
+    tr[TR_START] = globaltimer();
+    tr[TR_PUBLISH] = tr[TR_WAIT0] = tr[TR_WAIT1] = 0;
+  }
 
   // Zero the ring once so rows past the end of a short stage are finite on first use
   // (their scores are masked to -inf, p = 0, and 0 * finite = 0).
@@ -466,15 +487,18 @@ __global__ void __launch_bounds__(MhaCfg<T, D, NST, WPS>::THREADS, 1)
       if (t == 0) {
         __threadfence();
         st_release_gpu(&a.flags[g], a.epoch);
+        if (tr) tr[TR_PUBLISH] = globaltimer();
       }
     } else {
       if (!finishing) {
         // ---- host, not finishing: Wait(flags[cta]) for cta = g+1 .. last_cta (Alg2§26-28,
         //      reading C9), polled in parallel, then fold in ascending order (§29-35) -----
+        if (tr && t == 0) tr[TR_WAIT0] = globaltimer();
         for (int p = g + 1 + t; p <= u.last_cta; p += NCT) {
           while (ld_acquire_gpu(&a.flags[p]) != a.epoch) __nanosleep(20);
         }
         consumer_bar(NCT);
+        if (tr && t == 0) tr[TR_WAIT1] = globaltimer();
         for (int p = g + 1; p <= u.last_cta; ++p) {
           const float mp = ld_cg(&a.part_ml[2 * p]);
           const float lp = ld_cg(&a.part_ml[2 * p + 1]);
@@ -493,6 +517,7 @@ __global__ void __launch_bounds__(MhaCfg<T, D, NST, WPS>::THREADS, 1)
     ++seg;
     ++unit;
   }
+  if (tr && t == 0) tr[TR_END] = globaltimer();
 }
 
 // ---------------------------------------------------------------------------------------

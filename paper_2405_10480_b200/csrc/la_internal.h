@@ -70,6 +70,7 @@ struct DecodeArgs {
   float* part_ml;     // [G][group][2]  mp, lp of Alg2§21-22 (m in log2 units)
   uint32_t* flags;    // [G]            flags of Alg2§23/§28, epoch-valued (reading C17)
   uint32_t epoch;
+  unsigned long long* trace;  // [G][LA_TRACE_FIELDS] or nullptr
   int grid;
   int tile_n;
   int stage_tokens;

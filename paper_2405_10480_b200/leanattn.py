@@ -32,7 +32,7 @@ _SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL}
 # Every symbol include/la.h declares (tests check the library exports all of them).
 EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
            "la_decode_partial", "la_combine", "la_decode_host", "la_plan_destroy",
-           "la_launch_count", "la_status_string", "la_last_error", "la_version")
+           "la_launch_count", "la_status_string", "la_last_error", "la_version", "la_plan_trace")
 
 
 class LaError(RuntimeError):
@@ -44,7 +44,7 @@ class LaError(RuntimeError):
 class la_plan_opts(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_float), ("layout", ctypes.c_int), ("max_ctx", ctypes.c_int64),
                 ("grid", ctypes.c_int), ("num_sms", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
-                ("host_only", ctypes.c_int), ("schedule", ctypes.c_int)]
+                ("host_only", ctypes.c_int), ("schedule", ctypes.c_int), ("trace", ctypes.c_int)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -79,13 +79,15 @@ def lib() -> ctypes.CDLL:
     L.la_decode_partial.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.la_combine.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
     L.la_decode_host.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
+    L.la_plan_trace.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
+                                ctypes.POINTER(ctypes.c_size_t)]
     L.la_plan_destroy.argtypes = [vp]
     L.la_plan_destroy.restype = None
     L.la_launch_count.restype = i64
     L.la_status_string.restype = ctypes.c_char_p
     L.la_last_error.restype = ctypes.c_char_p
     for name in ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
-                 "la_decode_partial", "la_combine", "la_decode_host"):
+                 "la_decode_partial", "la_combine", "la_decode_host", "la_plan_trace"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -117,7 +119,7 @@ class Plan:
     def __init__(self, batch: int, heads_q: int, heads_kv: int, head_dim: int, ctx_lens: Sequence[int],
                  tile_n: int = 0, dtype: str = "bf16", scale: float = 0.0, layout: str = "bhsd",
                  max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
-                 ctas_per_sm: int = 1, schedule: str = "streamk"):
+                 ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -129,6 +131,7 @@ class Plan:
         opts.ctas_per_sm = int(ctas_per_sm)
         opts.host_only = 1 if host_only else 0
         opts.schedule = _SCHED_CODES[schedule]
+        opts.trace = 1 if trace else 0
         lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
         h = ctypes.c_void_p()
         self._h = None
@@ -153,6 +156,16 @@ class Plan:
         buf = np.zeros((n.value, 7), dtype=np.int32)
         _check(lib().la_plan_export(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n.value,
                                     ctypes.byref(n)), "la_plan_export")
+        return buf
+
+    def trace(self) -> np.ndarray:
+        """``la_plan_trace``: (G, 6) uint64 per-CTA timeline of the last decode
+        (smid, t_start, t_publish, t_wait_begin, t_wait_end, t_end) in ns."""
+        n = ctypes.c_size_t()
+        _check(lib().la_plan_trace(self._h, None, 0, ctypes.byref(n)), "la_plan_trace")
+        buf = np.zeros((n.value, 6), dtype=np.uint64)
+        _check(lib().la_plan_trace(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n.value,
+                                   ctypes.byref(n)), "la_plan_trace")
         return buf
 
     def _outputs(self, q, out, lse, need_lse):
