@@ -365,7 +365,7 @@ def bench_ours(args):
                        "parallelism": "single GPU" if world == 1 else f"sequence-sharded x{world} + NCCL all-gather + la_combine"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "la_decode_mha<bf16,128>", "kernel_us": kern_ms * 1e3,
+                         "kernel": ("la_decode_gqa<bf16,128>" if p.group > 1 else "la_decode_mha<bf16,128>"), "kernel_us": kern_ms * 1e3,
                          "algorithmic_bytes_per_launch": local_kv},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
         }

@@ -179,6 +179,10 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
                                                       plan->kinfo.smem_bytes);
     if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor"); }
     if (occ < 1) { delete plan; return fail(LA_ERR_UNSUPPORTED, "decode kernel does not fit on an SM"); }
+    if (plan->kinfo.uses_tma_tensor && p.kv_rows() >= (int64_t(1) << 31)) {
+      delete plan;
+      return fail(LA_ERR_UNSUPPORTED, "KV cache rows exceed the TMA int32 coordinate range");
+    }
     max_ctas = sms * occ;
   }
 
@@ -322,8 +326,12 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.group = plan->prob.group;
   a.scale_log2 = float(double(plan->prob.scale) * 1.4426950408889634);
   std::string err;
-  if (la::launch_decode(plan->kinfo, a, plan->needs_wait, stream, err) != 0)
-    return fail(LA_ERR_CUDA, err);
+  const la::Problem& p = plan->prob;
+  const int rc = plan->kinfo.uses_tma_tensor
+                     ? la::launch_decode_tma(plan->kinfo, a, p.kv_rows(), p.head_dim, p.dtype, plan->needs_wait,
+                                             stream, err)
+                     : la::launch_decode(plan->kinfo, a, plan->needs_wait, stream, err);
+  if (rc != 0) return fail(LA_ERR_CUDA, err);
   return LA_OK;
 }
 

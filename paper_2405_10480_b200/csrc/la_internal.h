@@ -84,9 +84,15 @@ struct KernelInfo {
   int threads = 0;
   int smem_bytes = 0;
   int stage_tokens_max = 0;
+  bool uses_tma_tensor = false;   // K/V tensor maps passed as a second kernel parameter
   const void* fn = nullptr;
 };
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group);
+KernelInfo gqa_kernel_info(int dtype, int head_dim, int group);
+// GQA tensor-core kernel: encodes the K/V TMA tensor maps (rows x head_dim) and launches.
+int launch_decode_tma(const KernelInfo& ki, const DecodeArgs& a, int64_t kv_rows, int head_dim, int dtype,
+                      bool cooperative, void* stream, std::string& err);
+void note_launch();
 // Launch the decode kernel (cooperative when any CTA waits on a peer).
 int launch_decode(const KernelInfo& ki, const DecodeArgs& a, bool cooperative, void* stream,
                   std::string& err);

@@ -1,5 +1,6 @@
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -5
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -30
-timeout 300 python bench.py --steps 200 --warmup 10 --no-cpu 2>&1 | tail -3
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -6
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -30
+timeout 300 python bench.py --steps 300 --warmup 10 --no-cpu 2>&1 | tail -1
+timeout 300 python bench.py --config c3 --steps 300 --warmup 10 --no-cpu --no-e2e 2>&1 | tail -1
+timeout 300 python bench.py --config c4 --steps 100 --warmup 5 --no-cpu --no-e2e 2>&1 | tail -1

@@ -154,3 +154,48 @@ def test_decode_host_e2e_path():
     plan.decode_host(q, k, v, out, lse)
     O_ref, L_ref = run_oracle(p)
     gate(out.numpy(), lse.numpy(), O_ref, L_ref, what="decode_host")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("group", [2, 4, 8])
+def test_gqa_small_multi_tile_ragged(dtype, d, group):
+    """GQA (tensor-core kernel): g q-heads per KV head (reading C3)."""
+    p = synth.Problem(2, 2 * group, 2, d, [1000, 777], dtype=dtype, dist="D2", seed=31, max_ctx=1024)
+    O_ref, L_ref = run_oracle(p)
+    inputs = cuda_inputs(p)
+    for tile_n in (32, 64, 128):
+        for grid in (1, 3, 0):
+            O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid)
+            gate(O, L, O_ref, L_ref, what=f"gqa g{group}/{dtype}/d{d}/T{tile_n}/G{grid}")
+
+
+def test_gqa_distributions_packed_and_determinism():
+    for dist in ("D0", "D1", "D3", "D4"):
+        p = synth.Problem(3, 16, 2, 128, [700, 1500, 64], dtype="bf16", dist=dist, seed=32, layout="packed")
+        O_ref, L_ref = run_oracle(p)
+        O, L, _ = run_cuda(p, tile_n=64, grid=0)
+        gate(O, L, O_ref, L_ref, what=f"gqa packed {dist}")
+    import paper_2405_10480_b200 as la
+    p = synth.Problem(1, 8, 1, 128, [5000], dtype="bf16", dist="D2", seed=33)
+    q, k, v = cuda_inputs(p)
+    plan = la.Plan(1, 8, 1, 128, [5000], grid=11, tile_n=64)
+    ref = plan.decode(q, k, v)[0].clone()
+    for _ in range(5):
+        assert torch.equal(plan.decode(q, k, v)[0], ref)
+
+
+def test_c3_gqa_full_size_sampled():
+    """BASELINE.json config 3: batch 8, 64 q-heads / 8 kv-heads, d 128, context 64k, bf16."""
+    p = synth.config("c3")
+    O, L, plan = run_cuda(p)
+    assert plan.info.total_iters == 32768 and plan.info.group == 8
+    for b, h in ((0, 0), (3, 5), (7, 7)):
+        O_ref, L_ref = oracle_unit(p, b, h)
+        gate(O[b, 8 * h:8 * h + 8], L[b, 8 * h:8 * h + 8], O_ref, L_ref, what=f"c3 b{b} h{h}")
+    torch.cuda.empty_cache()
+    p3 = synth.config("c3", dist="D3")
+    O3, L3, _ = run_cuda(p3)
+    o_exp, l_exp = census_expect(p3, 0)
+    assert np.max(np.abs(O3 - o_exp[None, None, :])) <= 1e-5
+    assert np.max(np.abs(L3 - l_exp)) <= 1e-5
