@@ -264,7 +264,7 @@ def bench_ours(args):
             plan.decode_partial(q, k, v, out, lse, stream=stream)
         if ev1 is not None:
             ev1.record(stream)
-        if world > 1:
+        if world > 1:   # sharded.sequence_sharded_decode with preallocated buffers
             dist.all_gather_into_tensor(o_all, out.view(rows, p.head_dim))
             dist.all_gather_into_tensor(l_all, lse.view(rows))
             la.la_combine(o_all, l_all, fin_o, fin_l, stream=stream)
