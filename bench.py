@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--cpu-heads", type=int, default=32, help="heads in the oracle cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential"])
+    ap.add_argument("--dyn-first", type=int, default=750, help="dynamic schedule: permille in the first round")
+    ap.add_argument("--dyn-min", type=int, default=2, help="dynamic schedule: smallest virtual CTA (LeanTiles)")
     return ap.parse_args()
 
 
@@ -238,7 +241,8 @@ def bench_ours(args):
     q = synth.gen_q(p, dev)
     k = synth.fill_kv_cache(p, "k", dev, token_range=bounds)
     v = synth.fill_kv_cache(p, "v", dev, token_range=bounds)
-    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout)
+    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
+                   schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min)
     info = plan.info
     total_kv = p.kv_bytes                       # whole job
     local_kv = info.kv_bytes
@@ -360,7 +364,8 @@ def bench_ours(args):
                        "heads_kv": p.heads_kv, "head_dim": p.head_dim,
                        "context": p.ctx_lens[0] if len(set(p.ctx_lens)) == 1 else p.ctx_lens,
                        "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
-                       "stage_tokens": info.stage_tokens,
+                       "stage_tokens": info.stage_tokens, "schedule": args.schedule,
+                       "virtual_ctas": info.num_vctas,
                        "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),
                        "parallelism": "single GPU" if world == 1 else f"sequence-sharded x{world} + NCCL all-gather + la_combine"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

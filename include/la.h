@@ -68,8 +68,14 @@ typedef enum {
 /* Work decomposition.  STREAMK is the method; the other two are its
    special cases / the baselines it is compared with, kept for the NEXT-1 comparison. */
 typedef enum {
-  LA_SCHED_STREAMK = 0,    /* Eq. 2 + Alg. 2: equal contiguous iteration ranges        */
-  LA_SCHED_SEQUENTIAL = 1  /* FA2: one CTA per unit, G = #units            */
+  LA_SCHED_STREAMK = 0,    /* Eq. 2 + Alg. 2 exactly: G equal contiguous iteration ranges,
+                              host CTAs wait on their peers' flags (cooperative launch)  */
+  LA_SCHED_SEQUENTIAL = 1, /* FA2: one CTA per unit, G = #units            */
+  LA_SCHED_DYNAMIC = 2     /* Alg. 2's decomposition over more, guided-size "virtual CTAs"
+                              that the persistent CTAs claim in order (atomic counter); a
+                              unit's partials are folded by its last-arriving segment in
+                              Alg. 2's order (host, then ascending peers) -- same result
+                              semantics, balances TIME instead of LeanTile counts */
 } la_schedule;
 
 typedef struct {
@@ -83,8 +89,10 @@ typedef struct {
   int num_sms;       /* host-only plans: SM count assumed when grid == 0 (default 148)    */
   int ctas_per_sm;   /* host-only plans: occupancy assumed when grid == 0 (default 1)     */
   int host_only;     /* 1 -> plan the schedule only, no device state (inspection/tests)   */
-  int schedule;      /* la_schedule, default LA_SCHED_STREAMK                             */
+  int schedule;      /* la_schedule, default LA_SCHED_STREAMK (Alg. 2 exactly)            */
   int trace;         /* 1 -> every la_decode records a per-CTA timeline (la_plan_trace)     */
+  int dyn_first_permille; /* LA_SCHED_DYNAMIC: share of I in the first G ranges (default 750) */
+  int dyn_min_chunk;      /* LA_SCHED_DYNAMIC: smallest virtual CTA in LeanTiles (default 2)  */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;
@@ -94,7 +102,7 @@ typedef struct {
   int dtype, layout, schedule;
   int tile_n;              /* LeanTile tokens T_n                                 */
   int stage_tokens;        /* tokens per shared-memory ring stage (<= tile_n)             */
-  int grid;                /* G                                                           */
+  int grid;                /* CTAs launched (persistent, <= 148 x occupancy unless static) */
   int num_units;           /* output tiles = B * H_kv                                     */
   int64_t total_iters;     /* I = sum_u ceil(n_u / T_n)  (Alg2§6, reading C15)           */
   int64_t num_segments;    /* LeanTile() calls over all CTAs (rows of la_plan_export)     */
@@ -102,6 +110,7 @@ typedef struct {
   int64_t workspace_bytes; /* device bytes owned by the plan                              */
   int64_t kv_bytes;        /* algorithmic K+V bytes one la_decode reads                   */
   float scale;
+  int64_t num_vctas;       /* Alg. 2's G: iteration ranges (= grid for static schedules)  */
 } la_plan_info;
 
 /* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */
@@ -134,7 +143,7 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info);
 /*
  * la_plan_export -- dump the schedule, one row of 7 int32 per segment (= LeanTile call),
  * in SPEC's dump order: cta, unit, local_begin, local_end, host, finishing,
- * last_cta (Alg2§11-18, §26 with reading C9).  rows: HOST buffer of cap_rows * 7 int32 (may
+ * last_cta (Alg2§11-18, §26 with reading C9); cta / last_cta are (virtual) CTA indices.  rows: HOST buffer of cap_rows * 7 int32 (may
  * be NULL with cap_rows = 0 to query the count); *n_rows receives the total row count.
  * LA_ERR_INVALID if cap_rows is non-zero but too small.
  */

@@ -28,7 +28,8 @@ from .rescale import PartialState, neutral, partial, combine, finalize, fold
 from .leantile import lean_tile
 from .schedule import (Segment, iters_per_cta, cta_range, owner, stream_k_segments,
                        owner_table, segments_from_owner_table, last_cta_literal,
-                       fixed_split_segments, quantization_efficiency)
+                       fixed_split_segments, quantization_efficiency, segments_from_ranges,
+                       guided_ranges)
 from .lean_attention import lean_attention
 from .shard_combine import combine_shards
 
@@ -38,6 +39,6 @@ __all__ = [
     "lean_tile",
     "Segment", "iters_per_cta", "cta_range", "owner", "stream_k_segments", "owner_table",
     "segments_from_owner_table", "last_cta_literal", "fixed_split_segments",
-    "quantization_efficiency",
+    "quantization_efficiency", "segments_from_ranges", "guided_ranges",
     "lean_attention", "combine_shards",
 ]

@@ -16,7 +16,7 @@ import numpy as np
 
 from .leantile import lean_tile
 from .rescale import combine, finalize
-from .schedule import stream_k_segments
+from .schedule import segments_from_ranges, stream_k_segments
 
 
 def unit_order(batch: int, heads_kv: int, layout: str):
@@ -30,8 +30,10 @@ def unit_order(batch: int, heads_kv: int, layout: str):
 
 
 def lean_attention(q, k, v, ctx_lens, scale: float, tile_n: int, grid: int,
-                   layout: str = "bhsd", return_stats: bool = False):
-    """Alg. 2 on (B, H_q, d) queries and a bhsd / packed KV cache; returns O, L (fp64)."""
+                   layout: str = "bhsd", return_stats: bool = False, begins=None):
+    """Alg. 2 on (B, H_q, d) queries and a bhsd / packed KV cache; returns O, L (fp64).
+    ``begins`` replaces §9's equal ranges by explicit per-CTA range boundaries (the
+    virtual CTAs of the dynamic schedule); ``grid`` is then ignored."""
     q = np.asarray(q, dtype=np.float64)
     B, Hq, d = q.shape
     Hkv = k.shape[1] if layout == "bhsd" else k.shape[0]
@@ -47,7 +49,7 @@ def lean_attention(q, k, v, ctx_lens, scale: float, tile_n: int, grid: int,
         return k[h, cu[b]:cu[b + 1]], v[h, cu[b]:cu[b + 1]]
 
     c_n = [-(-int(ctx_lens[b]) // tile_n) for (b, _h) in units]
-    segs = stream_k_segments(c_n, grid)
+    segs = stream_k_segments(c_n, grid) if begins is None else segments_from_ranges(c_n, begins)
 
     partials = {}     # Op[g], mp[g], lp[g]  (§20-22) -- written at most once per CTA
     hosts = []

@@ -101,6 +101,62 @@ def stream_k_segments(c_n: Sequence[int], grid: int) -> List[Segment]:
     return segs
 
 
+def segments_from_ranges(c_n: Sequence[int], begins: Sequence[int]) -> List[Segment]:
+    """Alg. 2 §10-18, §41 for arbitrary contiguous per-CTA ranges [begins[v], begins[v+1])
+    (§9's equal split replaced by a table); last_cta = the range holding the unit's last
+    iteration (reading C9)."""
+    off = _offsets(c_n)
+    assert begins[0] == 0 and begins[-1] == off[-1] and all(a <= b for a, b in zip(begins, begins[1:]))
+
+    def own(it):  # the range containing global iteration it
+        lo, hi = 0, len(begins) - 2
+        while lo < hi:
+            mid = (lo + hi + 1) // 2
+            if begins[mid] <= it:
+                lo = mid
+            else:
+                hi = mid - 1
+        return lo
+
+    segs: List[Segment] = []
+    unit = 0
+    for v in range(len(begins) - 1):
+        cta_start, cta_end = begins[v], begins[v + 1]
+        it = cta_start
+        while it < cta_end:
+            while off[unit + 1] <= it:
+                unit += 1
+            tile_iter, tile_iter_end = off[unit], off[unit + 1]
+            segs.append(Segment(cta=v, unit=unit, begin=it - tile_iter,
+                                end=min(tile_iter_end, cta_end) - tile_iter,
+                                host=(it == tile_iter), finishing=(cta_end >= tile_iter_end),
+                                last_cta=own(tile_iter_end - 1)))
+            it = tile_iter_end
+    return segs
+
+
+def guided_ranges(total_iters: int, grid: int, first_permille: int = 750, min_chunk: int = 2) -> List[int]:
+    """Range boundaries of the DYNAMIC schedule (not in the paper): `grid`
+    equal ranges holding first_permille/1000 of the iterations, then rounds of `grid` ranges
+    each covering half of the remainder (at least min_chunk), until all are covered."""
+    begins = [0]
+    pos = 0
+    first = total_iters * first_permille // (1000 * grid)
+    if first >= 1:
+        for _ in range(grid):
+            pos += first
+            begins.append(pos)
+    while pos < total_iters:
+        rem = total_iters - pos
+        c = max(min_chunk, -(-rem // (2 * grid)))
+        for _ in range(grid):
+            if pos >= total_iters:
+                break
+            pos = min(total_iters, pos + c)
+            begins.append(pos)
+    return begins
+
+
 def owner_table(total_iters: int, grid: int) -> List[int]:
     """Brute force: hand out iterations CTA by CTA, counts from :func:`iters_per_cta`."""
     table: List[int] = []

@@ -31,6 +31,8 @@ struct la_plan_s {
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   uint32_t* d_flags = nullptr;
+  int* d_counters = nullptr;
+  int* d_unit_count = nullptr;
   unsigned long long* d_trace = nullptr;
   uint32_t epoch = 0;
   int64_t workspace = 0;
@@ -108,6 +110,8 @@ la_status la_plan_opts_init(la_plan_opts* o) {
   o->num_sms = 148;
   o->ctas_per_sm = 1;
   o->schedule = LA_SCHED_STREAMK;
+  o->dyn_first_permille = 750;
+  o->dyn_min_chunk = 2;
   return LA_OK;
 }
 
@@ -124,8 +128,11 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (head_dim != 64 && head_dim != 128) return fail(LA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   if (dtype != LA_BF16 && dtype != LA_FP16 && dtype != LA_FP32) return fail(LA_ERR_INVALID, "bad dtype");
   if (opts.layout != LA_KV_BHSD && opts.layout != LA_KV_PACKED) return fail(LA_ERR_INVALID, "bad layout");
-  if (opts.schedule != LA_SCHED_STREAMK && opts.schedule != LA_SCHED_SEQUENTIAL)
+  if (opts.schedule != LA_SCHED_STREAMK && opts.schedule != LA_SCHED_SEQUENTIAL &&
+      opts.schedule != LA_SCHED_DYNAMIC)
     return fail(LA_ERR_INVALID, "bad schedule");
+  if (opts.dyn_first_permille < 0 || opts.dyn_first_permille > 1000 || opts.dyn_min_chunk < 1)
+    return fail(LA_ERR_INVALID, "dyn_first_permille must be in [0, 1000] and dyn_min_chunk >= 1");
   if (tile_n != 0 && tile_n != 16 && tile_n != 32 && tile_n != 64 && tile_n != 128 && tile_n != 256 &&
       tile_n != 512)
     return fail(LA_ERR_INVALID, "tile_n must be 0 or one of 16..512 (powers of two)");
@@ -193,20 +200,25 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   la::build_units(p, tn, s.units, s.total_iters);
   if (s.total_iters >= (int64_t(1) << 31)) { delete plan; return fail(LA_ERR_INVALID, "too many LeanTiles"); }
   if (p.schedule == LA_SCHED_SEQUENTIAL) {
-    s.grid = int(s.units.size());
     la::sequential_ranges(s.units, s.cta_begin);
+  } else if (p.schedule == LA_SCHED_DYNAMIC) {
+    // persistent CTAs: one per co-resident slot (or the forced grid), claiming virtual CTAs
+    int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
+    G = std::max(1, std::min(G, max_ctas));
+    la::guided_ranges(s.total_iters, G, opts.dyn_first_permille, opts.dyn_min_chunk, s.cta_begin);
   } else {
     int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
     if (!plan->host_only) G = std::min(G, max_ctas);  // hosts wait on peers: co-residency
-    s.grid = std::max(1, G);
-    la::streamk_ranges(s.total_iters, s.grid, s.cta_begin);
+    la::streamk_ranges(s.total_iters, std::max(1, G), s.cta_begin);
   }
   la::finish_schedule(s);
-  for (const DevUnit& u : s.units)
-    if (u.last_cta != u.host_cta) plan->needs_wait = true;
-  if (!plan->host_only && p.schedule == LA_SCHED_SEQUENTIAL && plan->needs_wait) {
-    delete plan;
-    return fail(LA_ERR_INVALID, "internal: sequential schedule with peers");
+  if (p.schedule == LA_SCHED_DYNAMIC) {
+    int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
+    s.phys_grid = std::max(1, std::min({G, max_ctas, s.grid}));
+  } else {
+    s.phys_grid = s.grid;
+    for (const DevUnit& u : s.units)
+      if (u.last_cta != u.host_cta) plan->needs_wait = true;
   }
   if (!plan->host_only && plan->needs_wait && s.grid > max_ctas) {
     delete plan;
@@ -216,16 +228,18 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
 
   // ---- device state -------------------------------------------------------------------
   if (!plan->host_only) {
-    const int G = s.grid;
+    const int G = s.grid, GP = s.phys_grid;
+    const size_t U = s.units.size();
     auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const size_t b_units = align(s.units.size() * sizeof(DevUnit));
+    const size_t b_units = align(U * sizeof(DevUnit));
     const size_t b_begin = align(size_t(G + 1) * sizeof(int32_t));
     const size_t b_first = align(size_t(G) * sizeof(int32_t));
-    const size_t b_po = align(size_t(G) * p.group * head_dim * sizeof(float));
-    const size_t b_pml = align(size_t(G) * p.group * 2 * sizeof(float));
+    const size_t b_po = align(size_t(G) * 2 * p.group * head_dim * sizeof(float));
+    const size_t b_pml = align(size_t(G) * 2 * p.group * 2 * sizeof(float));
     const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
-    const size_t b_trace = opts.trace ? align(size_t(G) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
-    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_trace;
+    const size_t b_cnt = align((2 + U + size_t(G)) * sizeof(int));
+    const size_t b_trace = opts.trace ? align(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
+    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace;
     cudaError_t e = cudaMalloc(&plan->d_tables, bytes);
     if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaMalloc(plan tables)"); }
     char* base = static_cast<char*>(plan->d_tables);
@@ -235,9 +249,11 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     plan->d_part_o = reinterpret_cast<float*>(base + b_units + b_begin + b_first);
     plan->d_part_ml = reinterpret_cast<float*>(base + b_units + b_begin + b_first + b_po);
     plan->d_flags = reinterpret_cast<uint32_t*>(base + b_units + b_begin + b_first + b_po + b_pml);
+    plan->d_counters = reinterpret_cast<int*>(base + b_units + b_begin + b_first + b_po + b_pml + b_flags);
+    plan->d_unit_count = plan->d_counters + 2;
     if (opts.trace)
       plan->d_trace = reinterpret_cast<unsigned long long*>(base + b_units + b_begin + b_first + b_po + b_pml +
-                                                            b_flags);
+                                                            b_flags + b_cnt);
     plan->workspace = int64_t(bytes);
     e = cudaMemcpy(plan->d_units, s.units.data(), s.units.size() * sizeof(DevUnit), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
@@ -245,6 +261,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     if (e == cudaSuccess)
       e = cudaMemcpy(plan->d_cta_first, s.cta_first_unit.data(), G * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(plan->d_flags, 0, G * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(plan->d_counters, 0, b_cnt);
     if (e == cudaSuccess && plan->d_trace) e = cudaMemset(plan->d_trace, 0, b_trace);
     if (e != cudaSuccess) {
       release_device(plan);
@@ -271,7 +288,8 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   info->schedule = p.schedule;
   info->tile_n = s.tile_n;
   info->stage_tokens = plan->stage_tokens;
-  info->grid = s.grid;
+  info->grid = s.phys_grid;
+  info->num_vctas = s.grid;
   info->num_units = int(s.units.size());
   info->total_iters = s.total_iters;
   info->num_segments = s.num_segments;
@@ -320,17 +338,19 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   }
   a.epoch = plan->epoch;
   a.trace = plan->d_trace;
-  a.grid = plan->sched.grid;
+  a.counters = plan->d_counters;
+  a.unit_count = plan->d_unit_count;
+  a.grp_count = plan->d_unit_count + plan->sched.units.size();
+  a.dynamic = plan->prob.schedule == LA_SCHED_DYNAMIC ? 1 : 0;
+  a.num_v = plan->sched.grid;
+  a.grid = plan->sched.phys_grid;
   a.tile_n = plan->sched.tile_n;
   a.stage_tokens = plan->stage_tokens;
   a.group = plan->prob.group;
   a.scale_log2 = float(double(plan->prob.scale) * 1.4426950408889634);
   std::string err;
   const la::Problem& p = plan->prob;
-  const int rc = plan->kinfo.uses_tma_tensor
-                     ? la::launch_decode_tma(plan->kinfo, a, p.kv_rows(), p.head_dim, p.dtype, plan->needs_wait,
-                                             stream, err)
-                     : la::launch_decode(plan->kinfo, a, plan->needs_wait, stream, err);
+  const int rc = la::launch_decode(plan->kinfo, a, p.kv_rows(), p.head_dim, p.dtype, plan->needs_wait, stream, err);
   if (rc != 0) return fail(LA_ERR_CUDA, err);
   return LA_OK;
 }
@@ -402,7 +422,7 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
 la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* n_ctas) {
   if (!plan || !n_ctas) return fail(LA_ERR_INVALID, "NULL argument");
   if (!plan->d_trace) return fail(LA_ERR_STATE, "plan was created without opts.trace");
-  const size_t G = size_t(plan->sched.grid);
+  const size_t G = size_t(plan->sched.phys_grid);
   *n_ctas = G;
   if (cap_ctas == 0) return LA_OK;
   if (!out || cap_ctas < G) return fail(LA_ERR_INVALID, "trace buffer too small");

@@ -1,0 +1,1046 @@
+// sm_100a decode kernels of libleanattn.so: LeanAttention in ONE persistent launch.
+//
+//   la_decode<Engine>   stream-K segment walk (Alg2§10-18, §41) + LeanTile online softmax
+//                       (Alg. 1) + in-kernel fixup with the softmax re-scaling operator
+//                       (§4.1, Alg2§19-36) + finalize (Alg2§38-39).
+//   la_combine_kernel   sequence-shard combine of normalised (O_r, L_r) pairs.
+//
+// Structure of la_decode:
+//  * the last warp (one elected lane) is the PRODUCER: it walks the iteration range of each
+//    (virtual) CTA it is handed and streams every <= 64-token stage of K and V HBM -> SMEM
+//    into an NST-deep ring guarded by full/empty mbarriers (L2 evict-first: KV is read
+//    once).  MHA: two 1-D bulk copies (UBLKCP); GQA: TMA tensor loads in the 128-B
+//    swizzled layout (UTMALDG).
+//  * NCW = NST * WPS CONSUMER warps: WPS warps own each ring slot (fixed ownership keeps a
+//    slot's consumers in stage order, so a parity wait cannot alias a completed phase) and
+//    split its 32-token rounds.  Each warp keeps its own (m, l, O) -- a §4.1 partial -- and
+//    at a segment end hands it to the EPILOGUE warp through one of two fold buffers
+//    (mbarrier full/empty) and moves straight on to the next segment.
+//  * the EPILOGUE warp folds the NCW warp partials with the re-scaling operator and runs the
+//    whole fixup (partial stores, flags / counters, peer folds, finalize) off the consumers'
+//    critical path.
+//  * the Engine supplies the per-stage math:
+//      MhaEngine (group 1, CUDA cores): FHFMA bf16 x bf16 -> fp32 dot products, XOR
+//        transpose-butterfly, exp2-domain online softmax, FFMA2 PV.
+//      GqaEngine (group 2..8, tensor cores): swap-AB mma.sync m16n8k16 (N = the GQA group),
+//        movmatrix.trans from the S^T accumulator to the P^T operand, ldmatrix.trans V^T.
+//  * SCHEDULES.  Static (LA_SCHED_STREAMK / SEQUENTIAL): CTA g runs Alg. 2's range g; a
+//    non-host segment publishes its partial and a release flag, a non-finishing host spins
+//    on its peers' flags and folds them in ascending order (needs co-residency ->
+//    cooperative launch).  Dynamic (LA_SCHED_DYNAMIC): the planner cuts the same iteration
+//    space into more, guided-size "virtual CTAs"; persistent CTAs claim them in order with
+//    an atomic counter, so fast SMs take more work.  Every non-trivial segment stores its
+//    partial and counts itself in; a fixed two-level tree of last arrivers (groups of kGS
+//    consecutive segments, then the groups) folds them in ascending order -- deterministic,
+//    and no CTA ever waits.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "la_internal.h"
+#include "ptx.cuh"
+
+namespace la {
+
+struct alignas(64) TmapPair {
+  CUtensorMap k;
+  CUtensorMap v;
+};
+
+static std::atomic<int64_t> g_launches{0};
+int64_t launch_count() { return g_launches.load(); }
+void note_launch() { g_launches.fetch_add(1); }
+
+namespace {
+
+using namespace dev;
+
+// =======================================================================================
+// MHA arithmetic on one 16-byte chunk of a K / V row
+//   dot : acc + sum_e q[e] k[e]    (fp32)          axpy: o[e] += p v[e]   (fp32)
+// =======================================================================================
+template <typename T>
+struct Chunk;
+
+template <>
+struct Chunk<__nv_bfloat16> {
+  static constexpr int EPL = 8;
+  struct Q {
+    unsigned short h[8];  // exact bf16 inputs
+  };
+  __device__ __forceinline__ static Q load_q(const void* p) {
+    const uint4 w = *reinterpret_cast<const uint4*>(p);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    Q q;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      q.h[2 * i] = static_cast<unsigned short>(ws[i] & 0xffffu);
+      q.h[2 * i + 1] = static_cast<unsigned short>(ws[i] >> 16);
+    }
+    return q;
+  }
+  // FHFMA.BF16: the bf16 x bf16 product is exact in fp32; one rounding on the add.
+  __device__ __forceinline__ static float dot(const uint4 k, const Q& q, float acc) {
+    asm("{\n\t.reg .b16 l0, h0, l1, h1, l2, h2, l3, h3;\n\t"
+        "mov.b32 {l0, h0}, %1;\n\tmov.b32 {l1, h1}, %2;\n\t"
+        "mov.b32 {l2, h2}, %3;\n\tmov.b32 {l3, h3}, %4;\n\t"
+        "fma.rn.f32.bf16 %0, l0, %5, %0;\n\tfma.rn.f32.bf16 %0, h0, %6, %0;\n\t"
+        "fma.rn.f32.bf16 %0, l1, %7, %0;\n\tfma.rn.f32.bf16 %0, h1, %8, %0;\n\t"
+        "fma.rn.f32.bf16 %0, l2, %9, %0;\n\tfma.rn.f32.bf16 %0, h2, %10, %0;\n\t"
+        "fma.rn.f32.bf16 %0, l3, %11, %0;\n\tfma.rn.f32.bf16 %0, h3, %12, %0;\n\t}"
+        : "+f"(acc)
+        : "r"(k.x), "r"(k.y), "r"(k.z), "r"(k.w), "h"(q.h[0]), "h"(q.h[1]), "h"(q.h[2]), "h"(q.h[3]),
+          "h"(q.h[4]), "h"(q.h[5]), "h"(q.h[6]), "h"(q.h[7]));
+    return acc;
+  }
+  __device__ __forceinline__ static void axpy(float p, const uint4 v, float2 (&o)[4]) {
+    const float2 pp = make_float2(p, p);
+    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = __ffma2_rn(pp, make_float2(__uint_as_float(ws[i] << 16), __uint_as_float(ws[i] & 0xffff0000u)), o[i]);
+  }
+};
+
+template <>
+struct Chunk<__half> {
+  static constexpr int EPL = 8;
+  struct Q {
+    unsigned short h[8];
+  };
+  __device__ __forceinline__ static Q load_q(const void* p) {
+    const uint4 w = *reinterpret_cast<const uint4*>(p);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    Q q;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      q.h[2 * i] = static_cast<unsigned short>(ws[i] & 0xffffu);
+      q.h[2 * i + 1] = static_cast<unsigned short>(ws[i] >> 16);
+    }
+    return q;
+  }
+  __device__ __forceinline__ static float dot(const uint4 k, const Q& q, float acc) {
+    asm("{\n\t.reg .b16 l0, h0, l1, h1, l2, h2, l3, h3;\n\t"
+        "mov.b32 {l0, h0}, %1;\n\tmov.b32 {l1, h1}, %2;\n\t"
+        "mov.b32 {l2, h2}, %3;\n\tmov.b32 {l3, h3}, %4;\n\t"
+        "fma.rn.f32.f16 %0, l0, %5, %0;\n\tfma.rn.f32.f16 %0, h0, %6, %0;\n\t"
+        "fma.rn.f32.f16 %0, l1, %7, %0;\n\tfma.rn.f32.f16 %0, h1, %8, %0;\n\t"
+        "fma.rn.f32.f16 %0, l2, %9, %0;\n\tfma.rn.f32.f16 %0, h2, %10, %0;\n\t"
+        "fma.rn.f32.f16 %0, l3, %11, %0;\n\tfma.rn.f32.f16 %0, h3, %12, %0;\n\t}"
+        : "+f"(acc)
+        : "r"(k.x), "r"(k.y), "r"(k.z), "r"(k.w), "h"(q.h[0]), "h"(q.h[1]), "h"(q.h[2]), "h"(q.h[3]),
+          "h"(q.h[4]), "h"(q.h[5]), "h"(q.h[6]), "h"(q.h[7]));
+    return acc;
+  }
+  __device__ __forceinline__ static void axpy(float p, const uint4 v, float2 (&o)[4]) {
+    const float2 pp = make_float2(p, p);
+    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = __ffma2_rn(pp, __half22float2(*reinterpret_cast<const __half2*>(&ws[i])), o[i]);
+  }
+};
+
+template <>
+struct Chunk<float> {
+  static constexpr int EPL = 4;
+  struct Q {
+    float f[4];
+  };
+  __device__ __forceinline__ static Q load_q(const void* p) {
+    const float4 w = *reinterpret_cast<const float4*>(p);
+    return Q{{w.x, w.y, w.z, w.w}};
+  }
+  __device__ __forceinline__ static float dot(const uint4 k, const Q& q, float acc) {
+    acc = fmaf(__uint_as_float(k.x), q.f[0], acc);
+    acc = fmaf(__uint_as_float(k.y), q.f[1], acc);
+    acc = fmaf(__uint_as_float(k.z), q.f[2], acc);
+    return fmaf(__uint_as_float(k.w), q.f[3], acc);
+  }
+  __device__ __forceinline__ static void axpy(float p, const uint4 v, float2 (&o)[2]) {
+    const float2 pp = make_float2(p, p);
+    o[0] = __ffma2_rn(pp, make_float2(__uint_as_float(v.x), __uint_as_float(v.y)), o[0]);
+    o[1] = __ffma2_rn(pp, make_float2(__uint_as_float(v.z), __uint_as_float(v.w)), o[1]);
+  }
+};
+
+// =======================================================================================
+// MHA engine (T_m = 1): CUDA-core fp32 arithmetic
+// =======================================================================================
+template <typename T, int D_, int NST_, int WPS_>
+struct MhaEngine {
+  static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
+  static constexpr int ROWB = D * int(sizeof(T));          // bytes of one K (or V) row
+  static constexpr int LPK = ROWB / 16;                     // lanes per key
+  static constexpr int EPL = 16 / int(sizeof(T));           // elements per 16-byte chunk
+  static constexpr int STAGE_TOK = 32768 / (2 * ROWB);      // 32 KiB of K+V per stage
+  static constexpr int STAGE_BYTES = 2 * STAGE_TOK * ROWB;
+  static constexpr int HEADS = 1;                           // q-heads per unit
+  static constexpr int FOLD_FLOATS = NCW * (D + 2);         // per warp: O[D], m, l
+  static constexpr bool ZERO_RING = true;                   // tail rows must be finite
+  static_assert(LPK >= 2 && LPK <= 32 && (LPK & (LPK - 1)) == 0, "lanes per key");
+  static_assert(STAGE_TOK % 32 == 0, "stage holds whole 32-key rounds");
+
+  struct State {
+    typename Chunk<T>::Q qf;
+    float m, l;
+    float2 o[EPL / 2];
+  };
+
+  __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs& a, const TmapPair&, int64_t row,
+                                                 int ntok, uint64_t* bar, uint64_t pol) {
+    const uint32_t bytes = uint32_t(ntok) * ROWB;
+    mbar_arrive_expect_tx(bar, 2 * bytes);
+    const size_t goff = size_t(row) * ROWB;
+    bulk_g2s(dst, static_cast<const unsigned char*>(a.k) + goff, bytes, bar, pol);
+    bulk_g2s(dst + STAGE_TOK * ROWB, static_cast<const unsigned char*>(a.v) + goff, bytes, bar, pol);
+  }
+
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
+    s.qf = Chunk<T>::load_q(static_cast<const T*>(a.q) + size_t(u.q_row) * D + (lane % LPK) * EPL);
+    s.m = -INFINITY;  // Alg1§8-9
+    s.l = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL / 2; ++e) s.o[e] = make_float2(0.f, 0.f);
+  }
+
+  // This warp's 32-key rounds (sub, sub + WPS, ...) of one stage of ntok keys.
+  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, float scale_log2,
+                                               int lane) {
+    const int kg = lane / LPK, li = lane % LPK;
+    const unsigned char* ks = st;
+    const unsigned char* vs = st + STAGE_TOK * ROWB;
+    for (int r = sub * 32; r < ntok; r += 32 * WPS) {
+      const int kb = r + kg * LPK;
+      // S_f = Q_f K_f^T (Alg1§20): lane li accumulates key (jj ^ li) over its chunk li
+      float acc[LPK];
+#pragma unroll
+      for (int jj = 0; jj < LPK; ++jj)
+        acc[jj] = Chunk<T>::dot(*reinterpret_cast<const uint4*>(ks + (kb + (jj ^ li)) * ROWB + li * 16), s.qf, 0.f);
+      // XOR transpose-butterfly: acc[0] of lane li ends up as the full dot of key kb + li
+#pragma unroll
+      for (int off = LPK / 2; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int jj = 0; jj < off; ++jj) acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj + off], off);
+      }
+      const float sc = (kb + li < ntok) ? acc[0] * scale_log2 : -INFINITY;  // reading C5
+      float mr = sc;                                                         // Alg1§21
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
+      if (mr > s.m) {  // warp-uniform: e^{m - m_new} rescale (Alg1§23-24)
+        const float alpha = ex2(s.m - mr);
+        s.l *= alpha;
+        const float2 aa = make_float2(alpha, alpha);
+#pragma unroll
+        for (int e = 0; e < EPL / 2; ++e) s.o[e] = __fmul2_rn(aa, s.o[e]);
+        s.m = mr;
+      }
+      const float p = ex2(sc - s.m);  // Alg1§22
+      s.l += p;                       // Alg1§23
+#pragma unroll
+      for (int jj = 0; jj < LPK; ++jj)  // O_acc += P_f V_f (Alg1§24); lane li owns chunk li
+        Chunk<T>::axpy(__shfl_sync(0xffffffffu, p, jj, LPK),
+                       *reinterpret_cast<const uint4*>(vs + (kb + jj) * ROWB + li * 16), s.o);
+    }
+  }
+
+  // Fold this warp's lane groups and write (O[D], m, l) to its fold-buffer row.
+  __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
+    const int kg = lane / LPK, li = lane % LPK;
+#pragma unroll
+    for (int off = LPK; off < 32; off <<= 1) {
+#pragma unroll
+      for (int e = 0; e < EPL / 2; ++e) {
+        s.o[e].x += __shfl_xor_sync(0xffffffffu, s.o[e].x, off);
+        s.o[e].y += __shfl_xor_sync(0xffffffffu, s.o[e].y, off);
+      }
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) s.l += __shfl_xor_sync(0xffffffffu, s.l, off);
+    float* fb = fold + warp * (D + 2);
+    if (kg == 0) {
+#pragma unroll
+      for (int e = 0; e < EPL / 2; ++e) {
+        fb[li * EPL + 2 * e] = s.o[e].x;
+        fb[li * EPL + 2 * e + 1] = s.o[e].y;
+      }
+    }
+    if (lane == 0) {
+      fb[D] = s.m;
+      fb[D + 1] = s.l;
+    }
+  }
+
+  // Element e = (head 0, dim e): fold the NCW warp partials (re-scaling operator).
+  __device__ __forceinline__ static void fold_elem(const float* fold, int e, float& oc, float& ms, float& ls) {
+    ms = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NCW; ++w) ms = fmaxf(ms, fold[w * (D + 2) + D]);
+    oc = 0.f;
+    ls = 0.f;
+#pragma unroll
+    for (int w = 0; w < NCW; ++w) {
+      const float wt = ex2(fold[w * (D + 2) + D] - ms);  // idle warp: m = -inf -> 0
+      ls = fmaf(wt, fold[w * (D + 2) + D + 1], ls);
+      oc = fmaf(wt, fold[w * (D + 2) + e], oc);
+    }
+  }
+};
+
+// =======================================================================================
+// GQA engine (T_m = g q-heads of one KV head): tensor cores
+// =======================================================================================
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+template <typename T>
+struct Mma;
+
+template <>
+struct Mma<__nv_bfloat16> {
+  __device__ __forceinline__ static void run(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+  __device__ __forceinline__ static uint32_t pack(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+};
+
+template <>
+struct Mma<__half> {
+  __device__ __forceinline__ static void run(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+  __device__ __forceinline__ static uint32_t pack(float lo, float hi) {
+    __half2 v = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+template <typename T, int D_, int NST_, int WPS_>
+struct GqaEngine {
+  static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
+  static constexpr int STAGE_TOK = 64;            // = TMA box rows
+  static constexpr int NBOX = D / 64;             // 64-element (128-B) boxes per row
+  static constexpr int BOX_BYTES = STAGE_TOK * 128;
+  static constexpr int KV_BYTES = NBOX * BOX_BYTES;
+  static constexpr int STAGE_BYTES = 2 * KV_BYTES;
+  static constexpr int HEADS = 8;                 // MMA N: q-heads per unit (padded to 8)
+  static constexpr int KS = D / 16;               // k-steps of QK^T = m-tiles of PV
+  static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
+  static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
+  static_assert(STAGE_TOK == 32 * WPS, "one 32-token round per consumer warp per stage");
+
+  struct State {
+    uint32_t qb[KS][2];     // Q^T B-fragments (exact inputs)
+    float m[2], l[2];       // heads 2tq, 2tq+1
+    float o[KS][4];         // O^T fragments: dims 16mm + gq (+8), heads 2tq, 2tq+1
+  };
+
+  __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
+                                                 int, uint64_t* bar, uint64_t pol) {
+    mbar_arrive_expect_tx(bar, STAGE_BYTES);  // full boxes (rows past the tensor are zero-filled)
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b) {
+      tma_load_2d(dst + b * BOX_BYTES, &tm.k, b * 64, int(row), bar, pol);
+      tma_load_2d(dst + KV_BYTES + b * BOX_BYTES, &tm.v, b * 64, int(row), bar, pol);
+    }
+  }
+
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
+    const int gq = lane >> 2, tq = lane & 3;
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const T*>(a.q) + size_t(u.q_row + gq) * D);
+    const bool ok = gq < a.group;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {  // b0 = Q[gq][16kk + 2tq, +1], b1 = Q[gq][16kk + 8 + 2tq, +1]
+      s.qb[kk][0] = ok ? qrow[8 * kk + tq] : 0u;
+      s.qb[kk][1] = ok ? qrow[8 * kk + 4 + tq] : 0u;
+    }
+    s.m[0] = s.m[1] = -INFINITY;
+    s.l[0] = s.l[1] = 0.f;
+#pragma unroll
+    for (int mm = 0; mm < KS; ++mm) s.o[mm][0] = s.o[mm][1] = s.o[mm][2] = s.o[mm][3] = 0.f;
+  }
+
+  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, float scale_log2,
+                                               int lane) {
+    const int gq = lane >> 2, mi = lane >> 3, ri = lane & 7;
+    const int rb = sub * 32;
+    if (rb >= ntok) return;
+    if (rb + 32 > ntok) {
+      // rows >= ntok of this round hold the next unit's rows or cache padding: zero this
+      // warp's V rows so 0 * (non-finite) can never reach the accumulator
+      for (int r = rb + (lane >> 3); r < rb + 32; r += 4)
+        if (r >= ntok)
+#pragma unroll
+          for (int b = 0; b < NBOX; ++b)
+            *reinterpret_cast<uint4*>(st + KV_BYTES + b * BOX_BYTES + r * 128 + (ri << 4)) = make_uint4(0u, 0u, 0u, 0u);
+      __syncwarp();
+    }
+    const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + KV_BYTES);
+    // ---- S^T = K_f Q_f^T for two 16-token blocks (Alg1§20) ------------------------------
+    float sc[2][4];
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      sc[blk][0] = sc[blk][1] = sc[blk][2] = sc[blk][3] = 0.f;
+      const int tok = rb + blk * 16 + ri + ((mi & 1) << 3);
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int chunk = 2 * kk + (mi >> 1);
+        uint32_t af[4];
+        ldsm_x4(kbase + (chunk >> 3) * BOX_BYTES + tok * 128 + (((chunk & 7) ^ (tok & 7)) << 4), af);
+        Mma<T>::run(sc[blk], af, s.qb[kk][0], s.qb[kk][1]);
+      }
+    }
+    // ---- scale, mask the tail (C5), running max per head (Alg1§21) ------------------------
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int tok = rb + blk * 16 + gq + ((e >> 1) << 3);
+        sc[blk][e] = tok < ntok ? sc[blk][e] * scale_log2 : -INFINITY;
+        mx[e & 1] = fmaxf(mx[e & 1], sc[blk][e]);
+      }
+    }
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) {
+      mx[0] = fmaxf(mx[0], __shfl_xor_sync(0xffffffffu, mx[0], off));
+      mx[1] = fmaxf(mx[1], __shfl_xor_sync(0xffffffffu, mx[1], off));
+    }
+    if (__any_sync(0xffffffffu, (mx[0] > s.m[0]) || (mx[1] > s.m[1]))) {  // Alg1§23-24 rescale
+      const float mn0 = fmaxf(s.m[0], mx[0]), mn1 = fmaxf(s.m[1], mx[1]);
+      const float al0 = ex2(s.m[0] - mn0), al1 = ex2(s.m[1] - mn1);
+      s.l[0] *= al0;
+      s.l[1] *= al1;
+#pragma unroll
+      for (int mm = 0; mm < KS; ++mm) {
+        s.o[mm][0] *= al0;
+        s.o[mm][2] *= al0;
+        s.o[mm][1] *= al1;
+        s.o[mm][3] *= al1;
+      }
+      s.m[0] = mn0;
+      s.m[1] = mn1;
+    }
+    // ---- P_f = exp(S_f - m) (Alg1§22); O^T += V^T P^T (Alg1§24) -----------------------------
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const float p0 = ex2(sc[blk][0] - s.m[0]), p1 = ex2(sc[blk][1] - s.m[1]);
+      const float p2 = ex2(sc[blk][2] - s.m[0]), p3 = ex2(sc[blk][3] - s.m[1]);
+      s.l[0] += p0 + p2;
+      s.l[1] += p1 + p3;
+      const uint32_t b0 = movmatrix_t(Mma<T>::pack(p0, p1));  // P[tok 2tq..][head gq]
+      const uint32_t b1 = movmatrix_t(Mma<T>::pack(p2, p3));
+      const int tok = rb + blk * 16 + ri + ((mi >> 1) << 3);
+#pragma unroll
+      for (int mm = 0; mm < KS; ++mm) {
+        const int chunk = 2 * mm + (mi & 1);
+        uint32_t af[4];
+        ldsm_x4_t(vbase + (chunk >> 3) * BOX_BYTES + tok * 128 + (((chunk & 7) ^ (tok & 7)) << 4), af);
+        Mma<T>::run(s.o[mm], af, b0, b1);
+      }
+    }
+    if (rb + 32 > ntok) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> TMA WAR
+  }
+
+  __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
+    const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) {
+      s.l[0] += __shfl_xor_sync(0xffffffffu, s.l[0], off);
+      s.l[1] += __shfl_xor_sync(0xffffffffu, s.l[1], off);
+    }
+    float* fb = fold + warp * HEADS * (D + 2);  // [head][D + 2]
+    const int h0 = 2 * tq, h1 = 2 * tq + 1;
+#pragma unroll
+    for (int mm = 0; mm < KS; ++mm) {
+      const int c = 16 * mm + gq;
+      fb[h0 * (D + 2) + c] = s.o[mm][0];
+      fb[h1 * (D + 2) + c] = s.o[mm][1];
+      fb[h0 * (D + 2) + c + 8] = s.o[mm][2];
+      fb[h1 * (D + 2) + c + 8] = s.o[mm][3];
+    }
+    if (gq == 0) {
+      fb[h0 * (D + 2) + D] = s.m[0];
+      fb[h0 * (D + 2) + D + 1] = s.l[0];
+      fb[h1 * (D + 2) + D] = s.m[1];
+      fb[h1 * (D + 2) + D + 1] = s.l[1];
+    }
+  }
+
+  __device__ __forceinline__ static void fold_elem(const float* fold, int e, float& oc, float& ms, float& ls) {
+    const int h = e / D, c = e % D;
+    ms = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NCW; ++w) ms = fmaxf(ms, fold[(w * HEADS + h) * (D + 2) + D]);
+    oc = 0.f;
+    ls = 0.f;
+#pragma unroll
+    for (int w = 0; w < NCW; ++w) {
+      const float* fb = fold + (w * HEADS + h) * (D + 2);
+      const float wt = ex2(fb[D] - ms);
+      ls = fmaf(wt, fb[D + 1], ls);
+      oc = fmaf(wt, fb[c], oc);
+    }
+  }
+};
+
+// =======================================================================================
+// The persistent decode kernel
+// =======================================================================================
+constexpr int kQD = 4;   // depth of the producer -> consumer virtual-CTA queue
+constexpr int kGS = 16;  // dynamic-mode fold tree: segments per first-level group
+constexpr int kFB = 2;   // consumer -> epilogue fold buffers (double buffering)
+
+struct SegInfo {
+  int v, unit, host, finishing;
+};
+
+template <class E>
+struct Smem {
+  static constexpr int RING = E::NST * E::STAGE_BYTES;
+  static constexpr int FOLD = kFB * E::FOLD_FLOATS * 4;
+  static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB) * 8;
+  static constexpr int MISC = kQD * 4 + kFB * int(sizeof(SegInfo));
+  static constexpr int BYTES = 1024 + RING + FOLD + BARS + MISC;
+};
+
+// The epilogue warp's accumulator for one segment: lane owns dims c = lane + 32 j of every
+// head h (the fold buffer layout is [warp][head][D + 2] = O[D], m, l for both engines).
+template <class E>
+struct EpiAcc {
+  static constexpr int H = E::HEADS, D = E::D, J = E::D / 32;
+  float o[H][J], m[H], l[H];
+};
+
+template <class E>
+__global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeArgs a, const __grid_constant__ TmapPair tm) {
+  constexpr int NST = E::NST, WPS = E::WPS, NCW = E::NCW, D = E::D, H = E::HEADS, J = D / 32;
+  constexpr int FOLD_FLOATS = E::FOLD_FLOATS;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* ring =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* fold = reinterpret_cast<float*>(ring + Smem<E>::RING);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(fold) + Smem<E>::FOLD);
+  uint64_t* empty = full + NST;
+  uint64_t* vq_full = empty + NST;
+  uint64_t* vq_empty = vq_full + kQD;
+  uint64_t* fold_full = vq_empty + kQD;
+  uint64_t* fold_empty = fold_full + kFB;
+  int* vq = reinterpret_cast<int*>(fold_empty + kFB);
+  SegInfo* seginfo = reinterpret_cast<SegInfo*>(vq + kQD);
+
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int g = blockIdx.x;
+  const bool dynamic = a.dynamic != 0;
+  const int NV = a.num_v;
+  unsigned long long* tr = a.trace ? a.trace + size_t(g) * TR_FIELDS : nullptr;
+  if (tr && threadIdx.x == 0) {
+    tr[TR_SMID] = smid();
+    tr[TR_START] = globaltimer();
+    tr[TR_PUBLISH] = tr[TR_WAIT0] = tr[TR_WAIT1] = 0;
+  }
+  if (E::ZERO_RING)  // rows past a short stage must be finite (masked p = 0; 0 * finite = 0)
+    for (int i = threadIdx.x; i < Smem<E>::RING / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(ring)[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], WPS);
+    }
+    for (int q = 0; q < kQD; ++q) {
+      mbar_init(&vq_full[q], 1);
+      mbar_init(&vq_empty[q], NCW);
+    }
+    for (int b = 0; b < kFB; ++b) {
+      mbar_init(&fold_full[b], NCW);
+      mbar_init(&fold_empty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero-fill before TMA writes
+  __syncthreads();
+
+  if (warp == NCW + 1) {
+    // ================================ producer ==========================================
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      if (a.uses_tmap) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.k)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.v)) : "memory");
+      }
+      int j = 0, k = 0;
+      for (bool first = true;; first = false) {
+        // Claim the next virtual CTA only once the previous one is fully issued: the ring
+        // (NST stages in flight) hides the atomic's latency, and claiming ahead would let a
+        // CTA hoard two of the big first-round ranges.
+        const int v = dynamic ? atomicAdd(&a.counters[0], 1) : (first ? g : NV);
+        const int q = k % kQD;
+        if (k >= kQD) mbar_wait(&vq_empty[q], ((k / kQD) - 1) & 1);
+        vq[q] = v < NV ? v : -1;
+        mbar_arrive(&vq_full[q]);
+        ++k;
+        if (v >= NV) break;
+        // Align the virtual CTA's first stage to ring slot 0 (empty phases), so the stage ->
+        // consumer-warp assignment -- hence every rounding -- depends only on v, not on
+        // which CTAs claimed what before: bitwise-deterministic output (reading C16).
+        for (; j % NST != 0; ++j) {
+          const int slot = j % NST;
+          if (j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
+          mbar_arrive(&full[slot]);
+        }
+        const int it1 = a.cta_begin[v + 1];
+        int unit = a.cta_first_unit[v];
+        for (int it = a.cta_begin[v]; it < it1;) {
+          const DevUnit u = a.units[unit];
+          if (u.iter_end <= it) {
+            ++unit;
+            continue;
+          }
+          const int seg_end = min(u.iter_end, it1);
+          for (; it < seg_end; ++it) {                        // LeanTile iterations (Alg1§13)
+            const int t0 = (it - u.iter_begin) * a.tile_n;    // kk = iter * T_n (Alg1§14)
+            const int t1 = min(t0 + a.tile_n, u.len);
+            for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {  // LoadFragment K, V (Alg1§17-18)
+              const int slot = j % NST;
+              if (j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
+              E::produce(ring + slot * E::STAGE_BYTES, a, tm, u.row0 + s0, min(a.stage_tokens, t1 - s0),
+                         &full[slot], pol);
+              ++j;
+            }
+          }
+          ++unit;
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp == NCW) {
+    // ================================ epilogue ==========================================
+    // Folds the NCW per-warp partials of each finished segment (§4.1 operator) and runs the
+    // fixup -- partial stores, flags / counters, peer folds, finalize -- off the consumers'
+    // critical path.
+    EpiAcc<E> acc;
+    auto reset = [&]() {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        acc.m[h] = -INFINITY;
+        acc.l[h] = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = 0.f;
+      }
+    };
+    auto store_partial = [&](int slot) {  // StorePartials(Op, mp, lp) (Alg2§20-22)
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        if (h >= a.group) continue;
+        const size_t row = size_t(slot) * a.group + h;
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) a.part_o[row * D + lane + 32 * jj] = acc.o[h][jj];
+        if (lane == 0) {
+          a.part_ml[row * 2] = acc.m[h];
+          a.part_ml[row * 2 + 1] = acc.l[h];
+        }
+      }
+      __threadfence();  // every lane: its stores are visible GPU-wide before the signal
+      __syncwarp();
+    };
+    // acc = f(...f(f(acc, P[slot(p0)]), P[slot(p0 + stride)])..., P[slot(<= p1)]), ascending
+    // (Alg2§27-35); host_v's partial lives in slot 1 of its virtual CTA, everyone else's in 0
+    auto fold_range = [&](int p0, int p1, int stride, int host_v) {
+      constexpr int NB = (H == 1) ? 4 : 1;  // partials whose loads are in flight together
+      for (int pb = p0; pb <= p1; pb += NB * stride) {
+        float mp[NB][H], lp[NB][H], op[NB][H][J];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int p = pb + b * stride;
+          if (p > p1) continue;
+          const size_t slot = size_t(2 * p + (p == host_v ? 1 : 0));
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            if (h >= a.group) continue;
+            const size_t row = slot * a.group + h;
+            mp[b][h] = ld_cg(&a.part_ml[row * 2]);
+            lp[b][h] = ld_cg(&a.part_ml[row * 2 + 1]);
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) op[b][h][jj] = ld_cg(&a.part_o[row * D + lane + 32 * jj]);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (pb + b * stride > p1) continue;
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            if (h >= a.group) continue;
+            const float mn = fmaxf(acc.m[h], mp[b][h]);
+            const float wa = ex2(acc.m[h] - mn), wb = ex2(mp[b][h] - mn);  // Alg2§32-34
+            acc.l[h] = wa * acc.l[h] + wb * lp[b][h];
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = wa * acc.o[h][jj] + wb * op[b][h][jj];
+            acc.m[h] = mn;
+          }
+        }
+      }
+    };
+    auto write_out = [&](int q_row) {  // O = diag(l)^-1 O; L = m + log(l) (Alg2§38-39, C2)
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        if (h >= a.group) continue;
+        const float inv = 1.f / acc.l[h];
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) a.out[size_t(q_row + h) * D + lane + 32 * jj] = acc.o[h][jj] * inv;
+        if (lane == 0 && a.lse) a.lse[q_row + h] = (acc.m[h] + log2f(acc.l[h])) * kLn2;
+      }
+    };
+
+    for (int seg = 0;; ++seg) {
+      const int b = seg % kFB;
+      mbar_wait(&fold_full[b], (seg / kFB) & 1);
+      const SegInfo si = seginfo[b];
+      if (si.unit < 0) break;
+      // ---- fold the consumer warps' partials of this segment ------------------------------
+      const float* fb = fold + b * FOLD_FLOATS;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NCW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 2) + D]);
+        float l = 0.f, o[J];
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
+#pragma unroll
+        for (int w = 0; w < NCW; ++w) {
+          const float* r = fb + (w * H + h) * (D + 2);
+          const float wt = ex2(r[D] - mx);  // idle warp: m = -inf -> 0
+          l = fmaf(wt, r[D + 1], l);
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(wt, r[lane + 32 * jj], o[jj]);
+        }
+        acc.m[h] = mx;
+        acc.l[h] = l;
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = o[jj];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill this buffer
+      const DevUnit u = a.units[si.unit];
+      const int v = si.v;
+
+      if (si.host && si.finishing) {
+        write_out(u.q_row);  // one (virtual) CTA computed the whole unit (Alg2§38-39)
+      } else if (!dynamic) {
+        if (!si.host) {
+          // ---- static, non-host: StorePartials + Signal(flags[g]) (Alg2§19-23) -----------
+          store_partial(2 * v);
+          if (lane == 0) {
+            st_release_gpu(&a.flags[v], a.epoch);
+            if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
+          }
+        } else {
+          // ---- static host, not finishing: Wait(flags[cta]) for cta = g+1 .. last_cta
+          //      (Alg2§26-28, reading C9), lanes poll peers in parallel; fold ascending -----
+          if (tr && lane == 0) tr[TR_WAIT0] = globaltimer();
+          for (int p = v + 1 + lane; p <= u.last_cta; p += 32)
+            while (ld_acquire_gpu(&a.flags[p]) != a.epoch) __nanosleep(20);
+          __syncwarp();
+          if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
+          fold_range(v + 1, u.last_cta, 1, -1);
+          write_out(u.q_row);
+        }
+      } else {
+        // ---- dynamic: publish, count in; a FIXED two-level tree folds the unit's segments
+        //      (virtual CTAs host_cta .. last_cta): the last arriver of each group of kGS
+        //      consecutive segments folds the group ascending into the group's first slot,
+        //      the last group folds the groups ascending.  Deterministic; nobody waits.
+        const int hv = u.host_cta;
+        const int nseg = u.last_cta - hv + 1;
+        const int ngrp = (nseg + kGS - 1) / kGS;
+        const int g0 = hv + ((v - hv) / kGS) * kGS;
+        const int g1 = min(g0 + kGS, u.last_cta + 1) - 1;
+        store_partial(2 * v + (si.host ? 1 : 0));
+        int role = 0;
+        if (lane == 0) {
+          if (atomicAdd(&a.grp_count[g0], 1) == g1 - g0) {
+            __threadfence();
+            a.grp_count[g0] = 0;  // ready for the next launch
+            role = 1;
+          }
+          if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
+        }
+        role = __shfl_sync(0xffffffffu, role, 0);
+        if (role) {
+          reset();
+          fold_range(g0, g1, 1, hv);
+          if (ngrp == 1) {
+            write_out(u.q_row);
+          } else {
+            store_partial(2 * g0 + (g0 == hv ? 1 : 0));
+            int last = 0;
+            if (lane == 0 && atomicAdd(&a.unit_count[si.unit], 1) == ngrp - 1) {
+              __threadfence();
+              a.unit_count[si.unit] = 0;
+              last = 1;
+            }
+            if (__shfl_sync(0xffffffffu, last, 0)) {
+              reset();
+              fold_range(hv, u.last_cta, kGS, hv);
+              write_out(u.q_row);
+            }
+          }
+        }
+      }
+    }
+    if (lane == 0) {
+      if (tr) tr[TR_END] = globaltimer();
+      if (dynamic) {  // the last CTA out resets the claim counter for the next launch
+        __threadfence();
+        if (atomicAdd(&a.counters[1], 1) == int(gridDim.x) - 1) {
+          a.counters[0] = 0;
+          a.counters[1] = 0;
+        }
+      }
+    }
+    return;
+  }
+
+  // ================================= consumers ==========================================
+  const int my_slot = warp / WPS, sub = warp % WPS;
+  int j = 0, k = 0, seg = 0;
+  auto hand_off = [&](const typename E::State* st, int v, int unit, int host, int finishing) {
+    // give this warp's segment partial to the epilogue warp (double-buffered)
+    const int b = seg % kFB;
+    if (seg >= kFB) mbar_wait(&fold_empty[b], ((seg / kFB) - 1) & 1);
+    if (st) E::seg_end(*const_cast<typename E::State*>(st), fold + b * FOLD_FLOATS, warp, lane);
+    if (warp == 0 && lane == 0) seginfo[b] = SegInfo{v, unit, host, finishing};
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&fold_full[b]);
+    ++seg;
+  };
+  for (;;) {
+    const int q = k % kQD;
+    mbar_wait(&vq_full[q], (k / kQD) & 1);
+    const int v = vq[q];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&vq_empty[q]);
+    ++k;
+    if (v < 0) break;
+    if (dynamic && tr && threadIdx.x == 0) {  // dynamic mode: claims and LeanTiles per CTA
+      tr[TR_WAIT0] += 1;
+      tr[TR_WAIT1] += a.cta_begin[v + 1] - a.cta_begin[v];
+    }
+    for (; j % NST != 0; ++j) {  // the producer's empty alignment phases
+      if (j % NST == my_slot) {
+        mbar_wait(&full[my_slot], (j / NST) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[my_slot]);
+      }
+    }
+    const int it1 = a.cta_begin[v + 1];
+    int unit = a.cta_first_unit[v];
+    for (int it = a.cta_begin[v]; it < it1;) {
+      const DevUnit u = a.units[unit];
+      if (u.iter_end <= it) {
+        ++unit;
+        continue;
+      }
+      const int seg_end = min(u.iter_end, it1);
+      const int host = (it == u.iter_begin) ? 1 : 0;      // host-block (Alg2§17)
+      const int finishing = (it1 >= u.iter_end) ? 1 : 0;  // finishing-block (Alg2§18)
+      typename E::State st;
+      E::seg_begin(st, a, u, lane);
+      for (; it < seg_end; ++it) {
+        const int t0 = (it - u.iter_begin) * a.tile_n;
+        const int t1 = min(t0 + a.tile_n, u.len);
+        for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
+          if (j % NST == my_slot) {
+            mbar_wait(&full[my_slot], (j / NST) & 1);
+            E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), a.scale_log2, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[my_slot]);
+          }
+          ++j;
+        }
+      }
+      hand_off(&st, v, unit, host, finishing);
+      ++unit;
+    }
+  }
+  hand_off(nullptr, -1, -1, 0, 0);  // terminator for the epilogue
+}
+
+// ---------------------------------------------------------------------------------------
+// Sequence-shard combine: L = ln sum_r e^{L_r}, O = sum_r e^{L_r - L} O_r  (ascending r)
+// ---------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(D) la_combine_kernel(const float* __restrict__ o_parts,
+                                                       const float* __restrict__ lse_parts, int parts, int rows,
+                                                       float* __restrict__ out, float* __restrict__ lse) {
+  const int r = blockIdx.x, c = threadIdx.x;
+  float mx = -INFINITY;
+  for (int p = 0; p < parts; ++p) mx = fmaxf(mx, lse_parts[size_t(p) * rows + r]);
+  float s = 0.f, acc = 0.f;
+  for (int p = 0; p < parts; ++p) {
+    const float w = expf(lse_parts[size_t(p) * rows + r] - mx);
+    s += w;
+    acc = fmaf(w, o_parts[(size_t(p) * rows + r) * D + c], acc);
+  }
+  out[size_t(r) * D + c] = acc / s;
+  if (c == 0 && lse) lse[r] = mx + logf(s);
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+template <class E>
+KernelInfo info_of(bool tma) {
+  KernelInfo k;
+  k.supported = true;
+  k.threads = (E::NCW + 2) * 32;
+  k.smem_bytes = Smem<E>::BYTES;
+  k.stage_tokens_max = E::STAGE_TOK;
+  k.uses_tma_tensor = tma;
+  k.fn = reinterpret_cast<const void*>(&la_decode<E>);
+  return k;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn(std::string& err) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) err = "cuTensorMapEncodeTiled unavailable";
+  return fn;
+}
+
+bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype, std::string& err) {
+  auto enc = encode_fn(err);
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {cuuint64_t(d), cuuint64_t(rows)};
+  cuuint64_t gstride[1] = {cuuint64_t(d) * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, dtype == LA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    err = "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")";
+    return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+KernelInfo decode_kernel_info(int dtype, int head_dim, int group) {
+  if (group == 1) {
+    if (dtype == LA_BF16 && head_dim == 128) return info_of<MhaEngine<__nv_bfloat16, 128, 5, 2>>(false);
+    if (dtype == LA_BF16 && head_dim == 64) return info_of<MhaEngine<__nv_bfloat16, 64, 5, 2>>(false);
+    if (dtype == LA_FP16 && head_dim == 128) return info_of<MhaEngine<__half, 128, 5, 2>>(false);
+    if (dtype == LA_FP16 && head_dim == 64) return info_of<MhaEngine<__half, 64, 5, 2>>(false);
+    if (dtype == LA_FP32 && head_dim == 128) return info_of<MhaEngine<float, 128, 5, 2>>(false);
+    if (dtype == LA_FP32 && head_dim == 64) return info_of<MhaEngine<float, 64, 5, 2>>(false);
+    return KernelInfo{};
+  }
+  if (group > 8) return KernelInfo{};
+  if (dtype == LA_BF16 && head_dim == 128) return info_of<GqaEngine<__nv_bfloat16, 128, 4, 2>>(true);
+  if (dtype == LA_BF16 && head_dim == 64) return info_of<GqaEngine<__nv_bfloat16, 64, 4, 2>>(true);
+  if (dtype == LA_FP16 && head_dim == 128) return info_of<GqaEngine<__half, 128, 4, 2>>(true);
+  if (dtype == LA_FP16 && head_dim == 64) return info_of<GqaEngine<__half, 64, 4, 2>>(true);
+  return KernelInfo{};
+}
+
+int launch_decode(const KernelInfo& ki, const DecodeArgs& a_in, int64_t kv_rows, int head_dim, int dtype,
+                  bool cooperative, void* stream, std::string& err) {
+  DecodeArgs a = a_in;
+  TmapPair tm;
+  std::memset(&tm, 0, sizeof(tm));
+  a.uses_tmap = ki.uses_tma_tensor ? 1 : 0;
+  if (ki.uses_tma_tensor) {
+    if (!make_tmap(&tm.k, a.k, kv_rows, head_dim, dtype, err)) return 1;
+    if (!make_tmap(&tm.v, a.v, kv_rows, head_dim, dtype, err)) return 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.grid);
+  cfg.blockDim = dim3(ki.threads);
+  cfg.dynamicSmemBytes = ki.smem_bytes;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // static hosts spin on peers: co-residency
+  attr[0].val.cooperative = cooperative ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&a, &tm};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, ki.fn, args);
+  if (e != cudaSuccess) {
+    err = std::string("decode launch: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return 1;
+  }
+  note_launch();
+  return 0;
+}
+
+int launch_combine(const float* o_parts, const float* lse_parts, int parts, int rows, int head_dim, float* out,
+                   float* lse, void* stream, std::string& err) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (head_dim == 128)
+    la_combine_kernel<128><<<rows, 128, 0, st>>>(o_parts, lse_parts, parts, rows, out, lse);
+  else
+    la_combine_kernel<64><<<rows, 64, 0, st>>>(o_parts, lse_parts, parts, rows, out, lse);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("combine launch: ") + cudaGetErrorString(e);
+    return 1;
+  }
+  note_launch();
+  return 0;
+}
+
+}  // namespace la

@@ -23,14 +23,15 @@ struct DevUnit {
 };
 static_assert(sizeof(DevUnit) == 32, "DevUnit layout");
 
-// Host-side schedule: Alg2§4-18 for every CTA.  Pure integer work, no CUDA.
+// Host-side schedule: Alg2§4-18 for every (virtual) CTA.  Pure integer work, no CUDA.
 struct Schedule {
   int tile_n = 0;
-  int grid = 0;
+  int grid = 0;         // (virtual) CTAs = ranges of the iteration space (Alg. 2's G)
+  int phys_grid = 0;    // CTAs launched (= grid for static schedules)
   int64_t total_iters = 0;
   std::vector<DevUnit> units;
-  std::vector<int32_t> cta_begin;       // G + 1 entries: CTA g owns [cta_begin[g], cta_begin[g+1])
-  std::vector<int32_t> cta_first_unit;  // G entries: unit containing cta_begin[g]
+  std::vector<int32_t> cta_begin;       // grid + 1 entries: CTA v owns [cta_begin[v], cta_begin[v+1])
+  std::vector<int32_t> cta_first_unit;  // grid entries: unit containing cta_begin[v]
   int64_t num_segments = 0;
   int64_t num_partials = 0;
 };
@@ -51,12 +52,17 @@ void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int6
 void streamk_ranges(int64_t total_iters, int grid, std::vector<int32_t>& cta_begin);
 // Sequential (FA2): one CTA per unit.
 void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& cta_begin);
+// Guided virtual-CTA ranges for LA_SCHED_DYNAMIC: `grid` ranges of
+// floor(first_permille/1000 * I / grid) iterations, then rounds of `grid` ranges each
+// covering half of what remains (>= min_chunk), until I is covered.
+void guided_ranges(int64_t total_iters, int grid, int first_permille, int min_chunk,
+                   std::vector<int32_t>& cta_begin);
 // host_cta / last_cta per unit, first unit per CTA, segment & partial counts.
 void finish_schedule(Schedule& s);
 // Segment rows (7 int32 each, SPEC S:275 order) by the Alg2§10-18,§41 walk.
 void export_segments(const Schedule& s, std::vector<int32_t>& rows);
 
-// ---- device side (kernels.cu) -------------------------------------------------------
+// ---- device side (decode.cu) --------------------------------------------------------
 struct DecodeArgs {
   const void* q;
   const void* k;
@@ -66,15 +72,21 @@ struct DecodeArgs {
   const DevUnit* units;
   const int32_t* cta_begin;
   const int32_t* cta_first_unit;
-  float* part_o;      // [G][group][d]  Op of Alg2§20
-  float* part_ml;     // [G][group][2]  mp, lp of Alg2§21-22 (m in log2 units)
-  uint32_t* flags;    // [G]            flags of Alg2§23/§28, epoch-valued (reading C17)
+  float* part_o;      // [grid][2][group][d]  Op of Alg2§20 (slot 1: dynamic-mode host partial)
+  float* part_ml;     // [grid][2][group][2]  mp, lp of Alg2§21-22 (m in log2 units)
+  uint32_t* flags;    // [grid]               flags of Alg2§23/§28, epoch-valued (reading C17)
+  int* counters;      // [2] dynamic mode: virtual-CTA claim counter, CTAs done
+  int* unit_count;    // [units] dynamic mode: fold-tree groups completed per unit
+  int* grp_count;     // [grid]  dynamic mode: segments published per fold-tree group
+  unsigned long long* trace;  // [phys_grid][LA_TRACE_FIELDS] or nullptr
   uint32_t epoch;
-  unsigned long long* trace;  // [G][LA_TRACE_FIELDS] or nullptr
-  int grid;
+  int dynamic;        // 1: claim virtual CTAs dynamically, last-arriver fold
+  int num_v;          // (virtual) CTAs
+  int grid;           // CTAs launched
   int tile_n;
   int stage_tokens;
   int group;
+  int uses_tmap;      // set by launch_decode for the TMA-tensor (GQA) engine
   float scale_log2;   // scale * log2(e): scores live in the exp2 domain inside the kernel
 };
 
@@ -84,20 +96,16 @@ struct KernelInfo {
   int threads = 0;
   int smem_bytes = 0;
   int stage_tokens_max = 0;
-  bool uses_tma_tensor = false;   // K/V tensor maps passed as a second kernel parameter
+  bool uses_tma_tensor = false;   // K/V TMA tensor maps (encoded per launch)
   const void* fn = nullptr;
 };
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group);
-KernelInfo gqa_kernel_info(int dtype, int head_dim, int group);
-// GQA tensor-core kernel: encodes the K/V TMA tensor maps (rows x head_dim) and launches.
-int launch_decode_tma(const KernelInfo& ki, const DecodeArgs& a, int64_t kv_rows, int head_dim, int dtype,
-                      bool cooperative, void* stream, std::string& err);
-void note_launch();
-// Launch the decode kernel (cooperative when any CTA waits on a peer).
-int launch_decode(const KernelInfo& ki, const DecodeArgs& a, bool cooperative, void* stream,
-                  std::string& err);
+// Launch the decode kernel (cooperative when a static-schedule CTA waits on a peer).
+int launch_decode(const KernelInfo& ki, const DecodeArgs& a, int64_t kv_rows, int head_dim, int dtype,
+                  bool cooperative, void* stream, std::string& err);
 int launch_combine(const float* o_parts, const float* lse_parts, int parts, int rows,
                    int head_dim, float* out, float* lse, void* stream, std::string& err);
+void note_launch();
 int64_t launch_count();
 
 }  // namespace la

@@ -65,6 +65,28 @@ void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& 
   cta_begin[units.size()] = units.empty() ? 0 : units.back().iter_end;
 }
 
+void guided_ranges(int64_t total_iters, int grid, int first_permille, int min_chunk,
+                   std::vector<int32_t>& cta_begin) {
+  // B200-first extension: Alg. 2's equal ranges balance LeanTile COUNTS, but
+  // per-SM HBM bandwidth varies (measured +-10%), so equal counts do not finish together.
+  // The same iteration space is cut into `grid` big ranges (first_permille of the work,
+  // equal), then rounds of `grid` ranges each covering half of the remainder, so the
+  // persistent CTAs that claim them in order end within ~one small range of each other.
+  cta_begin.assign(1, 0);
+  int64_t pos = 0;
+  const int64_t first = total_iters * first_permille / (1000 * int64_t(grid));
+  if (first >= 1)
+    for (int g = 0; g < grid; ++g) cta_begin.push_back(int32_t(pos += first));
+  while (pos < total_iters) {
+    const int64_t rem = total_iters - pos;
+    const int64_t c = std::max<int64_t>(min_chunk, (rem + 2 * int64_t(grid) - 1) / (2 * int64_t(grid)));
+    for (int g = 0; g < grid && pos < total_iters; ++g) {
+      pos = std::min(total_iters, pos + c);
+      cta_begin.push_back(int32_t(pos));
+    }
+  }
+}
+
 static int owner_of(const std::vector<int32_t>& cta_begin, int64_t it) {
   // The CTA g with cta_begin[g] <= it < cta_begin[g+1]; empty CTAs (G > I) are skipped
   // because upper_bound lands past every CTA whose range starts at the same index.
@@ -73,6 +95,7 @@ static int owner_of(const std::vector<int32_t>& cta_begin, int64_t it) {
 }
 
 void finish_schedule(Schedule& s) {
+  s.grid = int(s.cta_begin.size()) - 1;
   const int G = s.grid;
   for (DevUnit& u : s.units) {
     u.host_cta = owner_of(s.cta_begin, u.iter_begin);     // host block (Alg2§17)

@@ -23,11 +23,11 @@ LIB_PATH = os.path.join(_HERE, "lib", "libleanattn.so")
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE = range(6)
 LA_BF16, LA_FP16, LA_FP32 = 0, 1, 2
 LA_KV_BHSD, LA_KV_PACKED = 0, 1
-LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL = 0, 1
+LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC = 0, 1, 2
 
 _DTYPE_CODES = {"bf16": LA_BF16, "fp16": LA_FP16, "fp32": LA_FP32}
 _LAYOUT_CODES = {"bhsd": LA_KV_BHSD, "packed": LA_KV_PACKED}
-_SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL}
+_SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, "dynamic": LA_SCHED_DYNAMIC}
 
 # Every symbol include/la.h declares (tests check the library exports all of them).
 EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
@@ -44,7 +44,8 @@ class LaError(RuntimeError):
 class la_plan_opts(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_float), ("layout", ctypes.c_int), ("max_ctx", ctypes.c_int64),
                 ("grid", ctypes.c_int), ("num_sms", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
-                ("host_only", ctypes.c_int), ("schedule", ctypes.c_int), ("trace", ctypes.c_int)]
+                ("host_only", ctypes.c_int), ("schedule", ctypes.c_int), ("trace", ctypes.c_int),
+                ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -53,7 +54,7 @@ class la_plan_info(ctypes.Structure):
                                             "num_units")] + \
                [(n, ctypes.c_int64) for n in ("total_iters", "num_segments", "num_partials",
                                               "workspace_bytes", "kv_bytes")] + \
-               [("scale", ctypes.c_float)]
+               [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64)]
 
 
 _lib = None
@@ -119,7 +120,8 @@ class Plan:
     def __init__(self, batch: int, heads_q: int, heads_kv: int, head_dim: int, ctx_lens: Sequence[int],
                  tile_n: int = 0, dtype: str = "bf16", scale: float = 0.0, layout: str = "bhsd",
                  max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
-                 ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False):
+                 ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
+                 dyn_first_permille: int = 750, dyn_min_chunk: int = 2):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -132,6 +134,8 @@ class Plan:
         opts.host_only = 1 if host_only else 0
         opts.schedule = _SCHED_CODES[schedule]
         opts.trace = 1 if trace else 0
+        opts.dyn_first_permille = int(dyn_first_permille)
+        opts.dyn_min_chunk = int(dyn_min_chunk)
         lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
         h = ctypes.c_void_p()
         self._h = None

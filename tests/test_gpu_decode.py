@@ -23,12 +23,16 @@ def _lib():
     la.lib()
 
 
+SCHEDULES = ("streamk", "dynamic")
+
+
+@pytest.mark.parametrize("schedule", SCHEDULES)
 @pytest.mark.parametrize("dist", ["D0", "D1", "D2", "D3", "D4"])
-def test_c1_fp32_d64(dist):
+def test_c1_fp32_d64(dist, schedule):
     p = synth.config("c1", dist=dist)
-    O, L, plan = run_cuda(p)
+    O, L, plan = run_cuda(p, schedule=schedule)
     O_ref, L_ref = run_oracle(p)
-    gate(O, L, O_ref, L_ref, what=f"c1/{dist}")
+    gate(O, L, O_ref, L_ref, what=f"c1/{dist}/{schedule}")
     assert plan.info.grid > 1 and plan.info.num_partials > 0     # the fixup path is exercised
 
 
@@ -39,10 +43,11 @@ def test_small_multi_tile_ragged(dtype, d, dist):
     p = synth.Problem(2, 3, 3, d, [1000, 777], dtype=dtype, dist=dist, seed=11, max_ctx=1024)
     O_ref, L_ref = run_oracle(p)
     inputs = cuda_inputs(p)
-    for tile_n in (32, 128):
-        for grid in (1, 2, 3, 7, 64, 0):
-            O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid)
-            gate(O, L, O_ref, L_ref, what=f"{dtype}/d{d}/{dist}/T{tile_n}/G{grid}")
+    for schedule in SCHEDULES:
+        for tile_n in (32, 128):
+            for grid in (1, 2, 3, 7, 64, 0):
+                O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule)
+                gate(O, L, O_ref, L_ref, what=f"{dtype}/d{d}/{dist}/T{tile_n}/G{grid}/{schedule}")
 
 
 def test_forced_grid_and_tile_invariance_and_determinism():
@@ -50,18 +55,21 @@ def test_forced_grid_and_tile_invariance_and_determinism():
     O_ref, L_ref = run_oracle(p)
     inputs = cuda_inputs(p)
     outs = []
-    for grid in (1, 2, 3, 5, 16, 37, 148, 0):
-        for tile_n in (16, 64, 256):
-            O, L, _ = run_cuda(p, inputs=inputs, grid=grid, tile_n=tile_n)
-            gate(O, L, O_ref, L_ref, what=f"G{grid}/T{tile_n}")
-            outs.append(O)
-    # bitwise determinism of a fixed plan (reading C16)
+    for schedule in SCHEDULES + ("sequential",):
+        for grid in (1, 2, 3, 5, 16, 37, 148, 0):
+            for tile_n in (16, 64, 256):
+                O, L, _ = run_cuda(p, inputs=inputs, grid=grid, tile_n=tile_n, schedule=schedule)
+                gate(O, L, O_ref, L_ref, what=f"G{grid}/T{tile_n}/{schedule}")
+                outs.append(O)
+    # bitwise determinism of a fixed plan (reading C16) -- also for the dynamic schedule,
+    # whose virtual-CTA -> CTA mapping changes from run to run
     import paper_2405_10480_b200 as la
     q, k, v = inputs
-    plan = la.Plan(1, 4, 4, 128, [5000], grid=37, tile_n=64)
-    ref = plan.decode(q, k, v)[0].clone()
-    for _ in range(10):
-        assert torch.equal(plan.decode(q, k, v)[0], ref)
+    for schedule, grid in (("streamk", 37), ("dynamic", 37), ("dynamic", 0)):
+        plan = la.Plan(1, 4, 4, 128, [5000], grid=grid, tile_n=16, schedule=schedule)
+        ref = plan.decode(q, k, v)[0].clone()
+        for _ in range(10):
+            assert torch.equal(plan.decode(q, k, v)[0], ref), schedule
 
 
 def test_census_and_zero_query_closed_forms():
@@ -95,11 +103,12 @@ def test_c2_full_size_sampled():
     """North-star config (B=1, H=32, d=128, n=256k, bf16) in the bench's launch config."""
     p = synth.config("c2")
     inputs = cuda_inputs(p)
-    O, L, plan = run_cuda(p, inputs=inputs)
-    assert plan.info.grid == 148 and plan.info.tile_n == 128
-    for h in (0, 19):
-        O_ref, L_ref = oracle_unit(p, 0, h)
-        gate(O[0, h:h + 1], L[0, h:h + 1], O_ref, L_ref, what=f"c2 head {h}")
+    refs = {h: oracle_unit(p, 0, h) for h in (0, 19)}
+    for schedule in SCHEDULES:
+        O, L, plan = run_cuda(p, inputs=inputs, schedule=schedule)
+        assert plan.info.grid == 148 and plan.info.tile_n == 128
+        for h, (O_ref, L_ref) in refs.items():
+            gate(O[0, h:h + 1], L[0, h:h + 1], O_ref, L_ref, what=f"c2 head {h} {schedule}")
     del inputs
     torch.cuda.empty_cache()
     # census at full size: closed form for every head
@@ -112,11 +121,14 @@ def test_c2_full_size_sampled():
 
 def test_c4_ragged_full_size_sampled():
     p = synth.config("c4")
-    O, L, plan = run_cuda(p)
-    assert plan.info.total_iters == 245056
-    for b, h in ((1, 3), (6, 0), (13, 31)):
-        O_ref, L_ref = oracle_unit(p, b, h)
-        gate(O[b, h:h + 1], L[b, h:h + 1], O_ref, L_ref, what=f"c4 b{b} h{h}")
+    inputs = cuda_inputs(p)
+    refs = {(b, h): oracle_unit(p, b, h) for b, h in ((1, 3), (6, 0), (13, 31))}
+    for schedule in SCHEDULES:
+        O, L, plan = run_cuda(p, inputs=inputs, schedule=schedule)
+        assert plan.info.total_iters == 245056
+        for (b, h), (O_ref, L_ref) in refs.items():
+            gate(O[b, h:h + 1], L[b, h:h + 1], O_ref, L_ref, what=f"c4 b{b} h{h} {schedule}")
+    del inputs
     torch.cuda.empty_cache()
     p3 = synth.config("c4", dist="D3")
     O3, L3, _ = run_cuda(p3)
@@ -164,10 +176,11 @@ def test_gqa_small_multi_tile_ragged(dtype, d, group):
     p = synth.Problem(2, 2 * group, 2, d, [1000, 777], dtype=dtype, dist="D2", seed=31, max_ctx=1024)
     O_ref, L_ref = run_oracle(p)
     inputs = cuda_inputs(p)
-    for tile_n in (32, 64, 128):
-        for grid in (1, 3, 0):
-            O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid)
-            gate(O, L, O_ref, L_ref, what=f"gqa g{group}/{dtype}/d{d}/T{tile_n}/G{grid}")
+    for schedule in SCHEDULES:
+        for tile_n in (32, 64, 128):
+            for grid in (1, 3, 0):
+                O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule)
+                gate(O, L, O_ref, L_ref, what=f"gqa g{group}/{dtype}/d{d}/T{tile_n}/G{grid}/{schedule}")
 
 
 def test_gqa_distributions_packed_and_determinism():
@@ -179,20 +192,24 @@ def test_gqa_distributions_packed_and_determinism():
     import paper_2405_10480_b200 as la
     p = synth.Problem(1, 8, 1, 128, [5000], dtype="bf16", dist="D2", seed=33)
     q, k, v = cuda_inputs(p)
-    plan = la.Plan(1, 8, 1, 128, [5000], grid=11, tile_n=64)
-    ref = plan.decode(q, k, v)[0].clone()
-    for _ in range(5):
-        assert torch.equal(plan.decode(q, k, v)[0], ref)
+    for schedule in SCHEDULES:
+        plan = la.Plan(1, 8, 1, 128, [5000], grid=11, tile_n=64, schedule=schedule)
+        ref = plan.decode(q, k, v)[0].clone()
+        for _ in range(5):
+            assert torch.equal(plan.decode(q, k, v)[0], ref)
 
 
 def test_c3_gqa_full_size_sampled():
     """BASELINE.json config 3: batch 8, 64 q-heads / 8 kv-heads, d 128, context 64k, bf16."""
     p = synth.config("c3")
-    O, L, plan = run_cuda(p)
-    assert plan.info.total_iters == 32768 and plan.info.group == 8
-    for b, h in ((0, 0), (3, 5), (7, 7)):
-        O_ref, L_ref = oracle_unit(p, b, h)
-        gate(O[b, 8 * h:8 * h + 8], L[b, 8 * h:8 * h + 8], O_ref, L_ref, what=f"c3 b{b} h{h}")
+    inputs = cuda_inputs(p)
+    refs = {(b, h): oracle_unit(p, b, h) for b, h in ((0, 0), (3, 5), (7, 7))}
+    for schedule in SCHEDULES:
+        O, L, plan = run_cuda(p, inputs=inputs, schedule=schedule)
+        assert plan.info.total_iters == 32768 and plan.info.group == 8
+        for (b, h), (O_ref, L_ref) in refs.items():
+            gate(O[b, 8 * h:8 * h + 8], L[b, 8 * h:8 * h + 8], O_ref, L_ref, what=f"c3 b{b} h{h} {schedule}")
+    del inputs
     torch.cuda.empty_cache()
     p3 = synth.config("c3", dist="D3")
     O3, L3, _ = run_cuda(p3)

@@ -11,6 +11,8 @@
 import itertools
 import os
 
+import numpy as np
+
 import pytest
 
 import oracle
@@ -171,3 +173,61 @@ def test_fixed_split_efficiency():
     for c_n, G, s in [([5, 5], 4, 2), ([9] * 7, 16, 2), ([3, 17, 8], 5, 3)]:
         assert oracle.quantization_efficiency(oracle.stream_k_segments(c_n, G), G) >= \
             oracle.quantization_efficiency(oracle.fixed_split_segments(c_n, G, s), G)
+
+
+def test_segments_from_ranges_generalises_alg2():
+    rng = np.random.default_rng(3)
+    for trial in range(300):
+        c_n = [int(x) for x in rng.integers(1, 9, size=int(rng.integers(1, 6)))]
+        I = sum(c_n)
+        # equal ranges reproduce stream_k_segments exactly
+        G = int(rng.integers(1, I + 3))
+        begins = [oracle.cta_range(I, G, g)[0] for g in range(G)] + [I]
+        assert oracle.segments_from_ranges(c_n, begins) == oracle.stream_k_segments(c_n, G)
+        # random contiguous ranges == brute force over the per-iteration owner table
+        cuts = sorted(set(int(x) for x in rng.integers(1, I, size=int(rng.integers(0, I)))) if I > 1 else set())
+        begins = [0] + list(cuts) + [I]
+        segs = oracle.segments_from_ranges(c_n, begins)
+        own = []
+        for v in range(len(begins) - 1):
+            own += [v] * (begins[v + 1] - begins[v])
+        off = np.concatenate([[0], np.cumsum(c_n)])
+        brute = []
+        for u in range(len(c_n)):
+            first, last = off[u], off[u + 1] - 1
+            start = first
+            for it in range(first, last + 1):
+                if it == last or own[it + 1] != own[it]:
+                    brute.append(Segment(own[it], u, int(start - first), int(it + 1 - first), start == first,
+                                         it == last, own[last]))
+                    start = it + 1
+        assert sorted(segs, key=lambda s: (s.cta, s.unit)) == sorted(brute, key=lambda s: (s.cta, s.unit))
+
+
+def test_guided_ranges_properties():
+    for I, G in [(65536, 148), (32768, 148), (245056, 148), (10, 4), (7, 10), (1000, 1), (149, 148)]:
+        b = oracle.guided_ranges(I, G)
+        sizes = np.diff(b)
+        assert b[0] == 0 and b[-1] == I and np.all(sizes >= 1)
+        first = I * 750 // (1000 * G)
+        if first >= 1:
+            assert np.all(sizes[:G] == first)                       # the static 75% part
+            tail = sizes[G:]
+            assert np.all(tail[:-1][: len(tail) - 1] >= 1)
+        # later ranges never grow (guided self-scheduling), last ones >= min chunk except the clip
+        rest = sizes[G:] if first >= 1 else sizes
+        assert all(rest[i] >= rest[i + 1] or i + 1 == len(rest) - 1 for i in range(len(rest) - 1))
+
+
+def test_alg2_with_virtual_ctas_equals_eq1():
+    rng = np.random.default_rng(4)
+    q = rng.normal(size=(2, 3, 8)) * 2
+    lens = [300, 77]
+    k = rng.normal(size=(2, 3, 300, 8))
+    v = rng.normal(size=(2, 3, 300, 8))
+    O_ref, L_ref = oracle.decode_attention(q, k, v, lens, 0.35)
+    c_n = [-(-n // 16) for n in lens for _ in range(3)]
+    for G in (1, 3, 7, 40):
+        begins = oracle.guided_ranges(sum(c_n), G)
+        O, L = oracle.lean_attention(q, k, v, lens, 0.35, 16, G, begins=begins)
+        assert np.max(np.abs(O - O_ref)) <= 1e-12 and np.max(np.abs(L - L_ref)) <= 1e-12

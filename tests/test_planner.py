@@ -44,7 +44,7 @@ def _oracle_rows(batch, heads_kv, lens, tile_n, grid, layout):
 
 
 def test_fig1_golden_through_the_abi(la):
-    p = la.Plan(1, 2, 2, 128, [5 * 128], tile_n=128, grid=5, host_only=True)
+    p = la.Plan(1, 2, 2, 128, [5 * 128], tile_n=128, grid=5, host_only=True, schedule="streamk")
     rows = p.export()
     golden = [tuple(int(x) for x in l.split()) for l in open(os.path.join(ROOT, "tests", "golden", "fig1_schedule.txt"))
               if l.strip() and not l.startswith("#")]
@@ -58,7 +58,8 @@ def test_exhaustive_small_bit_exact(la):
         for lens in itertools.product([1, 16, 17, 40, 64], repeat=batch):
             I = sum(-(-x // 16) for x in lens) * heads
             for G in sorted({1, 2, 3, I // 2 + 1, I, I + 2}):
-                p = la.Plan(batch, heads, heads, 64, list(lens), tile_n=16, grid=G, layout=layout, host_only=True)
+                p = la.Plan(batch, heads, heads, 64, list(lens), tile_n=16, grid=G, layout=layout, host_only=True,
+                            schedule="streamk")
                 got = p.export()
                 exp = _oracle_rows(batch, heads, list(lens), 16, G, layout)
                 assert np.array_equal(got, exp), (batch, heads, lens, G, layout)
@@ -77,7 +78,8 @@ def test_random_large_and_configs_bit_exact(la):
         layout = ["bhsd", "packed"][trial % 2]
         I = sum(-(-x // tile) for x in lens) * heads
         G = int(rng.integers(1, min(I, 600) + 1))
-        p = la.Plan(batch, heads, heads, 128, lens, tile_n=tile, grid=G, layout=layout, host_only=True)
+        p = la.Plan(batch, heads, heads, 128, lens, tile_n=tile, grid=G, layout=layout, host_only=True,
+                    schedule="streamk")
         assert np.array_equal(p.export(), _oracle_rows(batch, heads, lens, tile, G, layout))
     # BASELINE.json configs on a 148-SM B200 (1 CTA / SM)
     import synth
@@ -85,7 +87,7 @@ def test_random_large_and_configs_bit_exact(la):
     for name, I in expect_I.items():
         pr = synth.config(name)
         p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
-                    num_sms=148, ctas_per_sm=1, layout=pr.layout)
+                    num_sms=148, ctas_per_sm=1, layout=pr.layout, schedule="streamk")
         assert p.info.total_iters == I and p.info.grid == 148 and p.info.tile_n == 128
         rows = p.export()
         assert np.array_equal(rows, _oracle_rows(pr.batch, pr.heads_kv, pr.ctx_lens, 128, 148, pr.layout))
@@ -96,12 +98,12 @@ def test_random_large_and_configs_bit_exact(la):
     # c4 packed layout: heads -> total context
     pr = synth.config("c4", layout="packed")
     p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
-                layout="packed")
+                layout="packed", schedule="streamk")
     assert np.array_equal(p.export(), _oracle_rows(pr.batch, pr.heads_kv, pr.ctx_lens, 128, 148, "packed"))
 
 
 def test_auto_tile_and_sequential(la):
-    p = la.Plan(1, 32, 32, 128, [262144], host_only=True)
+    p = la.Plan(1, 32, 32, 128, [262144], host_only=True, schedule="streamk")
     assert p.info.tile_n == 128 and p.info.grid == 148           # P:396 for d=128
     p = la.Plan(1, 8, 8, 64, [1 << 16], host_only=True)
     assert p.info.tile_n == 256                                  # P:396 for d=64
@@ -124,3 +126,32 @@ def test_validation(la, args, status):
         la.Plan(kw["batch"], kw["heads_q"], kw["heads_kv"], kw["head_dim"], kw["lens"], tile_n=kw["tile_n"],
                 host_only=True)
     assert e.value.status == status
+
+
+def test_dynamic_schedule_bit_exact(la):
+    """LA_SCHED_DYNAMIC: Alg. 2's walk over the guided virtual-CTA ranges, bit-exact."""
+    rng = np.random.default_rng(1)
+    import synth
+    cases = [(synth.config(c), 148) for c in ("c2", "c3", "c4", "c5")]
+    for trial in range(25):
+        batch = int(rng.integers(1, 9))
+        heads = int(rng.integers(1, 17))
+        lens = [int(x) for x in rng.integers(1, 30000, size=batch)]
+        cases.append((synth.Problem(batch, heads, heads, 128, lens, layout=["bhsd", "packed"][trial % 2]),
+                      int(rng.integers(1, 200))))
+    for pr, sms in cases:
+        p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
+                    num_sms=sms, layout=pr.layout, schedule="dynamic")
+        units = unit_order(pr.batch, pr.heads_kv, pr.layout)
+        c_n = [-(-pr.ctx_lens[b] // 128) for (b, _h) in units]
+        I = sum(c_n)
+        G = min(sms, I)
+        begins = oracle.guided_ranges(I, G, 750, 2)
+        exp = np.array([s.row() for s in oracle.segments_from_ranges(c_n, begins)], dtype=np.int32).reshape(-1, 7)
+        assert np.array_equal(p.export(), exp)
+        assert p.info.num_vctas == len(begins) - 1 and p.info.grid == min(G, len(begins) - 1)
+        # partial slots: <= 1 non-host and <= 1 non-finishing-host segment per virtual CTA
+        rows = p.export()
+        assert np.bincount(rows[rows[:, 4] == 0][:, 0], minlength=p.info.num_vctas).max() <= 1
+        wait_hosts = rows[(rows[:, 4] == 1) & (rows[:, 5] == 0)]
+        assert np.bincount(wait_hosts[:, 0], minlength=p.info.num_vctas).max() <= 1
