@@ -184,6 +184,7 @@ struct MhaEngine {
   static constexpr int STAGE_BYTES = 2 * STAGE_TOK * ROWB;
   static constexpr int HEADS = 1;                           // q-heads per unit
   static constexpr int FOLD_FLOATS = NCW * (D + 2);         // per warp: O[D], m, l
+  static constexpr int FOLD_BUFS = 2;                       // double-buffered hand-off
   static constexpr bool ZERO_RING = true;                   // tail rows must be finite
   static_assert(LPK >= 2 && LPK <= 32 && (LPK & (LPK - 1)) == 0, "lanes per key");
   static_assert(STAGE_TOK % 32 == 0, "stage holds whole 32-key rounds");
@@ -331,6 +332,9 @@ struct Mma<__nv_bfloat16> {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
   }
+  __device__ __forceinline__ static float2 unpack(uint32_t w) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+  }
 };
 
 template <>
@@ -345,6 +349,9 @@ struct Mma<__half> {
   __device__ __forceinline__ static uint32_t pack(float lo, float hi) {
     __half2 v = __floats2half2_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
+  }
+  __device__ __forceinline__ static float2 unpack(uint32_t w) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
   }
 };
 
@@ -368,6 +375,7 @@ struct GqaEngine {
   static constexpr int HEADS = 8;                 // MMA N: q-heads per unit (padded to 8)
   static constexpr int KS = D / 16;               // k-steps of QK^T = m-tiles of PV
   static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
+  static constexpr int FOLD_BUFS = 1;             // 41 KB each: single-buffered to afford NST=5
   static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
   static_assert(STAGE_TOK == 32 * WPS, "one 32-token round per consumer warp per stage");
 
@@ -470,8 +478,15 @@ struct GqaEngine {
       const float p2 = ex2(sc[blk][2] - s.m[0]), p3 = ex2(sc[blk][3] - s.m[1]);
       s.l[0] += p0 + p2;
       s.l[1] += p1 + p3;
-      const uint32_t b0 = movmatrix_t(Mma<T>::pack(p0, p1));  // P[tok 2tq..][head gq]
-      const uint32_t b1 = movmatrix_t(Mma<T>::pack(p2, p3));
+      // P = P_hi + P_lo, both in the KV type (P_lo = round(p - P_hi), exact subtraction):
+      // two MMAs on the same V^T fragments keep P to ~2^-16 relative instead of the KV
+      // type's 2^-8 (reading C18; the tensor pipe is ~10% busy, so the extra MMA is free).
+      const uint32_t h01 = Mma<T>::pack(p0, p1), h23 = Mma<T>::pack(p2, p3);
+      const float2 r01 = Mma<T>::unpack(h01), r23 = Mma<T>::unpack(h23);
+      const uint32_t b0 = movmatrix_t(h01);  // P_hi[tok 2tq..][head gq]
+      const uint32_t b1 = movmatrix_t(h23);
+      const uint32_t c0 = movmatrix_t(Mma<T>::pack(p0 - r01.x, p1 - r01.y));  // P_lo
+      const uint32_t c1 = movmatrix_t(Mma<T>::pack(p2 - r23.x, p3 - r23.y));
       const int tok = rb + blk * 16 + ri + ((mi >> 1) << 3);
 #pragma unroll
       for (int mm = 0; mm < KS; ++mm) {
@@ -479,6 +494,7 @@ struct GqaEngine {
         uint32_t af[4];
         ldsm_x4_t(vbase + (chunk >> 3) * BOX_BYTES + tok * 128 + (((chunk & 7) ^ (tok & 7)) << 4), af);
         Mma<T>::run(s.o[mm], af, b0, b1);
+        Mma<T>::run(s.o[mm], af, c0, c1);
       }
     }
     if (rb + 32 > ntok) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> TMA WAR
@@ -531,7 +547,6 @@ struct GqaEngine {
 // =======================================================================================
 constexpr int kQD = 4;   // depth of the producer -> consumer virtual-CTA queue
 constexpr int kGS = 16;  // dynamic-mode fold tree: segments per first-level group
-constexpr int kFB = 2;   // consumer -> epilogue fold buffers (double buffering)
 
 struct SegInfo {
   int v, unit, host, finishing;
@@ -540,6 +555,7 @@ struct SegInfo {
 template <class E>
 struct Smem {
   static constexpr int RING = E::NST * E::STAGE_BYTES;
+  static constexpr int kFB = E::FOLD_BUFS;  // consumer -> epilogue fold buffers
   static constexpr int FOLD = kFB * E::FOLD_FLOATS * 4;
   static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB) * 8;
   static constexpr int MISC = kQD * 4 + kFB * int(sizeof(SegInfo));
@@ -558,6 +574,7 @@ template <class E>
 __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeArgs a, const __grid_constant__ TmapPair tm) {
   constexpr int NST = E::NST, WPS = E::WPS, NCW = E::NCW, D = E::D, H = E::HEADS, J = D / 32;
   constexpr int FOLD_FLOATS = E::FOLD_FLOATS;
+  constexpr int kFB = E::FOLD_BUFS;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* ring =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -989,10 +1006,10 @@ KernelInfo decode_kernel_info(int dtype, int head_dim, int group) {
     return KernelInfo{};
   }
   if (group > 8) return KernelInfo{};
-  if (dtype == LA_BF16 && head_dim == 128) return info_of<GqaEngine<__nv_bfloat16, 128, 4, 2>>(true);
-  if (dtype == LA_BF16 && head_dim == 64) return info_of<GqaEngine<__nv_bfloat16, 64, 4, 2>>(true);
-  if (dtype == LA_FP16 && head_dim == 128) return info_of<GqaEngine<__half, 128, 4, 2>>(true);
-  if (dtype == LA_FP16 && head_dim == 64) return info_of<GqaEngine<__half, 64, 4, 2>>(true);
+  if (dtype == LA_BF16 && head_dim == 128) return info_of<GqaEngine<__nv_bfloat16, 128, 5, 2>>(true);
+  if (dtype == LA_BF16 && head_dim == 64) return info_of<GqaEngine<__nv_bfloat16, 64, 5, 2>>(true);
+  if (dtype == LA_FP16 && head_dim == 128) return info_of<GqaEngine<__half, 128, 5, 2>>(true);
+  if (dtype == LA_FP16 && head_dim == 64) return info_of<GqaEngine<__half, 64, 5, 2>>(true);
   return KernelInfo{};
 }
 
