@@ -71,11 +71,16 @@ typedef enum {
   LA_SCHED_STREAMK = 0,    /* Eq. 2 + Alg. 2 exactly: G equal contiguous iteration ranges,
                               host CTAs wait on their peers' flags (cooperative launch)  */
   LA_SCHED_SEQUENTIAL = 1, /* FA2: one CTA per unit, G = #units            */
-  LA_SCHED_DYNAMIC = 2     /* Alg. 2's decomposition over more, guided-size "virtual CTAs"
+  LA_SCHED_DYNAMIC = 2,    /* Alg. 2's decomposition over more, guided-size "virtual CTAs"
                               that the persistent CTAs claim in order (atomic counter); a
-                              unit's partials are folded by its last-arriving segment in
-                              Alg. 2's order (host, then ascending peers) -- same result
-                              semantics, balances TIME instead of LeanTile counts */
+                              unit's partials are folded by a fixed tree of last arrivers in
+                              ascending order -- same result semantics, balances TIME instead
+                              of LeanTile counts                              */
+  LA_SCHED_FIXED_SPLIT = 3 /* FlashDecoding's fixed-split decomposition: every
+                              unit cut into `split` near-equal chunks (first chunks take the
+                              extra LeanTile), chunks run in order on the persistent
+                              CTAs like hardware waves, folded in-kernel (the comparison
+                              baseline of the paper's evaluation, NEXT-1)                 */
 } la_schedule;
 
 typedef struct {
@@ -93,6 +98,8 @@ typedef struct {
   int trace;         /* 1 -> every la_decode records a per-CTA timeline (la_plan_trace)     */
   int dyn_first_permille; /* LA_SCHED_DYNAMIC: share of I in the first G ranges (default 750) */
   int dyn_min_chunk;      /* LA_SCHED_DYNAMIC: smallest virtual CTA in LeanTiles (default 2)  */
+  int split;              /* LA_SCHED_FIXED_SPLIT: chunks per unit; 0 -> FlashAttention-2's
+                             num_splits heuristic (wave efficiency >= 85% of the best)     */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;
@@ -111,6 +118,7 @@ typedef struct {
   int64_t kv_bytes;        /* algorithmic K+V bytes one la_decode reads                   */
   float scale;
   int64_t num_vctas;       /* Alg. 2's G: iteration ranges (= grid for static schedules)  */
+  int split;               /* LA_SCHED_FIXED_SPLIT: chunks per unit (0 otherwise)         */
 } la_plan_info;
 
 /* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */

@@ -23,6 +23,7 @@ Two independent constructions are provided and tested against each other:
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 from typing import List, Sequence, Tuple
 
@@ -155,6 +156,38 @@ def guided_ranges(total_iters: int, grid: int, first_permille: int = 750, min_ch
             pos = min(total_iters, pos + c)
             begins.append(pos)
     return begins
+
+
+def fixed_split_ranges(c_n: Sequence[int], split: int) -> List[int]:
+    """Range boundaries of FlashDecoding's fixed split: unit u cut into
+    s = min(split, C_n(u)) chunks, the first C_n mod s of them one LeanTile longer."""
+    begins = [0]
+    pos = 0
+    for c in c_n:
+        s = max(1, min(split, c))
+        q, r = divmod(c, s)
+        for j in range(s):
+            pos += q + (1 if j < r else 0)
+            begins.append(pos)
+    return begins
+
+
+def fa2_num_splits(units: int, max_cn: int, sms: int) -> int:
+    """FlashAttention-2's split heuristic used by FlashDecoding (the paper's FD baseline,
+    P:505): no split if the units fill 80% of the SMs, else the smallest s whose wave
+    efficiency units*s / (ceil(units*s/sms) * sms) reaches 85% of the best s <= 128."""
+    if units >= int(0.8 * sms):
+        return 1
+    max_s = min(128, sms, max_cn)
+    eff = {}
+    for s in range(1, max_s + 1):
+        waves = units * s / sms
+        eff[s] = waves / math.ceil(waves)
+    best = max(eff.values())
+    for s in range(1, max_s + 1):
+        if eff[s] >= 0.85 * best:
+            return s
+    return 1
 
 
 def owner_table(total_iters: int, grid: int) -> List[int]:

@@ -22,6 +22,7 @@ struct la_plan_s {
   int stage_tokens = 0;
   bool host_only = true;
   bool needs_wait = false;   // any non-finishing host -> cooperative launch required
+  int split = 0;             // LA_SCHED_FIXED_SPLIT: chunks per unit actually used
   int device = -1;
   // device state owned by the plan
   void* d_tables = nullptr;
@@ -129,8 +130,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (dtype != LA_BF16 && dtype != LA_FP16 && dtype != LA_FP32) return fail(LA_ERR_INVALID, "bad dtype");
   if (opts.layout != LA_KV_BHSD && opts.layout != LA_KV_PACKED) return fail(LA_ERR_INVALID, "bad layout");
   if (opts.schedule != LA_SCHED_STREAMK && opts.schedule != LA_SCHED_SEQUENTIAL &&
-      opts.schedule != LA_SCHED_DYNAMIC)
+      opts.schedule != LA_SCHED_DYNAMIC && opts.schedule != LA_SCHED_FIXED_SPLIT)
     return fail(LA_ERR_INVALID, "bad schedule");
+  if (opts.split < 0) return fail(LA_ERR_INVALID, "split must be >= 0");
   if (opts.dyn_first_permille < 0 || opts.dyn_first_permille > 1000 || opts.dyn_min_chunk < 1)
     return fail(LA_ERR_INVALID, "dyn_first_permille must be in [0, 1000] and dyn_min_chunk >= 1");
   if (tile_n != 0 && tile_n != 16 && tile_n != 32 && tile_n != 64 && tile_n != 128 && tile_n != 256 &&
@@ -206,13 +208,19 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
     G = std::max(1, std::min(G, max_ctas));
     la::guided_ranges(s.total_iters, G, opts.dyn_first_permille, opts.dyn_min_chunk, s.cta_begin);
+  } else if (p.schedule == LA_SCHED_FIXED_SPLIT) {
+    int64_t max_cn = 1;
+    for (const DevUnit& u : s.units) max_cn = std::max<int64_t>(max_cn, u.iter_end - u.iter_begin);
+    plan->split = opts.split ? opts.split : la::fa2_num_splits(int64_t(s.units.size()), max_cn, max_ctas);
+    la::fixed_split_ranges(s.units, plan->split, s.cta_begin);
   } else {
     int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
     if (!plan->host_only) G = std::min(G, max_ctas);  // hosts wait on peers: co-residency
     la::streamk_ranges(s.total_iters, std::max(1, G), s.cta_begin);
   }
   la::finish_schedule(s);
-  if (p.schedule == LA_SCHED_DYNAMIC) {
+  if (p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT) {
+    // persistent CTAs claim the ranges in order (hardware-wave order for fixed split)
     int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
     s.phys_grid = std::max(1, std::min({G, max_ctas, s.grid}));
   } else {
@@ -290,6 +298,7 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   info->stage_tokens = plan->stage_tokens;
   info->grid = s.phys_grid;
   info->num_vctas = s.grid;
+  info->split = plan->split;
   info->num_units = int(s.units.size());
   info->total_iters = s.total_iters;
   info->num_segments = s.num_segments;
@@ -341,7 +350,7 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.counters = plan->d_counters;
   a.unit_count = plan->d_unit_count;
   a.grp_count = plan->d_unit_count + plan->sched.units.size();
-  a.dynamic = plan->prob.schedule == LA_SCHED_DYNAMIC ? 1 : 0;
+  a.dynamic = (plan->prob.schedule == LA_SCHED_DYNAMIC || plan->prob.schedule == LA_SCHED_FIXED_SPLIT) ? 1 : 0;
   a.num_v = plan->sched.grid;
   a.grid = plan->sched.phys_grid;
   a.tile_n = plan->sched.tile_n;

@@ -57,6 +57,12 @@ void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& 
 // covering half of what remains (>= min_chunk), until I is covered.
 void guided_ranges(int64_t total_iters, int grid, int first_permille, int min_chunk,
                    std::vector<int32_t>& cta_begin);
+// FlashDecoding's fixed split: unit u cut into min(split, C_n(u)) chunks, the
+// first (C_n mod s) one LeanTile longer; ranges in unit order.
+void fixed_split_ranges(const std::vector<DevUnit>& units, int split, std::vector<int32_t>& cta_begin);
+// FlashAttention-2's split heuristic: 1 if units fill 80% of the SMs, else the smallest s
+// whose wave efficiency units*s / (ceil(units*s/sms)*sms) is >= 85% of the best s <= 128.
+int fa2_num_splits(int64_t units, int64_t max_cn, int sms);
 // host_cta / last_cta per unit, first unit per CTA, segment & partial counts.
 void finish_schedule(Schedule& s);
 // Segment rows (7 int32 each, SPEC S:275 order) by the Alg2§10-18,§41 walk.

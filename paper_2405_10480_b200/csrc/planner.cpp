@@ -10,6 +10,7 @@
 // Integer work only; tests check it bit-exactly against the oracle's independent
 // enumeration (tests/test_planner.py).
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
@@ -85,6 +86,35 @@ void guided_ranges(int64_t total_iters, int grid, int first_permille, int min_ch
       cta_begin.push_back(int32_t(pos));
     }
   }
+}
+
+void fixed_split_ranges(const std::vector<DevUnit>& units, int split, std::vector<int32_t>& cta_begin) {
+  cta_begin.assign(1, 0);
+  for (const DevUnit& u : units) {
+    const int32_t cn = u.iter_end - u.iter_begin;
+    const int32_t s = std::max(1, std::min<int32_t>(split, cn));
+    const int32_t q = cn / s, r = cn % s;
+    int32_t pos = u.iter_begin;
+    for (int32_t j = 0; j < s; ++j) {
+      pos += q + (j < r ? 1 : 0);
+      cta_begin.push_back(pos);
+    }
+  }
+}
+
+int fa2_num_splits(int64_t units, int64_t max_cn, int sms) {
+  if (units >= int64_t(0.8 * sms)) return 1;
+  const int64_t max_s = std::min<int64_t>({128, int64_t(sms), max_cn});
+  double best = 0.0;
+  std::vector<double> eff(size_t(max_s) + 1, 0.0);
+  for (int64_t s = 1; s <= max_s; ++s) {
+    const double waves = double(units * s) / sms;
+    eff[s] = waves / std::ceil(waves);
+    best = std::max(best, eff[s]);
+  }
+  for (int64_t s = 1; s <= max_s; ++s)
+    if (eff[s] >= 0.85 * best) return int(s);
+  return 1;
 }
 
 static int owner_of(const std::vector<int32_t>& cta_begin, int64_t it) {

@@ -23,11 +23,12 @@ LIB_PATH = os.path.join(_HERE, "lib", "libleanattn.so")
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE = range(6)
 LA_BF16, LA_FP16, LA_FP32 = 0, 1, 2
 LA_KV_BHSD, LA_KV_PACKED = 0, 1
-LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC = 0, 1, 2
+LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC, LA_SCHED_FIXED_SPLIT = 0, 1, 2, 3
 
 _DTYPE_CODES = {"bf16": LA_BF16, "fp16": LA_FP16, "fp32": LA_FP32}
 _LAYOUT_CODES = {"bhsd": LA_KV_BHSD, "packed": LA_KV_PACKED}
-_SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, "dynamic": LA_SCHED_DYNAMIC}
+_SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, "dynamic": LA_SCHED_DYNAMIC,
+                "fixed_split": LA_SCHED_FIXED_SPLIT}
 
 # Every symbol include/la.h declares (tests check the library exports all of them).
 EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
@@ -45,7 +46,7 @@ class la_plan_opts(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_float), ("layout", ctypes.c_int), ("max_ctx", ctypes.c_int64),
                 ("grid", ctypes.c_int), ("num_sms", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
                 ("host_only", ctypes.c_int), ("schedule", ctypes.c_int), ("trace", ctypes.c_int),
-                ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int)]
+                ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int), ("split", ctypes.c_int)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -54,7 +55,7 @@ class la_plan_info(ctypes.Structure):
                                             "num_units")] + \
                [(n, ctypes.c_int64) for n in ("total_iters", "num_segments", "num_partials",
                                               "workspace_bytes", "kv_bytes")] + \
-               [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64)]
+               [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64), ("split", ctypes.c_int)]
 
 
 _lib = None
@@ -121,7 +122,7 @@ class Plan:
                  tile_n: int = 0, dtype: str = "bf16", scale: float = 0.0, layout: str = "bhsd",
                  max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
                  ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
-                 dyn_first_permille: int = 750, dyn_min_chunk: int = 2):
+                 dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -136,6 +137,7 @@ class Plan:
         opts.trace = 1 if trace else 0
         opts.dyn_first_permille = int(dyn_first_permille)
         opts.dyn_min_chunk = int(dyn_min_chunk)
+        opts.split = int(split)
         lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
         h = ctypes.c_void_p()
         self._h = None

@@ -55,7 +55,7 @@ def test_forced_grid_and_tile_invariance_and_determinism():
     O_ref, L_ref = run_oracle(p)
     inputs = cuda_inputs(p)
     outs = []
-    for schedule in SCHEDULES + ("sequential",):
+    for schedule in SCHEDULES + ("sequential", "fixed_split"):
         for grid in (1, 2, 3, 5, 16, 37, 148, 0):
             for tile_n in (16, 64, 256):
                 O, L, _ = run_cuda(p, inputs=inputs, grid=grid, tile_n=tile_n, schedule=schedule)

@@ -231,3 +231,17 @@ def test_alg2_with_virtual_ctas_equals_eq1():
         begins = oracle.guided_ranges(sum(c_n), G)
         O, L = oracle.lean_attention(q, k, v, lens, 0.35, 16, G, begins=begins)
         assert np.max(np.abs(O - O_ref)) <= 1e-12 and np.max(np.abs(L - L_ref)) <= 1e-12
+
+
+def test_fixed_split_ranges_match_fixed_split_segments():
+    # the range form of FD's split == the chunk list of fixed_split_segments
+    for c_n, s in [([5, 5], 2), ([7, 3, 9], 3), ([1, 2, 3], 4), ([16] * 5, 4)]:
+        begins = oracle.fixed_split_ranges(c_n, s)
+        segs = oracle.segments_from_ranges(c_n, begins)
+        ref = oracle.fixed_split_segments(c_n, 10 ** 6, s)
+        assert [(x.unit, x.begin, x.end, x.host, x.finishing) for x in segs] == \
+               [(x.unit, x.begin, x.end, x.host, x.finishing) for x in ref]
+    # heuristic: efficiency-maximising split, no split once units fill 80% of the SMs
+    assert oracle.fa2_num_splits(1, 10 ** 6, 108) == 108 or oracle.fa2_num_splits(1, 10 ** 6, 108) >= 92
+    assert oracle.fa2_num_splits(200, 64, 148) == 1
+    assert oracle.fa2_num_splits(56, 2, 108) == 1 or oracle.fa2_num_splits(56, 2, 108) == 2

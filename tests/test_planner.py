@@ -155,3 +155,30 @@ def test_dynamic_schedule_bit_exact(la):
         assert np.bincount(rows[rows[:, 4] == 0][:, 0], minlength=p.info.num_vctas).max() <= 1
         wait_hosts = rows[(rows[:, 4] == 1) & (rows[:, 5] == 0)]
         assert np.bincount(wait_hosts[:, 0], minlength=p.info.num_vctas).max() <= 1
+
+
+def test_fixed_split_schedule_bit_exact(la):
+    """LA_SCHED_FIXED_SPLIT (NEXT-1, FlashDecoding's decomposition): chunk ranges and the
+    FA2 split heuristic, bit-exact against the oracle."""
+    import synth
+    rng = np.random.default_rng(2)
+    cases = [(synth.Problem(1, 56, 56, 64, [262144]), 0), (synth.Problem(4, 32, 32, 128, [262144] * 4), 0),
+             (synth.config("c2"), 0), (synth.config("c4"), 3)]
+    for trial in range(20):
+        batch = int(rng.integers(1, 9))
+        heads = int(rng.integers(1, 17))
+        lens = [int(x) for x in rng.integers(1, 30000, size=batch)]
+        cases.append((synth.Problem(batch, heads, heads, 128, lens), int(rng.integers(0, 9))))
+    for pr, split in cases:
+        p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
+                    num_sms=148, layout=pr.layout, schedule="fixed_split", split=split)
+        units = unit_order(pr.batch, pr.heads_kv, pr.layout)
+        c_n = [-(-pr.ctx_lens[b] // 128) for (b, _h) in units]
+        s = split or oracle.fa2_num_splits(len(c_n), max(c_n), 148)
+        assert p.info.split == s
+        begins = oracle.fixed_split_ranges(c_n, s)
+        exp = np.array([x.row() for x in oracle.segments_from_ranges(c_n, begins)], dtype=np.int32).reshape(-1, 7)
+        assert np.array_equal(p.export(), exp)
+    # the paper's motivating shapes (P:191, P:622): 56 heads x batch 1 -> FD splits; batch 4 x
+    # 32 heads fills 80% of 148 SMs -> no split at all (one partial wave)
+    assert oracle.fa2_num_splits(56, 2048, 148) > 1 and oracle.fa2_num_splits(128, 2048, 148) == 1
