@@ -122,6 +122,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def read_probe_gbs():
+    """Measured pure streaming-read ceiling (scripts/read_probe.cu, profiles/read_probe.json):
+    context for the roofline, not the contract's denominator."""
+    path = os.path.join(ROOT, "profiles", "read_probe.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return max(r["GBps"] for r in d["results"] if r["probe"] == "tma_bulk_ring")
+
+
 def ncu_traffic(config: str):
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(path):
@@ -371,7 +382,9 @@ def bench_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": ("la_decode_gqa<bf16,128>" if p.group > 1 else "la_decode_mha<bf16,128>"), "kernel_us": kern_ms * 1e3,
-                         "algorithmic_bytes_per_launch": local_kv},
+                         "algorithmic_bytes_per_launch": local_kv,
+                         "read_probe_gbs": read_probe_gbs(),
+                         "frac_of_read_probe": (achieved / read_probe_gbs()) if read_probe_gbs() else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -48,6 +48,26 @@
 #include "la_internal.h"
 #include "ptx.cuh"
 
+// Ring / warp configuration (build-time; the defaults are the measured best on B200).
+#ifndef LA_MHA_NST
+#define LA_MHA_NST 5  // MHA ring stages of 32 KiB
+#endif
+#ifndef LA_MHA_WPS
+#define LA_MHA_WPS 2  // MHA consumer warps per ring slot
+#endif
+#ifndef LA_GQA_NST
+#define LA_GQA_NST 4
+#endif
+#ifndef LA_GQA_WPS
+#define LA_GQA_WPS 2
+#endif
+#ifndef LA_GQA_FB
+#define LA_GQA_FB 2   // GQA consumer -> epilogue fold buffers (33 KB each at NCW = 8)
+#endif
+#ifndef LA_GQA_SPLITP
+#define LA_GQA_SPLITP 1  // P = P_hi + P_lo on the tensor cores (0: single KV-type P)
+#endif
+
 namespace la {
 
 struct alignas(64) TmapPair {
@@ -375,9 +395,8 @@ struct GqaEngine {
   static constexpr int HEADS = 8;                 // MMA N: q-heads per unit (padded to 8)
   static constexpr int KS = D / 16;               // k-steps of QK^T = m-tiles of PV
   static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
-  static constexpr int FOLD_BUFS = 1;             // 41 KB each: single-buffered to afford NST=5
+  static constexpr int FOLD_BUFS = LA_GQA_FB;     // double-buffered hand-off (measured best)
   static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
-  static_assert(STAGE_TOK == 32 * WPS, "one 32-token round per consumer warp per stage");
 
   struct State {
     uint32_t qb[KS][2];     // Q^T B-fragments (exact inputs)
@@ -410,11 +429,15 @@ struct GqaEngine {
     for (int mm = 0; mm < KS; ++mm) s.o[mm][0] = s.o[mm][1] = s.o[mm][2] = s.o[mm][3] = 0.f;
   }
 
+  // This warp's 32-token rounds (sub, sub + WPS, ...) of one stage of ntok tokens.
   __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, float scale_log2,
                                                int lane) {
+    for (int rb = sub * 32; rb < ntok; rb += 32 * WPS) round(s, st, rb, ntok, scale_log2, lane);
+  }
+
+  __device__ __forceinline__ static void round(State& s, unsigned char* st, int rb, int ntok, float scale_log2,
+                                               int lane) {
     const int gq = lane >> 2, mi = lane >> 3, ri = lane & 7;
-    const int rb = sub * 32;
-    if (rb >= ntok) return;
     if (rb + 32 > ntok) {
       // rows >= ntok of this round hold the next unit's rows or cache padding: zero this
       // warp's V rows so 0 * (non-finite) can never reach the accumulator
@@ -494,7 +517,7 @@ struct GqaEngine {
         uint32_t af[4];
         ldsm_x4_t(vbase + (chunk >> 3) * BOX_BYTES + tok * 128 + (((chunk & 7) ^ (tok & 7)) << 4), af);
         Mma<T>::run(s.o[mm], af, b0, b1);
-        Mma<T>::run(s.o[mm], af, c0, c1);
+        if (LA_GQA_SPLITP) Mma<T>::run(s.o[mm], af, c0, c1);
       }
     }
     if (rb + 32 > ntok) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> TMA WAR
@@ -997,19 +1020,19 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
 
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group) {
   if (group == 1) {
-    if (dtype == LA_BF16 && head_dim == 128) return info_of<MhaEngine<__nv_bfloat16, 128, 5, 2>>(false);
-    if (dtype == LA_BF16 && head_dim == 64) return info_of<MhaEngine<__nv_bfloat16, 64, 5, 2>>(false);
-    if (dtype == LA_FP16 && head_dim == 128) return info_of<MhaEngine<__half, 128, 5, 2>>(false);
-    if (dtype == LA_FP16 && head_dim == 64) return info_of<MhaEngine<__half, 64, 5, 2>>(false);
-    if (dtype == LA_FP32 && head_dim == 128) return info_of<MhaEngine<float, 128, 5, 2>>(false);
-    if (dtype == LA_FP32 && head_dim == 64) return info_of<MhaEngine<float, 64, 5, 2>>(false);
+    if (dtype == LA_BF16 && head_dim == 128) return info_of<MhaEngine<__nv_bfloat16, 128, LA_MHA_NST, LA_MHA_WPS>>(false);
+    if (dtype == LA_BF16 && head_dim == 64) return info_of<MhaEngine<__nv_bfloat16, 64, LA_MHA_NST, LA_MHA_WPS>>(false);
+    if (dtype == LA_FP16 && head_dim == 128) return info_of<MhaEngine<__half, 128, LA_MHA_NST, LA_MHA_WPS>>(false);
+    if (dtype == LA_FP16 && head_dim == 64) return info_of<MhaEngine<__half, 64, LA_MHA_NST, LA_MHA_WPS>>(false);
+    if (dtype == LA_FP32 && head_dim == 128) return info_of<MhaEngine<float, 128, LA_MHA_NST, LA_MHA_WPS>>(false);
+    if (dtype == LA_FP32 && head_dim == 64) return info_of<MhaEngine<float, 64, LA_MHA_NST, LA_MHA_WPS>>(false);
     return KernelInfo{};
   }
   if (group > 8) return KernelInfo{};
-  if (dtype == LA_BF16 && head_dim == 128) return info_of<GqaEngine<__nv_bfloat16, 128, 5, 2>>(true);
-  if (dtype == LA_BF16 && head_dim == 64) return info_of<GqaEngine<__nv_bfloat16, 64, 5, 2>>(true);
-  if (dtype == LA_FP16 && head_dim == 128) return info_of<GqaEngine<__half, 128, 5, 2>>(true);
-  if (dtype == LA_FP16 && head_dim == 64) return info_of<GqaEngine<__half, 64, 5, 2>>(true);
+  if (dtype == LA_BF16 && head_dim == 128) return info_of<GqaEngine<__nv_bfloat16, 128, LA_GQA_NST, LA_GQA_WPS>>(true);
+  if (dtype == LA_BF16 && head_dim == 64) return info_of<GqaEngine<__nv_bfloat16, 64, LA_GQA_NST, LA_GQA_WPS>>(true);
+  if (dtype == LA_FP16 && head_dim == 128) return info_of<GqaEngine<__half, 128, LA_GQA_NST, LA_GQA_WPS>>(true);
+  if (dtype == LA_FP16 && head_dim == 64) return info_of<GqaEngine<__half, 64, LA_GQA_NST, LA_GQA_WPS>>(true);
   return KernelInfo{};
 }
 

@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libleanattn.so")
+LIB_PATH = os.environ.get("LEANATTN_LIB") or os.path.join(_HERE, "lib", "libleanattn.so")  # env: variant sweeps
 
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE = range(6)
 LA_BF16, LA_FP16, LA_FP32 = 0, 1, 2
