@@ -52,7 +52,9 @@ def parse():
     ap.add_argument("--cpu-heads", type=int, default=32, help="heads in the oracle cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential"])
+    ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential", "fixed_split"])
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo only to test the multi-rank path on one GPU)")
     ap.add_argument("--dyn-first", type=int, default=750, help="dynamic schedule: permille in the first round")
     ap.add_argument("--dyn-min", type=int, default=2, help="dynamic schedule: smallest virtual CTA (LeanTiles)")
     return ap.parse_args()
@@ -239,11 +241,26 @@ def bench_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    local = local % torch.cuda.device_count()   # --backend gloo tests N ranks on fewer GPUs
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
+    from paper_2405_10480_b200 import sharded
+
+    def gather(o_part, l_part, o_all, l_all):
+        """The one exchange step of the sequence-sharded path (NCCL all-gather)."""
+        if args.backend == "nccl":
+            dist.all_gather_into_tensor(o_all, o_part)
+            dist.all_gather_into_tensor(l_all, l_part)
+        else:
+            oa, lb = sharded.gather_partials(o_part, l_part)
+            o_all.copy_(oa)
+            l_all.copy_(lb)
     cfg = args.config or ("c2" if world == 1 else "c5")
     p = synth.config(cfg)
     bounds = synth.shard_bounds(p, rank, world)
@@ -280,8 +297,7 @@ def bench_ours(args):
         if ev1 is not None:
             ev1.record(stream)
         if world > 1:   # sharded.sequence_sharded_decode with preallocated buffers
-            dist.all_gather_into_tensor(o_all, out.view(rows, p.head_dim))
-            dist.all_gather_into_tensor(l_all, lse.view(rows))
+            gather(out.view(rows, p.head_dim), lse.view(rows), o_all, l_all)
             la.la_combine(o_all, l_all, fin_o, fin_l, stream=stream)
 
     for _ in range(args.warmup):
@@ -337,8 +353,7 @@ def bench_ours(args):
             if world > 1:
                 o_dev = oh.to(dev, non_blocking=True).view(rows, p.head_dim)
                 l_dev = lh.to(dev, non_blocking=True).view(rows)
-                dist.all_gather_into_tensor(oh_all, o_dev)
-                dist.all_gather_into_tensor(lh_all, l_dev)
+                gather(o_dev, l_dev, oh_all, lh_all)
                 fo, fl = la.la_combine(oh_all, lh_all, stream=stream)
                 fo.cpu()
         e1.record(stream)
@@ -378,7 +393,8 @@ def bench_ours(args):
                        "stage_tokens": info.stage_tokens, "schedule": args.schedule,
                        "virtual_ctas": info.num_vctas,
                        "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),
-                       "parallelism": "single GPU" if world == 1 else f"sequence-sharded x{world} + NCCL all-gather + la_combine"},
+                       "parallelism": "single GPU" if world == 1 else
+                       f"sequence-sharded x{world} + {args.backend.upper()} all-gather + la_combine"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": ("la_decode_gqa<bf16,128>" if p.group > 1 else "la_decode_mha<bf16,128>"), "kernel_us": kern_ms * 1e3,
