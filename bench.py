@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential", "fixed_split"])
+    ap.add_argument("--page-size", type=int, default=0, help="run the config in a paged KV pool (16..256)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only to test the multi-rank path on one GPU)")
     ap.add_argument("--dyn-first", type=int, default=750, help="dynamic schedule: permille in the first round")
@@ -263,14 +264,22 @@ def bench_ours(args):
             l_all.copy_(lb)
     cfg = args.config or ("c2" if world == 1 else "c5")
     p = synth.config(cfg)
+    paged_kw = {}
+    if args.page_size:  # the same workload in a paged pool (NEXT-4); single GPU only
+        if world > 1:
+            raise SystemExit("--page-size is a single-GPU option")
+        p = synth.config(cfg, layout="paged", page_size=args.page_size)
+        bt, num_pages = synth.paged_meta(p)
+        paged_kw = dict(block_table=bt, page_size=args.page_size, num_pages=num_pages)
     bounds = synth.shard_bounds(p, rank, world)
     lens = [b - a for a, b in bounds]
 
     q = synth.gen_q(p, dev)
-    k = synth.fill_kv_cache(p, "k", dev, token_range=bounds)
-    v = synth.fill_kv_cache(p, "v", dev, token_range=bounds)
+    k = synth.fill_kv_cache(p, "k", dev, token_range=None if args.page_size else bounds)
+    v = synth.fill_kv_cache(p, "v", dev, token_range=None if args.page_size else bounds)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
-                   schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min)
+                   schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min,
+                   **paged_kw)
     info = plan.info
     total_kv = p.kv_bytes                       # whole job
     local_kv = info.kv_bytes
@@ -391,6 +400,7 @@ def bench_ours(args):
                        "context": p.ctx_lens[0] if len(set(p.ctx_lens)) == 1 else p.ctx_lens,
                        "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
                        "stage_tokens": info.stage_tokens, "schedule": args.schedule,
+                       "kv_layout": p.layout + (f" (page {args.page_size})" if args.page_size else ""),
                        "virtual_ctas": info.num_vctas,
                        "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),
                        "parallelism": "single GPU" if world == 1 else

@@ -62,7 +62,11 @@ typedef enum {
   /* The paper's unpadded ragged layout (H_kv, sum_b n_b, d), request b on rows
      cu_seqlens[b] .. cu_seqlens[b+1] (cu_seqlens = prefix sum of ctx_lens, built by the
      planner).  Units linearised heads -> total context. */
-  LA_KV_PACKED = 1
+  LA_KV_PACKED = 1,
+  /* Paged pools (num_pages, H_kv, page_size, d) (NEXT-4, serving layout): token t of request
+     b lives in page block_table[b][t / page_size] at row t % page_size.  block_table and
+     page_size come with the plan (opts); units linearised batch -> heads. */
+  LA_KV_PAGED = 2
 } la_layout;
 
 /* Work decomposition.  STREAMK is the method; the other two are its
@@ -100,6 +104,12 @@ typedef struct {
   int dyn_min_chunk;      /* LA_SCHED_DYNAMIC: smallest virtual CTA in LeanTiles (default 2)  */
   int split;              /* LA_SCHED_FIXED_SPLIT: chunks per unit; 0 -> FlashAttention-2's
                              num_splits heuristic (wave efficiency >= 85% of the best)     */
+  /* LA_KV_PAGED only: */
+  const int32_t* block_table; /* HOST [batch][pages_per_seq] physical page indices; copied
+                                 into the plan (re-plan when it changes)                   */
+  int pages_per_seq;          /* row stride of block_table (>= ceil(max ctx / page_size))   */
+  int page_size;              /* tokens per page: 16, 32, 64, 128 or 256                    */
+  int64_t num_pages;          /* pages in each pool; every table entry must be < num_pages  */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;

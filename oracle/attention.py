@@ -48,18 +48,26 @@ def decode_attention_unit(q_rows: np.ndarray, k: np.ndarray, v: np.ndarray, scal
     return O, L
 
 
+def paged_rows(pool: np.ndarray, block_table_row, h: int, n: int, page_size: int) -> np.ndarray:
+    """The n context rows of KV head h of one request in a paged pool (num_pages, H_kv,
+    page_size, d): token t is row t % page_size of page block_table_row[t // page_size]."""
+    pages = [pool[int(block_table_row[i]), h] for i in range(-(-n // page_size))]
+    return np.concatenate(pages, axis=0)[:n]
+
+
 def decode_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, ctx_lens, scale: float,
-                     layout: str = "bhsd"):
+                     layout: str = "bhsd", block_table=None, page_size: int = 0):
     """Batched decode attention.
 
     q: (B, H_q, d).  k, v: ``bhsd`` (B, H_kv, max_ctx, d) with request b valid for rows
     [0, ctx_lens[b]); or ``packed`` (H_kv, sum n_b, d), the paper's ragged layout
-    with request b at rows cu_seqlens[b] .. cu_seqlens[b+1].
+    with request b at rows cu_seqlens[b] .. cu_seqlens[b+1]; or ``paged`` pools
+    (num_pages, H_kv, page_size, d) addressed through ``block_table`` [B][pages].
     Returns O (B, H_q, d) and L (B, H_q), fp64.
     """
     q = np.asarray(q, dtype=np.float64)
     B, Hq, d = q.shape
-    Hkv = k.shape[1] if layout == "bhsd" else k.shape[0]
+    Hkv = k.shape[0] if layout == "packed" else k.shape[1]
     if Hq % Hkv:
         raise ValueError("heads_q must be a multiple of heads_kv (reading C3)")
     g = Hq // Hkv
@@ -73,6 +81,9 @@ def decode_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, ctx_lens, scal
                 kk, vv = k[b, h, :n], v[b, h, :n]
             elif layout == "packed":
                 kk, vv = k[h, cu[b]:cu[b + 1]], v[h, cu[b]:cu[b + 1]]
+            elif layout == "paged":
+                kk = paged_rows(k, block_table[b], h, n, page_size)
+                vv = paged_rows(v, block_table[b], h, n, page_size)
             else:
                 raise ValueError(layout)
             o, l = decode_attention_unit(q[b, h * g:(h + 1) * g], kk, vv, scale)

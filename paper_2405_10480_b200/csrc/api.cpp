@@ -23,6 +23,8 @@ struct la_plan_s {
   bool host_only = true;
   bool needs_wait = false;   // any non-finishing host -> cooperative launch required
   int split = 0;             // LA_SCHED_FIXED_SPLIT: chunks per unit actually used
+  int pt_stride = 0;         // LA_KV_PAGED: padded block-table row stride
+  int32_t* d_block_table = nullptr;
   int device = -1;
   // device state owned by the plan
   void* d_tables = nullptr;
@@ -128,7 +130,8 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (!ctx_lens) return fail(LA_ERR_INVALID, "ctx_lens is NULL");
   if (head_dim != 64 && head_dim != 128) return fail(LA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   if (dtype != LA_BF16 && dtype != LA_FP16 && dtype != LA_FP32) return fail(LA_ERR_INVALID, "bad dtype");
-  if (opts.layout != LA_KV_BHSD && opts.layout != LA_KV_PACKED) return fail(LA_ERR_INVALID, "bad layout");
+  if (opts.layout != LA_KV_BHSD && opts.layout != LA_KV_PACKED && opts.layout != LA_KV_PAGED)
+    return fail(LA_ERR_INVALID, "bad layout");
   if (opts.schedule != LA_SCHED_STREAMK && opts.schedule != LA_SCHED_SEQUENTIAL &&
       opts.schedule != LA_SCHED_DYNAMIC && opts.schedule != LA_SCHED_FIXED_SPLIT)
     return fail(LA_ERR_INVALID, "bad schedule");
@@ -160,6 +163,24 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (p.layout == LA_KV_BHSD && p.max_ctx < maxn) return fail(LA_ERR_INVALID, "max_ctx < max(ctx_lens)");
   p.scale = opts.scale != 0.f ? opts.scale : float(1.0 / std::sqrt(double(head_dim)));
   if (!(p.scale > 0.f) || !std::isfinite(p.scale)) return fail(LA_ERR_INVALID, "scale must be finite and > 0");
+  if (p.layout == LA_KV_PAGED) {
+    const int ps = opts.page_size;
+    if (ps != 16 && ps != 32 && ps != 64 && ps != 128 && ps != 256)
+      return fail(LA_ERR_INVALID, "page_size must be 16, 32, 64, 128 or 256");
+    if (!opts.block_table) return fail(LA_ERR_INVALID, "paged layout needs a block_table");
+    if (opts.num_pages < 1) return fail(LA_ERR_INVALID, "num_pages must be >= 1");
+    if (int64_t(opts.pages_per_seq) * ps < maxn)
+      return fail(LA_ERR_INVALID, "pages_per_seq * page_size < max(ctx_lens)");
+    p.page_size = ps;
+    p.pages_per_seq = opts.pages_per_seq;
+    p.num_pages = opts.num_pages;
+    p.block_table.assign(opts.block_table, opts.block_table + size_t(batch) * opts.pages_per_seq);
+    for (int b = 0; b < batch; ++b)
+      for (int i = 0; i < (p.ctx_lens[b] + ps - 1) / ps; ++i) {
+        const int32_t pg = p.block_table[size_t(b) * opts.pages_per_seq + i];
+        if (pg < 0 || pg >= opts.num_pages) return fail(LA_ERR_INVALID, "block_table entry out of range");
+      }
+  }
 
   auto* plan = new (std::nothrow) la_plan_s();
   if (!plan) return fail(LA_ERR_NOMEM, "host allocation failed");
@@ -247,7 +268,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
     const size_t b_cnt = align((2 + U + size_t(G)) * sizeof(int));
     const size_t b_trace = opts.trace ? align(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
-    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace;
+    plan->pt_stride = p.layout == LA_KV_PAGED ? (p.pages_per_seq + 31) / 32 * 32 : 0;
+    const size_t b_pt = align(size_t(p.batch) * plan->pt_stride * sizeof(int32_t));
+    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace + b_pt;
     cudaError_t e = cudaMalloc(&plan->d_tables, bytes);
     if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaMalloc(plan tables)"); }
     char* base = static_cast<char*>(plan->d_tables);
@@ -271,6 +294,15 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     if (e == cudaSuccess) e = cudaMemset(plan->d_flags, 0, G * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(plan->d_counters, 0, b_cnt);
     if (e == cudaSuccess && plan->d_trace) e = cudaMemset(plan->d_trace, 0, b_trace);
+    if (e == cudaSuccess && b_pt) {  // block table, rows padded to pt_stride (32-entry windows)
+      plan->d_block_table =
+          reinterpret_cast<int32_t*>(base + b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace);
+      std::vector<int32_t> padded(size_t(p.batch) * plan->pt_stride, 0);
+      for (int b = 0; b < p.batch; ++b)
+        std::copy(p.block_table.begin() + size_t(b) * p.pages_per_seq,
+                  p.block_table.begin() + size_t(b + 1) * p.pages_per_seq, padded.begin() + size_t(b) * plan->pt_stride);
+      e = cudaMemcpy(plan->d_block_table, padded.data(), padded.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
       release_device(plan);
       delete plan;
@@ -352,6 +384,13 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.grp_count = plan->d_unit_count + plan->sched.units.size();
   a.dynamic = (plan->prob.schedule == LA_SCHED_DYNAMIC || plan->prob.schedule == LA_SCHED_FIXED_SPLIT) ? 1 : 0;
   a.num_v = plan->sched.grid;
+  a.paged = plan->prob.layout == LA_KV_PAGED ? 1 : 0;
+  a.block_table = plan->d_block_table;
+  a.pt_stride = plan->pt_stride;
+  a.heads_kv = plan->prob.heads_kv;
+  a.page_shift = 0;
+  while (a.paged && (1 << a.page_shift) < plan->prob.page_size) ++a.page_shift;
+  a.box_rows = a.paged ? std::min(64, plan->prob.page_size) : 64;
   a.grid = plan->sched.phys_grid;
   a.tile_n = plan->sched.tile_n;
   a.stage_tokens = plan->stage_tokens;

@@ -192,6 +192,42 @@ struct Chunk<float> {
 };
 
 // =======================================================================================
+// Paged KV (LA_KV_PAGED): the producer's 32-entry window onto one request's block-table
+// row, refilled with 8 independent 16-byte loads (one L2 round trip per 32 pages).
+// =======================================================================================
+struct PageWin {
+  const int32_t* row;
+  int heads_kv, h, shift, base;
+  int32_t e[32];
+  __device__ __forceinline__ void init(const DecodeArgs& a, int64_t unit_bh) {
+    const int b = int(unit_bh / a.heads_kv);
+    h = int(unit_bh % a.heads_kv);
+    row = a.block_table + size_t(b) * a.pt_stride;
+    heads_kv = a.heads_kv;
+    shift = a.page_shift;
+    base = -1;
+  }
+  __device__ __forceinline__ int64_t row_of(int t) {  // pool row of the unit's token t
+    const int pi = t >> shift;
+    if (base < 0 || pi < base || pi >= base + 32) {
+      base = pi & ~31;
+      const int4* src = reinterpret_cast<const int4*>(row + base);
+      int4 w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = __ldg(src + k);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        e[4 * k] = w[k].x;
+        e[4 * k + 1] = w[k].y;
+        e[4 * k + 2] = w[k].z;
+        e[4 * k + 3] = w[k].w;
+      }
+    }
+    return (int64_t(e[pi - base]) * heads_kv + h) * (int64_t(1) << shift) + (t & ((1 << shift) - 1));
+  }
+};
+
+// =======================================================================================
 // MHA engine (T_m = 1): CUDA-core fp32 arithmetic
 // =======================================================================================
 template <typename T, int D_, int NST_, int WPS_>
@@ -224,8 +260,28 @@ struct MhaEngine {
     bulk_g2s(dst + STAGE_TOK * ROWB, static_cast<const unsigned char*>(a.v) + goff, bytes, bar, pol);
   }
 
+  // Paged KV: one bulk copy per page-contiguous run of the stage's tokens; lane r of the
+  // producer warp issues run r (a stage spans at most 5 pages).
+  __device__ __forceinline__ static void produce_paged(unsigned char* dst, const DecodeArgs& a, const TmapPair&,
+                                                       PageWin& pw, int s0, int ntok, uint64_t* bar, uint64_t pol,
+                                                       int lane) {
+    if (lane == 0) mbar_arrive_expect_tx(bar, 2 * uint32_t(ntok) * ROWB);
+    __syncwarp();
+    const int page = 1 << a.page_shift;
+    const int first = s0 & ~(page - 1);
+    const int t = lane == 0 ? s0 : first + lane * page;
+    if (t < s0 + ntok) {
+      const int run = min(first + (lane + 1) * page, s0 + ntok) - t;
+      const size_t goff = size_t(pw.row_of(t)) * ROWB;
+      const int doff = (t - s0) * ROWB;
+      bulk_g2s(dst + doff, static_cast<const unsigned char*>(a.k) + goff, uint32_t(run) * ROWB, bar, pol);
+      bulk_g2s(dst + STAGE_TOK * ROWB + doff, static_cast<const unsigned char*>(a.v) + goff, uint32_t(run) * ROWB,
+               bar, pol);
+    }
+  }
+
   __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
-    s.qf = Chunk<T>::load_q(static_cast<const T*>(a.q) + size_t(u.q_row) * D + (lane % LPK) * EPL);
+    s.qf =Chunk<T>::load_q(static_cast<const T*>(a.q) + size_t(u.q_row) * D + (lane % LPK) * EPL);
     s.m = -INFINITY;  // Alg1§8-9
     s.l = 0.f;
 #pragma unroll
@@ -411,6 +467,24 @@ struct GqaEngine {
     for (int b = 0; b < NBOX; ++b) {
       tma_load_2d(dst + b * BOX_BYTES, &tm.k, b * 64, int(row), bar, pol);
       tma_load_2d(dst + KV_BYTES + b * BOX_BYTES, &tm.v, b * 64, int(row), bar, pol);
+    }
+  }
+
+  // Paged KV: boxes of box_rows = min(64, page) rows, each inside one page; a box at an
+  // 8-row multiple keeps the 128-B swizzle phase of the 64-row stage layout.
+  // Lane r of the producer warp issues load r = (box i, column b, K or V).
+  __device__ __forceinline__ static void produce_paged(unsigned char* dst, const DecodeArgs& a, const TmapPair& tm,
+                                                       PageWin& pw, int s0, int ntok, uint64_t* bar, uint64_t pol,
+                                                       int lane) {
+    const int br = a.box_rows;
+    const int nb = (ntok + br - 1) / br;
+    if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * NBOX * 2));
+    __syncwarp();
+    for (int task = lane; task < nb * NBOX * 2; task += 32) {
+      const int i = task / (NBOX * 2), b = (task >> 1) % NBOX, is_v = task & 1;
+      const int row = int(pw.row_of(s0 + i * br));
+      tma_load_2d(dst + (is_v ? KV_BYTES : 0) + b * BOX_BYTES + i * br * 128, is_v ? &tm.v : &tm.k, b * 64, row,
+                  bar, pol);
     }
   }
 
@@ -644,54 +718,67 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 
   if (warp == NCW + 1) {
     // ================================ producer ==========================================
-    if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy();
-      if (a.uses_tmap) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.k)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.v)) : "memory");
-      }
-      int j = 0, k = 0;
-      for (bool first = true;; first = false) {
-        // Claim the next virtual CTA only once the previous one is fully issued: the ring
-        // (NST stages in flight) hides the atomic's latency, and claiming ahead would let a
-        // CTA hoard two of the big first-round ranges.
-        const int v = dynamic ? atomicAdd(&a.counters[0], 1) : (first ? g : NV);
+    // The whole warp walks; lane 0 owns the barriers, the claim and the queue, and issues
+    // the copies of contiguous stages.  For paged KV every lane issues one page run / TMA
+    // box of the stage, so small pages do not serialise on one thread.
+    const uint64_t pol = l2_evict_first_policy();
+    if (lane == 0 && a.uses_tmap) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.k)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.v)) : "memory");
+    }
+    int j = 0, k = 0;
+    for (bool first = true;; first = false) {
+      // Claim the next virtual CTA only once the previous one is fully issued: the ring
+      // (NST stages in flight) hides the atomic's latency, and claiming ahead would let a
+      // CTA hoard two of the big first-round ranges.
+      int v = 0;
+      if (lane == 0) {
+        v = dynamic ? atomicAdd(&a.counters[0], 1) : (first ? g : NV);
         const int q = k % kQD;
         if (k >= kQD) mbar_wait(&vq_empty[q], ((k / kQD) - 1) & 1);
         vq[q] = v < NV ? v : -1;
         mbar_arrive(&vq_full[q]);
-        ++k;
-        if (v >= NV) break;
-        // Align the virtual CTA's first stage to ring slot 0 (empty phases), so the stage ->
-        // consumer-warp assignment -- hence every rounding -- depends only on v, not on
-        // which CTAs claimed what before: bitwise-deterministic output (reading C16).
-        for (; j % NST != 0; ++j) {
-          const int slot = j % NST;
+      }
+      v = __shfl_sync(0xffffffffu, v, 0);
+      ++k;
+      if (v >= NV) break;
+      // Align the virtual CTA's first stage to ring slot 0 (empty phases), so the stage ->
+      // consumer-warp assignment -- hence every rounding -- depends only on v, not on
+      // which CTAs claimed what before: bitwise-deterministic output (reading C16).
+      for (; j % NST != 0; ++j) {
+        const int slot = j % NST;
+        if (lane == 0) {
           if (j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
           mbar_arrive(&full[slot]);
         }
-        const int it1 = a.cta_begin[v + 1];
-        int unit = a.cta_first_unit[v];
-        for (int it = a.cta_begin[v]; it < it1;) {
-          const DevUnit u = a.units[unit];
-          if (u.iter_end <= it) {
-            ++unit;
-            continue;
-          }
-          const int seg_end = min(u.iter_end, it1);
-          for (; it < seg_end; ++it) {                        // LeanTile iterations (Alg1§13)
-            const int t0 = (it - u.iter_begin) * a.tile_n;    // kk = iter * T_n (Alg1§14)
-            const int t1 = min(t0 + a.tile_n, u.len);
-            for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {  // LoadFragment K, V (Alg1§17-18)
-              const int slot = j % NST;
-              if (j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
-              E::produce(ring + slot * E::STAGE_BYTES, a, tm, u.row0 + s0, min(a.stage_tokens, t1 - s0),
-                         &full[slot], pol);
-              ++j;
-            }
-          }
+      }
+      const int it1 = a.cta_begin[v + 1];
+      int unit = a.cta_first_unit[v];
+      for (int it = a.cta_begin[v]; it < it1;) {
+        const DevUnit u = a.units[unit];
+        if (u.iter_end <= it) {
           ++unit;
+          continue;
         }
+        const int seg_end = min(u.iter_end, it1);
+        PageWin pw;
+        if (a.paged) pw.init(a, u.row0);
+        for (; it < seg_end; ++it) {                        // LeanTile iterations (Alg1§13)
+          const int t0 = (it - u.iter_begin) * a.tile_n;    // kk = iter * T_n (Alg1§14)
+          const int t1 = min(t0 + a.tile_n, u.len);
+          for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {  // LoadFragment K, V (Alg1§17-18)
+            const int slot = j % NST;
+            if (lane == 0 && j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
+            const int ntok = min(a.stage_tokens, t1 - s0);
+            if (!a.paged) {
+              if (lane == 0) E::produce(ring + slot * E::STAGE_BYTES, a, tm, u.row0 + s0, ntok, &full[slot], pol);
+            } else {
+              E::produce_paged(ring + slot * E::STAGE_BYTES, a, tm, pw, s0, ntok, &full[slot], pol, lane);
+            }
+            ++j;
+          }
+        }
+        ++unit;
       }
     }
     return;
@@ -999,12 +1086,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn(std::string& err) {
   return fn;
 }
 
-bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype, std::string& err) {
+bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype, int box_rows, std::string& err) {
   auto enc = encode_fn(err);
   if (!enc) return false;
   cuuint64_t gdim[2] = {cuuint64_t(d), cuuint64_t(rows)};
   cuuint64_t gstride[1] = {cuuint64_t(d) * 2};
-  cuuint32_t box[2] = {64, 64};
+  cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(tm, dtype == LA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1043,8 +1130,8 @@ int launch_decode(const KernelInfo& ki, const DecodeArgs& a_in, int64_t kv_rows,
   std::memset(&tm, 0, sizeof(tm));
   a.uses_tmap = ki.uses_tma_tensor ? 1 : 0;
   if (ki.uses_tma_tensor) {
-    if (!make_tmap(&tm.k, a.k, kv_rows, head_dim, dtype, err)) return 1;
-    if (!make_tmap(&tm.v, a.v, kv_rows, head_dim, dtype, err)) return 1;
+    if (!make_tmap(&tm.k, a.k, kv_rows, head_dim, dtype, a.box_rows, err)) return 1;
+    if (!make_tmap(&tm.v, a.v, kv_rows, head_dim, dtype, a.box_rows, err)) return 1;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.grid);

@@ -42,6 +42,10 @@ struct Problem {
   int64_t max_ctx = 0;
   float scale = 0.f;
   std::vector<int32_t> ctx_lens;
+  // LA_KV_PAGED
+  int page_size = 0, pages_per_seq = 0;
+  int64_t num_pages = 0;
+  std::vector<int32_t> block_table;  // [batch][pages_per_seq]
   int64_t kv_rows() const;   // rows of one K (or V) cache in its layout
   int elem_bytes() const { return dtype == LA_FP32 ? 4 : 2; }
 };
@@ -94,6 +98,14 @@ struct DecodeArgs {
   int group;
   int uses_tmap;      // set by launch_decode for the TMA-tensor (GQA) engine
   float scale_log2;   // scale * log2(e): scores live in the exp2 domain inside the kernel
+  // LA_KV_PAGED: DevUnit.row0 holds b * heads_kv + h; token t of the unit is row
+  // (block_table[b * pt_stride + (t >> page_shift)] * heads_kv + h) * page + (t & (page - 1))
+  const int32_t* block_table;
+  int paged;
+  int page_shift;
+  int pt_stride;      // padded to a multiple of 32 entries (the producer reads 32-entry windows)
+  int heads_kv;
+  int box_rows;       // GQA TMA box height: min(64, page_size) when paged, else 64
 };
 
 // Kernel configuration for (dtype, head_dim, group): threads, dynamic smem, max stage tokens.

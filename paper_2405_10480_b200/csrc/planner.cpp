@@ -20,6 +20,7 @@ namespace la {
 
 int64_t Problem::kv_rows() const {
   if (layout == LA_KV_BHSD) return int64_t(batch) * heads_kv * max_ctx;
+  if (layout == LA_KV_PAGED) return num_pages * heads_kv * page_size;
   int64_t total = 0;
   for (int32_t n : ctx_lens) total += n;
   return int64_t(heads_kv) * total;
@@ -34,8 +35,12 @@ void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int6
   auto add = [&](int b, int h) {
     DevUnit u{};
     u.len = p.ctx_lens[b];
-    u.row0 = (p.layout == LA_KV_BHSD) ? (int64_t(b) * p.heads_kv + h) * p.max_ctx
-                                      : int64_t(h) * cu[p.batch] + cu[b];
+    if (p.layout == LA_KV_BHSD)
+      u.row0 = (int64_t(b) * p.heads_kv + h) * p.max_ctx;
+    else if (p.layout == LA_KV_PACKED)
+      u.row0 = int64_t(h) * cu[p.batch] + cu[b];
+    else
+      u.row0 = int64_t(b) * p.heads_kv + h;  // paged: rows come from the block table
     u.q_row = b * p.heads_q + h * p.group;
     u.iter_begin = int32_t(it);
     it += (int64_t(u.len) + tile_n - 1) / tile_n;   // C_n = ceil(n_b / T_n)   (Alg2§5)
@@ -43,7 +48,7 @@ void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int6
     u.last_cta = u.host_cta = -1;
     units.push_back(u);
   };
-  if (p.layout == LA_KV_BHSD) {
+  if (p.layout != LA_KV_PACKED) {
     for (int b = 0; b < p.batch; ++b)           // batch -> heads -> context
       for (int h = 0; h < p.heads_kv; ++h) add(b, h);
   } else {

@@ -22,11 +22,11 @@ LIB_PATH = os.environ.get("LEANATTN_LIB") or os.path.join(_HERE, "lib", "liblean
 
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE = range(6)
 LA_BF16, LA_FP16, LA_FP32 = 0, 1, 2
-LA_KV_BHSD, LA_KV_PACKED = 0, 1
+LA_KV_BHSD, LA_KV_PACKED, LA_KV_PAGED = 0, 1, 2
 LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC, LA_SCHED_FIXED_SPLIT = 0, 1, 2, 3
 
 _DTYPE_CODES = {"bf16": LA_BF16, "fp16": LA_FP16, "fp32": LA_FP32}
-_LAYOUT_CODES = {"bhsd": LA_KV_BHSD, "packed": LA_KV_PACKED}
+_LAYOUT_CODES = {"bhsd": LA_KV_BHSD, "packed": LA_KV_PACKED, "paged": LA_KV_PAGED}
 _SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, "dynamic": LA_SCHED_DYNAMIC,
                 "fixed_split": LA_SCHED_FIXED_SPLIT}
 
@@ -46,7 +46,9 @@ class la_plan_opts(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_float), ("layout", ctypes.c_int), ("max_ctx", ctypes.c_int64),
                 ("grid", ctypes.c_int), ("num_sms", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
                 ("host_only", ctypes.c_int), ("schedule", ctypes.c_int), ("trace", ctypes.c_int),
-                ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int), ("split", ctypes.c_int)]
+                ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int), ("split", ctypes.c_int),
+                ("block_table", ctypes.POINTER(ctypes.c_int32)), ("pages_per_seq", ctypes.c_int),
+                ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -122,7 +124,8 @@ class Plan:
                  tile_n: int = 0, dtype: str = "bf16", scale: float = 0.0, layout: str = "bhsd",
                  max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
                  ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
-                 dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0):
+                 dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
+                 block_table=None, page_size: int = 0, num_pages: int = 0):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -138,6 +141,13 @@ class Plan:
         opts.dyn_first_permille = int(dyn_first_permille)
         opts.dyn_min_chunk = int(dyn_min_chunk)
         opts.split = int(split)
+        if block_table is not None:  # paged layout: [batch][pages_per_seq] int32 (host)
+            bt = np.ascontiguousarray(np.asarray(block_table, dtype=np.int32))
+            self._bt = bt
+            opts.block_table = bt.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            opts.pages_per_seq = int(bt.shape[1])
+            opts.page_size = int(page_size)
+            opts.num_pages = int(num_pages)
         lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
         h = ctypes.c_void_p()
         self._h = None

@@ -113,6 +113,7 @@ class Problem:
     max_ctx: Optional[int] = None  # bhsd row stride; default max(ctx_lens)
     needles: Sequence[int] = field(default_factory=tuple)  # extra needle tokens (D2)
     census_block: int = 0          # T_c for D3 (0 -> n_b // 16 rounded to a power of two)
+    page_size: int = 0             # layout "paged": tokens per page (pools (pages, H_kv, page, d))
 
     def __post_init__(self):
         if self.max_ctx is None:
@@ -240,6 +241,9 @@ def fill_kv_cache(p: Problem, which: str, device="cpu", chunk_rows: int = 1 << 2
     a sequence shard -- laid out as a cache of lengths ``b - a`` (max_ctx = max length).
     """
     D = p.head_dim
+    if p.layout == "paged":
+        assert token_range is None, "sequence shards of a paged cache are not generated"
+        return _fill_paged(p, which, device, chunk_rows)
     if token_range is None:
         token_range = [(0, n) for n in p.ctx_lens]
     lens = [b - a for a, b in token_range]
@@ -264,6 +268,39 @@ def fill_kv_cache(p: Problem, which: str, device="cpu", chunk_rows: int = 1 << 2
                     out[b, h, r0:r1] = slab
                 else:
                     out[h, cu[b] + r0: cu[b] + r1] = slab
+    return out
+
+
+def paged_meta(p: Problem, spare_pages: int = 3):
+    """Block table of a paged problem: the sum_b ceil(n_b / page) used pages plus a few spare
+    ones, handed out in a seeded random order (pages of one request are NOT contiguous).
+    Returns (block_table int32 [B, pages_per_seq], num_pages)."""
+    import numpy as np
+    ps = p.page_size
+    need = [-(-n // ps) for n in p.ctx_lens]
+    num_pages = sum(need) + spare_pages
+    order = torch.argsort(_uniform_from_index(torch.arange(num_pages, dtype=torch.int64), _key(p.seed, 5)))
+    bt = np.full((p.batch, max(need)), num_pages - 1, dtype=np.int32)   # unused slots: a valid page
+    pos = 0
+    for b, k in enumerate(need):
+        bt[b, :k] = order[pos:pos + k].numpy()
+        pos += k
+    return bt, num_pages
+
+
+def _fill_paged(p: Problem, which: str, device, chunk_rows: int):
+    bt, num_pages = paged_meta(p)
+    ps = p.page_size
+    out = torch.zeros(num_pages, p.heads_kv, ps, p.head_dim, dtype=_DTYPES[p.dtype], device=device)
+    for b in range(p.batch):
+        n = p.ctx_lens[b]
+        for h in range(p.heads_kv):
+            for t0 in range(0, n, chunk_rows):
+                t1 = min(n, t0 + chunk_rows)
+                slab = gen_kv_unit(p, b, h, which, device, t0, t1)
+                for pi in range(t0 // ps, -(-t1 // ps)):
+                    a0, a1 = max(t0, pi * ps), min(t1, (pi + 1) * ps)
+                    out[int(bt[b, pi]), h, a0 - pi * ps:a1 - pi * ps] = slab[a0 - t0:a1 - t0]
     return out
 
 

@@ -47,6 +47,9 @@ def run_cuda(p: synth.Problem, inputs=None, **plan_kw):
     import paper_2405_10480_b200 as la
     q, k, v = inputs if inputs is not None else cuda_inputs(p)
     lens = p.ctx_lens
+    if p.layout == "paged":
+        bt, num_pages = synth.paged_meta(p)
+        plan_kw = dict(plan_kw, block_table=bt, page_size=p.page_size, num_pages=num_pages)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
                    max_ctx=p.max_ctx if p.layout == "bhsd" else 0, **plan_kw)
     out, lse = plan.decode(q, k, v)
@@ -59,6 +62,10 @@ def run_oracle(p: synth.Problem):
     q = synth.to_f64(synth.gen_q(p))
     k = synth.to_f64(synth.fill_kv_cache(p, "k"))
     v = synth.to_f64(synth.fill_kv_cache(p, "v"))
+    if p.layout == "paged":
+        bt, _ = synth.paged_meta(p)
+        return oracle.decode_attention(q, k, v, p.ctx_lens, p.scale, "paged", block_table=bt,
+                                       page_size=p.page_size)
     return oracle.decode_attention(q, k, v, p.ctx_lens, p.scale, p.layout)
 
 

@@ -216,3 +216,27 @@ def test_c3_gqa_full_size_sampled():
     o_exp, l_exp = census_expect(p3, 0)
     assert np.max(np.abs(O3 - o_exp[None, None, :])) <= 1e-5
     assert np.max(np.abs(L3 - l_exp)) <= 1e-5
+
+
+@pytest.mark.parametrize("group", [1, 8])
+@pytest.mark.parametrize("page_size", [16, 32, 64, 256])
+def test_paged_kv(group, page_size):
+    """NEXT-4: paged KV pools through a block table, MHA and GQA, static and dynamic."""
+    p = synth.Problem(3, 2 * group, 2, 128, [1000, 77, 2500], dtype="bf16", dist="D2", seed=51,
+                      layout="paged", page_size=page_size)
+    O_ref, L_ref = run_oracle(p)
+    inputs = cuda_inputs(p)
+    for schedule in SCHEDULES:
+        for tile_n, grid in ((32, 5), (128, 0)):
+            O, L, _ = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule)
+            gate(O, L, O_ref, L_ref, what=f"paged g{group} ps{page_size} T{tile_n} G{grid} {schedule}")
+
+
+def test_c4_paged_full_size_sampled():
+    """Ragged c4 in a 16-token paged pool (serving layout)."""
+    p = synth.config("c4", layout="paged", page_size=16)
+    O, L, plan = run_cuda(p)
+    for b, h in ((1, 3), (9, 17)):
+        O_ref, L_ref = oracle_unit(p, b, h)
+        gate(O[b, h:h + 1], L[b, h:h + 1], O_ref, L_ref, what=f"c4 paged b{b} h{h}")
+    torch.cuda.empty_cache()

@@ -147,3 +147,27 @@ def test_errors():
         oracle.decode_attention_unit(np.zeros((1, 4)), np.zeros((3, 5)), np.zeros((3, 5)), 1.0)
     with pytest.raises(ValueError):
         oracle.decode_attention_unit(np.zeros((1, 4)), np.zeros((0, 4)), np.zeros((0, 4)), 1.0)
+
+
+def test_paged_layout_is_the_same_rows():
+    # NEXT-4 paged pools: the oracle's gather through the block table reproduces the BHSD
+    # result bit for bit (the layouts hold the same bf16 rows)
+    import synth
+    for ps in (16, 64):
+        base = dict(batch=3, heads_q=4, heads_kv=2, head_dim=32, ctx_lens=[100, 17, 64], dtype="bf16",
+                    dist="D2", seed=9)
+        pb = synth.Problem(**base)
+        pp = synth.Problem(**base, layout="paged", page_size=ps)
+        q = synth.to_f64(synth.gen_q(pb))
+        O1, L1 = oracle.decode_attention(q, synth.to_f64(synth.fill_kv_cache(pb, "k")),
+                                         synth.to_f64(synth.fill_kv_cache(pb, "v")), pb.ctx_lens, pb.scale)
+        bt, npages = synth.paged_meta(pp)
+        assert sorted(set(bt[0, :-(-100 // ps)].tolist()) | set(bt[1, :2].tolist())) is not None
+        kp = synth.fill_kv_cache(pp, "k")
+        assert kp.shape == (npages, 2, ps, 32)
+        O2, L2 = oracle.decode_attention(q, synth.to_f64(kp), synth.to_f64(synth.fill_kv_cache(pp, "v")),
+                                         pp.ctx_lens, pp.scale, "paged", block_table=bt, page_size=ps)
+        assert np.array_equal(O1, O2) and np.array_equal(L1, L2)
+        # pages of one request are scattered, and no page is shared between requests
+        used = [bt[b, i] for b, n in enumerate(pp.ctx_lens) for i in range(-(-n // ps))]
+        assert len(set(used)) == len(used)

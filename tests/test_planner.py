@@ -182,3 +182,18 @@ def test_fixed_split_schedule_bit_exact(la):
     # the paper's motivating shapes: 56 heads x batch 1 -> FD splits; batch 4 x
     # 32 heads fills 80% of 148 SMs -> no split at all (one partial wave)
     assert oracle.fa2_num_splits(56, 2048, 148) > 1 and oracle.fa2_num_splits(128, 2048, 148) == 1
+
+
+def test_paged_plan_validation_and_schedule(la):
+    import synth
+    p = synth.Problem(3, 4, 4, 128, [100, 17, 640], layout="paged", page_size=16)
+    bt, npages = synth.paged_meta(p)
+    plan = la.Plan(3, 4, 4, 128, p.ctx_lens, tile_n=64, host_only=True, layout="paged", block_table=bt,
+                   page_size=16, num_pages=npages, schedule="streamk", grid=7)
+    ref = la.Plan(3, 4, 4, 128, p.ctx_lens, tile_n=64, host_only=True, schedule="streamk", grid=7)
+    assert np.array_equal(plan.export(), ref.export())      # units batch -> heads, like BHSD
+    for bad in (dict(page_size=24), dict(num_pages=3), dict(page_size=16, block_table=bt[:, :2])):
+        kw = dict(block_table=bt, page_size=16, num_pages=npages)
+        kw.update(bad)
+        with pytest.raises(la.LaError):
+            la.Plan(3, 4, 4, 128, p.ctx_lens, host_only=True, layout="paged", **kw)
