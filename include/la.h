@@ -110,6 +110,13 @@ typedef struct {
   int pages_per_seq;          /* row stride of block_table (>= ceil(max ctx / page_size))   */
   int page_size;              /* tokens per page: 16, 32, 64, 128 or 256                    */
   int64_t num_pages;          /* pages in each pool; every table entry must be < num_pages  */
+  /* N_q > 1 (NEXT-3: speculative / multi-token decode; the paper's T_m rows, Alg2§4): */
+  int q_len;                  /* query tokens per request N_q (default 1); q, out are then
+                                 (B, H_q, N_q, d) and lse (B, H_q, N_q).  An output tile is
+                                 the g * N_q rows of one KV head: g * N_q <= 8 in this build */
+  int causal;                 /* 1 (default): query i of N_q is the token at position
+                                 n - N_q + i and attends to keys [0, n - N_q + i]; 0: every
+                                 query attends to all n keys                                 */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;
@@ -129,6 +136,7 @@ typedef struct {
   float scale;
   int64_t num_vctas;       /* Alg. 2's G: iteration ranges (= grid for static schedules)  */
   int split;               /* LA_SCHED_FIXED_SPLIT: chunks per unit (0 otherwise)         */
+  int q_len;               /* N_q                                                          */
 } la_plan_info;
 
 /* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */

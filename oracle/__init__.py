@@ -23,7 +23,7 @@ Modules
 
 Parity status of every function is listed in DESIGN.md §"Oracle and pins"; all are pinned.
 """
-from .attention import decode_attention, decode_attention_unit, scores
+from .attention import decode_attention, decode_attention_unit, decode_attention_multi, paged_rows, scores
 from .rescale import PartialState, neutral, partial, combine, finalize, fold
 from .leantile import lean_tile
 from .schedule import (Segment, iters_per_cta, cta_range, owner, stream_k_segments,

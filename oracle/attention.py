@@ -48,6 +48,49 @@ def decode_attention_unit(q_rows: np.ndarray, k: np.ndarray, v: np.ndarray, scal
     return O, L
 
 
+def decode_attention_multi(q: np.ndarray, k: np.ndarray, v: np.ndarray, ctx_lens, scale: float,
+                           causal: bool = True, layout: str = "bhsd", block_table=None, page_size: int = 0):
+    """N_q > 1 queries per request (NEXT-3; the paper's general N_q, Alg2§4 C_m):
+    q (B, H_q, N_q, d).  Query i of request b is the cached token at position n_b - N_q + i;
+    with ``causal`` it attends to keys [0, n_b - N_q + i] (the prefill-phase mask restricted
+    to the new tokens), otherwise to all n_b keys.  Eq. 1 per query row.
+    Returns O (B, H_q, N_q, d), L (B, H_q, N_q)."""
+    q = np.asarray(q, dtype=np.float64)
+    B, Hq, Nq, d = q.shape
+    O = np.empty((B, Hq, Nq, d))
+    L = np.empty((B, Hq, Nq))
+    for i in range(Nq):
+        lens_i = [int(n) - Nq + i + 1 if causal else int(n) for n in ctx_lens]
+        o, l = _sliced(q[:, :, i], k, v, ctx_lens, lens_i, scale, layout, block_table, page_size)
+        O[:, :, i], L[:, :, i] = o, l
+    return O, L
+
+
+def _sliced(q, k, v, ctx_lens, lens_i, scale, layout, block_table, page_size):
+    """decode_attention over the first lens_i[b] keys of every request."""
+    B, Hq, d = q.shape
+    Hkv = k.shape[0] if layout == "packed" else k.shape[1]
+    g = Hq // Hkv
+    cu = np.concatenate([[0], np.cumsum(ctx_lens)]).astype(np.int64)
+    O = np.empty((B, Hq, d))
+    L = np.empty((B, Hq))
+    for b in range(B):
+        n = int(ctx_lens[b])
+        for h in range(Hkv):
+            if layout == "bhsd":
+                kk, vv = k[b, h, :n], v[b, h, :n]
+            elif layout == "packed":
+                kk, vv = k[h, cu[b]:cu[b + 1]], v[h, cu[b]:cu[b + 1]]
+            else:
+                kk = paged_rows(k, block_table[b], h, n, page_size)
+                vv = paged_rows(v, block_table[b], h, n, page_size)
+            m = lens_i[b]
+            o, l = decode_attention_unit(q[b, h * g:(h + 1) * g], kk[:m], vv[:m], scale)
+            O[b, h * g:(h + 1) * g] = o
+            L[b, h * g:(h + 1) * g] = l
+    return O, L
+
+
 def paged_rows(pool: np.ndarray, block_table_row, h: int, n: int, page_size: int) -> np.ndarray:
     """The n context rows of KV head h of one request in a paged pool (num_pages, H_kv,
     page_size, d): token t is row t % page_size of page block_table_row[t // page_size]."""

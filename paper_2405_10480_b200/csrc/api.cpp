@@ -115,6 +115,8 @@ la_status la_plan_opts_init(la_plan_opts* o) {
   o->schedule = LA_SCHED_STREAMK;
   o->dyn_first_permille = 750;
   o->dyn_min_chunk = 2;
+  o->q_len = 1;
+  o->causal = 1;
   return LA_OK;
 }
 
@@ -149,6 +151,11 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   p.heads_kv = heads_kv;
   p.head_dim = head_dim;
   p.group = heads_q / heads_kv;
+  if (opts.q_len < 1) return fail(LA_ERR_INVALID, "q_len must be >= 1");
+  p.q_len = opts.q_len;
+  p.causal = opts.causal ? 1 : 0;
+  if (p.rows() > 8 && p.rows() != p.group)
+    return fail(LA_ERR_UNSUPPORTED, "group * q_len must be <= 8 for q_len > 1 in this build");
   p.dtype = dtype;
   p.layout = opts.layout;
   p.schedule = opts.schedule;
@@ -156,6 +163,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   int64_t maxn = 0, total = 0;
   for (int32_t n : p.ctx_lens) {
     if (n < 1) return fail(LA_ERR_INVALID, "every ctx_lens[b] must be >= 1 (reading C6)");
+    if (n < p.q_len) return fail(LA_ERR_INVALID, "ctx_lens[b] must be >= q_len (the queries are cached tokens)");
     maxn = std::max<int64_t>(maxn, n);
     total += n;
   }
@@ -192,7 +200,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (plan->host_only) {
     max_ctas = std::max(1, opts.num_sms) * std::max(1, opts.ctas_per_sm);
   } else {
-    plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.group);
+    plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows());
     if (!plan->kinfo.supported) {
       delete plan;
       return fail(LA_ERR_UNSUPPORTED, "no decode kernel for this (dtype, head_dim, group) in this build");
@@ -263,8 +271,8 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     const size_t b_units = align(U * sizeof(DevUnit));
     const size_t b_begin = align(size_t(G + 1) * sizeof(int32_t));
     const size_t b_first = align(size_t(G) * sizeof(int32_t));
-    const size_t b_po = align(size_t(G) * 2 * p.group * head_dim * sizeof(float));
-    const size_t b_pml = align(size_t(G) * 2 * p.group * 2 * sizeof(float));
+    const size_t b_po = align(size_t(G) * 2 * p.rows() * head_dim * sizeof(float));
+    const size_t b_pml = align(size_t(G) * 2 * p.rows() * 2 * sizeof(float));
     const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
     const size_t b_cnt = align((2 + U + size_t(G)) * sizeof(int));
     const size_t b_trace = opts.trace ? align(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
@@ -331,6 +339,7 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   info->grid = s.phys_grid;
   info->num_vctas = s.grid;
   info->split = plan->split;
+  info->q_len = p.q_len;
   info->num_units = int(s.units.size());
   info->total_iters = s.total_iters;
   info->num_segments = s.num_segments;
@@ -394,7 +403,9 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.grid = plan->sched.phys_grid;
   a.tile_n = plan->sched.tile_n;
   a.stage_tokens = plan->stage_tokens;
-  a.group = plan->prob.group;
+  a.group = plan->prob.rows();
+  a.q_len = plan->prob.q_len;
+  a.causal = plan->prob.causal;
   a.scale_log2 = float(double(plan->prob.scale) * 1.4426950408889634);
   std::string err;
   const la::Problem& p = plan->prob;
@@ -433,10 +444,10 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
   const la::Problem& p = plan->prob;
   if (kv_rows != p.kv_rows()) return fail(LA_ERR_INVALID, "kv_rows does not match the plan");
   const size_t eb = size_t(p.elem_bytes());
-  const size_t q_bytes = size_t(p.batch) * p.heads_q * p.head_dim * eb;
+  const size_t q_bytes = size_t(p.batch) * p.heads_q * p.q_len * p.head_dim * eb;
   const size_t kv_bytes = size_t(kv_rows) * p.head_dim * eb;
-  const size_t o_bytes = size_t(p.batch) * p.heads_q * p.head_dim * sizeof(float);
-  const size_t l_bytes = size_t(p.batch) * p.heads_q * sizeof(float);
+  const size_t o_bytes = size_t(p.batch) * p.heads_q * p.q_len * p.head_dim * sizeof(float);
+  const size_t l_bytes = size_t(p.batch) * p.heads_q * p.q_len * sizeof(float);
   auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t need = align(q_bytes) + 2 * align(kv_bytes) + align(o_bytes) + align(l_bytes);
   if (plan->stage_bytes < need) {

@@ -289,7 +289,8 @@ struct MhaEngine {
   }
 
   // This warp's 32-key rounds (sub, sub + WPS, ...) of one stage of ntok keys.
-  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, float scale_log2,
+  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, int /*tok0*/,
+                                               float scale_log2,
                                                int lane) {
     const int kg = lane / LPK, li = lane % LPK;
     const unsigned char* ks = st;
@@ -352,21 +353,6 @@ struct MhaEngine {
     if (lane == 0) {
       fb[D] = s.m;
       fb[D + 1] = s.l;
-    }
-  }
-
-  // Element e = (head 0, dim e): fold the NCW warp partials (re-scaling operator).
-  __device__ __forceinline__ static void fold_elem(const float* fold, int e, float& oc, float& ms, float& ls) {
-    ms = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < NCW; ++w) ms = fmaxf(ms, fold[w * (D + 2) + D]);
-    oc = 0.f;
-    ls = 0.f;
-#pragma unroll
-    for (int w = 0; w < NCW; ++w) {
-      const float wt = ex2(fold[w * (D + 2) + D] - ms);  // idle warp: m = -inf -> 0
-      ls = fmaf(wt, fold[w * (D + 2) + D + 1], ls);
-      oc = fmaf(wt, fold[w * (D + 2) + e], oc);
     }
   }
 };
@@ -456,8 +442,9 @@ struct GqaEngine {
 
   struct State {
     uint32_t qb[KS][2];     // Q^T B-fragments (exact inputs)
-    float m[2], l[2];       // heads 2tq, 2tq+1
-    float o[KS][4];         // O^T fragments: dims 16mm + gq (+8), heads 2tq, 2tq+1
+    float m[2], l[2];       // rows 2tq, 2tq+1 (row = head j * N_q + query i)
+    float o[KS][4];         // O^T fragments: dims 16mm + gq (+8), rows 2tq, 2tq+1
+    int lim[2];             // causal key limit of rows 2tq, 2tq+1 (unit-local, exclusive)
   };
 
   __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
@@ -501,16 +488,21 @@ struct GqaEngine {
     s.l[0] = s.l[1] = 0.f;
 #pragma unroll
     for (int mm = 0; mm < KS; ++mm) s.o[mm][0] = s.o[mm][1] = s.o[mm][2] = s.o[mm][3] = 0.f;
+    // N_q > 1, causal: query i (row r = j * N_q + i) is the token at n - N_q + i (NEXT-3)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      s.lim[e] = a.causal ? u.len - a.q_len + ((2 * tq + e) % a.q_len) + 1 : u.len;
   }
 
-  // This warp's 32-token rounds (sub, sub + WPS, ...) of one stage of ntok tokens.
-  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, float scale_log2,
-                                               int lane) {
-    for (int rb = sub * 32; rb < ntok; rb += 32 * WPS) round(s, st, rb, ntok, scale_log2, lane);
+  // This warp's 32-token rounds (sub, sub + WPS, ...) of one stage of ntok tokens starting
+  // at unit-local token tok0.
+  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, int tok0,
+                                               float scale_log2, int lane) {
+    for (int rb = sub * 32; rb < ntok; rb += 32 * WPS) round(s, st, rb, ntok, tok0, scale_log2, lane);
   }
 
-  __device__ __forceinline__ static void round(State& s, unsigned char* st, int rb, int ntok, float scale_log2,
-                                               int lane) {
+  __device__ __forceinline__ static void round(State& s, unsigned char* st, int rb, int ntok, int tok0,
+                                               float scale_log2, int lane) {
     const int gq = lane >> 2, mi = lane >> 3, ri = lane & 7;
     if (rb + 32 > ntok) {
       // rows >= ntok of this round hold the next unit's rows or cache padding: zero this
@@ -544,7 +536,8 @@ struct GqaEngine {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int tok = rb + blk * 16 + gq + ((e >> 1) << 3);
-        sc[blk][e] = tok < ntok ? sc[blk][e] * scale_log2 : -INFINITY;
+        const bool ok = tok < ntok && tok0 + tok < s.lim[e & 1];  // tail (C5) and causal limit
+        sc[blk][e] = ok ? sc[blk][e] * scale_log2 : -INFINITY;
         mx[e & 1] = fmaxf(mx[e & 1], sc[blk][e]);
       }
     }
@@ -555,7 +548,7 @@ struct GqaEngine {
     }
     if (__any_sync(0xffffffffu, (mx[0] > s.m[0]) || (mx[1] > s.m[1]))) {  // Alg1§23-24 rescale
       const float mn0 = fmaxf(s.m[0], mx[0]), mn1 = fmaxf(s.m[1], mx[1]);
-      const float al0 = ex2(s.m[0] - mn0), al1 = ex2(s.m[1] - mn1);
+      const float al0 = ex2_sub(s.m[0], mn0), al1 = ex2_sub(s.m[1], mn1);
       s.l[0] *= al0;
       s.l[1] *= al1;
 #pragma unroll
@@ -571,8 +564,9 @@ struct GqaEngine {
     // ---- P_f = exp(S_f - m) (Alg1§22); O^T += V^T P^T (Alg1§24) -----------------------------
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
-      const float p0 = ex2(sc[blk][0] - s.m[0]), p1 = ex2(sc[blk][1] - s.m[1]);
-      const float p2 = ex2(sc[blk][2] - s.m[0]), p3 = ex2(sc[blk][3] - s.m[1]);
+      // ex2_sub: a row that has seen no key yet (m = -inf, fully masked) gets p = 0, not NaN
+      const float p0 = ex2_sub(sc[blk][0], s.m[0]), p1 = ex2_sub(sc[blk][1], s.m[1]);
+      const float p2 = ex2_sub(sc[blk][2], s.m[0]), p3 = ex2_sub(sc[blk][3], s.m[1]);
       s.l[0] += p0 + p2;
       s.l[1] += p1 + p3;
       // P = P_hi + P_lo, both in the KV type (P_lo = round(p - P_hi), exact subtraction):
@@ -619,22 +613,6 @@ struct GqaEngine {
       fb[h0 * (D + 2) + D + 1] = s.l[0];
       fb[h1 * (D + 2) + D] = s.m[1];
       fb[h1 * (D + 2) + D + 1] = s.l[1];
-    }
-  }
-
-  __device__ __forceinline__ static void fold_elem(const float* fold, int e, float& oc, float& ms, float& ls) {
-    const int h = e / D, c = e % D;
-    ms = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < NCW; ++w) ms = fmaxf(ms, fold[(w * HEADS + h) * (D + 2) + D]);
-    oc = 0.f;
-    ls = 0.f;
-#pragma unroll
-    for (int w = 0; w < NCW; ++w) {
-      const float* fb = fold + (w * HEADS + h) * (D + 2);
-      const float wt = ex2(fb[D] - ms);
-      ls = fmaf(wt, fb[D + 1], ls);
-      oc = fmaf(wt, fb[c], oc);
     }
   }
 };
@@ -842,7 +820,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           for (int h = 0; h < H; ++h) {
             if (h >= a.group) continue;
             const float mn = fmaxf(acc.m[h], mp[b][h]);
-            const float wa = ex2(acc.m[h] - mn), wb = ex2(mp[b][h] - mn);  // Alg2§32-34
+            const float wa = ex2_sub(acc.m[h], mn), wb = ex2_sub(mp[b][h], mn);  // Alg2§32-34
             acc.l[h] = wa * acc.l[h] + wb * lp[b][h];
 #pragma unroll
             for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = wa * acc.o[h][jj] + wb * op[b][h][jj];
@@ -880,7 +858,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #pragma unroll
         for (int w = 0; w < NCW; ++w) {
           const float* r = fb + (w * H + h) * (D + 2);
-          const float wt = ex2(r[D] - mx);  // idle warp: m = -inf -> 0
+          const float wt = ex2_sub(r[D], mx);  // idle warp / masked row: m = -inf -> 0
           l = fmaf(wt, r[D + 1], l);
 #pragma unroll
           for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(wt, r[lane + 32 * jj], o[jj]);
@@ -1023,7 +1001,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
           if (j % NST == my_slot) {
             mbar_wait(&full[my_slot], (j / NST) & 1);
-            E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), a.scale_log2, lane);
+            E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
+                     lane);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[my_slot]);
           }

@@ -38,6 +38,8 @@ struct Schedule {
 
 struct Problem {
   int batch = 0, heads_q = 0, heads_kv = 0, head_dim = 0, group = 0;
+  int q_len = 1, causal = 1;   // N_q and its mask (NEXT-3)
+  int rows() const { return group * q_len; }   // T_m: output rows of one unit
   int dtype = LA_BF16, layout = LA_KV_BHSD, schedule = LA_SCHED_STREAMK;
   int64_t max_ctx = 0;
   float scale = 0.f;
@@ -95,7 +97,9 @@ struct DecodeArgs {
   int grid;           // CTAs launched
   int tile_n;
   int stage_tokens;
-  int group;
+  int group;          // output rows per unit T_m = g * N_q (rows r = head j * N_q + query i)
+  int q_len;          // N_q
+  int causal;         // N_q > 1: query i attends to unit-local keys [0, n - N_q + i]
   int uses_tmap;      // set by launch_decode for the TMA-tensor (GQA) engine
   float scale_log2;   // scale * log2(e): scores live in the exp2 domain inside the kernel
   // LA_KV_PAGED: DevUnit.row0 holds b * heads_kv + h; token t of the unit is row

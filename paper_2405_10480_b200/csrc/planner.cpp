@@ -41,7 +41,7 @@ void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int6
       u.row0 = int64_t(h) * cu[p.batch] + cu[b];
     else
       u.row0 = int64_t(b) * p.heads_kv + h;  // paged: rows come from the block table
-    u.q_row = b * p.heads_q + h * p.group;
+    u.q_row = (b * p.heads_q + h * p.group) * p.q_len;  // rows (head j, query i) = j * N_q + i
     u.iter_begin = int32_t(it);
     it += (int64_t(u.len) + tile_n - 1) / tile_n;   // C_n = ceil(n_b / T_n)   (Alg2§5)
     u.iter_end = int32_t(it);

@@ -100,6 +100,10 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2; ex2(-inf) = +
   return y;
 }
 
+// 2^(x - m) with the neutral element's m = -inf mapped to weight 0 (never -inf - -inf = NaN):
+// x <= m always holds for the callers, so m = -inf implies x = -inf.
+__device__ __forceinline__ float ex2_sub(float x, float m) { return ex2(x - (m == -INFINITY ? 0.f : m)); }
+
 
 }  // namespace dev
 }  // namespace la

@@ -48,7 +48,8 @@ class la_plan_opts(ctypes.Structure):
                 ("host_only", ctypes.c_int), ("schedule", ctypes.c_int), ("trace", ctypes.c_int),
                 ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int), ("split", ctypes.c_int),
                 ("block_table", ctypes.POINTER(ctypes.c_int32)), ("pages_per_seq", ctypes.c_int),
-                ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64)]
+                ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64), ("q_len", ctypes.c_int),
+                ("causal", ctypes.c_int)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -57,7 +58,8 @@ class la_plan_info(ctypes.Structure):
                                             "num_units")] + \
                [(n, ctypes.c_int64) for n in ("total_iters", "num_segments", "num_partials",
                                               "workspace_bytes", "kv_bytes")] + \
-               [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64), ("split", ctypes.c_int)]
+               [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64), ("split", ctypes.c_int),
+                ("q_len", ctypes.c_int)]
 
 
 _lib = None
@@ -125,7 +127,8 @@ class Plan:
                  max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
                  ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
                  dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
-                 block_table=None, page_size: int = 0, num_pages: int = 0):
+                 block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
+                 causal: bool = True):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -148,6 +151,8 @@ class Plan:
             opts.pages_per_seq = int(bt.shape[1])
             opts.page_size = int(page_size)
             opts.num_pages = int(num_pages)
+        opts.q_len = int(q_len)
+        opts.causal = 1 if causal else 0
         lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
         h = ctypes.c_void_p()
         self._h = None
@@ -186,11 +191,12 @@ class Plan:
 
     def _outputs(self, q, out, lse, need_lse):
         import torch
-        B, H, D = self.info.batch, self.info.heads_q, self.info.head_dim
+        B, H, D, nq = self.info.batch, self.info.heads_q, self.info.head_dim, self.info.q_len
+        rows = (B, H) if nq == 1 else (B, H, nq)
         if out is None:
-            out = torch.empty(B, H, D, dtype=torch.float32, device=q.device)
+            out = torch.empty(rows + (D,), dtype=torch.float32, device=q.device)
         if lse is None and need_lse:
-            lse = torch.empty(B, H, dtype=torch.float32, device=q.device)
+            lse = torch.empty(rows, dtype=torch.float32, device=q.device)
         return out, lse
 
     def _check_inputs(self, q, k, v):

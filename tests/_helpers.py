@@ -47,6 +47,8 @@ def run_cuda(p: synth.Problem, inputs=None, **plan_kw):
     import paper_2405_10480_b200 as la
     q, k, v = inputs if inputs is not None else cuda_inputs(p)
     lens = p.ctx_lens
+    if p.q_len > 1:
+        plan_kw = dict(plan_kw, q_len=p.q_len)
     if p.layout == "paged":
         bt, num_pages = synth.paged_meta(p)
         plan_kw = dict(plan_kw, block_table=bt, page_size=p.page_size, num_pages=num_pages)
@@ -57,11 +59,15 @@ def run_cuda(p: synth.Problem, inputs=None, **plan_kw):
     return out.cpu().numpy().astype(np.float64), lse.cpu().numpy().astype(np.float64), plan
 
 
-def run_oracle(p: synth.Problem):
+def run_oracle(p: synth.Problem, causal: bool = True):
     """Full oracle on host-generated inputs (small problems)."""
     q = synth.to_f64(synth.gen_q(p))
     k = synth.to_f64(synth.fill_kv_cache(p, "k"))
     v = synth.to_f64(synth.fill_kv_cache(p, "v"))
+    if p.q_len > 1:
+        bt = synth.paged_meta(p)[0] if p.layout == "paged" else None
+        return oracle.decode_attention_multi(q, k, v, p.ctx_lens, p.scale, causal, p.layout, block_table=bt,
+                                             page_size=p.page_size)
     if p.layout == "paged":
         bt, _ = synth.paged_meta(p)
         return oracle.decode_attention(q, k, v, p.ctx_lens, p.scale, "paged", block_table=bt,

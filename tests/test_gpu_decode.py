@@ -240,3 +240,27 @@ def test_c4_paged_full_size_sampled():
         O_ref, L_ref = oracle_unit(p, b, h)
         gate(O[b, h:h + 1], L[b, h:h + 1], O_ref, L_ref, what=f"c4 paged b{b} h{h}")
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("group,q_len", [(1, 2), (1, 4), (1, 8), (2, 2), (2, 4), (4, 2)])
+@pytest.mark.parametrize("causal", [True, False])
+def test_multi_token_decode(dtype, group, q_len, causal):
+    """NEXT-3: N_q > 1 query tokens per request (T_m = g * N_q rows on the tensor cores)."""
+    p = synth.Problem(2, 2 * group, 2, 128, [900, 333], dtype=dtype, dist="D2", seed=61, q_len=q_len)
+    O_ref, L_ref = run_oracle(p, causal=causal)
+    inputs = cuda_inputs(p)
+    for schedule in SCHEDULES:
+        for tile_n, grid in ((32, 7), (128, 0)):
+            O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule, causal=causal)
+            assert O.shape == (2, 2 * group, q_len, 128)
+            gate(O, L, O_ref, L_ref, what=f"Nq{q_len} g{group} {dtype} causal={causal} T{tile_n} {schedule}")
+
+
+def test_multi_token_paged_and_tiny():
+    # causal block on a paged pool, and contexts barely longer than N_q
+    p = synth.Problem(3, 4, 2, 128, [1000, 4, 70], dtype="bf16", dist="D1", seed=62, q_len=4,
+                      layout="paged", page_size=16)
+    O_ref, L_ref = run_oracle(p)
+    O, L, _ = run_cuda(p, tile_n=32, grid=0)
+    gate(O, L, O_ref, L_ref, what="Nq4 paged")

@@ -171,3 +171,29 @@ def test_paged_layout_is_the_same_rows():
         # pages of one request are scattered, and no page is shared between requests
         used = [bt[b, i] for b, n in enumerate(pp.ctx_lens) for i in range(-(-n // ps))]
         assert len(set(used)) == len(used)
+
+
+def test_multi_query_causal_against_mpmath_and_truncation():
+    # NEXT-3 (N_q > 1): query i is the cached token n - N_q + i; causally it sees keys
+    # [0, n - N_q + i].  Pinned against mpmath with the mask written out, and against
+    # single-query attention over the truncated cache.
+    rng = np.random.default_rng(21)
+    B, Hkv, g, Nq, d = 2, 2, 2, 3, 6
+    lens = [9, 5]
+    k = rng.normal(size=(B, Hkv, 9, d))
+    v = rng.normal(size=(B, Hkv, 9, d))
+    q = rng.normal(size=(B, Hkv * g, Nq, d))
+    O, L = oracle.decode_attention_multi(q, k, v, lens, 0.4, causal=True)
+    for b in range(B):
+        for hq in range(Hkv * g):
+            for i in range(Nq):
+                m = lens[b] - Nq + i + 1
+                o_mp, l_mp = _mp_attention(q[b, hq, i], k[b, hq // g, :m], v[b, hq // g, :m], 0.4)
+                assert np.max(np.abs(O[b, hq, i] - o_mp)) <= 1e-13 and abs(L[b, hq, i] - l_mp) <= 1e-13
+    On, Ln = oracle.decode_attention_multi(q, k, v, lens, 0.4, causal=False)
+    for i in range(Nq):
+        Oi, Li = oracle.decode_attention(q[:, :, i], k, v, lens, 0.4)
+        assert np.array_equal(On[:, :, i], Oi) and np.array_equal(Ln[:, :, i], Li)
+    # the last query of a causal block sees the whole cache
+    Ol, Ll = oracle.decode_attention(q[:, :, Nq - 1], k, v, lens, 0.4)
+    assert np.max(np.abs(O[:, :, Nq - 1] - Ol)) <= 1e-13
