@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential", "fixed_split"])
     ap.add_argument("--page-size", type=int, default=0, help="run the config in a paged KV pool (16..256)")
+    ap.add_argument("--tile-n", type=int, default=0, help="LeanTile size T_n (0 = planner's auto rule)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only to test the multi-rank path on one GPU)")
     ap.add_argument("--dyn-first", type=int, default=750, help="dynamic schedule: permille in the first round")
@@ -279,7 +280,7 @@ def bench_ours(args):
     v = synth.fill_kv_cache(p, "v", dev, token_range=None if args.page_size else bounds)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
                    schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min,
-                   **paged_kw)
+                   tile_n=args.tile_n, **paged_kw)
     info = plan.info
     total_kv = p.kv_bytes                       # whole job
     local_kv = info.kv_bytes

@@ -795,7 +795,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     // acc = f(...f(f(acc, P[slot(p0)]), P[slot(p0 + stride)])..., P[slot(<= p1)]), ascending
     // (Alg2§27-35); host_v's partial lives in slot 1 of its virtual CTA, everyone else's in 0
     auto fold_range = [&](int p0, int p1, int stride, int host_v) {
-      constexpr int NB = (H == 1) ? 4 : 1;  // partials whose loads are in flight together
+      // partials whose loads are in flight together: one L2 round trip per NB peers
+      constexpr int NB = (H == 1) ? (J <= 2 ? 16 : 8) : 1;
       for (int pb = p0; pb <= p1; pb += NB * stride) {
         float mp[NB][H], lp[NB][H], op[NB][H][J];
 #pragma unroll
