@@ -222,7 +222,8 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
  * la_plan_trace -- per-CTA timeline of the most recent la_decode on a plan created with
  * opts.trace = 1 (SURVEY §5 tracing; the E2 SM-balance analog of P:191).  Synchronises the
  * device.  out: HOST buffer of cap_ctas * LA_TRACE_FIELDS uint64, one record per CTA:
- * smid, t_start, t_publish (non-host partial signalled, Alg2§23; 0 if none), t_wait_begin,
+ * smid, t_start, t_publish (non-host partial signalled, Alg2§23; for a static waiting host:
+ * its peers' partials folded; 0 if none), t_wait_begin,
  * t_wait_end (host fold wait, Alg2§28; 0 if none), t_end -- %globaltimer nanoseconds.
  * *n_ctas receives G.  LA_ERR_STATE if the plan has no trace buffer.
  */

@@ -272,7 +272,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     const size_t b_begin = align(size_t(G + 1) * sizeof(int32_t));
     const size_t b_first = align(size_t(G) * sizeof(int32_t));
     const size_t b_po = align(size_t(G) * 2 * p.rows() * head_dim * sizeof(float));
-    const size_t b_pml = align(size_t(G) * 2 * p.rows() * 2 * sizeof(float));
+    const size_t b_pml = align(size_t(G) * 2 * p.rows() * 4 * sizeof(float));
     const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
     const size_t b_cnt = align((2 + U + size_t(G)) * sizeof(int));
     const size_t b_trace = opts.trace ? align(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;

@@ -632,7 +632,7 @@ struct Smem {
   static constexpr int RING = E::NST * E::STAGE_BYTES;
   static constexpr int kFB = E::FOLD_BUFS;  // consumer -> epilogue fold buffers
   static constexpr int FOLD = kFB * E::FOLD_FLOATS * 4;
-  static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB) * 8;
+  static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB + 1) * 8;
   static constexpr int MISC = kQD * 4 + kFB * int(sizeof(SegInfo));
   static constexpr int BYTES = 1024 + RING + FOLD + BARS + MISC;
 };
@@ -660,7 +660,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   uint64_t* vq_empty = vq_full + kQD;
   uint64_t* fold_full = vq_empty + kQD;
   uint64_t* fold_empty = fold_full + kFB;
-  int* vq = reinterpret_cast<int*>(fold_empty + kFB);
+  uint64_t* stage_bar = fold_empty + kFB;  // static host: peers' partials staged into the ring
+  int* vq = reinterpret_cast<int*>(stage_bar + 1);
   SegInfo* seginfo = reinterpret_cast<SegInfo*>(vq + kQD);
 
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -689,6 +690,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       mbar_init(&fold_full[b], NCW);
       mbar_init(&fold_empty[b], 1);
     }
+    mbar_init(stage_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero-fill before TMA writes
@@ -785,8 +787,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) a.part_o[row * D + lane + 32 * jj] = acc.o[h][jj];
         if (lane == 0) {
-          a.part_ml[row * 2] = acc.m[h];
-          a.part_ml[row * 2 + 1] = acc.l[h];
+          a.part_ml[row * 4] = acc.m[h];
+          a.part_ml[row * 4 + 1] = acc.l[h];
         }
       }
       __threadfence();  // every lane: its stores are visible GPU-wide before the signal
@@ -795,39 +797,130 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     // acc = f(...f(f(acc, P[slot(p0)]), P[slot(p0 + stride)])..., P[slot(<= p1)]), ascending
     // (Alg2§27-35); host_v's partial lives in slot 1 of its virtual CTA, everyone else's in 0
     auto fold_range = [&](int p0, int p1, int stride, int host_v) {
-      // partials whose loads are in flight together: one L2 round trip per NB peers
-      constexpr int NB = (H == 1) ? (J <= 2 ? 16 : 8) : 1;
-      for (int pb = p0; pb <= p1; pb += NB * stride) {
-        float mp[NB][H], lp[NB][H], op[NB][H][J];
+      // The §4.1 operator is associative (reading C22), so the fold is evaluated in the
+      // max-first form: every peer's m is read lane-parallel, the final M = max(m_acc, m_p..)
+      // is known before any O~_p is touched, and each O~_p then enters with its own weight
+      // 2^(m_p - M) (Alg2§32-34) -- the peers' loads carry no serial dependence on a running
+      // max and stream back to back, NB peers per round trip.  Rows are folded one after the
+      // other (few live registers).  Fixed order: bitwise deterministic.
+      const int n = p1 < p0 ? 0 : (p1 - p0) / stride + 1;
+      auto row_of = [&](int i, int h) {
+        const int p = p0 + i * stride;
+        return (size_t(p + (p == host_v ? NV : 0))) * a.group + h;
+      };
+      constexpr int NB = 8;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const int p = pb + b * stride;
-          if (p > p1) continue;
-          const size_t slot = size_t(2 * p + (p == host_v ? 1 : 0));
+      for (int h = 0; h < H; ++h) {
+        if (h >= a.group) continue;
+        float M = acc.m[h], lsum = 0.f;
+        for (int i = lane; i < n; i += 32) M = fmaxf(M, ld_cg(&a.part_ml[row_of(i, h) * 4]));
 #pragma unroll
-          for (int h = 0; h < H; ++h) {
-            if (h >= a.group) continue;
-            const size_t row = slot * a.group + h;
-            mp[b][h] = ld_cg(&a.part_ml[row * 2]);
-            lp[b][h] = ld_cg(&a.part_ml[row * 2 + 1]);
+        for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float wa = ex2_sub(acc.m[h], M);  // idle / masked accumulator: -inf -> 0
 #pragma unroll
-            for (int jj = 0; jj < J; ++jj) op[b][h][jj] = ld_cg(&a.part_o[row * D + lane + 32 * jj]);
+        for (int jj = 0; jj < J; ++jj) acc.o[h][jj] *= wa;
+        for (int c = 0; c < n; c += 32) {
+          float w = 0.f;
+          if (c + lane < n) {
+            const size_t row = row_of(c + lane, h);
+            w = ex2_sub(ld_cg(&a.part_ml[row * 4]), M);
+            lsum = fmaf(w, ld_cg(&a.part_ml[row * 4 + 1]), lsum);
+          }
+          const int cn = min(32, n - c);
+          for (int jb = 0; jb < cn; jb += NB) {
+            float op[NB][J];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              if (jb + b >= cn) continue;
+              const size_t row = row_of(c + jb + b, h);
+#pragma unroll
+              for (int jj = 0; jj < J; ++jj) op[b][jj] = ld_cg(&a.part_o[row * D + lane + 32 * jj]);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              const float wb = __shfl_sync(0xffffffffu, w, (jb + b) & 31);
+              if (jb + b >= cn) continue;
+#pragma unroll
+              for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = fmaf(wb, op[b][jj], acc.o[h][jj]);
+            }
           }
         }
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          if (pb + b * stride > p1) continue;
-#pragma unroll
-          for (int h = 0; h < H; ++h) {
-            if (h >= a.group) continue;
-            const float mn = fmaxf(acc.m[h], mp[b][h]);
-            const float wa = ex2_sub(acc.m[h], mn), wb = ex2_sub(mp[b][h], mn);  // Alg2§32-34
-            acc.l[h] = wa * acc.l[h] + wb * lp[b][h];
-#pragma unroll
-            for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = wa * acc.o[h][jj] + wb * op[b][h][jj];
-            acc.m[h] = mn;
-          }
+        for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        acc.l[h] = fmaf(wa, acc.l[h], lsum);
+        acc.m[h] = M;
+      }
+    };
+    // Static host: the same max-first fold of peers p0..p1, staged through the ring.  A
+    // non-finishing host segment is its CTA's last (its unit runs past the CTA's range), so
+    // the ring is idle.  Slot-0 partials of consecutive virtual CTAs are contiguous, so ONE
+    // 1-D bulk copy brings every peer's O~ rows and one more their (m, l) rows: a single
+    // round trip and two issues (per-peer or per-16-byte copies are issue-bound on the one
+    // epilogue warp -- measured ~7 us for 127 peers).  Then folded from smem with four
+    // independent accumulator chains (fixed order: deterministic).
+    auto fold_staged = [&](int p0, int p1) {
+      float* stg = reinterpret_cast<float*>(ring);
+      const int rows = a.group;
+      const int po = rows * D, pm = rows * 4;  // floats per peer: O~ rows, (m, l, -, -) rows
+      const int cap = max(1, (Smem<E>::RING / 4) / (po + pm));
+      const int n = p1 - p0 + 1;
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired partials -> TMA reads
+      for (int c0 = 0, ph = 0; c0 < n; c0 += cap, ph ^= 1) {
+        const int cn = min(cap, n - c0);
+        float* so = stg;            // [cn][rows][D]
+        float* sm = stg + cn * po;  // [cn][rows][4]
+        if (lane == 0) {
+          mbar_arrive_expect_tx(stage_bar, uint32_t(cn) * (po + pm) * 4);
+          bulk_g2s_plain(so, a.part_o + size_t(p0 + c0) * po, uint32_t(cn) * po * 4, stage_bar);
+          bulk_g2s_plain(sm, a.part_ml + size_t(p0 + c0) * pm, uint32_t(cn) * pm * 4, stage_bar);
         }
+        mbar_wait(stage_bar, ph);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          if (h >= rows) continue;
+          float M = acc.m[h], lsum = 0.f;
+          for (int i = lane; i < cn; i += 32) M = fmaxf(M, sm[i * pm + 4 * h]);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+          for (int i = lane; i < cn; i += 32) {
+            float* ml = sm + i * pm + 4 * h;
+            const float w = ex2_sub(ml[0], M);
+            lsum = fmaf(w, ml[1], lsum);
+            ml[2] = w;
+          }
+          __syncwarp();
+          const float wa = ex2_sub(acc.m[h], M);
+          float o4[4][J];
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) {
+            o4[0][jj] = acc.o[h][jj] * wa;
+            o4[1][jj] = o4[2][jj] = o4[3][jj] = 0.f;
+          }
+          int i = 0;
+          for (; i + 4 <= cn; i += 4) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float w = sm[(i + c) * pm + 4 * h + 2];
+              const float* r = so + (i + c) * po + h * D;
+#pragma unroll
+              for (int jj = 0; jj < J; ++jj) o4[c][jj] = fmaf(w, r[lane + 32 * jj], o4[c][jj]);
+            }
+          }
+          for (; i < cn; ++i) {
+            const float w = sm[i * pm + 4 * h + 2];
+            const float* r = so + i * po + h * D;
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) o4[0][jj] = fmaf(w, r[lane + 32 * jj], o4[0][jj]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = (o4[0][jj] + o4[1][jj]) + (o4[2][jj] + o4[3][jj]);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+          acc.l[h] = fmaf(wa, acc.l[h], lsum);
+          acc.m[h] = M;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the next TMA
+        __syncwarp();
       }
     };
     auto write_out = [&](int q_row) {  // O = diag(l)^-1 O; L = m + log(l) (Alg2§38-39, C2)
@@ -879,7 +972,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       } else if (!dynamic) {
         if (!si.host) {
           // ---- static, non-host: StorePartials + Signal(flags[g]) (Alg2§19-23) -----------
-          store_partial(2 * v);
+          store_partial(v);
           if (lane == 0) {
             st_release_gpu(&a.flags[v], a.epoch);
             if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
@@ -892,7 +985,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
             while (ld_acquire_gpu(&a.flags[p]) != a.epoch) __nanosleep(20);
           __syncwarp();
           if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
-          fold_range(v + 1, u.last_cta, 1, -1);
+          fold_staged(v + 1, u.last_cta);
+          if (tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
           write_out(u.q_row);
         }
       } else {
@@ -905,7 +999,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         const int ngrp = (nseg + kGS - 1) / kGS;
         const int g0 = hv + ((v - hv) / kGS) * kGS;
         const int g1 = min(g0 + kGS, u.last_cta + 1) - 1;
-        store_partial(2 * v + (si.host ? 1 : 0));
+        store_partial(v + (si.host ? NV : 0));
         int role = 0;
         if (lane == 0) {
           if (atomicAdd(&a.grp_count[g0], 1) == g1 - g0) {
@@ -922,7 +1016,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           if (ngrp == 1) {
             write_out(u.q_row);
           } else {
-            store_partial(2 * g0 + (g0 == hv ? 1 : 0));
+            store_partial(g0 + (g0 == hv ? NV : 0));
             int last = 0;
             if (lane == 0 && atomicAdd(&a.unit_count[si.unit], 1) == ngrp - 1) {
               __threadfence();

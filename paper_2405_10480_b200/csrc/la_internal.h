@@ -84,8 +84,8 @@ struct DecodeArgs {
   const DevUnit* units;
   const int32_t* cta_begin;
   const int32_t* cta_first_unit;
-  float* part_o;      // [grid][2][group][d]  Op of Alg2§20 (slot 1: dynamic-mode host partial)
-  float* part_ml;     // [grid][2][group][2]  mp, lp of Alg2§21-22 (m in log2 units)
+  float* part_o;      // [2][grid][group][d]  Op of Alg2§20 (slot 1: dynamic-mode host partial)
+  float* part_ml;     // [2][grid][group][4]  mp, lp, -, - of Alg2§21-22 (m in log2 units; 16 B rows)
   uint32_t* flags;    // [grid]               flags of Alg2§23/§28, epoch-valued (reading C17)
   int* counters;      // [2] dynamic mode: virtual-CTA claim counter, CTAs done
   int* unit_count;    // [units] dynamic mode: fold-tree groups completed per unit

@@ -63,6 +63,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 1-D TMA bulk copy global -> shared without a cache hint.
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -103,7 +111,6 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2; ex2(-inf) = +
 // 2^(x - m) with the neutral element's m = -inf mapped to weight 0 (never -inf - -inf = NaN):
 // x <= m always holds for the callers, so m = -inf implies x = -inf.
 __device__ __forceinline__ float ex2_sub(float x, float m) { return ex2(x - (m == -INFINITY ? 0.f : m)); }
-
 
 }  // namespace dev
 }  // namespace la
