@@ -394,7 +394,7 @@ def bench_ours(args):
             "metric": METRIC, "value": total_kv / (step_ms * 1e-3) / 1e9, "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "latency_us": step_ms * 1e3, "higher_is_better": True,
-            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": p.dtype,
             "data": "synthetic (seeded counter-based generator, distribution D1; DESIGN.md input recipe)",
             "config": {"workload": f"{cfg}: {WORKLOADS[cfg]}", "batch": p.batch, "heads_q": p.heads_q,
                        "heads_kv": p.heads_kv, "head_dim": p.head_dim,
@@ -408,7 +408,7 @@ def bench_ours(args):
                        f"sequence-sharded x{world} + {args.backend.upper()} all-gather + la_combine"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": ("la_decode_gqa<bf16,128>" if p.group > 1 else "la_decode_mha<bf16,128>"), "kernel_us": kern_ms * 1e3,
+                         "kernel": f"la_decode<{'Gqa' if info.group > 1 else 'Mha'}Engine<{p.dtype},{p.head_dim}>>", "kernel_us": kern_ms * 1e3,
                          "algorithmic_bytes_per_launch": local_kv,
                          "read_probe_gbs": read_probe_gbs(),
                          "frac_of_read_probe": (achieved / read_probe_gbs()) if read_probe_gbs() else None},

@@ -61,20 +61,14 @@ la_status cuda_fail(cudaError_t e, const char* what) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int auto_tile_n(const la::Problem& p, int max_ctas) {
+int auto_tile_n(const la::Problem& p, int /*max_ctas*/) {
   // 64 KiB of K+V per LeanTile: 128 tokens at d=128 and 256 at d=64 for 16-bit inputs,
-  // the sizes the paper's sweep found; halved while the problem has fewer
-  // LeanTiles than resident CTAs so small problems still spread over the machine.
+  // the sizes the paper's sweep found, whatever the problem size.  Smaller tiles
+  // for problems with fewer LeanTiles than SMs were measured never faster on B200 and up to
+  // 18% slower (scripts/sweep_tile.py: a single-unit problem split over more CTAs has its
+  // host fold more peers; the load is latency-, not bandwidth-bound at that size).
   const int row_bytes = p.head_dim * p.elem_bytes();
-  int t = 65536 / (2 * row_bytes);
-  t = std::max(32, std::min(512, t));
-  auto iters = [&](int tn) {
-    int64_t I = 0;
-    for (int32_t n : p.ctx_lens) I += (int64_t(n) + tn - 1) / tn;
-    return I * p.heads_kv;
-  };
-  while (t > 32 && iters(t) < max_ctas) t /= 2;
-  return t;
+  return std::max(32, std::min(512, 65536 / (2 * row_bytes)));
 }
 
 void release_device(la_plan_s* p) {

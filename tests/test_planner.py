@@ -108,7 +108,7 @@ def test_auto_tile_and_sequential(la):
     p = la.Plan(1, 8, 8, 64, [1 << 16], host_only=True)
     assert p.info.tile_n == 256                                  # P:396 for d=64
     p = la.Plan(1, 1, 1, 64, [4096], dtype="fp32", host_only=True)
-    assert p.info.total_iters >= 64                              # small problem spread out
+    assert p.info.tile_n == 128 and p.info.grid == 32            # 64 KiB LeanTiles, not split further
     p = la.Plan(2, 3, 3, 128, [300, 1000], tile_n=64, host_only=True, schedule="sequential")
     rows = p.export()
     assert p.info.grid == 6 and len(rows) == 6
