@@ -36,7 +36,7 @@ WORKLOADS = {
     "c2": "batch 1, 32 heads, head_dim 128, context 256k, bf16 KV cache, 1 B200",
     "c3": "batch 8, 64 q-heads / 8 kv-heads (GQA), head_dim 128, context 64k, bf16",
     "c4": "batch 16, 32 heads, head_dim 128, ragged context lengths 1k-128k per request",
-    "c5": "batch 1, 32 heads, head_dim 128, context 1M, KV sequence-sharded across N B200 with NCCL partial combine",
+    "c5": "batch 1, 32 heads, head_dim 128, context 1M, KV sequence-sharded across N B200 (partials exchanged and combined across GPUs)",
 }
 L2_BYTES = 126 * 1024 * 1024
 
@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--tile-n", type=int, default=0, help="LeanTile size T_n (0 = planner's auto rule)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only to test the multi-rank path on one GPU)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N > 1: the fused in-kernel NVLink exchange (p2p, NEXT-2) or NCCL all-gather + "
+                         "la_combine; auto = p2p on the nccl backend")
     ap.add_argument("--dyn-first", type=int, default=750, help="dynamic schedule: permille in the first round")
     ap.add_argument("--dyn-min", type=int, default=2, help="dynamic schedule: smallest virtual CTA (LeanTiles)")
     return ap.parse_args()
@@ -274,13 +277,22 @@ def bench_ours(args):
         paged_kw = dict(block_table=bt, page_size=args.page_size, num_pages=num_pages)
     bounds = synth.shard_bounds(p, rank, world)
     lens = [b - a for a, b in bounds]
+    fused = world > 1 and (args.exchange == "p2p" or (args.exchange == "auto" and args.backend == "nccl"))
 
     q = synth.gen_q(p, dev)
     k = synth.fill_kv_cache(p, "k", dev, token_range=None if args.page_size else bounds)
     v = synth.fill_kv_cache(p, "v", dev, token_range=None if args.page_size else bounds)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
                    schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min,
-                   tile_n=args.tile_n, **paged_kw)
+                   tile_n=args.tile_n, **paged_kw,
+                   **(dict(xchg_world=world, xchg_rank=rank) if fused else {}))
+    xchg_note = None
+    if fused:   # collective decision: every rank maps every peer's buffer, or all use NCCL
+        try:
+            sharded.connect_exchange(plan)
+        except RuntimeError as e:   # raised identically on every rank
+            fused = False
+            xchg_note = {"p2p_unavailable": str(e).splitlines()[0][:300]}
     info = plan.info
     total_kv = p.kv_bytes                       # whole job
     local_kv = info.kv_bytes
@@ -300,19 +312,41 @@ def bench_ours(args):
             flush.zero_()
         if ev0 is not None:
             ev0.record(stream)
-        if world == 1:
+        if world == 1 or fused:   # fused: the exchange and the fold run inside this launch
             plan.decode(q, k, v, out, lse, stream=stream)
         else:
             plan.decode_partial(q, k, v, out, lse, stream=stream)
         if ev1 is not None:
             ev1.record(stream)
-        if world > 1:   # sharded.sequence_sharded_decode with preallocated buffers
+        if world > 1 and not fused:   # sharded.sequence_sharded_decode with preallocated buffers
             gather(out.view(rows, p.head_dim), lse.view(rows), o_all, l_all)
             la.la_combine(o_all, l_all, fin_o, fin_l, stream=stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    if fused:   # the fused exchange must agree with partial + all-gather + la_combine
+        bad = 0.0
+        try:
+            plan.xchg_status()
+        except la.LaError:
+            bad = 1.0
+        plan.decode_partial(q, k, v, out, lse, stream=stream)
+        gather(out.view(rows, p.head_dim), lse.view(rows), o_all, l_all)
+        ref_o, ref_l = la.la_combine(o_all, l_all, stream=stream)
+        plan.decode(q, k, v, out, lse, stream=stream)
+        try:
+            plan.xchg_status()
+        except la.LaError:
+            bad = 1.0
+        chk = torch.tensor([bad, (out.view(rows, -1) - ref_o).abs().max().item(),
+                            (lse.view(rows) - ref_l).abs().max().item()], dtype=torch.float64, device=dev)
+        dist.all_reduce(chk, op=dist.ReduceOp.MAX)   # one collective decision for all ranks
+        bad, do, dl = chk.tolist()
+        xchg_note = {"max_abs_diff_vs_nccl_combine": [do, dl]}
+        if bad or max(do, dl) > 1e-5:
+            fused = False
+            xchg_note["p2p_rejected"] = "exchange wait timed out" if bad else "disagrees with the NCCL combine"
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -360,7 +394,7 @@ def bench_ours(args):
         e0.record(stream)
         for _ in range(args.e2e_steps):
             plan.decode_host(qh, kh, vh, oh, lh, stream=stream)
-            if world > 1:
+            if world > 1 and not fused:
                 o_dev = oh.to(dev, non_blocking=True).view(rows, p.head_dim)
                 l_dev = lh.to(dev, non_blocking=True).view(rows)
                 gather(o_dev, l_dev, oh_all, lh_all)
@@ -405,7 +439,9 @@ def bench_ours(args):
                        "virtual_ctas": info.num_vctas,
                        "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),
                        "parallelism": "single GPU" if world == 1 else
-                       f"sequence-sharded x{world} + {args.backend.upper()} all-gather + la_combine"},
+                       (f"sequence-sharded x{world}, fused in-kernel NVLink exchange (NEXT-2)" if fused else
+                        f"sequence-sharded x{world} + {args.backend.upper()} all-gather + la_combine"),
+                       **({"exchange_check": xchg_note} if xchg_note else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": f"la_decode<{'Gqa' if info.group > 1 else 'Mha'}Engine<{p.dtype},{p.head_dim}>>", "kernel_us": kern_ms * 1e3,

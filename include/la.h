@@ -48,7 +48,8 @@ typedef enum {
   LA_ERR_UNSUPPORTED = 2,  /* valid request this build does not implement (dtype, d, g)  */
   LA_ERR_CUDA = 3,         /* a CUDA runtime call failed (message in la_last_error)     */
   LA_ERR_NOMEM = 4,        /* device or host allocation failed                          */
-  LA_ERR_STATE = 5         /* e.g. la_decode on a host-only plan                         */
+  LA_ERR_STATE = 5,        /* e.g. la_decode on a host-only plan                         */
+  LA_ERR_TIMEOUT = 6       /* a cross-GPU exchange wait gave up (a peer never arrived)   */
 } la_status;
 
 /* Storage type of Q, K and V ("FP16->32": 16-bit inputs, fp32 arithmetic). */
@@ -117,6 +118,11 @@ typedef struct {
   int causal;                 /* 1 (default): query i of N_q is the token at position
                                  n - N_q + i and attends to keys [0, n - N_q + i]; 0: every
                                  query attends to all n keys                                 */
+  /* Fused cross-GPU sequence-shard exchange (NEXT-2; see la_plan_xchg_handle): */
+  int xchg_world;             /* P ranks (2..8) each holding a contiguous shard of every
+                                 request's context; 0 or 1 = off.  With P > 1, la_decode on
+                                 rank r's shard returns the FULL result on every rank      */
+  int xchg_rank;              /* this plan's rank r in [0, P)                               */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;
@@ -148,8 +154,7 @@ la_status la_plan_opts_init(la_plan_opts* opts);
  * batch, heads_q, heads_kv >= 1, heads_q % heads_kv == 0 (reading C3); head_dim in
  * {64, 128}; ctx_lens: HOST array of `batch` int32, each >= 1 (reading C6); tile_n: LeanTile
  * tokens in {16, 32, 64, 128, 256, 512}, or 0 for the default (T_n giving 64 KiB of K+V per
- * LeanTile -- 128 tokens at d=128 bf16, 256 at d=64, as the paper's sweep found, P:396 --
- * halved while I < #SMs so small problems still fill the machine).
+ * LeanTile -- 128 tokens at d=128 bf16, 256 at d=64, as the paper's sweep found).
  * dtype: storage type of q, k, v.  opts may be NULL (defaults).
  *
  * Implements Alg2§4-18: units in memory order, C_n(u) = ceil(n_u / T_n), I = sum C_n,
@@ -191,7 +196,8 @@ la_status la_decode(la_plan_t plan, const void* q, const void* k_cache, const vo
 /*
  * la_decode_partial -- la_decode on one sequence shard of the KV cache (BASELINE.json
  * north star, multi-GPU): identical computation, `lse` is mandatory because the shard's
- * (O_r, L_r) is then combined across ranks with la_combine.
+ * (O_r, L_r) is then combined across ranks with la_combine.  On a plan with a cross-GPU
+ * exchange (opts.xchg_world > 1) it returns this shard's partial only (no exchange).
  */
 la_status la_decode_partial(la_plan_t plan, const void* q, const void* k_shard,
                             const void* v_shard, float* o_part, float* lse_part, void* stream);
@@ -229,6 +235,37 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
  */
 #define LA_TRACE_FIELDS 6
 la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* n_ctas);
+
+/*
+ * Fused cross-GPU fixup: Alg. 2's in-kernel fixup (Alg2§19-36) extended
+ * across the NVLink domain for a sequence-sharded decode.  Rank r's plan covers its shard
+ * of every request's context (same batch, heads, head_dim, dtype, q_len on every rank).
+ * When the kernel has reduced unit u (b, h_kv) on its shard, the CTA that would write the
+ * output instead pushes the normalised shard partial (O_r, L_r) of the unit's rows into
+ * EVERY rank's exchange buffer (plain stores to peer HBM over NVLink), releases flag
+ * [r][u] there (st.release.sys), then acquires the P flags [*][u] in its own buffer and
+ * folds the P partials with the §4.1 operator in ascending rank order -- bitwise the same
+ * result on every rank, no NCCL launch and no combine kernel.  Exact by associativity
+ * (P:264).  Buffers are double-buffered by launch parity, so ranks may run one launch
+ * apart.  Every rank must issue the same sequence of la_decode calls.
+ *
+ * la_plan_xchg_handle: the CUDA IPC handle (LA_XCHG_HANDLE_BYTES bytes into `handle`) of
+ *   this plan's exchange buffer, to be sent to the other ranks (e.g. all_gather_object).
+ * la_plan_xchg_open: map peer `peer`'s buffer from its handle (cudaIpcOpenMemHandle; the
+ *   peer must live in another process on a peer-accessible GPU).
+ * la_plan_xchg_attach: use the buffer of `peer_plan` (same process) as rank `peer`'s --
+ *   for one process driving several GPUs with peer access enabled, or several "ranks"
+ *   sharing one GPU (tests).
+ * la_decode on an exchange plan needs every peer opened/attached (LA_ERR_STATE otherwise).
+ * la_plan_xchg_status: synchronises the device; LA_ERR_TIMEOUT if any wait of a previous
+ *   la_decode on this plan gave up after 5 s (its output is then invalid), else LA_OK.
+ * Requires q_len == 1 or causal == 0 (a causal multi-token mask is not shard-local).
+ */
+#define LA_XCHG_HANDLE_BYTES 64
+la_status la_plan_xchg_handle(la_plan_t plan, void* handle);
+la_status la_plan_xchg_open(la_plan_t plan, int peer, const void* handle);
+la_status la_plan_xchg_attach(la_plan_t plan, int peer, la_plan_t peer_plan);
+la_status la_plan_xchg_status(la_plan_t plan);
 
 /* Release a plan and all device memory it owns.  NULL is a no-op. */
 void la_plan_destroy(la_plan_t plan);

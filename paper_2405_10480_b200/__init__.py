@@ -4,6 +4,10 @@ The hot path lives in ``csrc/`` (CUDA kernels for sm_100a + host planner + C ABI
 into ``lib/libleanattn.so``); :mod:`.leanattn` marshals torch tensors into it.  There is no
 CPU or library fallback on the product path.
 """
-from .leanattn import (Plan, la_plan, la_combine, launch_count, lib, LaError, LIB_PATH, EXPORTS)
+from .leanattn import (Plan, la_plan, la_combine, launch_count, lib, LaError, LIB_PATH, EXPORTS,
+                       LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE,
+                       LA_ERR_TIMEOUT)
 
-__all__ = ["Plan", "la_plan", "la_combine", "launch_count", "lib", "LaError", "LIB_PATH", "EXPORTS"]
+__all__ = ["Plan", "la_plan", "la_combine", "launch_count", "lib", "LaError", "LIB_PATH", "EXPORTS",
+           "LA_OK", "LA_ERR_INVALID", "LA_ERR_UNSUPPORTED", "LA_ERR_CUDA", "LA_ERR_NOMEM", "LA_ERR_STATE",
+           "LA_ERR_TIMEOUT"]

@@ -42,6 +42,12 @@ struct la_plan_s {
   // la_decode_host staging
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
+  // NEXT-2 cross-GPU exchange (xw > 1)
+  int xw = 0, xr = 0;
+  void* d_xchg = nullptr;           // own buffer (separate allocation: it is IPC-exported)
+  size_t xflag_off = 0;
+  float* xpeer[la::kMaxXchgWorld] = {};
+  bool xpeer_ipc[la::kMaxXchgWorld] = {};
 };
 
 namespace {
@@ -72,10 +78,23 @@ int auto_tile_n(const la::Problem& p, int /*max_ctas*/) {
 }
 
 void release_device(la_plan_s* p) {
+  for (int r = 0; r < la::kMaxXchgWorld; ++r)
+    if (p->xpeer_ipc[r] && p->xpeer[r]) cudaIpcCloseMemHandle(p->xpeer[r]);
+  if (p->d_xchg) cudaFree(p->d_xchg);
   if (p->d_tables) cudaFree(p->d_tables);
   if (p->d_stage) cudaFree(p->d_stage);
   p->d_tables = nullptr;
   p->d_stage = nullptr;
+  p->d_xchg = nullptr;
+}
+
+// Exchange buffer layout (DecodeArgs::xpeer): [2][P][rows][d + 4] fp32, then [P][units]
+// uint32 flags, then one int error word.
+size_t xchg_flag_off(const la::Problem& p, int P) {
+  return (size_t(2) * P * p.batch * p.heads_q * p.q_len * (p.head_dim + 4) * sizeof(float) + 255) & ~size_t(255);
+}
+size_t xchg_bytes(const la::Problem& p, int P) {
+  return xchg_flag_off(p, P) + ((size_t(P) * p.batch * p.heads_kv * sizeof(uint32_t) + 255) & ~size_t(255)) + 256;
 }
 
 }  // namespace
@@ -94,6 +113,7 @@ const char* la_status_string(la_status s) {
     case LA_ERR_CUDA: return "LA_ERR_CUDA";
     case LA_ERR_NOMEM: return "LA_ERR_NOMEM";
     case LA_ERR_STATE: return "LA_ERR_STATE";
+    case LA_ERR_TIMEOUT: return "LA_ERR_TIMEOUT";
   }
   return "LA_ERR_UNKNOWN";
 }
@@ -138,6 +158,12 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
       tile_n != 512)
     return fail(LA_ERR_INVALID, "tile_n must be 0 or one of 16..512 (powers of two)");
   if (opts.grid < 0) return fail(LA_ERR_INVALID, "grid must be >= 0");
+  const int xw = opts.xchg_world > 1 ? opts.xchg_world : 0;
+  if (opts.xchg_world < 0 || xw > la::kMaxXchgWorld)
+    return fail(LA_ERR_INVALID, "xchg_world must be in 0..8");
+  if (xw && (opts.xchg_rank < 0 || opts.xchg_rank >= xw)) return fail(LA_ERR_INVALID, "xchg_rank out of range");
+  if (xw && opts.q_len > 1 && opts.causal)
+    return fail(LA_ERR_UNSUPPORTED, "sequence-shard exchange needs q_len == 1 or causal == 0");
 
   la::Problem p;
   p.batch = batch;
@@ -188,6 +214,8 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (!plan) return fail(LA_ERR_NOMEM, "host allocation failed");
   plan->prob = p;
   plan->host_only = opts.host_only != 0;
+  plan->xw = xw;
+  plan->xr = xw ? opts.xchg_rank : 0;
 
   // ---- co-resident CTA budget (reading C15) -----------------------------------------
   int max_ctas = 0;
@@ -310,6 +338,19 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
       delete plan;
       return cuda_fail(e, "plan upload");
     }
+    if (plan->xw) {
+      const size_t xb = xchg_bytes(p, plan->xw);
+      plan->xflag_off = xchg_flag_off(p, plan->xw);
+      e = cudaMalloc(&plan->d_xchg, xb);
+      if (e == cudaSuccess) e = cudaMemset(plan->d_xchg, 0, xb);
+      if (e != cudaSuccess) {
+        release_device(plan);
+        delete plan;
+        return cuda_fail(e, "exchange buffer");
+      }
+      plan->xpeer[plan->xr] = static_cast<float*>(plan->d_xchg);
+      plan->workspace += int64_t(xb);
+    }
   }
   *out = plan;
   return LA_OK;
@@ -358,7 +399,7 @@ la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t*
 }
 
 static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const void* v, float* out,
-                             float* lse, void* stream) {
+                             float* lse, void* stream, bool xchg = true) {
   if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
   if (plan->host_only) return fail(LA_ERR_STATE, "host-only plan cannot decode");
   if (!q || !k || !v || !out) return fail(LA_ERR_INVALID, "NULL tensor pointer");
@@ -401,6 +442,17 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.q_len = plan->prob.q_len;
   a.causal = plan->prob.causal;
   a.scale_log2 = float(double(plan->prob.scale) * 1.4426950408889634);
+  if (plan->xw && xchg) {
+    for (int r = 0; r < plan->xw; ++r)
+      if (!plan->xpeer[r]) return fail(LA_ERR_STATE, "exchange peer " + std::to_string(r) + " not opened/attached");
+    a.xw = plan->xw;
+    a.xr = plan->xr;
+    a.xrows = plan->prob.batch * plan->prob.heads_q * plan->prob.q_len;
+    a.xunits = plan->prob.batch * plan->prob.heads_kv;
+    a.xflag_off = plan->xflag_off;
+    for (int r = 0; r < plan->xw; ++r) a.xpeer[r] = plan->xpeer[r];
+    a.xerr = reinterpret_cast<int*>(static_cast<char*>(plan->d_xchg) + xchg_bytes(plan->prob, plan->xw) - 256);
+  }
   std::string err;
   const la::Problem& p = plan->prob;
   const int rc = la::launch_decode(plan->kinfo, a, p.kv_rows(), p.head_dim, p.dtype, plan->needs_wait, stream, err);
@@ -416,7 +468,7 @@ la_status la_decode(la_plan_t plan, const void* q, const void* k_cache, const vo
 la_status la_decode_partial(la_plan_t plan, const void* q, const void* k_shard, const void* v_shard,
                             float* o_part, float* lse_part, void* stream) {
   if (!lse_part) return fail(LA_ERR_INVALID, "la_decode_partial needs lse_part");
-  return decode_impl(plan, q, k_shard, v_shard, o_part, lse_part, stream);
+  return decode_impl(plan, q, k_shard, v_shard, o_part, lse_part, stream, /*xchg=*/false);
 }
 
 la_status la_combine(const float* o_parts, const float* lse_parts, int parts, int rows, int head_dim,
@@ -483,6 +535,59 @@ la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* 
   if (e == cudaSuccess)
     e = cudaMemcpy(out, plan->d_trace, G * LA_TRACE_FIELDS * sizeof(uint64_t), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "la_plan_trace");
+  return LA_OK;
+}
+
+la_status la_plan_xchg_handle(la_plan_t plan, void* handle) {
+  if (!plan || !handle) return fail(LA_ERR_INVALID, "NULL argument");
+  if (!plan->d_xchg) return fail(LA_ERR_STATE, "plan has no exchange buffer (xchg_world <= 1 or host-only)");
+  static_assert(sizeof(cudaIpcMemHandle_t) == LA_XCHG_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, plan->d_xchg);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, sizeof(h));
+  return LA_OK;
+}
+
+la_status la_plan_xchg_open(la_plan_t plan, int peer, const void* handle) {
+  if (!plan || !handle) return fail(LA_ERR_INVALID, "NULL argument");
+  if (!plan->d_xchg) return fail(LA_ERR_STATE, "plan has no exchange buffer");
+  if (peer < 0 || peer >= plan->xw || peer == plan->xr) return fail(LA_ERR_INVALID, "bad peer rank");
+  if (plan->xpeer[peer]) return fail(LA_ERR_STATE, "peer already opened/attached");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* ptr = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  plan->xpeer[peer] = static_cast<float*>(ptr);
+  plan->xpeer_ipc[peer] = true;
+  return LA_OK;
+}
+
+la_status la_plan_xchg_attach(la_plan_t plan, int peer, la_plan_t peer_plan) {
+  if (!plan || !peer_plan) return fail(LA_ERR_INVALID, "NULL argument");
+  if (!plan->d_xchg || !peer_plan->d_xchg) return fail(LA_ERR_STATE, "plan has no exchange buffer");
+  if (peer < 0 || peer >= plan->xw || peer == plan->xr) return fail(LA_ERR_INVALID, "bad peer rank");
+  if (peer_plan->xw != plan->xw || peer_plan->xr != peer) return fail(LA_ERR_INVALID, "peer plan has another rank/world");
+  const la::Problem &p = plan->prob, &q = peer_plan->prob;
+  if (p.batch != q.batch || p.heads_q != q.heads_q || p.heads_kv != q.heads_kv || p.head_dim != q.head_dim ||
+      p.q_len != q.q_len)
+    return fail(LA_ERR_INVALID, "peer plan has another shape");
+  if (plan->xpeer[peer]) return fail(LA_ERR_STATE, "peer already opened/attached");
+  plan->xpeer[peer] = static_cast<float*>(peer_plan->d_xchg);
+  return LA_OK;
+}
+
+la_status la_plan_xchg_status(la_plan_t plan) {
+  if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
+  if (!plan->d_xchg) return fail(LA_ERR_STATE, "plan has no exchange buffer");
+  int err = 0;
+  int* d_err = reinterpret_cast<int*>(static_cast<char*>(plan->d_xchg) + xchg_bytes(plan->prob, plan->xw) - 256);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && err) e = cudaMemset(d_err, 0, sizeof(int));
+  if (e != cudaSuccess) return cuda_fail(e, "la_plan_xchg_status");
+  if (err) return fail(LA_ERR_TIMEOUT, "a cross-GPU exchange wait timed out (a peer rank never arrived)");
   return LA_OK;
 }
 

@@ -923,7 +923,68 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         __syncwarp();
       }
     };
-    auto write_out = [&](int q_row) {  // O = diag(l)^-1 O; L = m + log(l) (Alg2§38-39, C2)
+    // NEXT-2: push this rank's normalised shard partial of unit `unit` into every rank's
+    // exchange buffer, release flag [xr][unit] there, acquire the P flags of the unit here
+    // and fold the P partials ascending (§4.1 operator; bitwise equal on every rank).
+    auto xchg_out = [&](int q_row, int unit) {
+      constexpr int RS = D + 4;
+      const int P = a.xw, par = int(a.epoch & 1u);
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        if (h >= a.group) continue;
+        const float inv = 1.f / acc.l[h], l2 = acc.m[h] + log2f(acc.l[h]);
+        for (int d = 0; d < P; ++d) {
+          float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + q_row + h) * RS;
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) dst[lane + 32 * jj] = acc.o[h][jj] * inv;
+          if (lane == 0) dst[D] = l2;
+        }
+      }
+      __threadfence_system();
+      __syncwarp();
+      if (lane < P) {
+        uint32_t* f = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(a.xpeer[lane]) + a.xflag_off);
+        st_release_sys(f + size_t(a.xr) * a.xunits + unit, a.epoch);
+        const uint32_t* mine = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(a.xpeer[a.xr]) +
+                                                                 a.xflag_off) + size_t(lane) * a.xunits + unit;
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_sys(mine) != a.epoch) {
+          // a peer never arrived: flag it and move on (later waits then give up at once)
+          if (*reinterpret_cast<volatile int*>(a.xerr) || globaltimer() - t0 > 5000000000ull) {
+            atomicExch(a.xerr, 1);
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      __syncwarp();
+      const float* xb = a.xpeer[a.xr] + size_t(par) * P * a.xrows * RS;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        if (h >= a.group) continue;
+        float M = -INFINITY;
+        for (int r = 0; r < P; ++r) M = fmaxf(M, ld_cg(xb + (size_t(r) * a.xrows + q_row + h) * RS + D));
+        float l = 0.f, o[J];
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
+        for (int r = 0; r < P; ++r) {
+          const float* src = xb + (size_t(r) * a.xrows + q_row + h) * RS;
+          const float w = ex2_sub(ld_cg(src + D), M);
+          l += w;
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(w, ld_cg(src + lane + 32 * jj), o[jj]);
+        }
+        const float inv = 1.f / l;
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) a.out[size_t(q_row + h) * D + lane + 32 * jj] = o[jj] * inv;
+        if (lane == 0 && a.lse) a.lse[q_row + h] = (M + log2f(l)) * kLn2;
+      }
+    };
+    auto write_out = [&](int q_row, int unit) {  // O = diag(l)^-1 O; L = m + log(l) (Alg2§38-39, C2)
+      if (a.xw > 1) {
+        xchg_out(q_row, unit);
+        return;
+      }
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         if (h >= a.group) continue;
@@ -968,7 +1029,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       const int v = si.v;
 
       if (si.host && si.finishing) {
-        write_out(u.q_row);  // one (virtual) CTA computed the whole unit (Alg2§38-39)
+        write_out(u.q_row, si.unit);  // one (virtual) CTA computed the whole unit (Alg2§38-39)
       } else if (!dynamic) {
         if (!si.host) {
           // ---- static, non-host: StorePartials + Signal(flags[g]) (Alg2§19-23) -----------
@@ -987,7 +1048,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
           fold_staged(v + 1, u.last_cta);
           if (tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
-          write_out(u.q_row);
+          write_out(u.q_row, si.unit);
         }
       } else {
         // ---- dynamic: publish, count in; a FIXED two-level tree folds the unit's segments
@@ -1014,7 +1075,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           reset();
           fold_range(g0, g1, 1, hv);
           if (ngrp == 1) {
-            write_out(u.q_row);
+            write_out(u.q_row, si.unit);
           } else {
             store_partial(g0 + (g0 == hv ? NV : 0));
             int last = 0;
@@ -1026,7 +1087,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
             if (__shfl_sync(0xffffffffu, last, 0)) {
               reset();
               fold_range(hv, u.last_cta, kGS, hv);
-              write_out(u.q_row);
+              write_out(u.q_row, si.unit);
             }
           }
         }

@@ -110,7 +110,19 @@ struct DecodeArgs {
   int pt_stride;      // padded to a multiple of 32 entries (the producer reads 32-entry windows)
   int heads_kv;
   int box_rows;       // GQA TMA box height: min(64, page_size) when paged, else 64
+  // NEXT-2 fused cross-GPU exchange (xw > 1).  Every rank's buffer holds
+  // [2 launch parity][xw source ranks][xrows][d + 4] fp32 (normalised O_r, then L_r in log2
+  // units) followed, at byte offset xflag_off, by [xw source ranks][xunits] uint32 flags.
+  int xw;             // ranks P (0/1: off)
+  int xr;             // this rank
+  int xrows;          // output rows B * H_q * N_q
+  int xunits;         // units B * H_kv
+  size_t xflag_off;
+  float* xpeer[8];    // every rank's buffer (xpeer[xr] = own), device-accessible addresses
+  int* xerr;          // own buffer's error word: 1 after a wait timed out
 };
+
+constexpr int kMaxXchgWorld = 8;
 
 // Kernel configuration for (dtype, head_dim, group): threads, dynamic smem, max stage tokens.
 struct KernelInfo {

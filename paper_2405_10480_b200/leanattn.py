@@ -20,7 +20,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LEANATTN_LIB") or os.path.join(_HERE, "lib", "libleanattn.so")  # env: variant sweeps
 
-LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE = range(6)
+LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE, LA_ERR_TIMEOUT = range(7)
+LA_XCHG_HANDLE_BYTES = 64
 LA_BF16, LA_FP16, LA_FP32 = 0, 1, 2
 LA_KV_BHSD, LA_KV_PACKED, LA_KV_PAGED = 0, 1, 2
 LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC, LA_SCHED_FIXED_SPLIT = 0, 1, 2, 3
@@ -33,7 +34,8 @@ _SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, 
 # Every symbol include/la.h declares (tests check the library exports all of them).
 EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
            "la_decode_partial", "la_combine", "la_decode_host", "la_plan_destroy",
-           "la_launch_count", "la_status_string", "la_last_error", "la_version", "la_plan_trace")
+           "la_launch_count", "la_status_string", "la_last_error", "la_version", "la_plan_trace",
+           "la_plan_xchg_handle", "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status")
 
 
 class LaError(RuntimeError):
@@ -49,7 +51,7 @@ class la_plan_opts(ctypes.Structure):
                 ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int), ("split", ctypes.c_int),
                 ("block_table", ctypes.POINTER(ctypes.c_int32)), ("pages_per_seq", ctypes.c_int),
                 ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64), ("q_len", ctypes.c_int),
-                ("causal", ctypes.c_int)]
+                ("causal", ctypes.c_int), ("xchg_world", ctypes.c_int), ("xchg_rank", ctypes.c_int)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -87,13 +89,18 @@ def lib() -> ctypes.CDLL:
     L.la_decode_host.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
     L.la_plan_trace.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
                                 ctypes.POINTER(ctypes.c_size_t)]
+    L.la_plan_xchg_handle.argtypes = [vp, ctypes.c_char_p]
+    L.la_plan_xchg_open.argtypes = [vp, i32, ctypes.c_char_p]
+    L.la_plan_xchg_attach.argtypes = [vp, i32, vp]
+    L.la_plan_xchg_status.argtypes = [vp]
     L.la_plan_destroy.argtypes = [vp]
     L.la_plan_destroy.restype = None
     L.la_launch_count.restype = i64
     L.la_status_string.restype = ctypes.c_char_p
     L.la_last_error.restype = ctypes.c_char_p
     for name in ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
-                 "la_decode_partial", "la_combine", "la_decode_host", "la_plan_trace"):
+                 "la_decode_partial", "la_combine", "la_decode_host", "la_plan_trace", "la_plan_xchg_handle",
+                 "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -128,7 +135,7 @@ class Plan:
                  ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
                  dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
-                 causal: bool = True):
+                 causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -153,6 +160,8 @@ class Plan:
             opts.num_pages = int(num_pages)
         opts.q_len = int(q_len)
         opts.causal = 1 if causal else 0
+        opts.xchg_world = int(xchg_world)
+        opts.xchg_rank = int(xchg_rank)
         lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
         h = ctypes.c_void_p()
         self._h = None
@@ -226,6 +235,25 @@ class Plan:
         _check(lib().la_decode_host(self._h, _ptr(q), _ptr(k), _ptr(v), int(rows), _ptr(out), _ptr(lse),
                                     _stream(stream)), "la_decode_host")
         return out, lse
+
+    # ---- NEXT-2 fused cross-GPU exchange (plans created with xchg_world = P > 1) ----------
+    def xchg_handle(self) -> bytes:
+        """``la_plan_xchg_handle``: this rank's exchange-buffer IPC handle (64 bytes)."""
+        buf = ctypes.create_string_buffer(LA_XCHG_HANDLE_BYTES)
+        _check(lib().la_plan_xchg_handle(self._h, buf), "la_plan_xchg_handle")
+        return buf.raw
+
+    def xchg_open(self, peer: int, handle: bytes):
+        """``la_plan_xchg_open``: map rank ``peer``'s buffer (another process) from its handle."""
+        _check(lib().la_plan_xchg_open(self._h, int(peer), bytes(handle)), "la_plan_xchg_open")
+
+    def xchg_attach(self, peer: int, peer_plan: "Plan"):
+        """``la_plan_xchg_attach``: rank ``peer`` is ``peer_plan`` in this process."""
+        _check(lib().la_plan_xchg_attach(self._h, int(peer), peer_plan._h), "la_plan_xchg_attach")
+
+    def xchg_status(self):
+        """``la_plan_xchg_status``: synchronises; raises LaError(LA_ERR_TIMEOUT) if a wait gave up."""
+        _check(lib().la_plan_xchg_status(self._h), "la_plan_xchg_status")
 
     def close(self):
         if self._h is not None:

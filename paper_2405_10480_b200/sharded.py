@@ -8,6 +8,12 @@ folds them with the softmax re-scaling operator (§4.1; exact for any
 associativity).  Head- or batch-sharded layouts (the paper's tensor parallelism,
 P:511) need no collective at all: every rank simply plans and decodes its own units.
 
+``fused`` path: the exchange moves INTO the decode kernel.  Each rank's
+plan is built with ``xchg_world = P``; the ranks swap the CUDA IPC handles of their
+exchange buffers once (:func:`connect_exchange`), after which every ``plan.decode`` pushes
+the rank's normalised shard partials straight into every peer's HBM over NVLink and folds
+the P partials in-kernel -- no NCCL launch, no combine kernel (la.h ``la_plan_xchg_*``).
+
 Host-side glue only; the arithmetic runs in libleanattn.so kernels.
 """
 from __future__ import annotations
@@ -53,3 +59,38 @@ def sequence_sharded_decode(plan, q, k_shard, v_shard, group=None, stream=None):
     o_all, l_all = gather_partials(o, l, group)
     out, lse = la_combine(o_all, l_all, stream=stream)
     return out.view_as(o), lse.view_as(l)
+
+
+def exchange_handles(handle: bytes, group=None) -> List[bytes]:
+    """All-gather every rank's 64-byte exchange handle, in rank order (any backend)."""
+    import torch.distributed as dist
+    out: List[bytes] = [b""] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(handle), group=group)
+    return out
+
+
+def connect_exchange(plan, group=None) -> None:
+    """Open every peer rank's exchange buffer in ``plan`` (built with xchg_world = P and
+    xchg_rank = this rank).  Collective: every rank must call it.  If any rank fails to map
+    a peer, EVERY rank raises the same RuntimeError (so all ranks can agree on a fallback)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    handles = exchange_handles(plan.xchg_handle(), group)
+    err = ""
+    for peer, h in enumerate(handles):
+        if peer != rank and not err:
+            try:
+                plan.xchg_open(peer, h)
+            except Exception as e:  # noqa: BLE001 -- reported collectively below
+                err = f"rank {rank} -> peer {peer}: {e}"
+    errs: List[str] = [""] * dist.get_world_size(group)
+    dist.all_gather_object(errs, err, group=group)
+    bad = [e for e in errs if e]
+    if bad:
+        raise RuntimeError("exchange setup failed: " + "; ".join(bad))
+
+
+def fused_sequence_sharded_decode(plan, q, k_shard, v_shard, stream=None):
+    """One decode step of the fused path: ``plan`` (this rank's shard, exchange connected)
+    returns the full (O, L) on every rank from ONE kernel launch."""
+    return plan.decode(q, k_shard, v_shard, stream=stream)

@@ -62,3 +62,42 @@ def test_sequence_sharded_glue_gloo(world, tmp_path):
     err = float(open(result).read())
     # fp32 exchange of the partials (as on the GPU path) bounds the error
     assert err <= 1e-6
+
+
+class _FakeXchgPlan:
+    """Stands in for a Plan built with xchg_world = P: records which peer handles it opens."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = {}
+
+    def xchg_handle(self):
+        return bytes([self.rank]) * 64
+
+    def xchg_open(self, peer, handle):
+        self.opened[peer] = handle
+
+
+def _xchg_worker(rank, world, port, result_path):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2405_10480_b200 import sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = _FakeXchgPlan(rank)
+    sharded.connect_exchange(plan)
+    ok = sorted(plan.opened) == [r for r in range(world) if r != rank] and \
+        all(h == bytes([r]) * 64 for r, h in plan.opened.items())
+    with open(f"{result_path}.{rank}", "w") as f:
+        f.write("ok" if ok else repr(plan.opened))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_handle_swap_gloo(world, tmp_path):
+    """NEXT-2 host glue: every rank opens every OTHER rank's exchange handle, in rank order."""
+    result = str(tmp_path / "xchg")
+    mp.spawn(_xchg_worker, args=(world, _free_port(), result), nprocs=world, join=True)
+    for r in range(world):
+        assert open(f"{result}.{r}").read() == "ok"

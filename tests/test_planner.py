@@ -197,3 +197,18 @@ def test_paged_plan_validation_and_schedule(la):
         kw.update(bad)
         with pytest.raises(la.LaError):
             la.Plan(3, 4, 4, 128, p.ctx_lens, host_only=True, layout="paged", **kw)
+
+
+def test_xchg_validation(la):
+    """NEXT-2 exchange options are validated at la_plan (host-only plans: no buffer)."""
+    for kw, status in [(dict(xchg_world=9), la.LA_ERR_INVALID), (dict(xchg_world=2, xchg_rank=2), la.LA_ERR_INVALID),
+                       (dict(xchg_world=2, xchg_rank=-1), la.LA_ERR_INVALID),
+                       (dict(xchg_world=2, q_len=2), la.LA_ERR_UNSUPPORTED)]:
+        with pytest.raises(la.LaError) as e:
+            la.Plan(1, 2, 2, 128, [100], host_only=True, **kw)
+        assert e.value.status == status, kw
+    p = la.Plan(1, 2, 2, 128, [100], host_only=True, xchg_world=4, xchg_rank=3)
+    with pytest.raises(la.LaError) as e:
+        p.xchg_handle()
+    assert e.value.status == la.LA_ERR_STATE
+    la.Plan(1, 2, 2, 128, [100], host_only=True, xchg_world=2, q_len=2, causal=False)  # full mask: shard-local
