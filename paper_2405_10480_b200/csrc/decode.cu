@@ -926,6 +926,10 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     // NEXT-2: push this rank's normalised shard partial of unit `unit` into every rank's
     // exchange buffer, release flag [xr][unit] there, acquire the P flags of the unit here
     // and fold the P partials ascending (§4.1 operator; bitwise equal on every rank).
+    // Deadlock freedom: every CTA (and the virtual-CTA claim order) visits units in
+    // increasing order and pushes unit u before waiting on it.  Take the smallest unit m
+    // anyone waits on: on every rank, all work of m precedes (in its CTA's order) any wait
+    // on a unit > m, and no CTA is stuck on a unit < m, so every rank completes m's push.
     auto xchg_out = [&](int q_row, int unit) {
       constexpr int RS = D + 4;
       const int P = a.xw, par = int(a.epoch & 1u);
