@@ -23,7 +23,8 @@ Modules
 
 Parity status of every function is listed in DESIGN.md §"Oracle and pins"; all are pinned.
 """
-from .attention import decode_attention, decode_attention_unit, decode_attention_multi, paged_rows, scores
+from .attention import (decode_attention, decode_attention_unit, decode_attention_multi, decode_attention_varq,
+                        paged_rows, scores)
 from .rescale import PartialState, neutral, partial, combine, finalize, fold
 from .leantile import lean_tile
 from .schedule import (Segment, iters_per_cta, cta_range, owner, stream_k_segments,
@@ -34,7 +35,7 @@ from .lean_attention import lean_attention
 from .shard_combine import combine_shards
 
 __all__ = [
-    "decode_attention", "decode_attention_unit", "scores",
+    "decode_attention", "decode_attention_unit", "decode_attention_multi", "decode_attention_varq", "scores",
     "PartialState", "neutral", "partial", "combine", "finalize", "fold",
     "lean_tile",
     "Segment", "iters_per_cta", "cta_range", "owner", "stream_k_segments", "owner_table",

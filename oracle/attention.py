@@ -66,6 +66,43 @@ def decode_attention_multi(q: np.ndarray, k: np.ndarray, v: np.ndarray, ctx_lens
     return O, L
 
 
+def decode_attention_varq(q_rows: np.ndarray, k: np.ndarray, v: np.ndarray, ctx_lens, q_lens, scale: float,
+                          causal: bool = True, layout: str = "bhsd", block_table=None, page_size: int = 0):
+    """Heterogeneous batch (NEXT-3: decode mixed with speculative / chunked-prefill query
+    blocks; the paper's general N_q per request): request b brings N_b =
+    q_lens[b] query tokens.  q_rows holds, request after request, an (H_q, N_b, d) block:
+    row (b, h_q, i) = sum_{b' < b} H_q N_b' + h_q N_b + i.  Query i of request b is the
+    cached token n_b - N_b + i; with ``causal`` it attends to keys [0, n_b - N_b + i], else
+    to all n_b keys.  Eq. 1 per row.  Returns O (rows, d), L (rows,)."""
+    q_rows = np.asarray(q_rows, dtype=np.float64)
+    Hkv = k.shape[0] if layout == "packed" else k.shape[1]
+    d = q_rows.shape[-1]
+    B = len(ctx_lens)
+    Hq = q_rows.shape[0] // int(np.sum(q_lens))
+    g = Hq // Hkv
+    cu = np.concatenate([[0], np.cumsum(ctx_lens)]).astype(np.int64)
+    O = np.empty((q_rows.shape[0], d))
+    L = np.empty((q_rows.shape[0],))
+    row = 0
+    for b in range(B):
+        n, nb = int(ctx_lens[b]), int(q_lens[b])
+        for hq in range(Hq):
+            h = hq // g
+            if layout == "bhsd":
+                kk, vv = k[b, h, :n], v[b, h, :n]
+            elif layout == "packed":
+                kk, vv = k[h, cu[b]:cu[b + 1]], v[h, cu[b]:cu[b + 1]]
+            else:
+                kk = paged_rows(k, block_table[b], h, n, page_size)
+                vv = paged_rows(v, block_table[b], h, n, page_size)
+            for i in range(nb):
+                m = n - nb + i + 1 if causal else n
+                o, l = decode_attention_unit(q_rows[row], kk[:m], vv[:m], scale)
+                O[row], L[row] = o[0], l[0]
+                row += 1
+    return O, L
+
+
 def _sliced(q, k, v, ctx_lens, lens_i, scale, layout, block_table, page_size):
     """decode_attention over the first lens_i[b] keys of every request."""
     B, Hq, d = q.shape

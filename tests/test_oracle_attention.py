@@ -197,3 +197,28 @@ def test_multi_query_causal_against_mpmath_and_truncation():
     # the last query of a causal block sees the whole cache
     Ol, Ll = oracle.decode_attention(q[:, :, Nq - 1], k, v, lens, 0.4)
     assert np.max(np.abs(O[:, :, Nq - 1] - Ol)) <= 1e-13
+
+
+def test_heterogeneous_batch_against_mpmath():
+    # NEXT-3 heterogeneous batches: request b brings N_b queries (rows (b, h_q, i) in
+    # per-request (H_q, N_b) blocks); query i sees keys [0, n_b - N_b + i] when causal.
+    # Pinned against mpmath with the row layout and the mask written out independently.
+    rng = np.random.default_rng(22)
+    Hkv, g, d = 2, 3, 5
+    lens, qls = [7, 4, 9], [1, 4, 2]
+    Hq = Hkv * g
+    k = rng.normal(size=(3, Hkv, 9, d))
+    v = rng.normal(size=(3, Hkv, 9, d))
+    rows = sum(Hq * n for n in qls)
+    q = rng.normal(size=(rows, d))
+    for causal in (True, False):
+        O, L = oracle.decode_attention_varq(q, k, v, lens, qls, 0.7, causal=causal)
+        assert O.shape == (rows, d) and L.shape == (rows,)
+        r = 0
+        for b in range(3):
+            for hq in range(Hq):
+                for i in range(qls[b]):
+                    m = lens[b] - qls[b] + i + 1 if causal else lens[b]
+                    o_mp, l_mp = _mp_attention(q[r], k[b, hq // g, :m], v[b, hq // g, :m], 0.7)
+                    assert np.max(np.abs(O[r] - o_mp)) <= 1e-13 and abs(L[r] - l_mp) <= 1e-13
+                    r += 1
