@@ -113,8 +113,10 @@ typedef struct {
   int64_t num_pages;          /* pages in each pool; every table entry must be < num_pages  */
   /* N_q > 1 (NEXT-3: speculative / multi-token decode; the paper's T_m rows, Alg2§4): */
   int q_len;                  /* query tokens per request N_q (default 1); q, out are then
-                                 (B, H_q, N_q, d) and lse (B, H_q, N_q).  An output tile is
-                                 the g * N_q rows of one KV head: g * N_q <= 8 in this build */
+                                 (B, H_q, N_q, d) and lse (B, H_q, N_q).  The g * N_q rows of
+                                 one KV head are cut into C_m = ceil(g N_q / T_m) query tiles
+                                 of T_m <= 8 rows (Alg2§4); each tile is a work unit that
+                                 streams the head's KV (MQA / large groups included)          */
   int causal;                 /* 1 (default): query i of N_q is the token at position
                                  n - N_q + i and attends to keys [0, n - N_q + i]; 0: every
                                  query attends to all n keys                                 */
@@ -123,6 +125,11 @@ typedef struct {
                                  request's context; 0 or 1 = off.  With P > 1, la_decode on
                                  rank r's shard returns the FULL result on every rank      */
   int xchg_rank;              /* this plan's rank r in [0, P)                               */
+  /* Heterogeneous batches (NEXT-3: decode mixed with speculative / chunked-prefill blocks): */
+  const int32_t* q_lens;      /* HOST [batch] query tokens N_b per request (>= 1, <= ctx_lens[b]),
+                                 or NULL for q_len everywhere.  q / out / lse then hold, per
+                                 request in order, an (H_q, N_b[, d]) block (rows (b, h_q, i)
+                                 contiguous); with NULL this is exactly (B, H_q, N_q[, d])    */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;
@@ -142,7 +149,9 @@ typedef struct {
   float scale;
   int64_t num_vctas;       /* Alg. 2's G: iteration ranges (= grid for static schedules)  */
   int split;               /* LA_SCHED_FIXED_SPLIT: chunks per unit (0 otherwise)         */
-  int q_len;               /* N_q                                                          */
+  int q_len;               /* N_q (0 when per-request q_lens differ)                      */
+  int tile_rows;           /* T_m: query rows per work unit                               */
+  int64_t q_rows;          /* query / output rows = sum_b H_q N_b                          */
 } la_plan_info;
 
 /* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */
@@ -151,7 +160,7 @@ la_status la_plan_opts_init(la_plan_opts* opts);
 /*
  * la_plan -- build the stream-K schedule for one decode step (host, synchronous).
  *
- * batch, heads_q, heads_kv >= 1, heads_q % heads_kv == 0 (reading C3); head_dim in
+ * batch, heads_q, heads_kv >= 1, heads_q % heads_kv == 0 (reading C3; any group size); head_dim in
  * {64, 128}; ctx_lens: HOST array of `batch` int32, each >= 1 (reading C6); tile_n: LeanTile
  * tokens in {16, 32, 64, 128, 256, 512}, or 0 for the default (T_n giving 64 KiB of K+V per
  * LeanTile -- 128 tokens at d=128 bf16, 256 at d=64, as the paper's sweep found).

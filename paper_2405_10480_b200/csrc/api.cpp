@@ -91,10 +91,10 @@ void release_device(la_plan_s* p) {
 // Exchange buffer layout (DecodeArgs::xpeer): [2][P][rows][d + 4] fp32, then [P][units]
 // uint32 flags, then one int error word.
 size_t xchg_flag_off(const la::Problem& p, int P) {
-  return (size_t(2) * P * p.batch * p.heads_q * p.q_len * (p.head_dim + 4) * sizeof(float) + 255) & ~size_t(255);
+  return (size_t(2) * P * p.q_rows() * (p.head_dim + 4) * sizeof(float) + 255) & ~size_t(255);
 }
 size_t xchg_bytes(const la::Problem& p, int P) {
-  return xchg_flag_off(p, P) + ((size_t(P) * p.batch * p.heads_kv * sizeof(uint32_t) + 255) & ~size_t(255)) + 256;
+  return xchg_flag_off(p, P) + ((size_t(P) * p.num_units() * sizeof(uint32_t) + 255) & ~size_t(255)) + 256;
 }
 
 }  // namespace
@@ -162,8 +162,6 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (opts.xchg_world < 0 || xw > la::kMaxXchgWorld)
     return fail(LA_ERR_INVALID, "xchg_world must be in 0..8");
   if (xw && (opts.xchg_rank < 0 || opts.xchg_rank >= xw)) return fail(LA_ERR_INVALID, "xchg_rank out of range");
-  if (xw && opts.q_len > 1 && opts.causal)
-    return fail(LA_ERR_UNSUPPORTED, "sequence-shard exchange needs q_len == 1 or causal == 0");
 
   la::Problem p;
   p.batch = batch;
@@ -172,10 +170,26 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   p.head_dim = head_dim;
   p.group = heads_q / heads_kv;
   if (opts.q_len < 1) return fail(LA_ERR_INVALID, "q_len must be >= 1");
-  p.q_len = opts.q_len;
   p.causal = opts.causal ? 1 : 0;
-  if (p.rows() > 8 && p.rows() != p.group)
-    return fail(LA_ERR_UNSUPPORTED, "group * q_len must be <= 8 for q_len > 1 in this build");
+  if (opts.q_lens) {
+    p.q_lens.assign(opts.q_lens, opts.q_lens + batch);
+    for (int32_t n : p.q_lens)
+      if (n < 1) return fail(LA_ERR_INVALID, "every q_lens[b] must be >= 1");
+  } else {
+    p.q_lens.assign(batch, opts.q_len);
+  }
+  int max_rows = 0;
+  bool uniform = true;
+  for (int32_t n : p.q_lens) {
+    max_rows = std::max(max_rows, p.group * n);
+    uniform = uniform && n == p.q_lens[0];
+  }
+  p.q_len = uniform ? p.q_lens[0] : 0;
+  p.tile_rows = std::min(8, max_rows);   // T_m: 1 -> CUDA-core engine, else tensor-core tiles
+  if (xw && p.causal)
+    for (int32_t n : p.q_lens)
+      if (n > 1) return fail(LA_ERR_UNSUPPORTED, "sequence-shard exchange needs N_b == 1 or causal == 0");
+  if (p.q_rows() >= (int64_t(1) << 31)) return fail(LA_ERR_INVALID, "too many query rows");
   p.dtype = dtype;
   p.layout = opts.layout;
   p.schedule = opts.schedule;
@@ -183,10 +197,12 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   int64_t maxn = 0, total = 0;
   for (int32_t n : p.ctx_lens) {
     if (n < 1) return fail(LA_ERR_INVALID, "every ctx_lens[b] must be >= 1 (reading C6)");
-    if (n < p.q_len) return fail(LA_ERR_INVALID, "ctx_lens[b] must be >= q_len (the queries are cached tokens)");
     maxn = std::max<int64_t>(maxn, n);
     total += n;
   }
+  for (int b = 0; b < batch; ++b)
+    if (p.ctx_lens[b] < p.q_lens[b])
+      return fail(LA_ERR_INVALID, "ctx_lens[b] must be >= q_lens[b] (the queries are cached tokens)");
   p.max_ctx = opts.max_ctx ? opts.max_ctx : maxn;
   if (p.layout == LA_KV_BHSD && p.max_ctx < maxn) return fail(LA_ERR_INVALID, "max_ctx < max(ctx_lens)");
   p.scale = opts.scale != 0.f ? opts.scale : float(1.0 / std::sqrt(double(head_dim)));
@@ -375,6 +391,8 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   info->num_vctas = s.grid;
   info->split = plan->split;
   info->q_len = p.q_len;
+  info->tile_rows = p.tile_rows;
+  info->q_rows = p.q_rows();
   info->num_units = int(s.units.size());
   info->total_iters = s.total_iters;
   info->num_segments = s.num_segments;
@@ -447,8 +465,8 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
       if (!plan->xpeer[r]) return fail(LA_ERR_STATE, "exchange peer " + std::to_string(r) + " not opened/attached");
     a.xw = plan->xw;
     a.xr = plan->xr;
-    a.xrows = plan->prob.batch * plan->prob.heads_q * plan->prob.q_len;
-    a.xunits = plan->prob.batch * plan->prob.heads_kv;
+    a.xrows = int(plan->prob.q_rows());
+    a.xunits = int(plan->sched.units.size());
     a.xflag_off = plan->xflag_off;
     for (int r = 0; r < plan->xw; ++r) a.xpeer[r] = plan->xpeer[r];
     a.xerr = reinterpret_cast<int*>(static_cast<char*>(plan->d_xchg) + xchg_bytes(plan->prob, plan->xw) - 256);
@@ -490,10 +508,10 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
   const la::Problem& p = plan->prob;
   if (kv_rows != p.kv_rows()) return fail(LA_ERR_INVALID, "kv_rows does not match the plan");
   const size_t eb = size_t(p.elem_bytes());
-  const size_t q_bytes = size_t(p.batch) * p.heads_q * p.q_len * p.head_dim * eb;
+  const size_t q_bytes = size_t(p.q_rows()) * p.head_dim * eb;
   const size_t kv_bytes = size_t(kv_rows) * p.head_dim * eb;
-  const size_t o_bytes = size_t(p.batch) * p.heads_q * p.q_len * p.head_dim * sizeof(float);
-  const size_t l_bytes = size_t(p.batch) * p.heads_q * p.q_len * sizeof(float);
+  const size_t o_bytes = size_t(p.q_rows()) * p.head_dim * sizeof(float);
+  const size_t l_bytes = size_t(p.q_rows()) * sizeof(float);
   auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t need = align(q_bytes) + 2 * align(kv_bytes) + align(o_bytes) + align(l_bytes);
   if (plan->stage_bytes < need) {
@@ -571,7 +589,7 @@ la_status la_plan_xchg_attach(la_plan_t plan, int peer, la_plan_t peer_plan) {
   if (peer_plan->xw != plan->xw || peer_plan->xr != peer) return fail(LA_ERR_INVALID, "peer plan has another rank/world");
   const la::Problem &p = plan->prob, &q = peer_plan->prob;
   if (p.batch != q.batch || p.heads_q != q.heads_q || p.heads_kv != q.heads_kv || p.head_dim != q.head_dim ||
-      p.q_len != q.q_len)
+      p.q_lens != q.q_lens)
     return fail(LA_ERR_INVALID, "peer plan has another shape");
   if (plan->xpeer[peer]) return fail(LA_ERR_STATE, "peer already opened/attached");
   plan->xpeer[peer] = static_cast<float*>(peer_plan->d_xchg);

@@ -442,7 +442,7 @@ struct GqaEngine {
 
   struct State {
     uint32_t qb[KS][2];     // Q^T B-fragments (exact inputs)
-    float m[2], l[2];       // rows 2tq, 2tq+1 (row = head j * N_q + query i)
+    float m[2], l[2];       // tile rows 2tq, 2tq+1 (unit row r0 + r = head j * N_b + query i)
     float o[KS][4];         // O^T fragments: dims 16mm + gq (+8), rows 2tq, 2tq+1
     int lim[2];             // causal key limit of rows 2tq, 2tq+1 (unit-local, exclusive)
   };
@@ -478,7 +478,7 @@ struct GqaEngine {
   __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
     const int gq = lane >> 2, tq = lane & 3;
     const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const T*>(a.q) + size_t(u.q_row + gq) * D);
-    const bool ok = gq < a.group;
+    const bool ok = gq < u.rows;
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {  // b0 = Q[gq][16kk + 2tq, +1], b1 = Q[gq][16kk + 8 + 2tq, +1]
       s.qb[kk][0] = ok ? qrow[8 * kk + tq] : 0u;
@@ -488,10 +488,10 @@ struct GqaEngine {
     s.l[0] = s.l[1] = 0.f;
 #pragma unroll
     for (int mm = 0; mm < KS; ++mm) s.o[mm][0] = s.o[mm][1] = s.o[mm][2] = s.o[mm][3] = 0.f;
-    // N_q > 1, causal: query i (row r = j * N_q + i) is the token at n - N_q + i (NEXT-3)
+    // N_b > 1, causal: query i (row r0 + r = j * N_b + i) is the token at n - N_b + i (NEXT-3)
 #pragma unroll
     for (int e = 0; e < 2; ++e)
-      s.lim[e] = a.causal ? u.len - a.q_len + ((2 * tq + e) % a.q_len) + 1 : u.len;
+      s.lim[e] = a.causal ? u.len - u.nq + ((u.r0 + 2 * tq + e) % u.nq) + 1 : u.len;
   }
 
   // This warp's 32-token rounds (sub, sub + WPS, ...) of one stage of ntok tokens starting
@@ -779,10 +779,11 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = 0.f;
       }
     };
+    int nr = 0;  // output rows of the current segment's unit (its query tile, <= H)
     auto store_partial = [&](int slot) {  // StorePartials(Op, mp, lp) (Alg2§20-22)
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        if (h >= a.group) continue;
+        if (h >= nr) continue;
         const size_t row = size_t(slot) * a.group + h;
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) a.part_o[row * D + lane + 32 * jj] = acc.o[h][jj];
@@ -811,7 +812,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       constexpr int NB = 8;
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        if (h >= a.group) continue;
+        if (h >= nr) continue;
         float M = acc.m[h], lsum = 0.f;
         for (int i = lane; i < n; i += 32) M = fmaxf(M, ld_cg(&a.part_ml[row_of(i, h) * 4]));
 #pragma unroll
@@ -877,7 +878,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         mbar_wait(stage_bar, ph);
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-          if (h >= rows) continue;
+          if (h >= nr) continue;
           float M = acc.m[h], lsum = 0.f;
           for (int i = lane; i < cn; i += 32) M = fmaxf(M, sm[i * pm + 4 * h]);
 #pragma unroll
@@ -935,7 +936,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       const int P = a.xw, par = int(a.epoch & 1u);
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        if (h >= a.group) continue;
+        if (h >= nr) continue;
         const float inv = 1.f / acc.l[h], l2 = acc.m[h] + log2f(acc.l[h]);
         for (int d = 0; d < P; ++d) {
           float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + q_row + h) * RS;
@@ -965,7 +966,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       const float* xb = a.xpeer[a.xr] + size_t(par) * P * a.xrows * RS;
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        if (h >= a.group) continue;
+        if (h >= nr) continue;
         float M = -INFINITY;
         for (int r = 0; r < P; ++r) M = fmaxf(M, ld_cg(xb + (size_t(r) * a.xrows + q_row + h) * RS + D));
         float l = 0.f, o[J];
@@ -991,7 +992,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       }
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        if (h >= a.group) continue;
+        if (h >= nr) continue;
         const float inv = 1.f / acc.l[h];
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) a.out[size_t(q_row + h) * D + lane + 32 * jj] = acc.o[h][jj] * inv;
@@ -1031,6 +1032,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       if (lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill this buffer
       const DevUnit u = a.units[si.unit];
       const int v = si.v;
+      nr = u.rows;
 
       if (si.host && si.finishing) {
         write_out(u.q_row, si.unit);  // one (virtual) CTA computed the whole unit (Alg2§38-39)

@@ -12,16 +12,23 @@ namespace la {
 
 // One work unit (= output tile): the T_m = g query heads of (b, h_kv) against
 // that KV head's n_b cached rows.  32 bytes, uploaded as-is to the device.
+// A work unit = one output tile: (request b, KV head h_kv, query tile m).  Its rows are
+// r0 .. r0 + rows - 1 of the g * N_b rows of (b, h_kv), row r = q-head j * N_b + query i
+// (Alg2§4's C_m query tiles of T_m rows; C_m = 1 whenever g * N_b <= T_m).
 struct DevUnit {
   int64_t row0;        // first K/V row of the unit (a row = head_dim elements)
   int32_t len;         // n_b
   int32_t iter_begin;  // tile_iter of Alg2§12: global index of the unit's first LeanTile
   int32_t iter_end;    // tile_iter_end of Alg2§13
-  int32_t q_row;       // row of the unit's first q-head in the (B*H_q) query/output rows
+  int32_t q_row;       // first query/output row of the unit (rows are contiguous)
   int32_t last_cta;    // owner(iter_end - 1): reading C9 of Alg2§26
   int32_t host_cta;    // owner(iter_begin): the host block of P:412 / Alg2§17
+  int32_t rows;        // output rows of this unit (<= T_m)
+  int32_t r0;          // index of its first row among the g * N_b rows of (b, h_kv)
+  int32_t nq;          // N_b: query tokens of request b
+  int32_t pad_;
 };
-static_assert(sizeof(DevUnit) == 32, "DevUnit layout");
+static_assert(sizeof(DevUnit) == 48, "DevUnit layout");
 
 // Host-side schedule: Alg2§4-18 for every (virtual) CTA.  Pure integer work, no CUDA.
 struct Schedule {
@@ -38,8 +45,20 @@ struct Schedule {
 
 struct Problem {
   int batch = 0, heads_q = 0, heads_kv = 0, head_dim = 0, group = 0;
-  int q_len = 1, causal = 1;   // N_q and its mask (NEXT-3)
-  int rows() const { return group * q_len; }   // T_m: output rows of one unit
+  int q_len = 1, causal = 1;   // uniform N_q (0 if per-request q_lens differ) and the mask (NEXT-3)
+  std::vector<int32_t> q_lens; // N_b per request
+  int tile_rows = 1;           // T_m: output rows per unit (1: MHA engine; else <= 8)
+  int rows() const { return tile_rows; }
+  int64_t num_units() const {  // sum_b H_kv * C_m(b), C_m(b) = ceil(g N_b / T_m)
+    int64_t u = 0;
+    for (int32_t n : q_lens) u += int64_t(heads_kv) * ((int64_t(group) * n + tile_rows - 1) / tile_rows);
+    return u;
+  }
+  int64_t q_rows() const {     // query/output rows: sum_b H_q * N_b
+    int64_t r = 0;
+    for (int32_t n : q_lens) r += int64_t(heads_q) * n;
+    return r;
+  }
   int dtype = LA_BF16, layout = LA_KV_BHSD, schedule = LA_SCHED_STREAMK;
   int64_t max_ctx = 0;
   float scale = 0.f;
@@ -97,8 +116,8 @@ struct DecodeArgs {
   int grid;           // CTAs launched
   int tile_n;
   int stage_tokens;
-  int group;          // output rows per unit T_m = g * N_q (rows r = head j * N_q + query i)
-  int q_len;          // N_q
+  int group;          // T_m: rows of a partial slot (a unit's own row count is DevUnit::rows)
+  int q_len;          // N_q (unused by the kernels: per-unit DevUnit::nq)
   int causal;         // N_q > 1: query i attends to unit-local keys [0, n - N_q + i]
   int uses_tmap;      // set by launch_decode for the TMA-tensor (GQA) engine
   float scale_log2;   // scale * log2(e): scores live in the exp2 domain inside the kernel

@@ -29,24 +29,36 @@ int64_t Problem::kv_rows() const {
 void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int64_t& total_iters) {
   units.clear();
   units.reserve(size_t(p.batch) * p.heads_kv);
-  std::vector<int64_t> cu(p.batch + 1, 0);  // cu_seqlens
-  for (int b = 0; b < p.batch; ++b) cu[b + 1] = cu[b] + p.ctx_lens[b];
+  std::vector<int64_t> cu(p.batch + 1, 0), cq(p.batch + 1, 0);  // cu_seqlens, query rows
+  for (int b = 0; b < p.batch; ++b) {
+    cu[b + 1] = cu[b] + p.ctx_lens[b];
+    cq[b + 1] = cq[b] + int64_t(p.heads_q) * p.q_lens[b];
+  }
   int64_t it = 0;
   auto add = [&](int b, int h) {
-    DevUnit u{};
-    u.len = p.ctx_lens[b];
-    if (p.layout == LA_KV_BHSD)
-      u.row0 = (int64_t(b) * p.heads_kv + h) * p.max_ctx;
-    else if (p.layout == LA_KV_PACKED)
-      u.row0 = int64_t(h) * cu[p.batch] + cu[b];
-    else
-      u.row0 = int64_t(b) * p.heads_kv + h;  // paged: rows come from the block table
-    u.q_row = (b * p.heads_q + h * p.group) * p.q_len;  // rows (head j, query i) = j * N_q + i
-    u.iter_begin = int32_t(it);
-    it += (int64_t(u.len) + tile_n - 1) / tile_n;   // C_n = ceil(n_b / T_n)   (Alg2§5)
-    u.iter_end = int32_t(it);
-    u.last_cta = u.host_cta = -1;
-    units.push_back(u);
+    // query tiles m = 0 .. C_m - 1 of T_m rows over the g * N_b rows (Alg2§4 C_m), each a
+    // unit that streams the whole KV of (b, h) -- innermost, so tiles of one KV run together
+    const int nq = p.q_lens[b], rows = p.group * nq;
+    for (int r0 = 0; r0 < rows; r0 += p.tile_rows) {
+      DevUnit u{};
+      u.len = p.ctx_lens[b];
+      if (p.layout == LA_KV_BHSD)
+        u.row0 = (int64_t(b) * p.heads_kv + h) * p.max_ctx;
+      else if (p.layout == LA_KV_PACKED)
+        u.row0 = int64_t(h) * cu[p.batch] + cu[b];
+      else
+        u.row0 = int64_t(b) * p.heads_kv + h;  // paged: rows come from the block table
+      // request b's rows: (H_q, N_b) blocks, row (head j of the group, query i) = j N_b + i
+      u.q_row = int32_t(cq[b] + int64_t(h) * rows + r0);
+      u.rows = std::min(p.tile_rows, rows - r0);
+      u.r0 = r0;
+      u.nq = nq;
+      u.iter_begin = int32_t(it);
+      it += (int64_t(u.len) + tile_n - 1) / tile_n;   // C_n = ceil(n_b / T_n)   (Alg2§5)
+      u.iter_end = int32_t(it);
+      u.last_cta = u.host_cta = -1;
+      units.push_back(u);
+    }
   };
   if (p.layout != LA_KV_PACKED) {
     for (int b = 0; b < p.batch; ++b)           // batch -> heads -> context

@@ -51,7 +51,8 @@ class la_plan_opts(ctypes.Structure):
                 ("dyn_first_permille", ctypes.c_int), ("dyn_min_chunk", ctypes.c_int), ("split", ctypes.c_int),
                 ("block_table", ctypes.POINTER(ctypes.c_int32)), ("pages_per_seq", ctypes.c_int),
                 ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64), ("q_len", ctypes.c_int),
-                ("causal", ctypes.c_int), ("xchg_world", ctypes.c_int), ("xchg_rank", ctypes.c_int)]
+                ("causal", ctypes.c_int), ("xchg_world", ctypes.c_int), ("xchg_rank", ctypes.c_int),
+                ("q_lens", ctypes.POINTER(ctypes.c_int32))]
 
 
 class la_plan_info(ctypes.Structure):
@@ -61,7 +62,7 @@ class la_plan_info(ctypes.Structure):
                [(n, ctypes.c_int64) for n in ("total_iters", "num_segments", "num_partials",
                                               "workspace_bytes", "kv_bytes")] + \
                [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64), ("split", ctypes.c_int),
-                ("q_len", ctypes.c_int)]
+                ("q_len", ctypes.c_int), ("tile_rows", ctypes.c_int), ("q_rows", ctypes.c_int64)]
 
 
 _lib = None
@@ -135,7 +136,7 @@ class Plan:
                  ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
                  dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
-                 causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0):
+                 causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -162,6 +163,10 @@ class Plan:
         opts.causal = 1 if causal else 0
         opts.xchg_world = int(xchg_world)
         opts.xchg_rank = int(xchg_rank)
+        if q_lens is not None:  # heterogeneous batch: N_b per request
+            ql = np.ascontiguousarray(np.asarray(q_lens, dtype=np.int32))
+            self._ql = ql
+            opts.q_lens = ql.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
         lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
         h = ctypes.c_void_p()
         self._h = None
@@ -201,7 +206,9 @@ class Plan:
     def _outputs(self, q, out, lse, need_lse):
         import torch
         B, H, D, nq = self.info.batch, self.info.heads_q, self.info.head_dim, self.info.q_len
-        rows = (B, H) if nq == 1 else (B, H, nq)
+        # uniform N_q: (B, H_q[, N_q]); per-request q_lens: (sum_b H_q N_b,) rows, request
+        # blocks (H_q, N_b) in order
+        rows = (B, H) if nq == 1 else ((B, H, nq) if nq > 1 else (int(self.info.q_rows),))
         if out is None:
             out = torch.empty(rows + (D,), dtype=torch.float32, device=q.device)
         if lse is None and need_lse:

@@ -115,6 +115,8 @@ class Problem:
     census_block: int = 0          # T_c for D3 (0 -> n_b // 16 rounded to a power of two)
     page_size: int = 0             # layout "paged": tokens per page (pools (pages, H_kv, page, d))
     q_len: int = 1                 # N_q query tokens per request (q: (B, H_q, N_q, d) if > 1)
+    q_lens: Optional[Sequence[int]] = None  # per-request N_b (heterogeneous batch): q is then
+                                            # (sum_b H_q N_b, d), request blocks (H_q, N_b, d)
 
     def __post_init__(self):
         if self.max_ctx is None:
@@ -147,12 +149,21 @@ class Problem:
 # element generators (all return fp64 tensors before rounding)
 # ----------------------------------------------------------------------------------------
 
+def q_row_of(p: Problem, b: int, hq: int, i: int = 0) -> int:
+    """Row of query token i of q-head hq of request b in the flat (rows, d) view of q."""
+    qls = list(p.q_lens) if p.q_lens is not None else [p.q_len] * p.batch
+    return sum(p.heads_q * n for n in qls[:b]) + hq * qls[b] + i
+
+
 def _q64(p: Problem, device) -> torch.Tensor:
     B, H, D = p.batch, p.heads_q, p.head_dim
-    shape = (B, H, D) if p.q_len == 1 else (B, H, p.q_len, D)
+    if p.q_lens is not None:
+        shape = (H * sum(p.q_lens), D)
+    else:
+        shape = (B, H, D) if p.q_len == 1 else (B, H, p.q_len, D)
     if p.dist == "D3":
         return torch.zeros(shape, dtype=torch.float64, device=device)
-    idx = torch.arange(B * H * p.q_len * D, dtype=torch.int64, device=device)
+    idx = torch.arange(math.prod(shape), dtype=torch.int64, device=device)
     x = _normal_from_index(idx, _key(p.seed, 0)).reshape(shape)
     if p.dist in ("D1", "D2", "D4"):
         x = x * 2.0
@@ -166,9 +177,8 @@ def gen_q(p: Problem, device="cpu") -> torch.Tensor:
 
 def _qhat_for_unit(p: Problem, b: int, h: int, device) -> torch.Tensor:
     """Unit vector along the (rounded) query of the group's first q-head, fp64."""
-    q = gen_q(p, device)[b, h * p.group].to(torch.float64)
-    if p.q_len > 1:
-        q = q[0]                      # the first query token of the group's first head
+    q = gen_q(p, device).reshape(-1, p.head_dim)[q_row_of(p, b, h * p.group)].to(torch.float64)
+    # (the first query token of the group's first head)
     nrm = torch.linalg.vector_norm(q)
     return q / nrm, float(nrm)
 

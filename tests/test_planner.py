@@ -212,3 +212,42 @@ def test_xchg_validation(la):
         p.xchg_handle()
     assert e.value.status == la.LA_ERR_STATE
     la.Plan(1, 2, 2, 128, [100], host_only=True, xchg_world=2, q_len=2, causal=False)  # full mask: shard-local
+
+
+def test_query_tiles_and_heterogeneous_batches_bit_exact(la):
+    """NEXT-3: the g * N_b rows of (b, h_kv) are cut into C_m = ceil(g N_b / T_m) query
+    tiles (Alg2§4), T_m = min(8, max_b g N_b); each tile is a unit streaming the whole KV of
+    (b, h_kv), tiles innermost in the memory-order linearisation (C14).  The planner's
+    segments must equal the oracle's stream-K walk over that unit list, bit for bit."""
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        batch = int(rng.integers(1, 6))
+        hkv = int(rng.integers(1, 4))
+        g = int(rng.choice([1, 2, 3, 4, 8, 16]))
+        lens = [int(x) for x in rng.integers(16, 3000, size=batch)]
+        qls = [int(x) for x in rng.integers(1, 6, size=batch)]
+        layout = ["bhsd", "packed"][trial % 2]
+        tile = int(rng.choice([32, 64, 128]))
+        p = la.Plan(batch, hkv * g, hkv, 128, lens, tile_n=tile, grid=int(rng.integers(1, 300)), layout=layout,
+                    host_only=True, schedule="streamk", q_lens=qls)
+        tm = min(8, max(g * n for n in qls))
+        c_n = []
+        for (b, _h) in unit_order(batch, hkv, layout):
+            c_n += [-(-lens[b] // tile)] * (-(-(g * qls[b]) // tm))
+        exp = np.array([s.row() for s in oracle.stream_k_segments(c_n, p.info.grid)], dtype=np.int32).reshape(-1, 7)
+        assert np.array_equal(p.export(), exp), trial
+        assert p.info.tile_rows == tm and p.info.num_units == len(c_n)
+        assert p.info.q_rows == sum(hkv * g * n for n in qls)
+        assert p.info.q_len == (qls[0] if len(set(qls)) == 1 else 0)
+
+
+def test_heterogeneous_validation(la):
+    for qls, status in [([1, 0], la.LA_ERR_INVALID), ([1, 101], la.LA_ERR_INVALID)]:
+        with pytest.raises(la.LaError) as e:
+            la.Plan(2, 2, 2, 128, [100, 100], host_only=True, q_lens=qls)
+        assert e.value.status == status
+    with pytest.raises(la.LaError) as e:   # causal multi-token blocks are not shard-local
+        la.Plan(2, 2, 2, 128, [100, 100], host_only=True, q_lens=[1, 2], xchg_world=2)
+    assert e.value.status == la.LA_ERR_UNSUPPORTED
+    p = la.Plan(1, 32, 2, 128, [1000], host_only=True)         # MQA-like g = 16: two 8-row tiles
+    assert p.info.tile_rows == 8 and p.info.num_units == 4
