@@ -366,7 +366,19 @@ def bench_ours(args):
         dist.barrier()
     torch.cuda.synchronize(dev)
     total_ms = t_start.elapsed_time(t_end)
-    kern_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1)) / args.steps
+    kern_each = sorted(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    kern_ms = sum(kern_each) / args.steps
+    pct = {f"p{q}": kern_each[min(len(kern_each) - 1, int(q / 100 * len(kern_each)))] * 1e3 for q in (10, 50, 90)}
+    unflushed_us = None
+    if flush is not None and world == 1:   # L2-resident config: also the warm-L2 kernel time
+        u0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        u1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for i in range(args.steps):
+            u0[i].record(stream)
+            plan.decode(q, k, v, out, lse, stream=stream)
+            u1[i].record(stream)
+        torch.cuda.synchronize(dev)
+        unflushed_us = sorted(a.elapsed_time(b) for a, b in zip(u0, u1))[args.steps // 2] * 1e3
     step_ms = total_ms / args.steps
     if flush is not None:   # the flush is not part of the step: report the kernel time
         step_ms = kern_ms if world == 1 else step_ms
@@ -419,6 +431,15 @@ def bench_ours(args):
         cpu = {"value": sample_bytes(units, synth.DTYPE_BYTES[p.dtype]) / secs / 1e9, "unit": "GB/s",
                "cores": blas_threads(), "kind": "oracle", "seconds": secs,
                "sample": f"{len(units)} of {p.batch * p.heads_kv} (b, h_kv) units of {cfg} (full context each)"}
+        try:   # the same oracle on ONE core, on a smaller bounded sample
+            from threadpoolctl import threadpool_limits
+            one = units[:max(1, len(units) // 8)]
+            with threadpool_limits(1):
+                secs1 = run_oracle_sample(one, p.scale)
+            cpu["single_thread"] = {"value": sample_bytes(one, synth.DTYPE_BYTES[p.dtype]) / secs1 / 1e9,
+                                    "seconds": secs1, "sample": f"{len(one)} unit(s)"}
+        except ImportError:
+            pass
 
     if rank == 0:
         peak, peak_src = peaks()
@@ -444,7 +465,8 @@ def bench_ours(args):
                        **({"exchange_check": xchg_note} if xchg_note else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": f"la_decode<{'Gqa' if info.group > 1 else 'Mha'}Engine<{p.dtype},{p.head_dim}>>", "kernel_us": kern_ms * 1e3,
+                         "kernel": f"la_decode<{'Gqa' if info.group > 1 else 'Mha'}Engine<{p.dtype},{p.head_dim}>>", "kernel_us": kern_ms * 1e3, "kernel_us_pct": pct,
+                         **({"kernel_us_unflushed_p50": unflushed_us} if unflushed_us is not None else {}),
                          "algorithmic_bytes_per_launch": local_kv,
                          "read_probe_gbs": read_probe_gbs(),
                          "frac_of_read_probe": (achieved / read_probe_gbs()) if read_probe_gbs() else None},

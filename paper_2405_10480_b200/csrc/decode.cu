@@ -625,6 +625,7 @@ constexpr int kGS = 16;  // dynamic-mode fold tree: segments per first-level gro
 
 struct SegInfo {
   int v, unit, host, finishing;
+  int s0;  // ring slot of the segment's first stage
 };
 
 template <class E>
@@ -722,16 +723,6 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       v = __shfl_sync(0xffffffffu, v, 0);
       ++k;
       if (v >= NV) break;
-      // Align the virtual CTA's first stage to ring slot 0 (empty phases), so the stage ->
-      // consumer-warp assignment -- hence every rounding -- depends only on v, not on
-      // which CTAs claimed what before: bitwise-deterministic output (reading C16).
-      for (; j % NST != 0; ++j) {
-        const int slot = j % NST;
-        if (lane == 0) {
-          if (j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
-          mbar_arrive(&full[slot]);
-        }
-      }
       const int it1 = a.cta_begin[v + 1];
       int unit = a.cta_first_unit[v];
       for (int it = a.cta_begin[v]; it < it1;) {
@@ -780,6 +771,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       }
     };
     int nr = 0;  // output rows of the current segment's unit (its query tile, <= H)
+    uint32_t stage_ph = 0;  // phase of stage_bar (peers' partials staged for a fold)
     auto store_partial = [&](int slot) {  // StorePartials(Op, mp, lp) (Alg2§20-22)
 #pragma unroll
       for (int h = 0; h < H; ++h) {
@@ -797,92 +789,55 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     };
     // acc = f(...f(f(acc, P[slot(p0)]), P[slot(p0 + stride)])..., P[slot(<= p1)]), ascending
     // (Alg2§27-35); host_v's partial lives in slot 1 of its virtual CTA, everyone else's in 0
-    auto fold_range = [&](int p0, int p1, int stride, int host_v) {
-      // The §4.1 operator is associative (reading C22), so the fold is evaluated in the
-      // max-first form: every peer's m is read lane-parallel, the final M = max(m_acc, m_p..)
-      // is known before any O~_p is touched, and each O~_p then enters with its own weight
-      // 2^(m_p - M) (Alg2§32-34) -- the peers' loads carry no serial dependence on a running
-      // max and stream back to back, NB peers per round trip.  Rows are folded one after the
-      // other (few live registers).  Fixed order: bitwise deterministic.
+    // Fold peers p0, p0 + stride, .. <= p1 into acc (Alg2§27-35), their partials staged in
+    // smem `stg` (stg_floats): the ring when idle (static host) or the segment's consumed
+    // fold buffer (dynamic tree).  A peer's O~ rows and its (m, l) rows are contiguous, so
+    // a chunk arrives by 1-D bulk copies on stage_bar -- ONE pair for a contiguous run of
+    // slot-0 peers (per-peer copies cost ~50 issue cycles each on this one warp, measured)
+    // -- one round trip per chunk.  Each chunk is folded in the max-first form (reading
+    // C22): M = max(m_acc, m_p..) first, then every O~_p enters with weight 2^(m_p - M),
+    // with four independent accumulator chains; fixed order: bitwise deterministic.
+    auto fold_smem = [&](int p0, int p1, int stride, int host_v, float* stg, int stg_floats) {
       const int n = p1 < p0 ? 0 : (p1 - p0) / stride + 1;
-      auto row_of = [&](int i, int h) {
-        const int p = p0 + i * stride;
-        return (size_t(p + (p == host_v ? NV : 0))) * a.group + h;
-      };
-      constexpr int NB = 8;
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        if (h >= nr) continue;
-        float M = acc.m[h], lsum = 0.f;
-        for (int i = lane; i < n; i += 32) M = fmaxf(M, ld_cg(&a.part_ml[row_of(i, h) * 4]));
-#pragma unroll
-        for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const float wa = ex2_sub(acc.m[h], M);  // idle / masked accumulator: -inf -> 0
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) acc.o[h][jj] *= wa;
-        for (int c = 0; c < n; c += 32) {
-          float w = 0.f;
-          if (c + lane < n) {
-            const size_t row = row_of(c + lane, h);
-            w = ex2_sub(ld_cg(&a.part_ml[row * 4]), M);
-            lsum = fmaf(w, ld_cg(&a.part_ml[row * 4 + 1]), lsum);
-          }
-          const int cn = min(32, n - c);
-          for (int jb = 0; jb < cn; jb += NB) {
-            float op[NB][J];
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              if (jb + b >= cn) continue;
-              const size_t row = row_of(c + jb + b, h);
-#pragma unroll
-              for (int jj = 0; jj < J; ++jj) op[b][jj] = ld_cg(&a.part_o[row * D + lane + 32 * jj]);
-            }
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              const float wb = __shfl_sync(0xffffffffu, w, (jb + b) & 31);
-              if (jb + b >= cn) continue;
-#pragma unroll
-              for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = fmaf(wb, op[b][jj], acc.o[h][jj]);
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-        acc.l[h] = fmaf(wa, acc.l[h], lsum);
-        acc.m[h] = M;
-      }
-    };
-    // Static host: the same max-first fold of peers p0..p1, staged through the ring.  A
-    // non-finishing host segment is its CTA's last (its unit runs past the CTA's range), so
-    // the ring is idle.  Slot-0 partials of consecutive virtual CTAs are contiguous, so ONE
-    // 1-D bulk copy brings every peer's O~ rows and one more their (m, l) rows: a single
-    // round trip and two issues (per-peer or per-16-byte copies are issue-bound on the one
-    // epilogue warp -- measured ~7 us for 127 peers).  Then folded from smem with four
-    // independent accumulator chains (fixed order: deterministic).
-    auto fold_staged = [&](int p0, int p1) {
-      float* stg = reinterpret_cast<float*>(ring);
-      const int rows = a.group;
-      const int po = rows * D, pm = rows * 4;  // floats per peer: O~ rows, (m, l, -, -) rows
-      const int cap = max(1, (Smem<E>::RING / 4) / (po + pm));
-      const int n = p1 - p0 + 1;
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired partials -> TMA reads
-      for (int c0 = 0, ph = 0; c0 < n; c0 += cap, ph ^= 1) {
+      const int po = a.group * D, pm = a.group * 4;  // staged per peer: whole slots (rows >= nr unused)
+      const int cap = max(1, stg_floats / (po + pm));
+      const bool contiguous = stride == 1 && (host_v < p0 || host_v > p1);
+      asm volatile("fence.proxy.async.global;" ::: "memory");      // acquired partials -> TMA
+      #pragma unroll 1
+      for (int c0 = 0; c0 < n; c0 += cap) {
         const int cn = min(cap, n - c0);
-        float* so = stg;            // [cn][rows][D]
-        float* sm = stg + cn * po;  // [cn][rows][4]
-        if (lane == 0) {
-          mbar_arrive_expect_tx(stage_bar, uint32_t(cn) * (po + pm) * 4);
-          bulk_g2s_plain(so, a.part_o + size_t(p0 + c0) * po, uint32_t(cn) * po * 4, stage_bar);
-          bulk_g2s_plain(sm, a.part_ml + size_t(p0 + c0) * pm, uint32_t(cn) * pm * 4, stage_bar);
+        float* so = stg;            // [cn][nr][D]
+        float* sm = stg + cn * po;  // [cn][nr][4]
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier smem reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(cn) * (po + pm) * 4);
+        __syncwarp();
+        if (contiguous) {
+          if (lane == 0) {
+            const size_t r = size_t(p0 + c0) * a.group;
+            bulk_g2s_plain(so, a.part_o + r * D, uint32_t(cn) * po * 4, stage_bar);
+            bulk_g2s_plain(sm, a.part_ml + r * 4, uint32_t(cn) * pm * 4, stage_bar);
+          }
+        } else {
+          #pragma unroll 1
+          for (int i = lane; i < cn; i += 32) {
+            const int p = p0 + (c0 + i) * stride;
+            const size_t r = size_t(p + (p == host_v ? NV : 0)) * a.group;
+            bulk_g2s_plain(so + i * po, a.part_o + r * D, uint32_t(po) * 4, stage_bar);
+            bulk_g2s_plain(sm + i * pm, a.part_ml + r * 4, uint32_t(pm) * 4, stage_bar);
+          }
         }
-        mbar_wait(stage_bar, ph);
+        mbar_wait(stage_bar, stage_ph);
+        stage_ph ^= 1u;
 #pragma unroll
         for (int h = 0; h < H; ++h) {
           if (h >= nr) continue;
           float M = acc.m[h], lsum = 0.f;
+          #pragma unroll 1
           for (int i = lane; i < cn; i += 32) M = fmaxf(M, sm[i * pm + 4 * h]);
 #pragma unroll
           for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+          #pragma unroll 1
           for (int i = lane; i < cn; i += 32) {
             float* ml = sm + i * pm + 4 * h;
             const float w = ex2_sub(ml[0], M);
@@ -890,7 +845,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
             ml[2] = w;
           }
           __syncwarp();
-          const float wa = ex2_sub(acc.m[h], M);
+          const float wa = ex2_sub(acc.m[h], M);  // idle / masked accumulator: -inf -> 0
           float o4[4][J];
 #pragma unroll
           for (int jj = 0; jj < J; ++jj) {
@@ -898,6 +853,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
             o4[1][jj] = o4[2][jj] = o4[3][jj] = 0.f;
           }
           int i = 0;
+          #pragma unroll 1
           for (; i + 4 <= cn; i += 4) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -907,6 +863,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
               for (int jj = 0; jj < J; ++jj) o4[c][jj] = fmaf(w, r[lane + 32 * jj], o4[c][jj]);
             }
           }
+          #pragma unroll 1
           for (; i < cn; ++i) {
             const float w = sm[i * pm + 4 * h + 2];
             const float* r = so + i * po + h * D;
@@ -920,8 +877,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           acc.l[h] = fmaf(wa, acc.l[h], lsum);
           acc.m[h] = M;
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the next TMA
-        __syncwarp();
+        __syncwarp();  // the next chunk overwrites the stage
       }
     };
     // NEXT-2: push this rank's normalised shard partial of unit `unit` into every rank's
@@ -938,6 +894,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       for (int h = 0; h < H; ++h) {
         if (h >= nr) continue;
         const float inv = 1.f / acc.l[h], l2 = acc.m[h] + log2f(acc.l[h]);
+        #pragma unroll 1
         for (int d = 0; d < P; ++d) {
           float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + q_row + h) * RS;
 #pragma unroll
@@ -968,10 +925,12 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       for (int h = 0; h < H; ++h) {
         if (h >= nr) continue;
         float M = -INFINITY;
+        #pragma unroll 1
         for (int r = 0; r < P; ++r) M = fmaxf(M, ld_cg(xb + (size_t(r) * a.xrows + q_row + h) * RS + D));
         float l = 0.f, o[J];
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
+        #pragma unroll 1
         for (int r = 0; r < P; ++r) {
           const float* src = xb + (size_t(r) * a.xrows + q_row + h) * RS;
           const float w = ex2_sub(ld_cg(src + D), M);
@@ -1015,8 +974,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         float l = 0.f, o[J];
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
+        // Summed in the order of the slots RELATIVE to the segment's first stage: warp
+        // (slot (s0 + c) % NST, sub) holds the segment's stages c, c + NST, ... whatever s0
+        // is, so the rounding depends only on the segment, never on where the ring stood
+        // when it began (dynamic claims need no ring alignment; reading C16).
 #pragma unroll
-        for (int w = 0; w < NCW; ++w) {
+        for (int cw = 0; cw < NCW; ++cw) {
+          const int w = ((si.s0 + cw / WPS) % NST) * WPS + cw % WPS;
           const float* r = fb + (w * H + h) * (D + 2);
           const float wt = ex2_sub(r[D], mx);  // idle warp / masked row: m = -inf -> 0
           l = fmaf(wt, r[D + 1], l);
@@ -1029,13 +993,21 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = o[jj];
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill this buffer
       const DevUnit u = a.units[si.unit];
       const int v = si.v;
       nr = u.rows;
+      // the dynamic tree fold stages its peers in this (consumed) fold buffer: release later
+      const bool keep_fb = dynamic && !(si.host && si.finishing);
+      if (!keep_fb && lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill it
 
-      if (si.host && si.finishing) {
-        write_out(u.q_row, si.unit);  // one (virtual) CTA computed the whole unit (Alg2§38-39)
+      // Every path below ends in at most one fold loop and one write_out: ONE call site
+      // each keeps the epilogue code small (it runs rarely; an inlined copy per path blew
+      // the kernel up to 48k instructions and its folds ran from instruction-cache misses).
+      bool out = si.host && si.finishing;  // one (virtual) CTA computed the whole unit (Alg2§38-39)
+      int fp0 = 0, fp1 = -1, fstride = 1, fhv = -1, ngrp = 1, g0 = 0;
+      float* fstg = nullptr;
+      int fn = 0;
+      if (out) {
       } else if (!dynamic) {
         if (!si.host) {
           // ---- static, non-host: StorePartials + Signal(flags[g]) (Alg2§19-23) -----------
@@ -1048,23 +1020,24 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           // ---- static host, not finishing: Wait(flags[cta]) for cta = g+1 .. last_cta
           //      (Alg2§26-28, reading C9), lanes poll peers in parallel; fold ascending -----
           if (tr && lane == 0) tr[TR_WAIT0] = globaltimer();
+#pragma unroll 1
           for (int p = v + 1 + lane; p <= u.last_cta; p += 32)
             while (ld_acquire_gpu(&a.flags[p]) != a.epoch) __nanosleep(20);
           __syncwarp();
           if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
-          fold_staged(v + 1, u.last_cta);
-          if (tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
-          write_out(u.q_row, si.unit);
+          fp0 = v + 1;
+          fp1 = u.last_cta;
+          fstg = reinterpret_cast<float*>(ring);  // idle: this is the CTA's last segment
+          fn = Smem<E>::RING / 4;
         }
       } else {
         // ---- dynamic: publish, count in; a FIXED two-level tree folds the unit's segments
         //      (virtual CTAs host_cta .. last_cta): the last arriver of each group of kGS
         //      consecutive segments folds the group ascending into the group's first slot,
         //      the last group folds the groups ascending.  Deterministic; nobody waits.
-        const int hv = u.host_cta;
-        const int nseg = u.last_cta - hv + 1;
-        const int ngrp = (nseg + kGS - 1) / kGS;
-        const int g0 = hv + ((v - hv) / kGS) * kGS;
+        fhv = u.host_cta;
+        ngrp = (u.last_cta - fhv + 1 + kGS - 1) / kGS;
+        g0 = fhv + ((v - fhv) / kGS) * kGS;
         const int g1 = min(g0 + kGS, u.last_cta + 1) - 1;
         store_partial(v + (si.host ? NV : 0));
         int role = 0;
@@ -1076,27 +1049,39 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           }
           if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
         }
-        role = __shfl_sync(0xffffffffu, role, 0);
-        if (role) {
-          reset();
-          fold_range(g0, g1, 1, hv);
-          if (ngrp == 1) {
-            write_out(u.q_row, si.unit);
-          } else {
-            store_partial(g0 + (g0 == hv ? NV : 0));
-            int last = 0;
-            if (lane == 0 && atomicAdd(&a.unit_count[si.unit], 1) == ngrp - 1) {
-              __threadfence();
-              a.unit_count[si.unit] = 0;
-              last = 1;
-            }
-            if (__shfl_sync(0xffffffffu, last, 0)) {
-              reset();
-              fold_range(hv, u.last_cta, kGS, hv);
-              write_out(u.q_row, si.unit);
-            }
-          }
+        if (__shfl_sync(0xffffffffu, role, 0)) {
+          fp0 = g0;
+          fp1 = g1;
+          fstg = fold + b * FOLD_FLOATS;  // this segment's consumed fold buffer
+          fn = FOLD_FLOATS;
         }
+      }
+#pragma unroll 1
+      while (fstg) {
+        if (dynamic) reset();
+        fold_smem(fp0, fp1, fstride, fhv, fstg, fn);
+        if (!dynamic || fstride == kGS || ngrp == 1) {
+          out = true;
+          break;
+        }
+        // dynamic, a group of a multi-group unit: publish the group's fold, count it in
+        store_partial(g0 + (g0 == fhv ? NV : 0));
+        int last = 0;
+        if (lane == 0 && atomicAdd(&a.unit_count[si.unit], 1) == ngrp - 1) {
+          __threadfence();
+          a.unit_count[si.unit] = 0;
+          last = 1;
+        }
+        if (!__shfl_sync(0xffffffffu, last, 0)) break;
+        fp0 = fhv;
+        fp1 = u.last_cta;
+        fstride = kGS;
+      }
+      if (!dynamic && fstg && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
+      if (out) write_out(u.q_row, si.unit);
+      if (keep_fb) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fold_empty[b]);  // staging done: consumers may refill it
       }
     }
     if (lane == 0) {
@@ -1115,12 +1100,12 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   // ================================= consumers ==========================================
   const int my_slot = warp / WPS, sub = warp % WPS;
   int j = 0, k = 0, seg = 0;
-  auto hand_off = [&](const typename E::State* st, int v, int unit, int host, int finishing) {
+  auto hand_off = [&](const typename E::State* st, int v, int unit, int host, int finishing, int s0) {
     // give this warp's segment partial to the epilogue warp (double-buffered)
     const int b = seg % kFB;
     if (seg >= kFB) mbar_wait(&fold_empty[b], ((seg / kFB) - 1) & 1);
     if (st) E::seg_end(*const_cast<typename E::State*>(st), fold + b * FOLD_FLOATS, warp, lane);
-    if (warp == 0 && lane == 0) seginfo[b] = SegInfo{v, unit, host, finishing};
+    if (warp == 0 && lane == 0) seginfo[b] = SegInfo{v, unit, host, finishing, s0};
     __syncwarp();
     if (lane == 0) mbar_arrive(&fold_full[b]);
     ++seg;
@@ -1137,13 +1122,6 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       tr[TR_WAIT0] += 1;
       tr[TR_WAIT1] += a.cta_begin[v + 1] - a.cta_begin[v];
     }
-    for (; j % NST != 0; ++j) {  // the producer's empty alignment phases
-      if (j % NST == my_slot) {
-        mbar_wait(&full[my_slot], (j / NST) & 1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[my_slot]);
-      }
-    }
     const int it1 = a.cta_begin[v + 1];
     int unit = a.cta_first_unit[v];
     for (int it = a.cta_begin[v]; it < it1;) {
@@ -1157,6 +1135,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       const int finishing = (it1 >= u.iter_end) ? 1 : 0;  // finishing-block (Alg2§18)
       typename E::State st;
       E::seg_begin(st, a, u, lane);
+      const int seg_s0 = j % NST;
       for (; it < seg_end; ++it) {
         const int t0 = (it - u.iter_begin) * a.tile_n;
         const int t1 = min(t0 + a.tile_n, u.len);
@@ -1171,11 +1150,11 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           ++j;
         }
       }
-      hand_off(&st, v, unit, host, finishing);
+      hand_off(&st, v, unit, host, finishing, seg_s0);
       ++unit;
     }
   }
-  hand_off(nullptr, -1, -1, 0, 0);  // terminator for the epilogue
+  hand_off(nullptr, -1, -1, 0, 0, 0);  // terminator for the epilogue
 }
 
 // ---------------------------------------------------------------------------------------

@@ -90,10 +90,11 @@ def lib() -> ctypes.CDLL:
     L.la_decode_host.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
     L.la_plan_trace.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
                                 ctypes.POINTER(ctypes.c_size_t)]
-    L.la_plan_xchg_handle.argtypes = [vp, ctypes.c_char_p]
-    L.la_plan_xchg_open.argtypes = [vp, i32, ctypes.c_char_p]
-    L.la_plan_xchg_attach.argtypes = [vp, i32, vp]
-    L.la_plan_xchg_status.argtypes = [vp]
+    if hasattr(L, "la_plan_xchg_handle"):  # (older builds, e.g. LEANATTN_LIB bisects, lack it)
+        L.la_plan_xchg_handle.argtypes = [vp, ctypes.c_char_p]
+        L.la_plan_xchg_open.argtypes = [vp, i32, ctypes.c_char_p]
+        L.la_plan_xchg_attach.argtypes = [vp, i32, vp]
+        L.la_plan_xchg_status.argtypes = [vp]
     L.la_plan_destroy.argtypes = [vp]
     L.la_plan_destroy.restype = None
     L.la_launch_count.restype = i64
@@ -102,7 +103,8 @@ def lib() -> ctypes.CDLL:
     for name in ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
                  "la_decode_partial", "la_combine", "la_decode_host", "la_plan_trace", "la_plan_xchg_handle",
                  "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status"):
-        getattr(L, name).restype = ctypes.c_int
+        if hasattr(L, name):
+            getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
 
