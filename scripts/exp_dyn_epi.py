@@ -11,6 +11,6 @@ for cfg in ("c3", "c2"):
     t0 = tr[:, 1].min(); end = (tr[:, 5] - t0) / 1e3
     epi = (tr[:, 0] >> 16) / 1e3
     o = np.argsort(end)[::-1]
-    fold = tr[:, 2] / 1e3; nf = tr[:, 2] * 0
-    print(cfg, "copy-wait of slowest (us)", [(round(fold[g], 1), int(nf[g])) for g in o[:8]], "fold med", np.median(fold))
-    print(cfg, "end med", np.median(end), "max", end.max(), "epi med", np.median(epi), "compute of slowest (us)", [(round(end[g],1), round(epi[g],1), int(tr[g,3]), int(tr[g,4])) for g in o[:8]])
+    fold = tr[:, 2] * 1.0; nf = tr[:, 2] * 0
+    print(cfg, "segments of slowest", [(round(fold[g], 1), int(nf[g])) for g in o[:8]], "segments med", np.median(fold), "epi busy med", np.median((tr[:, 0] >> 16) / 1e3))
+    print(cfg, "end med", np.median(end), "max", end.max(), "epi med", np.median(epi), "epilogue busy (us) of slowest", [(round(end[g],1), round(epi[g],1), int(tr[g,3]), int(tr[g,4])) for g in o[:8]])
