@@ -453,6 +453,8 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.page_shift = 0;
   while (a.paged && (1 << a.page_shift) < plan->prob.page_size) ++a.page_shift;
   a.box_rows = a.paged ? std::min(64, plan->prob.page_size) : 64;
+  a.box_shift = 0;
+  while ((1 << a.box_shift) < a.box_rows) ++a.box_shift;
   a.grid = plan->sched.phys_grid;
   a.tile_n = plan->sched.tile_n;
   a.stage_tokens = plan->stage_tokens;

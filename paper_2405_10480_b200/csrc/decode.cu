@@ -290,8 +290,7 @@ struct MhaEngine {
 
   // This warp's 32-key rounds (sub, sub + WPS, ...) of one stage of ntok keys.
   __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, int /*tok0*/,
-                                               float scale_log2,
-                                               int lane) {
+                                               float scale_log2, int lane, int /*bs*/) {
     const int kg = lane / LPK, li = lane % LPK;
     const unsigned char* ks = st;
     const unsigned char* vs = st + STAGE_TOK * ROWB;
@@ -426,6 +425,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, in
       : "memory");
 }
 
+// 3-D tile: coordinates {element, row, 64-element half}; the d = 128 K/V maps view a row as
+// two 128-B halves so ONE box brings both halves of box_rows rows: smem [half][rows][128 B].
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 template <typename T, int D_, int NST_, int WPS_>
 struct GqaEngine {
   static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
@@ -450,16 +460,27 @@ struct GqaEngine {
   __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
                                                  int, uint64_t* bar, uint64_t pol) {
     mbar_arrive_expect_tx(bar, STAGE_BYTES);  // full boxes (rows past the tensor are zero-filled)
-#pragma unroll
-    for (int b = 0; b < NBOX; ++b) {
-      tma_load_2d(dst + b * BOX_BYTES, &tm.k, b * 64, int(row), bar, pol);
-      tma_load_2d(dst + KV_BYTES + b * BOX_BYTES, &tm.v, b * 64, int(row), bar, pol);
+    if (NBOX == 1) {
+      tma_load_2d(dst, &tm.k, 0, int(row), bar, pol);
+      tma_load_2d(dst + KV_BYTES, &tm.v, 0, int(row), bar, pol);
+    } else {  // both 128-B halves of 64 rows per op: [half][64 rows][128 B]
+      tma_load_3d(dst, &tm.k, 0, int(row), 0, bar, pol);
+      tma_load_3d(dst + KV_BYTES, &tm.v, 0, int(row), 0, bar, pol);
     }
   }
 
-  // Paged KV: boxes of box_rows = min(64, page) rows, each inside one page; a box at an
-  // 8-row multiple keeps the 128-B swizzle phase of the 64-row stage layout.
-  // Lane r of the producer warp issues load r = (box i, column b, K or V).
+  // Byte offset of the first 128-B line of stage row `tok` and the distance between the two
+  // halves of a row: a stage is 64 / box_rows boxes of [half][box_rows][128 B] (box_rows =
+  // 2^bs: 64 unpaged -- the plain [half][64][128 B] layout -- or min(64, page) paged).
+  __device__ __forceinline__ static uint32_t row_off(int tok, int bs) {
+    return NBOX == 1 ? uint32_t(tok) << 7
+                     : (uint32_t(tok >> bs) << (bs + 8)) + (uint32_t(tok & ((1 << bs) - 1)) << 7);
+  }
+  __device__ __forceinline__ static uint32_t half_stride(int bs) { return NBOX == 1 ? 0u : (1u << (bs + 7)); }
+
+  // Paged KV: boxes of box_rows = min(64, page) rows (both halves), each inside one page,
+  // at 1024-B multiples so the 128-B swizzle phase is the row index (see row_off).  Lane r
+  // of the producer warp issues load r = (box i, K or V): 2 ops per page, not 2 * NBOX.
   __device__ __forceinline__ static void produce_paged(unsigned char* dst, const DecodeArgs& a, const TmapPair& tm,
                                                        PageWin& pw, int s0, int ntok, uint64_t* bar, uint64_t pol,
                                                        int lane) {
@@ -467,11 +488,14 @@ struct GqaEngine {
     const int nb = (ntok + br - 1) / br;
     if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * NBOX * 2));
     __syncwarp();
-    for (int task = lane; task < nb * NBOX * 2; task += 32) {
-      const int i = task / (NBOX * 2), b = (task >> 1) % NBOX, is_v = task & 1;
+    for (int task = lane; task < nb * 2; task += 32) {
+      const int i = task >> 1, is_v = task & 1;
       const int row = int(pw.row_of(s0 + i * br));
-      tma_load_2d(dst + (is_v ? KV_BYTES : 0) + b * BOX_BYTES + i * br * 128, is_v ? &tm.v : &tm.k, b * 64, row,
-                  bar, pol);
+      unsigned char* d = dst + (is_v ? KV_BYTES : 0) + i * br * 128 * NBOX;
+      if (NBOX == 1)
+        tma_load_2d(d, is_v ? &tm.v : &tm.k, 0, row, bar, pol);
+      else
+        tma_load_3d(d, is_v ? &tm.v : &tm.k, 0, row, 0, bar, pol);
     }
   }
 
@@ -497,12 +521,13 @@ struct GqaEngine {
   // This warp's 32-token rounds (sub, sub + WPS, ...) of one stage of ntok tokens starting
   // at unit-local token tok0.
   __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, int tok0,
-                                               float scale_log2, int lane) {
-    for (int rb = sub * 32; rb < ntok; rb += 32 * WPS) round(s, st, rb, ntok, tok0, scale_log2, lane);
+                                               float scale_log2, int lane, int bs) {
+    for (int rb = sub * 32; rb < ntok; rb += 32 * WPS) round(s, st, rb, ntok, tok0, scale_log2, lane, bs);
   }
 
   __device__ __forceinline__ static void round(State& s, unsigned char* st, int rb, int ntok, int tok0,
-                                               float scale_log2, int lane) {
+                                               float scale_log2, int lane, int bs) {
+    const uint32_t hs = half_stride(bs);
     const int gq = lane >> 2, mi = lane >> 3, ri = lane & 7;
     if (rb + 32 > ntok) {
       // rows >= ntok of this round hold the next unit's rows or cache padding: zero this
@@ -511,7 +536,7 @@ struct GqaEngine {
         if (r >= ntok)
 #pragma unroll
           for (int b = 0; b < NBOX; ++b)
-            *reinterpret_cast<uint4*>(st + KV_BYTES + b * BOX_BYTES + r * 128 + (ri << 4)) = make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(st + KV_BYTES + b * hs + row_off(r, bs) + (ri << 4)) = make_uint4(0u, 0u, 0u, 0u);
       __syncwarp();
     }
     const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + KV_BYTES);
@@ -521,11 +546,12 @@ struct GqaEngine {
     for (int blk = 0; blk < 2; ++blk) {
       sc[blk][0] = sc[blk][1] = sc[blk][2] = sc[blk][3] = 0.f;
       const int tok = rb + blk * 16 + ri + ((mi & 1) << 3);
+      const uint32_t ro = kbase + row_off(tok, bs);
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int chunk = 2 * kk + (mi >> 1);
         uint32_t af[4];
-        ldsm_x4(kbase + (chunk >> 3) * BOX_BYTES + tok * 128 + (((chunk & 7) ^ (tok & 7)) << 4), af);
+        ldsm_x4(ro + (chunk >> 3) * hs + (((chunk & 7) ^ (tok & 7)) << 4), af);
         Mma<T>::run(sc[blk], af, s.qb[kk][0], s.qb[kk][1]);
       }
     }
@@ -579,11 +605,12 @@ struct GqaEngine {
       const uint32_t c0 = movmatrix_t(Mma<T>::pack(p0 - r01.x, p1 - r01.y));  // P_lo
       const uint32_t c1 = movmatrix_t(Mma<T>::pack(p2 - r23.x, p3 - r23.y));
       const int tok = rb + blk * 16 + ri + ((mi >> 1) << 3);
+      const uint32_t ro = vbase + row_off(tok, bs);
 #pragma unroll
       for (int mm = 0; mm < KS; ++mm) {
         const int chunk = 2 * mm + (mi & 1);
         uint32_t af[4];
-        ldsm_x4_t(vbase + (chunk >> 3) * BOX_BYTES + tok * 128 + (((chunk & 7) ^ (tok & 7)) << 4), af);
+        ldsm_x4_t(ro + (chunk >> 3) * hs + (((chunk & 7) ^ (tok & 7)) << 4), af);
         Mma<T>::run(s.o[mm], af, b0, b1);
         if (LA_GQA_SPLITP) Mma<T>::run(s.o[mm], af, c0, c1);
       }
@@ -1143,7 +1170,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           if (j % NST == my_slot) {
             mbar_wait(&full[my_slot], (j / NST) & 1);
             E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
-                     lane);
+                     lane, a.box_shift);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[my_slot]);
           }
@@ -1209,11 +1236,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn(std::string& err) {
 bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype, int box_rows, std::string& err) {
   auto enc = encode_fn(err);
   if (!enc) return false;
-  cuuint64_t gdim[2] = {cuuint64_t(d), cuuint64_t(rows)};
-  cuuint64_t gstride[1] = {cuuint64_t(d) * 2};
-  cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, dtype == LA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  // d = 64: 2-D {element, row}.  d = 128: 3-D {element, row, half} (half stride 128 B), so
+  // one box carries both 128-B halves of box_rows rows (GqaEngine::row_off).
+  const int rank = d == 64 ? 2 : 3;
+  cuuint64_t gdim[3] = {64, cuuint64_t(rows), 2};
+  cuuint64_t gstride[2] = {cuuint64_t(d) * 2, 128};
+  cuuint32_t box[3] = {64, cuuint32_t(box_rows), 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(tm, dtype == LA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
                    const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {

@@ -129,6 +129,7 @@ struct DecodeArgs {
   int pt_stride;      // padded to a multiple of 32 entries (the producer reads 32-entry windows)
   int heads_kv;
   int box_rows;       // GQA TMA box height: min(64, page_size) when paged, else 64
+  int box_shift;      // log2(box_rows)
   // NEXT-2 fused cross-GPU exchange (xw > 1).  Every rank's buffer holds
   // [2 launch parity][xw source ranks][xrows][d + 4] fp32 (normalised O_r, then L_r in log2
   // units) followed, at byte offset xflag_off, by [xw source ranks][xunits] uint32 flags.
