@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential", "fixed_split"])
     ap.add_argument("--page-size", type=int, default=0, help="run the config in a paged KV pool (16..256)")
     ap.add_argument("--tile-n", type=int, default=0, help="LeanTile size T_n (0 = planner's auto rule)")
+    ap.add_argument("--dtype", default=None, choices=["bf16", "fp16", "fp8"],
+                    help="KV storage type (default: the config's; fp8 = E4M3 codes + scales, bf16 q; NEXT-4)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only to test the multi-rank path on one GPU)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
@@ -267,14 +269,17 @@ def bench_ours(args):
             o_all.copy_(oa)
             l_all.copy_(lb)
     cfg = args.config or ("c2" if world == 1 else "c5")
-    p = synth.config(cfg)
+    dkw = {"dtype": args.dtype} if args.dtype else {}
+    p = synth.config(cfg, **dkw)
     paged_kw = {}
+    if p.dtype == "fp8":
+        paged_kw = dict(k_scale=p.k_scale, v_scale=p.v_scale)
     if args.page_size:  # the same workload in a paged pool (NEXT-4); single GPU only
         if world > 1:
             raise SystemExit("--page-size is a single-GPU option")
-        p = synth.config(cfg, layout="paged", page_size=args.page_size)
+        p = synth.config(cfg, layout="paged", page_size=args.page_size, **dkw)
         bt, num_pages = synth.paged_meta(p)
-        paged_kw = dict(block_table=bt, page_size=args.page_size, num_pages=num_pages)
+        paged_kw.update(block_table=bt, page_size=args.page_size, num_pages=num_pages)
     bounds = synth.shard_bounds(p, rank, world)
     lens = [b - a for a, b in bounds]
     fused = world > 1 and (args.exchange == "p2p" or (args.exchange == "auto" and args.backend == "nccl"))
@@ -444,14 +449,17 @@ def bench_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         achieved = local_kv / (kern_ms * 1e-3) / 1e9   # dominant kernel, per launch
-        traffic = ncu_traffic(cfg)
+        traffic = ncu_traffic(cfg + ("-fp8" if p.dtype == "fp8" else ""))
+        engine = "Fp8" if p.dtype == "fp8" else ("Gqa" if info.tile_rows > 1 else "Mha")
         line = {
             "metric": METRIC, "value": total_kv / (step_ms * 1e-3) / 1e9, "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "latency_us": step_ms * 1e3, "higher_is_better": True,
             "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": p.dtype,
             "data": "synthetic (seeded counter-based generator, distribution D1; DESIGN.md input recipe)",
-            "config": {"workload": f"{cfg}: {WORKLOADS[cfg]}", "batch": p.batch, "heads_q": p.heads_q,
+            "config": {"workload": f"{cfg}: {WORKLOADS[cfg]}" + (
+                           f" -- FP8 E4M3 KV variant (k_scale {p.k_scale}, v_scale {p.v_scale}, bf16 q)"
+                           if p.dtype == "fp8" else ""), "batch": p.batch, "heads_q": p.heads_q,
                        "heads_kv": p.heads_kv, "head_dim": p.head_dim,
                        "context": p.ctx_lens[0] if len(set(p.ctx_lens)) == 1 else p.ctx_lens,
                        "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
@@ -465,7 +473,7 @@ def bench_ours(args):
                        **({"exchange_check": xchg_note} if xchg_note else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": f"la_decode<{'Gqa' if info.group > 1 else 'Mha'}Engine<{p.dtype},{p.head_dim}>>", "kernel_us": kern_ms * 1e3, "kernel_us_pct": pct,
+                         "kernel": f"la_decode<{engine}Engine<{p.dtype},{p.head_dim}>>", "kernel_us": kern_ms * 1e3, "kernel_us_pct": pct,
                          **({"kernel_us_unflushed_p50": unflushed_us} if unflushed_us is not None else {}),
                          "algorithmic_bytes_per_launch": local_kv,
                          "read_probe_gbs": read_probe_gbs(),

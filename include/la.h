@@ -52,8 +52,12 @@ typedef enum {
   LA_ERR_TIMEOUT = 6       /* a cross-GPU exchange wait gave up (a peer never arrived)   */
 } la_status;
 
-/* Storage type of Q, K and V ("FP16->32": 16-bit inputs, fp32 arithmetic). */
-typedef enum { LA_BF16 = 0, LA_FP16 = 1, LA_FP32 = 2 } la_dtype;
+/* Storage type of Q, K and V ("FP16->32": 16-bit inputs, fp32 arithmetic).
+   LA_FP8_E4M3 (NEXT-4, not in the paper): K and V hold OCP FP8 E4M3 codes (1 byte each;
+   the cache is K = code x opts.k_scale, V = code x opts.v_scale) and q is bf16; head_dim
+   128 only.  The codes are widened exactly to f16 on chip; q is rounded bf16 -> f16 for
+   the tensor-core QK^T (reading C23: exact for 2^-14 <= |q| < 65504). */
+typedef enum { LA_BF16 = 0, LA_FP16 = 1, LA_FP32 = 2, LA_FP8_E4M3 = 3 } la_dtype;
 
 /* KV cache layouts (reading C14 fixes the unit linearisation order). */
 typedef enum {
@@ -130,6 +134,9 @@ typedef struct {
                                  or NULL for q_len everywhere.  q / out / lse then hold, per
                                  request in order, an (H_q, N_b[, d]) block (rows (b, h_q, i)
                                  contiguous); with NULL this is exactly (B, H_q, N_q[, d])    */
+  /* LA_FP8_E4M3 only (per-tensor dequantisation scales; 0 -> 1): */
+  float k_scale;              /* K = code x k_scale (folded into the score scale)             */
+  float v_scale;              /* V = code x v_scale (applied once, at finalize: O x v_scale)  */
 } la_plan_opts;
 
 typedef struct la_plan_s* la_plan_t;
@@ -164,7 +171,8 @@ la_status la_plan_opts_init(la_plan_opts* opts);
  * {64, 128}; ctx_lens: HOST array of `batch` int32, each >= 1 (reading C6); tile_n: LeanTile
  * tokens in {16, 32, 64, 128, 256, 512}, or 0 for the default (T_n giving 64 KiB of K+V per
  * LeanTile -- 128 tokens at d=128 bf16, 256 at d=64, as the paper's sweep found).
- * dtype: storage type of q, k, v.  opts may be NULL (defaults).
+ * dtype: storage type of q, k, v (LA_FP8_E4M3: E4M3 k, v codes with a bf16 q).  opts may be
+ * NULL (defaults).
  *
  * Implements Alg2§4-18: units in memory order, C_n(u) = ceil(n_u / T_n), I = sum C_n,
  * per-CTA ranges by the remainder rule (reading C8), per unit the owning host CTA and the
@@ -192,7 +200,7 @@ la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t*
 /*
  * la_decode -- one decode-attention step on `stream` (asynchronous).
  *
- * q: device (B, H_q, d) of the plan's dtype, contiguous.  k_cache, v_cache: device, plan's
+ * q: device (B, H_q, d) of the plan's dtype (bf16 for LA_FP8_E4M3), contiguous.  k_cache, v_cache: device, plan's
  * layout and dtype, contiguous, 16-byte aligned.  out: device (B, H_q, d) fp32.  lse:
  * device (B, H_q) fp32 natural-log logsumexp L, or NULL to skip it.  ctx_lens are the
  * plan's (a serving loop re-plans when they change; planning is O(B*H_kv + G)).

@@ -18,6 +18,8 @@ Modules
 * :mod:`oracle.schedule`   -- Alg. 2 §4-18/§41 stream-K segment walk and
   an independent per-iteration owner enumeration (the planner's bit-exact reference).
 * :mod:`oracle.lean_attention` -- Alg. 2 executed serially in fp64 (partials, host folds).
+* :mod:`oracle.fp8`         -- E4M3 byte -> value (the OCP format definition) and the
+  per-tensor dequantisation of an FP8 KV cache (NEXT-4; not in the paper).
 * :mod:`oracle.shard_combine` -- the sequence-shard combine of normalised (O_r, L_r) pairs
   (BASELINE.json north star; exact by §4.1's associativity).
 
@@ -33,6 +35,7 @@ from .schedule import (Segment, iters_per_cta, cta_range, owner, stream_k_segmen
                        guided_ranges, fixed_split_ranges, fa2_num_splits)
 from .lean_attention import lean_attention
 from .shard_combine import combine_shards
+from .fp8 import e4m3_decode, dequantize
 
 __all__ = [
     "decode_attention", "decode_attention_unit", "decode_attention_multi", "decode_attention_varq", "scores",
@@ -42,5 +45,5 @@ __all__ = [
     "segments_from_owner_table", "last_cta_literal", "fixed_split_segments",
     "quantization_efficiency", "segments_from_ranges", "guided_ranges", "fixed_split_ranges",
     "fa2_num_splits",
-    "lean_attention", "combine_shards",
+    "lean_attention", "combine_shards", "e4m3_decode", "dequantize",
 ]

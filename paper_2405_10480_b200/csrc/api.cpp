@@ -145,7 +145,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (heads_q % heads_kv) return fail(LA_ERR_INVALID, "heads_q must be a multiple of heads_kv (reading C3)");
   if (!ctx_lens) return fail(LA_ERR_INVALID, "ctx_lens is NULL");
   if (head_dim != 64 && head_dim != 128) return fail(LA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
-  if (dtype != LA_BF16 && dtype != LA_FP16 && dtype != LA_FP32) return fail(LA_ERR_INVALID, "bad dtype");
+  if (dtype != LA_BF16 && dtype != LA_FP16 && dtype != LA_FP32 && dtype != LA_FP8_E4M3)
+    return fail(LA_ERR_INVALID, "bad dtype");
+  if (dtype == LA_FP8_E4M3 && head_dim != 128) return fail(LA_ERR_UNSUPPORTED, "FP8 KV needs head_dim 128");
   if (opts.layout != LA_KV_BHSD && opts.layout != LA_KV_PACKED && opts.layout != LA_KV_PAGED)
     return fail(LA_ERR_INVALID, "bad layout");
   if (opts.schedule != LA_SCHED_STREAMK && opts.schedule != LA_SCHED_SEQUENTIAL &&
@@ -207,6 +209,12 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (p.layout == LA_KV_BHSD && p.max_ctx < maxn) return fail(LA_ERR_INVALID, "max_ctx < max(ctx_lens)");
   p.scale = opts.scale != 0.f ? opts.scale : float(1.0 / std::sqrt(double(head_dim)));
   if (!(p.scale > 0.f) || !std::isfinite(p.scale)) return fail(LA_ERR_INVALID, "scale must be finite and > 0");
+  if (dtype == LA_FP8_E4M3) {
+    p.k_scale = opts.k_scale != 0.f ? opts.k_scale : 1.f;
+    p.v_scale = opts.v_scale != 0.f ? opts.v_scale : 1.f;
+    if (!(p.k_scale > 0.f) || !std::isfinite(p.k_scale) || !(p.v_scale > 0.f) || !std::isfinite(p.v_scale))
+      return fail(LA_ERR_INVALID, "k_scale / v_scale must be finite and > 0");
+  }
   if (p.layout == LA_KV_PAGED) {
     const int ps = opts.page_size;
     if (ps != 16 && ps != 32 && ps != 64 && ps != 128 && ps != 256)
@@ -452,7 +460,8 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.heads_kv = plan->prob.heads_kv;
   a.page_shift = 0;
   while (a.paged && (1 << a.page_shift) < plan->prob.page_size) ++a.page_shift;
-  a.box_rows = a.paged ? std::min(64, plan->prob.page_size) : 64;
+  const int box = plan->kinfo.stage_tokens_max;  // GQA / FP8 TMA box height = a full stage
+  a.box_rows = a.paged ? std::min(box, plan->prob.page_size) : box;
   a.box_shift = 0;
   while ((1 << a.box_shift) < a.box_rows) ++a.box_shift;
   a.grid = plan->sched.phys_grid;
@@ -461,7 +470,8 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.group = plan->prob.rows();
   a.q_len = plan->prob.q_len;
   a.causal = plan->prob.causal;
-  a.scale_log2 = float(double(plan->prob.scale) * 1.4426950408889634);
+  a.scale_log2 = float(double(plan->prob.scale) * double(plan->prob.k_scale) * 1.4426950408889634);
+  a.out_scale = plan->prob.v_scale;
   if (plan->xw && xchg) {
     for (int r = 0; r < plan->xw; ++r)
       if (!plan->xpeer[r]) return fail(LA_ERR_STATE, "exchange peer " + std::to_string(r) + " not opened/attached");
@@ -510,7 +520,7 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
   const la::Problem& p = plan->prob;
   if (kv_rows != p.kv_rows()) return fail(LA_ERR_INVALID, "kv_rows does not match the plan");
   const size_t eb = size_t(p.elem_bytes());
-  const size_t q_bytes = size_t(p.q_rows()) * p.head_dim * eb;
+  const size_t q_bytes = size_t(p.q_rows()) * p.head_dim * p.q_elem_bytes();
   const size_t kv_bytes = size_t(kv_rows) * p.head_dim * eb;
   const size_t o_bytes = size_t(p.q_rows()) * p.head_dim * sizeof(float);
   const size_t l_bytes = size_t(p.q_rows()) * sizeof(float);

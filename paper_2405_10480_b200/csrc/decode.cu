@@ -645,6 +645,223 @@ struct GqaEngine {
 };
 
 // =======================================================================================
+// FP8 engine (NEXT-4: E4M3 KV cache, bf16 Q; any T_m <= 8 incl. MHA): tensor cores
+// =======================================================================================
+// The KV codes are widened to f16 in registers (cvt.rn.f16x2.e4m3x2: exact, every E4M3
+// value is an f16 normal or zero) straight from ldmatrix fragments, and the GQA engine's
+// swap-AB m16n8k16 MMAs run in f16 (Q rounded bf16 -> f16, reading C23).  The fragments
+// come from ldmatrix on byte PAIRS, so their element order differs from a 16-bit tile:
+//  * S^T = K_f Q_f^T: a plain ldmatrix of 8 tokens x 16 codes gives lane (gq, tq) the four
+//    codes at dims 4tq .. 4tq+3 of one token -- the A fragment's k pairs (2tq, 2tq+1) and
+//    (2tq+8, 2tq+9) take dims (4tq, 4tq+1) and (4tq+2, 4tq+3).  The contraction index may
+//    be permuted freely, so Q's B fragment is built with the same permutation.
+//  * O^T += V^T P^T: ldmatrix.trans of 8 tokens x 16 codes gives lane (gq, tq) the codes
+//    of dims (2gq, 2gq+1) of tokens (2tq, 2tq+1); one byte permute regroups them per dim,
+//    so A row gq holds dim 2gq and row gq + 8 dim 2gq + 1 of the 16-dim slice (an output-
+//    row permutation, undone where the accumulator is written out).
+__device__ __forceinline__ uint32_t e4m3x2_lo(uint32_t x) {  // codes in bits 0-15 -> f16x2
+  uint32_t y;
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, lo;\n\t}" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t e4m3x2_hi(uint32_t x) {  // codes in bits 16-31 -> f16x2
+  uint32_t y;
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, hi;\n\t}" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t sel) {
+  uint32_t y;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(y) : "r"(x), "r"(sel));
+  return y;
+}
+
+template <int D_, int NST_, int WPS_>
+struct Fp8Engine {
+  static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
+  static_assert(D == 128, "an E4M3 row of d = 128 is exactly one 128-B swizzle span");
+  static constexpr int STAGE_TOK = 128;           // = TMA box rows (32 KiB of K+V per stage)
+  static constexpr int KV_BYTES = STAGE_TOK * 128;
+  static constexpr int STAGE_BYTES = 2 * KV_BYTES;
+  static constexpr int HEADS = 8;
+  static constexpr int KS = D / 16;
+  static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
+  static constexpr int FOLD_BUFS = LA_GQA_FB;
+  static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
+
+  struct State {
+    uint32_t qb[KS][2];  // Q^T B-fragments (f16, permuted contraction order, see above)
+    float m[2], l[2];
+    float o[KS][4];      // O^T: dims 16mm + 2gq (+1), rows 2tq, 2tq+1
+    int lim[2];
+  };
+
+  __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
+                                                 int, uint64_t* bar, uint64_t pol) {
+    mbar_arrive_expect_tx(bar, STAGE_BYTES);
+    tma_load_2d(dst, &tm.k, 0, int(row), bar, pol);
+    tma_load_2d(dst + KV_BYTES, &tm.v, 0, int(row), bar, pol);
+  }
+
+  // Paged: boxes of box_rows = min(128, page) rows inside one page; lane r issues load r.
+  __device__ __forceinline__ static void produce_paged(unsigned char* dst, const DecodeArgs& a, const TmapPair& tm,
+                                                       PageWin& pw, int s0, int ntok, uint64_t* bar, uint64_t pol,
+                                                       int lane) {
+    const int br = a.box_rows;
+    const int nb = (ntok + br - 1) / br;
+    if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * 2));
+    __syncwarp();
+    for (int task = lane; task < nb * 2; task += 32) {
+      const int i = task >> 1, is_v = task & 1;
+      const int row = int(pw.row_of(s0 + i * br));
+      tma_load_2d(dst + (is_v ? KV_BYTES : 0) + i * br * 128, is_v ? &tm.v : &tm.k, 0, row, bar, pol);
+    }
+  }
+
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
+    const int gq = lane >> 2, tq = lane & 3;
+    const __nv_bfloat16* qrow = static_cast<const __nv_bfloat16*>(a.q) + size_t(u.q_row + gq) * D;
+    const bool ok = gq < u.rows;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {  // b0 = Q[gq][16kk + 4tq, +1], b1 = Q[gq][16kk + 4tq + 2, +3]
+      const uint2 w = ok ? *reinterpret_cast<const uint2*>(qrow + 16 * kk + 4 * tq) : make_uint2(0u, 0u);
+      const float2 f01 = Mma<__nv_bfloat16>::unpack(w.x), f23 = Mma<__nv_bfloat16>::unpack(w.y);
+      s.qb[kk][0] = Mma<__half>::pack(f01.x, f01.y);
+      s.qb[kk][1] = Mma<__half>::pack(f23.x, f23.y);
+    }
+    s.m[0] = s.m[1] = -INFINITY;
+    s.l[0] = s.l[1] = 0.f;
+#pragma unroll
+    for (int mm = 0; mm < KS; ++mm) s.o[mm][0] = s.o[mm][1] = s.o[mm][2] = s.o[mm][3] = 0.f;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      s.lim[e] = a.causal ? u.len - u.nq + ((u.r0 + 2 * tq + e) % u.nq) + 1 : u.len;
+  }
+
+  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, int tok0,
+                                               float scale_log2, int lane, int /*bs*/) {
+    for (int rb = sub * 32; rb < ntok; rb += 32 * WPS) round(s, st, rb, ntok, tok0, scale_log2, lane);
+  }
+
+  __device__ __forceinline__ static void round(State& s, unsigned char* st, int rb, int ntok, int tok0,
+                                               float scale_log2, int lane) {
+    const int gq = lane >> 2, mi = lane >> 3, ri = lane & 7;
+    if (rb + 32 > ntok) {  // rows past the stage's tokens: zero this warp's V rows (codes may be NaN)
+      for (int r = rb + (lane >> 3); r < rb + 32; r += 4)
+        if (r >= ntok) *reinterpret_cast<uint4*>(st + KV_BYTES + r * 128 + (ri << 4)) = make_uint4(0u, 0u, 0u, 0u);
+      __syncwarp();
+    }
+    const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + KV_BYTES);
+    // ---- S^T = K_f Q_f^T (Alg1§20): matrices (token half mi&1, 16-dim chunk 2kp + mi>>1) ---
+    float sc[2][4];
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      sc[blk][0] = sc[blk][1] = sc[blk][2] = sc[blk][3] = 0.f;
+      const int tok = rb + blk * 16 + ((mi & 1) << 3) + ri;
+      const uint32_t ro = kbase + uint32_t(tok) * 128;
+#pragma unroll
+      for (int kp = 0; kp < KS / 2; ++kp) {
+        uint32_t r[4];
+        ldsm_x4(ro + (((2 * kp + (mi >> 1)) ^ (tok & 7)) << 4), r);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t af[4] = {e4m3x2_lo(r[2 * h]), e4m3x2_lo(r[2 * h + 1]), e4m3x2_hi(r[2 * h]),
+                                  e4m3x2_hi(r[2 * h + 1])};
+          Mma<__half>::run(sc[blk], af, s.qb[2 * kp + h][0], s.qb[2 * kp + h][1]);
+        }
+      }
+    }
+    // ---- scale, mask (C5, causal), running max per row (Alg1§21) ----------------------------
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int tok = rb + blk * 16 + gq + ((e >> 1) << 3);
+        const bool ok = tok < ntok && tok0 + tok < s.lim[e & 1];
+        sc[blk][e] = ok ? sc[blk][e] * scale_log2 : -INFINITY;
+        mx[e & 1] = fmaxf(mx[e & 1], sc[blk][e]);
+      }
+    }
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) {
+      mx[0] = fmaxf(mx[0], __shfl_xor_sync(0xffffffffu, mx[0], off));
+      mx[1] = fmaxf(mx[1], __shfl_xor_sync(0xffffffffu, mx[1], off));
+    }
+    if (__any_sync(0xffffffffu, (mx[0] > s.m[0]) || (mx[1] > s.m[1]))) {  // Alg1§23-24 rescale
+      const float mn0 = fmaxf(s.m[0], mx[0]), mn1 = fmaxf(s.m[1], mx[1]);
+      const float al0 = ex2_sub(s.m[0], mn0), al1 = ex2_sub(s.m[1], mn1);
+      s.l[0] *= al0;
+      s.l[1] *= al1;
+#pragma unroll
+      for (int mm = 0; mm < KS; ++mm) {
+        s.o[mm][0] *= al0;
+        s.o[mm][2] *= al0;
+        s.o[mm][1] *= al1;
+        s.o[mm][3] *= al1;
+      }
+      s.m[0] = mn0;
+      s.m[1] = mn1;
+    }
+    // ---- P_f = exp(S_f - m) (Alg1§22); O^T += V^T P^T (Alg1§24) -----------------------------
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const float p0 = ex2_sub(sc[blk][0], s.m[0]), p1 = ex2_sub(sc[blk][1], s.m[1]);
+      const float p2 = ex2_sub(sc[blk][2], s.m[0]), p3 = ex2_sub(sc[blk][3], s.m[1]);
+      s.l[0] += p0 + p2;
+      s.l[1] += p1 + p3;
+      // P in f16 (11-bit significand); P_lo carries the rest when LA_GQA_SPLITP (reading C18)
+      const uint32_t h01 = Mma<__half>::pack(p0, p1), h23 = Mma<__half>::pack(p2, p3);
+      const uint32_t b0 = movmatrix_t(h01), b1 = movmatrix_t(h23);
+      uint32_t c0 = 0u, c1 = 0u;
+      if (LA_GQA_SPLITP) {
+        const float2 r01 = Mma<__half>::unpack(h01), r23 = Mma<__half>::unpack(h23);
+        c0 = movmatrix_t(Mma<__half>::pack(p0 - r01.x, p1 - r01.y));
+        c1 = movmatrix_t(Mma<__half>::pack(p2 - r23.x, p3 - r23.y));
+      }
+      const int tok = rb + blk * 16 + ((mi & 1) << 3) + ri;
+      const uint32_t ro = vbase + uint32_t(tok) * 128;
+#pragma unroll
+      for (int mp = 0; mp < KS / 2; ++mp) {
+        uint32_t r[4];
+        ldsm_x4_t(ro + (((2 * mp + (mi >> 1)) ^ (tok & 7)) << 4), r);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          // bytes (t 2tq: dim 2gq, 2gq+1 | t 2tq+1: dim 2gq, 2gq+1) -> per dim: (t 2tq, t 2tq+1)
+          const uint32_t x0 = prmt(r[2 * h], 0x3120u), x1 = prmt(r[2 * h + 1], 0x3120u);
+          const uint32_t af[4] = {e4m3x2_lo(x0), e4m3x2_hi(x0), e4m3x2_lo(x1), e4m3x2_hi(x1)};
+          Mma<__half>::run(s.o[2 * mp + h], af, b0, b1);
+          if (LA_GQA_SPLITP) Mma<__half>::run(s.o[2 * mp + h], af, c0, c1);
+        }
+      }
+    }
+    if (rb + 32 > ntok) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> TMA WAR
+  }
+
+  __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
+    const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) {
+      s.l[0] += __shfl_xor_sync(0xffffffffu, s.l[0], off);
+      s.l[1] += __shfl_xor_sync(0xffffffffu, s.l[1], off);
+    }
+    float* fb = fold + warp * HEADS * (D + 2);  // [head][D + 2]
+    const int h0 = 2 * tq, h1 = 2 * tq + 1;
+#pragma unroll
+    for (int mm = 0; mm < KS; ++mm) {
+      const int c = 16 * mm + 2 * gq;  // accumulator rows gq / gq + 8 = dims c / c + 1
+      *reinterpret_cast<float2*>(fb + h0 * (D + 2) + c) = make_float2(s.o[mm][0], s.o[mm][2]);
+      *reinterpret_cast<float2*>(fb + h1 * (D + 2) + c) = make_float2(s.o[mm][1], s.o[mm][3]);
+    }
+    if (gq == 0) {
+      fb[h0 * (D + 2) + D] = s.m[0];
+      fb[h0 * (D + 2) + D + 1] = s.l[0];
+      fb[h1 * (D + 2) + D] = s.m[1];
+      fb[h1 * (D + 2) + D + 1] = s.l[1];
+    }
+  }
+};
+
+// =======================================================================================
 // The persistent decode kernel
 // =======================================================================================
 constexpr int kQD = 4;   // depth of the producer -> consumer virtual-CTA queue
@@ -920,7 +1137,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         if (h >= nr) continue;
-        const float inv = 1.f / acc.l[h], l2 = acc.m[h] + log2f(acc.l[h]);
+        const float inv = a.out_scale / acc.l[h], l2 = acc.m[h] + log2f(acc.l[h]);
         #pragma unroll 1
         for (int d = 0; d < P; ++d) {
           float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + q_row + h) * RS;
@@ -979,7 +1196,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         if (h >= nr) continue;
-        const float inv = 1.f / acc.l[h];
+        const float inv = a.out_scale / acc.l[h];  // V = codes x v_scale (FP8 KV; 1 otherwise)
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) a.out[size_t(q_row + h) * D + lane + 32 * jj] = acc.o[h][jj] * inv;
         if (lane == 0 && a.lse) a.lse[q_row + h] = (acc.m[h] + log2f(acc.l[h])) * kLn2;
@@ -1238,12 +1455,17 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
   if (!enc) return false;
   // d = 64: 2-D {element, row}.  d = 128: 3-D {element, row, half} (half stride 128 B), so
   // one box carries both 128-B halves of box_rows rows (GqaEngine::row_off).
-  const int rank = d == 64 ? 2 : 3;
-  cuuint64_t gdim[3] = {64, cuuint64_t(rows), 2};
-  cuuint64_t gstride[2] = {cuuint64_t(d) * 2, 128};
-  cuuint32_t box[3] = {64, cuuint32_t(box_rows), 2};
+  // FP8 (d = 128): 2-D {code, row}, one 128-B box row per token.
+  const bool fp8 = dtype == LA_FP8_E4M3;
+  const int rank = (d == 64 || fp8) ? 2 : 3;
+  cuuint64_t gdim[3] = {cuuint64_t(fp8 ? 128 : 64), cuuint64_t(rows), 2};
+  cuuint64_t gstride[2] = {cuuint64_t(d) * (fp8 ? 1 : 2), 128};
+  cuuint32_t box[3] = {cuuint32_t(fp8 ? 128 : 64), cuuint32_t(box_rows), 2};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(tm, dtype == LA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+  const CUtensorMapDataType ty = fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                     : (dtype == LA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                         : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+  CUresult r = enc(tm, ty, rank,
                    const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -1256,6 +1478,10 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
 }  // namespace
 
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group) {
+  if (dtype == LA_FP8_E4M3) {  // one tensor-core engine for every T_m <= 8 (MHA included)
+    if (head_dim == 128 && group <= 8) return info_of<Fp8Engine<128, LA_GQA_NST, LA_GQA_WPS>>(true);
+    return KernelInfo{};
+  }
   if (group == 1) {
     if (dtype == LA_BF16 && head_dim == 128) return info_of<MhaEngine<__nv_bfloat16, 128, LA_MHA_NST, LA_MHA_WPS>>(false);
     if (dtype == LA_BF16 && head_dim == 64) return info_of<MhaEngine<__nv_bfloat16, 64, LA_MHA_NST, LA_MHA_WPS>>(false);

@@ -68,7 +68,9 @@ struct Problem {
   int64_t num_pages = 0;
   std::vector<int32_t> block_table;  // [batch][pages_per_seq]
   int64_t kv_rows() const;   // rows of one K (or V) cache in its layout
-  int elem_bytes() const { return dtype == LA_FP32 ? 4 : 2; }
+  float k_scale = 1.f, v_scale = 1.f;  // LA_FP8_E4M3: K = codes x k_scale, V = codes x v_scale
+  int elem_bytes() const { return dtype == LA_FP32 ? 4 : (dtype == LA_FP8_E4M3 ? 1 : 2); }  // K/V
+  int q_elem_bytes() const { return dtype == LA_FP32 ? 4 : 2; }  // Q (bf16 with FP8 KV)
 };
 
 // Build units in memory order (reading C14) with their row bases and C_n = ceil(n/T_n).
@@ -120,7 +122,8 @@ struct DecodeArgs {
   int q_len;          // N_q (unused by the kernels: per-unit DevUnit::nq)
   int causal;         // N_q > 1: query i attends to unit-local keys [0, n - N_q + i]
   int uses_tmap;      // set by launch_decode for the TMA-tensor (GQA) engine
-  float scale_log2;   // scale * log2(e): scores live in the exp2 domain inside the kernel
+  float scale_log2;   // scale * log2(e) (* k_scale for FP8 KV): scores live in the exp2 domain
+  float out_scale;    // finalize multiplies O by this: v_scale for FP8 KV, else 1
   // LA_KV_PAGED: DevUnit.row0 holds b * heads_kv + h; token t of the unit is row
   // (block_table[b * pt_stride + (t >> page_shift)] * heads_kv + h) * page + (t & (page - 1))
   const int32_t* block_table;

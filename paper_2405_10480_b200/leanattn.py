@@ -22,11 +22,11 @@ LIB_PATH = os.environ.get("LEANATTN_LIB") or os.path.join(_HERE, "lib", "liblean
 
 LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STATE, LA_ERR_TIMEOUT = range(7)
 LA_XCHG_HANDLE_BYTES = 64
-LA_BF16, LA_FP16, LA_FP32 = 0, 1, 2
+LA_BF16, LA_FP16, LA_FP32, LA_FP8_E4M3 = 0, 1, 2, 3
 LA_KV_BHSD, LA_KV_PACKED, LA_KV_PAGED = 0, 1, 2
 LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC, LA_SCHED_FIXED_SPLIT = 0, 1, 2, 3
 
-_DTYPE_CODES = {"bf16": LA_BF16, "fp16": LA_FP16, "fp32": LA_FP32}
+_DTYPE_CODES = {"bf16": LA_BF16, "fp16": LA_FP16, "fp32": LA_FP32, "fp8": LA_FP8_E4M3}  # fp8: E4M3 K/V, bf16 q
 _LAYOUT_CODES = {"bhsd": LA_KV_BHSD, "packed": LA_KV_PACKED, "paged": LA_KV_PAGED}
 _SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, "dynamic": LA_SCHED_DYNAMIC,
                 "fixed_split": LA_SCHED_FIXED_SPLIT}
@@ -52,7 +52,8 @@ class la_plan_opts(ctypes.Structure):
                 ("block_table", ctypes.POINTER(ctypes.c_int32)), ("pages_per_seq", ctypes.c_int),
                 ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64), ("q_len", ctypes.c_int),
                 ("causal", ctypes.c_int), ("xchg_world", ctypes.c_int), ("xchg_rank", ctypes.c_int),
-                ("q_lens", ctypes.POINTER(ctypes.c_int32))]
+                ("q_lens", ctypes.POINTER(ctypes.c_int32)), ("k_scale", ctypes.c_float),
+                ("v_scale", ctypes.c_float)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -138,7 +139,8 @@ class Plan:
                  ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
                  dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
-                 causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None):
+                 causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None,
+                 k_scale: float = 0.0, v_scale: float = 0.0):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -165,6 +167,8 @@ class Plan:
         opts.causal = 1 if causal else 0
         opts.xchg_world = int(xchg_world)
         opts.xchg_rank = int(xchg_rank)
+        opts.k_scale = float(k_scale)  # dtype "fp8": K = codes x k_scale, V = codes x v_scale
+        opts.v_scale = float(v_scale)
         if q_lens is not None:  # heterogeneous batch: N_b per request
             ql = np.ascontiguousarray(np.asarray(q_lens, dtype=np.int32))
             self._ql = ql

@@ -40,8 +40,10 @@ from typing import List, Optional, Sequence
 import torch
 
 _M32 = 0xFFFFFFFF
-_DTYPES = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
-DTYPE_BYTES = {"bf16": 2, "fp16": 2, "fp32": 4}
+_DTYPES = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32, "fp8": torch.float8_e4m3fn}
+DTYPE_BYTES = {"bf16": 2, "fp16": 2, "fp32": 4, "fp8": 1}   # K/V bytes per element
+Q_DTYPE = {"bf16": "bf16", "fp16": "fp16", "fp32": "fp32", "fp8": "bf16"}  # FP8 KV keeps a bf16 q
+E4M3_MAX = 448.0
 
 
 def _hash32_int(x: int) -> int:
@@ -89,8 +91,12 @@ def _uniform_from_index(idx: torch.Tensor, key: int) -> torch.Tensor:
 
 
 def _round(x64: torch.Tensor, dtype: str) -> torch.Tensor:
-    """fp64 -> fp32 -> storage dtype, each a correctly rounded (RNE) cast."""
-    return x64.to(torch.float32).to(_DTYPES[dtype])
+    """fp64 -> fp32 -> storage dtype, each a correctly rounded (RNE) cast (E4M3: saturated
+    to +-448 first -- torch's cast would turn out-of-range values into NaN)."""
+    x32 = x64.to(torch.float32)
+    if dtype == "fp8":
+        x32 = x32.clamp(-E4M3_MAX, E4M3_MAX)
+    return x32.to(_DTYPES[dtype])
 
 
 @dataclass
@@ -117,10 +123,18 @@ class Problem:
     q_len: int = 1                 # N_q query tokens per request (q: (B, H_q, N_q, d) if > 1)
     q_lens: Optional[Sequence[int]] = None  # per-request N_b (heterogeneous batch): q is then
                                             # (sum_b H_q N_b, d), request blocks (H_q, N_b, d)
+    k_scale: Optional[float] = None  # dtype "fp8": stored code = value / scale (E4M3, RNE,
+    v_scale: Optional[float] = None  # saturating); the cache IS code x scale.  Defaults below.
 
     def __post_init__(self):
         if self.max_ctx is None:
             self.max_ctx = max(self.ctx_lens)
+        # FP8 defaults: amax-style per-tensor scales (non powers of two, so a dropped scale
+        # cannot hide); the census's integer V uses 1/2 so its codes stay exact
+        if self.k_scale is None:
+            self.k_scale = 0.0123 if self.dtype == "fp8" else 1.0
+        if self.v_scale is None:
+            self.v_scale = (0.5 if self.dist == "D3" else 0.0171) if self.dtype == "fp8" else 1.0
         assert len(self.ctx_lens) == self.batch
         assert self.heads_q % self.heads_kv == 0
 
@@ -171,8 +185,8 @@ def _q64(p: Problem, device) -> torch.Tensor:
 
 
 def gen_q(p: Problem, device="cpu") -> torch.Tensor:
-    """Q as (B, H_q, d) in the storage dtype."""
-    return _round(_q64(p, device), p.dtype)
+    """Q as (B, H_q, d) in the storage dtype (bf16 for an FP8 KV cache)."""
+    return _round(_q64(p, device), Q_DTYPE[p.dtype])
 
 
 def _qhat_for_unit(p: Problem, b: int, h: int, device) -> torch.Tensor:
@@ -228,19 +242,19 @@ def gen_kv_unit(p: Problem, b: int, h: int, which: str, device="cpu",
             else:
                 alpha = 8.0 / (p.scale * qn)
                 x = x + (alpha * (t.to(torch.float64) / n))[:, None] * qhat[None, :]
-        return _round(x, p.dtype)
+        return _round(x / p.k_scale, p.dtype) if p.dtype == "fp8" else _round(x, p.dtype)
     if which == "v":
         if p.dist == "D3":
             tc = _census_block(p, n)
             C = float(n // tc) if n % tc == 0 else 1.0
             hit = ((t // tc) % D)[:, None] == c[None, :]
-            return _round(hit.to(torch.float64) * C, p.dtype)
+            return _round(hit.to(torch.float64) * (C / p.v_scale), p.dtype)
         x = _normal_from_index(idx, _key(p.seed, 2))
-        if p.dist == "D0":
-            return _round(x, p.dtype)
-        mu_idx = ((b * p.heads_kv + h) * D + c)
-        mu = _uniform_from_index(mu_idx, _key(p.seed, 3)) * 2.0 - 1.0
-        return _round(mu[None, :] + 0.5 * x, p.dtype)
+        if p.dist != "D0":
+            mu_idx = ((b * p.heads_kv + h) * D + c)
+            mu = _uniform_from_index(mu_idx, _key(p.seed, 3)) * 2.0 - 1.0
+            x = mu[None, :] + 0.5 * x
+        return _round(x / p.v_scale, p.dtype) if p.dtype == "fp8" else _round(x, p.dtype)
     raise ValueError(which)
 
 
@@ -332,17 +346,19 @@ C4_CTX_LENS = [131072, 1024, 16586, 17950, 26213, 19032, 99749, 50527, 46403, 81
 
 
 def config(name: str, dist: str = "D1", **kw) -> Problem:
-    """BASELINE.json configs[0..4] as Problems (seed = 1000 + config index)."""
-    if name == "c1":
-        return Problem(1, 1, 1, 64, [4096], dtype="fp32", dist=dist, seed=1001, **kw)
-    if name == "c2":
-        return Problem(1, 32, 32, 128, [262144], dtype="bf16", dist=dist, seed=1002, **kw)
-    if name == "c3":
-        return Problem(8, 64, 8, 128, [65536] * 8, dtype="bf16", dist=dist, seed=1003, **kw)
-    if name == "c4":
-        return Problem(16, 32, 32, 128, list(C4_CTX_LENS), dtype="bf16", dist=dist, seed=1004, **kw)
-    if name == "c5":
-        return Problem(1, 32, 32, 128, [1 << 20], dtype="bf16", dist=dist, seed=1005, **kw)
+    """BASELINE.json configs[0..4] as Problems (seed = 1000 + config index); ``dtype=`` may
+    override the storage type (e.g. "fp8" for the FP8-KV variant of a workload)."""
+    shapes = {
+        "c1": ((1, 1, 1, 64, [4096]), "fp32", 1001),
+        "c2": ((1, 32, 32, 128, [262144]), "bf16", 1002),
+        "c3": ((8, 64, 8, 128, [65536] * 8), "bf16", 1003),
+        "c4": ((16, 32, 32, 128, list(C4_CTX_LENS)), "bf16", 1004),
+        "c5": ((1, 32, 32, 128, [1 << 20]), "bf16", 1005),
+    }
+    if name in shapes:
+        args, dtype, seed = shapes[name]
+        kw.setdefault("dtype", dtype)
+        return Problem(*args, dist=dist, seed=seed, **kw)
     raise ValueError(name)
 
 

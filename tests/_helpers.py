@@ -52,6 +52,8 @@ def run_cuda(p: synth.Problem, inputs=None, **plan_kw):
     if p.layout == "paged":
         bt, num_pages = synth.paged_meta(p)
         plan_kw = dict(plan_kw, block_table=bt, page_size=p.page_size, num_pages=num_pages)
+    if p.dtype == "fp8":
+        plan_kw = dict(plan_kw, k_scale=p.k_scale, v_scale=p.v_scale)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
                    max_ctx=p.max_ctx if p.layout == "bhsd" else 0, **plan_kw)
     out, lse = plan.decode(q, k, v)
@@ -59,11 +61,19 @@ def run_cuda(p: synth.Problem, inputs=None, **plan_kw):
     return out.cpu().numpy().astype(np.float64), lse.cpu().numpy().astype(np.float64), plan
 
 
+def kv_f64(p: synth.Problem, x: torch.Tensor, which: str):
+    """The cache values the oracle sees: FP8 codes decoded by the oracle's own E4M3 decoder
+    (the format definition) times the per-tensor scale (reading C23); else an exact upcast."""
+    if p.dtype == "fp8":
+        return oracle.dequantize(x.detach().cpu().view(torch.uint8).numpy(), p.k_scale if which == "k" else p.v_scale)
+    return synth.to_f64(x)
+
+
 def run_oracle(p: synth.Problem, causal: bool = True):
     """Full oracle on host-generated inputs (small problems)."""
     q = synth.to_f64(synth.gen_q(p))
-    k = synth.to_f64(synth.fill_kv_cache(p, "k"))
-    v = synth.to_f64(synth.fill_kv_cache(p, "v"))
+    k = kv_f64(p, synth.fill_kv_cache(p, "k"), "k")
+    v = kv_f64(p, synth.fill_kv_cache(p, "v"), "v")
     if p.q_len > 1:
         bt = synth.paged_meta(p)[0] if p.layout == "paged" else None
         return oracle.decode_attention_multi(q, k, v, p.ctx_lens, p.scale, causal, p.layout, block_table=bt,
@@ -78,8 +88,8 @@ def run_oracle(p: synth.Problem, causal: bool = True):
 def oracle_unit(p: synth.Problem, b: int, h: int):
     """Oracle output of one work unit (b, h_kv) -- for sampled checks at full size."""
     q = synth.to_f64(synth.gen_q(p))[b, h * p.group:(h + 1) * p.group]
-    k = synth.to_f64(synth.gen_kv_unit(p, b, h, "k"))
-    v = synth.to_f64(synth.gen_kv_unit(p, b, h, "v"))
+    k = kv_f64(p, synth.gen_kv_unit(p, b, h, "k"), "k")
+    v = kv_f64(p, synth.gen_kv_unit(p, b, h, "v"), "v")
     return oracle.decode_attention_unit(q, k, v, p.scale)
 
 

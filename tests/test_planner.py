@@ -251,3 +251,15 @@ def test_heterogeneous_validation(la):
     assert e.value.status == la.LA_ERR_UNSUPPORTED
     p = la.Plan(1, 32, 2, 128, [1000], host_only=True)         # MQA-like g = 16: two 8-row tiles
     assert p.info.tile_rows == 8 and p.info.num_units == 4
+
+
+def test_fp8_plan(la):
+    # FP8 KV (NEXT-4): 64 KiB LeanTiles are 256 tokens at d = 128; d = 64 is not built
+    p = la.Plan(1, 32, 32, 128, [262144], dtype="fp8", host_only=True)
+    assert p.info.tile_n == 256 and p.info.grid == 148 and p.info.kv_bytes == 2 * 32 * 262144 * 128
+    with pytest.raises(la.LaError) as e:
+        la.Plan(1, 2, 2, 64, [100], dtype="fp8", host_only=True)
+    assert e.value.status == 2
+    with pytest.raises(la.LaError) as e:
+        la.Plan(1, 2, 2, 128, [100], dtype="fp8", host_only=True, k_scale=-1.0)
+    assert e.value.status == 1
