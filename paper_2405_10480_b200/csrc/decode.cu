@@ -67,6 +67,27 @@
 #ifndef LA_GQA_SPLITP
 #define LA_GQA_SPLITP 1  // P = P_hi + P_lo on the tensor cores (0: single KV-type P)
 #endif
+#ifndef LA_FP8_NST
+#define LA_FP8_NST 5   // FP8 engine (T_m up to 8) ring stages of 32 KiB (128 tokens)
+#endif
+#ifndef LA_FP8_WPS
+#define LA_FP8_WPS 2
+#endif
+#ifndef LA_FP8_FB
+#define LA_FP8_FB 1    // fold buffers: 1 x 41.6 KB (NCW = 10) leaves room for the 5-deep ring
+#endif
+#ifndef LA_FP8M_NST
+#define LA_FP8M_NST 6  // FP8 engine, MHA (T_m = 1): 1-row fold buffers allow a 6-deep ring
+#endif
+#ifndef LA_FP8M_WPS
+#define LA_FP8M_WPS 2
+#endif
+#ifndef LA_FP8M_FB
+#define LA_FP8M_FB 2
+#endif
+#ifndef LA_FP8_SPLITP
+#define LA_FP8_SPLITP 0  // one f16 P (2^-12 relative, 256x finer than the E4M3 data); 1: P_hi + P_lo
+#endif
 
 namespace la {
 
@@ -675,17 +696,21 @@ __device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t sel) {
   return y;
 }
 
-template <int D_, int NST_, int WPS_>
+// ROWS_: output rows a unit can have (T_m): 8, or 1 for MHA decode -- the MMA still spans
+// 8 columns, but the fold buffer (and the epilogue's accumulator) only keep ROWS_ of them,
+// which frees shared memory for a deeper ring.
+template <int D_, int NST_, int WPS_, int ROWS_>
 struct Fp8Engine {
   static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
+  static_assert(ROWS_ == 1 || ROWS_ == 8, "fold rows");
   static_assert(D == 128, "an E4M3 row of d = 128 is exactly one 128-B swizzle span");
   static constexpr int STAGE_TOK = 128;           // = TMA box rows (32 KiB of K+V per stage)
   static constexpr int KV_BYTES = STAGE_TOK * 128;
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;
-  static constexpr int HEADS = 8;
+  static constexpr int HEADS = ROWS_;             // fold-buffer rows (MMA N is 8 regardless)
   static constexpr int KS = D / 16;
   static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
-  static constexpr int FOLD_BUFS = LA_GQA_FB;
+  static constexpr int FOLD_BUFS = ROWS_ == 1 ? LA_FP8M_FB : LA_FP8_FB;
   static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
 
   struct State {
@@ -813,7 +838,7 @@ struct Fp8Engine {
       const uint32_t h01 = Mma<__half>::pack(p0, p1), h23 = Mma<__half>::pack(p2, p3);
       const uint32_t b0 = movmatrix_t(h01), b1 = movmatrix_t(h23);
       uint32_t c0 = 0u, c1 = 0u;
-      if (LA_GQA_SPLITP) {
+      if (LA_FP8_SPLITP) {
         const float2 r01 = Mma<__half>::unpack(h01), r23 = Mma<__half>::unpack(h23);
         c0 = movmatrix_t(Mma<__half>::pack(p0 - r01.x, p1 - r01.y));
         c1 = movmatrix_t(Mma<__half>::pack(p2 - r23.x, p3 - r23.y));
@@ -830,7 +855,7 @@ struct Fp8Engine {
           const uint32_t x0 = prmt(r[2 * h], 0x3120u), x1 = prmt(r[2 * h + 1], 0x3120u);
           const uint32_t af[4] = {e4m3x2_lo(x0), e4m3x2_hi(x0), e4m3x2_lo(x1), e4m3x2_hi(x1)};
           Mma<__half>::run(s.o[2 * mp + h], af, b0, b1);
-          if (LA_GQA_SPLITP) Mma<__half>::run(s.o[2 * mp + h], af, c0, c1);
+          if (LA_FP8_SPLITP) Mma<__half>::run(s.o[2 * mp + h], af, c0, c1);
         }
       }
     }
@@ -846,17 +871,23 @@ struct Fp8Engine {
     }
     float* fb = fold + warp * HEADS * (D + 2);  // [head][D + 2]
     const int h0 = 2 * tq, h1 = 2 * tq + 1;
+    if (h0 < HEADS) {
 #pragma unroll
-    for (int mm = 0; mm < KS; ++mm) {
-      const int c = 16 * mm + 2 * gq;  // accumulator rows gq / gq + 8 = dims c / c + 1
-      *reinterpret_cast<float2*>(fb + h0 * (D + 2) + c) = make_float2(s.o[mm][0], s.o[mm][2]);
-      *reinterpret_cast<float2*>(fb + h1 * (D + 2) + c) = make_float2(s.o[mm][1], s.o[mm][3]);
+      for (int mm = 0; mm < KS; ++mm)  // accumulator rows gq / gq + 8 = dims c / c + 1
+        *reinterpret_cast<float2*>(fb + h0 * (D + 2) + 16 * mm + 2 * gq) = make_float2(s.o[mm][0], s.o[mm][2]);
+      if (gq == 0) {
+        fb[h0 * (D + 2) + D] = s.m[0];
+        fb[h0 * (D + 2) + D + 1] = s.l[0];
+      }
     }
-    if (gq == 0) {
-      fb[h0 * (D + 2) + D] = s.m[0];
-      fb[h0 * (D + 2) + D + 1] = s.l[0];
-      fb[h1 * (D + 2) + D] = s.m[1];
-      fb[h1 * (D + 2) + D + 1] = s.l[1];
+    if (h1 < HEADS) {
+#pragma unroll
+      for (int mm = 0; mm < KS; ++mm)
+        *reinterpret_cast<float2*>(fb + h1 * (D + 2) + 16 * mm + 2 * gq) = make_float2(s.o[mm][1], s.o[mm][3]);
+      if (gq == 0) {
+        fb[h1 * (D + 2) + D] = s.m[1];
+        fb[h1 * (D + 2) + D + 1] = s.l[1];
+      }
     }
   }
 };
@@ -1479,7 +1510,8 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
 
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group) {
   if (dtype == LA_FP8_E4M3) {  // one tensor-core engine for every T_m <= 8 (MHA included)
-    if (head_dim == 128 && group <= 8) return info_of<Fp8Engine<128, LA_GQA_NST, LA_GQA_WPS>>(true);
+    if (head_dim == 128 && group == 1) return info_of<Fp8Engine<128, LA_FP8M_NST, LA_FP8M_WPS, 1>>(true);
+    if (head_dim == 128 && group <= 8) return info_of<Fp8Engine<128, LA_FP8_NST, LA_FP8_WPS, 8>>(true);
     return KernelInfo{};
   }
   if (group == 1) {
