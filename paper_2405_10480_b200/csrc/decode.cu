@@ -1548,7 +1548,7 @@ int launch_decode(const KernelInfo& ki, const DecodeArgs& a_in, int64_t kv_rows,
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // static hosts spin on peers: co-residency
-  attr[0].val.cooperative = cooperative ? 1 : 0;
+  attr[0].val.cooperative = cooperative ? 1 : 0;  // measured: no cost vs a plain launch
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {&a, &tm};

@@ -29,8 +29,10 @@ def _run_fused(p, world, schedule="streamk", launches=3, causal=True):
         lens = [b - a for a, b in bounds]
         kv.append((synth.fill_kv_cache(p, "k", dev, token_range=bounds),
                    synth.fill_kv_cache(p, "v", dev, token_range=bounds)))
+        fp8 = dict(k_scale=p.k_scale, v_scale=p.v_scale) if p.dtype == "fp8" else {}
         plans.append(la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, grid=grid,
-                             schedule=schedule, xchg_world=world, xchg_rank=r, q_len=p.q_len, causal=causal))
+                             schedule=schedule, xchg_world=world, xchg_rank=r, q_len=p.q_len, causal=causal,
+                             **fp8))
     for r in range(world):
         for s in range(world):
             if s != r:
@@ -71,6 +73,18 @@ def test_fused_exchange_gqa_and_ragged(world):
     for per_rank in _run_fused(p, world, launches=2):
         for O, L in per_rank:
             gate(O, L, O_ref, L_ref, what=f"fused GQA P={world}")
+
+
+@pytest.mark.parametrize("group", [1, 8])
+def test_fused_exchange_fp8(group):
+    """FP8 KV shards (NEXT-4) through the fused exchange: v_scale is applied before the push."""
+    p = synth.Problem(2, 2 * group, 2, 128, [3000, 5333], dtype="fp8", dist="D2", seed=74)
+    O_ref, L_ref = run_oracle(p)
+    for per_rank in _run_fused(p, 4, launches=2):
+        O0, L0 = per_rank[0]
+        for O, L in per_rank:
+            assert np.array_equal(O, O0) and np.array_equal(L, L0)
+        gate(O0, L0, O_ref, L_ref, what=f"fused fp8 g{group}")
 
 
 def test_fused_exchange_multi_token_full():
