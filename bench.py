@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential", "fixed_split"])
     ap.add_argument("--page-size", type=int, default=0, help="run the config in a paged KV pool (16..256)")
+    ap.add_argument("--engine", default="mma", choices=["mma", "tcgen05"],
+                    help="tensor-core engine for T_m > 1 tiles (GQA): mma.sync or tcgen05 + TMEM")
     ap.add_argument("--tile-n", type=int, default=0, help="LeanTile size T_n (0 = planner's auto rule)")
     ap.add_argument("--dtype", default=None, choices=["bf16", "fp16", "fp8"],
                     help="KV storage type (default: the config's; fp8 = E4M3 codes + scales, bf16 q; NEXT-4)")
@@ -289,7 +291,7 @@ def bench_ours(args):
     v = synth.fill_kv_cache(p, "v", dev, token_range=None if args.page_size else bounds)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
                    schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min,
-                   tile_n=args.tile_n, **paged_kw,
+                   tile_n=args.tile_n, engine=args.engine, **paged_kw,
                    **(dict(xchg_world=world, xchg_rank=rank) if fused else {}))
     xchg_note = None
     if fused:   # collective decision: every rank maps every peer's buffer, or all use NCCL
@@ -449,8 +451,10 @@ def bench_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         achieved = local_kv / (kern_ms * 1e-3) / 1e9   # dominant kernel, per launch
-        traffic = ncu_traffic(cfg + ("-fp8" if p.dtype == "fp8" else ""))
-        engine = "Fp8" if p.dtype == "fp8" else ("Gqa" if info.tile_rows > 1 else "Mha")
+        traffic = ncu_traffic(cfg + ("-fp8" if p.dtype == "fp8" else "")
+                              + ("-tc5" if args.engine == "tcgen05" and info.tile_rows > 1 else ""))
+        engine = "Fp8" if p.dtype == "fp8" else (("Tc5" if args.engine == "tcgen05" else "Gqa")
+                                                 if info.tile_rows > 1 else "Mha")
         line = {
             "metric": METRIC, "value": total_kv / (step_ms * 1e-3) / 1e9, "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
@@ -464,6 +468,7 @@ def bench_ours(args):
                        "context": p.ctx_lens[0] if len(set(p.ctx_lens)) == 1 else p.ctx_lens,
                        "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
                        "stage_tokens": info.stage_tokens, "schedule": args.schedule,
+                       **({"engine": args.engine} if info.tile_rows > 1 and p.dtype != "fp8" else {}),
                        "kv_layout": p.layout + (f" (page {args.page_size})" if args.page_size else ""),
                        "virtual_ctas": info.num_vctas,
                        "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),

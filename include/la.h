@@ -137,7 +137,21 @@ typedef struct {
   /* LA_FP8_E4M3 only (per-tensor dequantisation scales; 0 -> 1): */
   float k_scale;              /* K = code x k_scale (folded into the score scale)             */
   float v_scale;              /* V = code x v_scale (applied once, at finalize: O x v_scale)  */
+  /* Tensor-core engine for T_m > 1 tiles (GQA groups / N_q > 1; MHA always runs on CUDA cores): */
+  int engine;                 /* la_engine, default LA_ENGINE_MMA_SYNC.  LA_ENGINE_TCGEN05
+                                 needs bf16 / fp16, head_dim 128 and a non-paged layout when
+                                 T_m > 1, else la_plan fails with LA_ERR_UNSUPPORTED; it is
+                                 ignored for T_m = 1 (MHA: a GEMV, CUDA cores)               */
 } la_plan_opts;
+
+/* Which tensor-core instructions contract the T_m x T_n tiles (Alg1§20, §24). */
+typedef enum {
+  LA_ENGINE_MMA_SYNC = 0, /* warp-level mma.sync m16n8k16: every consumer warp owns its own
+                             32-token rounds and accumulators in registers      */
+  LA_ENGINE_TCGEN05 = 1   /* 5th-gen tensor cores: one warpgroup per 128-token stage, one
+                             thread issues tcgen05.mma (M = 128 tokens / dims, N = 16) with
+                             S^T and the per-stage O^T in TMEM, read back by tcgen05.ld    */
+} la_engine;
 
 typedef struct la_plan_s* la_plan_t;
 

@@ -246,7 +246,15 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (plan->host_only) {
     max_ctas = std::max(1, opts.num_sms) * std::max(1, opts.ctas_per_sm);
   } else {
-    plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows());
+    if (opts.engine != LA_ENGINE_MMA_SYNC && opts.engine != LA_ENGINE_TCGEN05) {
+      delete plan;
+      return fail(LA_ERR_INVALID, "engine must be LA_ENGINE_MMA_SYNC or LA_ENGINE_TCGEN05");
+    }
+    if (opts.engine == LA_ENGINE_TCGEN05 && p.rows() > 1 && (p.layout == LA_KV_PAGED || dtype == LA_FP8_E4M3)) {
+      delete plan;
+      return fail(LA_ERR_UNSUPPORTED, "LA_ENGINE_TCGEN05 covers T_m > 1 tiles of a bf16 / fp16, non-paged cache");
+    }
+    plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows(), p.rows() > 1 ? opts.engine : 0);
     if (!plan->kinfo.supported) {
       delete plan;
       return fail(LA_ERR_UNSUPPORTED, "no decode kernel for this (dtype, head_dim, group) in this build");

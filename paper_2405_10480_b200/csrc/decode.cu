@@ -44,9 +44,11 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "la_internal.h"
 #include "ptx.cuh"
+#include "tc5.cuh"
 
 // Ring / warp configuration (build-time; the defaults are the measured best on B200).
 #ifndef LA_MHA_NST
@@ -84,6 +86,9 @@
 #endif
 #ifndef LA_FP8M_FB
 #define LA_FP8M_FB 2
+#endif
+#ifndef LA_TC5_NST
+#define LA_TC5_NST 3   // tcgen05 engine: ring stages of 64 KiB (128 tokens), one warpgroup each
 #endif
 #ifndef LA_FP8_SPLITP
 #define LA_FP8_SPLITP 0  // one f16 P (2^-12 relative, 256x finer than the E4M3 data); 1: P_hi + P_lo
@@ -893,6 +898,222 @@ struct Fp8Engine {
 };
 
 // =======================================================================================
+// tcgen05 engine (T_m <= 8 q-rows of one KV head, bf16 / fp16, d = 128): 5th-gen tensor
+// cores with TMEM accumulators (option LA_ENGINE_TCGEN05)
+// =======================================================================================
+// One WARPGROUP per ring slot (WPS = 4: warp sub reads TMEM lanes 32 sub .. 32 sub + 31)
+// takes every stage of 128 tokens that lands in its slot:
+//   S^T[128 tok][16] = K_f Q_f^T      tcgen05.mma M=128 N=16 K=16 x 8, A = K (K-major, the
+//                                     TMA 128-B swizzled box), B = Q (rows >= T_m zero)
+//   thread t <- token t's 8 scores    tcgen05.ld 32x32b; mask (C5, causal), per-row max over
+//                                     the warp (shuffles) and the warpgroup (smem, bar.sync)
+//   P^T[16][128 tok] (bf16 / fp16)    rows 0-7 P_hi, rows 8-15 P_lo = p - P_hi (reading C18),
+//                                     written K-major SW128 over the stage's dead K tile
+//   O^T[128 dim][16] = V_f^T P_f^T    tcgen05.mma M=128 N=16, A = V read MN-major from the
+//                                     same TMA box (no transpose pass), B = P
+//   thread t <- dim t's 16 columns    O_t[h] = alpha_h O_t[h] + O^T[t][h] + O^T[t][8 + h]
+// Each slot owns 32 TMEM columns (S at +0, O-tile at +16).  The per-tile O^T is a fresh
+// accumulator that is re-scaled and summed in registers (Alg1§24-25), so the tensor core
+// never needs the running max.
+template <typename T>
+__device__ __forceinline__ T to_kv(float x);
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_kv<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <>
+__device__ __forceinline__ __half to_kv<__half>(float x) { return __float2half_rn(x); }
+__device__ __forceinline__ float kv_to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ float kv_to_f(__half x) { return __half2float(x); }
+
+template <typename T, int NST_>
+struct Tc5Engine {
+  static constexpr int D = 128, NST = NST_, WPS = 4, NCW = NST * WPS;
+  static constexpr int STAGE_TOK = 128;             // = TMA box rows = MMA M
+  static constexpr int KV_BYTES = 2 * STAGE_TOK * 128;  // [half][128 rows][128 B]
+  static constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KiB
+  static constexpr int HEADS = 8;
+  static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
+  static constexpr int FOLD_FLOATS = NST * HEADS * (D + 2);
+  static constexpr int FOLD_BUFS = 1;
+  static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
+  static constexpr int TMEM_COLS = NST * 32 <= 32 ? 32 : NST * 32 <= 64 ? 64 : NST * 32 <= 128 ? 128 : 256;
+  // extra smem per slot: Q^T operand [half][16 rows][128 B] (4 KiB, 1024-aligned), the
+  // warpgroup's max exchange red[4][8] + l exchange red2[4][8], two MMA-completion barriers
+  static constexpr int XS = 5120;
+  static constexpr int EXTRA_BYTES = NST * XS + 1024;  // + the TMEM base address
+  static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, 16, false, false);
+  static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, 16, true, false);
+
+  struct State {
+    float m[HEADS], l[HEADS];  // m: the warpgroup's running max (uniform); l: this token lane's share
+    float o[HEADS];            // O~ of dim 32 sub + lane, every row
+    int lim[HEADS];            // causal key limit per row (unit-local, exclusive)
+  };
+
+  __device__ __forceinline__ static unsigned char* extra() {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* ring =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    return ring + NST * STAGE_BYTES;
+  }
+  __device__ __forceinline__ static int slot_of_thread() { return int(threadIdx.x >> 5) / WPS; }
+  __device__ __forceinline__ static uint32_t* tmem_base_ptr() { return reinterpret_cast<uint32_t*>(extra() + NST * XS); }
+  __device__ __forceinline__ static void wg_bar(int slot) {  // the slot's 4 warps
+    asm volatile("bar.sync %0, 128;" ::"r"(2 + slot) : "memory");
+  }
+  __device__ __forceinline__ static void init_barriers() {  // thread 0, before __syncthreads
+    for (int s = 0; s < NST; ++s) {
+      uint64_t* b = reinterpret_cast<uint64_t*>(extra() + s * XS + 4096 + 256);
+      mbar_init(&b[0], 1);
+      mbar_init(&b[1], 1);
+    }
+  }
+
+  __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
+                                                 int, uint64_t* bar, uint64_t pol) {
+    mbar_arrive_expect_tx(bar, STAGE_BYTES);  // full boxes (rows past the tensor are zero-filled)
+    tma_load_3d(dst, &tm.k, 0, int(row), 0, bar, pol);
+    tma_load_3d(dst + KV_BYTES, &tm.v, 0, int(row), 0, bar, pol);
+  }
+  __device__ __forceinline__ static void produce_paged(unsigned char*, const DecodeArgs&, const TmapPair&, PageWin&, int,
+                                                       int, uint64_t*, uint64_t, int) {}  // not selected when paged
+
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
+    const int slot = slot_of_thread(), tid = (int(threadIdx.x >> 5) % WPS) * 32 + lane;
+    unsigned char* qs = extra() + slot * XS;
+    // Q^T operand, K-major 128-B swizzle: row r (q-row of the tile, zero past u.rows),
+    // dims 64 half .. 64 half + 63 in the 128-B line (half * 2048 + r * 128)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = tid + 128 * i, r = c >> 4, ch = c & 15, half = ch >> 3, cc = ch & 7;
+      uint4 w = make_uint4(0u, 0u, 0u, 0u);
+      if (r < u.rows) w = *reinterpret_cast<const uint4*>(static_cast<const T*>(a.q) + size_t(u.q_row + r) * D + 8 * ch);
+      *reinterpret_cast<uint4*>(qs + half * 2048 + r * 128 + ((cc ^ (r & 7)) << 4)) = w;
+    }
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) {
+      s.m[h] = -INFINITY;
+      s.l[h] = 0.f;
+      s.o[h] = 0.f;
+      s.lim[h] = a.causal ? u.len - u.nq + ((u.r0 + h) % u.nq) + 1 : u.len;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // Q writes -> tensor core
+    wg_bar(slot);
+  }
+
+  __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, int tok0,
+                                               float scale_log2, int lane, int /*bs*/, uint32_t par) {
+    const int slot = slot_of_thread(), tid = sub * 32 + lane;
+    unsigned char* xs = extra() + slot * XS;
+    float* red = reinterpret_cast<float*>(xs + 4096);  // [4][8]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + 4096 + 256);
+    const uint32_t tbase = *tmem_base_ptr() + uint32_t(32 * slot);
+    const uint32_t tlane = uint32_t(32 * sub) << 16;
+    const uint32_t kaddr = smem_u32(st), vaddr = smem_u32(st + KV_BYTES), qaddr = smem_u32(xs);
+    // ---- S^T = K_f Q_f^T (Alg1§20) -----------------------------------------------------------
+    if (tid == 0) {
+      tc5::fence_after();
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+        tc5::mma_f16(tbase, tc5::sdesc(kaddr + off, 16, 1024), tc5::sdesc(qaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024),
+                     IDESC_S, kk > 0);
+      }
+      tc5::commit(&bars[0]);
+    }
+    if (ntok < STAGE_TOK && tid >= ntok) {  // rows past the stage's tokens: zero V (may be non-finite)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(st + KV_BYTES + hf * 16384 + tid * 128 + (c << 4)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    mbar_wait(&bars[0], par);
+    tc5::fence_after();
+    float sc[16];
+    tc5::ld16(tbase + tlane, sc);
+    // ---- scale, mask (C5, causal), running max per row (Alg1§21) ----------------------------
+    float mx[HEADS];
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) {
+      const bool ok = tid < ntok && tok0 + tid < s.lim[h];
+      sc[h] = ok ? sc[h] * scale_log2 : -INFINITY;
+      mx[h] = sc[h];
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+#pragma unroll
+      for (int h = 0; h < HEADS; ++h) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], off));
+    if (lane < HEADS) {
+      float v = mx[0];
+#pragma unroll
+      for (int h = 1; h < HEADS; ++h) v = lane == h ? mx[h] : v;
+      red[sub * HEADS + lane] = v;
+    }
+    wg_bar(slot);
+    float al[HEADS];
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) {
+      const float t = fmaxf(fmaxf(red[h], red[HEADS + h]), fmaxf(red[2 * HEADS + h], red[3 * HEADS + h]));
+      const float mn = fmaxf(s.m[h], t);
+      al[h] = ex2_sub(s.m[h], mn);  // Alg1§23: e^{m - m_new}; m = -inf -> 0
+      s.m[h] = mn;
+    }
+    // ---- P_f = exp(S_f - m) (Alg1§22) into the dead K tile as the PV B operand ---------------
+    unsigned char* pb = st + (tid >> 6) * 2048;  // [token half][16 rows][128 B]
+    const int pc = (tid & 63) >> 3, pe = (tid & 7) * 2;
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) {
+      const float p = ex2_sub(sc[h], s.m[h]);
+      s.l[h] = fmaf(al[h], s.l[h], p);
+      const T hi = to_kv<T>(p);
+      const T lo = to_kv<T>(p - kv_to_f(hi));
+      *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ h) << 4) + pe) = hi;
+      *reinterpret_cast<T*>(pb + (h + 8) * 128 + ((pc ^ h) << 4) + pe) = lo;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (+ zeroed V) -> tensor core
+    tc5::fence_before();                                           // S loads done before reuse
+    wg_bar(slot);
+    // ---- O^T_tile = V_f^T P_f^T (Alg1§24) ----------------------------------------------------
+    if (tid == 0) {
+      tc5::fence_after();
+#pragma unroll
+      for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
+        tc5::mma_f16(tbase + 16, tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
+                     tc5::sdesc(kaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), IDESC_O, kk > 0);
+      tc5::commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], par);
+    tc5::fence_after();
+    float ov[16];
+    tc5::ld16(tbase + tlane + 16, ov);
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) s.o[h] = fmaf(al[h], s.o[h], ov[h] + ov[8 + h]);  // Alg1§25
+    tc5::fence_before();
+  }
+
+  __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
+    const int slot = warp / WPS, sub = warp % WPS;
+    float* red2 = reinterpret_cast<float*>(extra() + slot * XS + 4096 + 128);  // [4][8]
+    float* fb = fold + slot * HEADS * (D + 2);                                  // [row][D + 2]
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) {
+      fb[h * (D + 2) + 32 * sub + lane] = s.o[h];
+      float l = s.l[h];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      if (lane == h) red2[sub * HEADS + h] = l;
+    }
+    wg_bar(slot);
+    if (sub == 0 && lane < HEADS) {
+      const int h = lane;
+      fb[h * (D + 2) + D] = s.m[h];
+      fb[h * (D + 2) + D + 1] = (red2[h] + red2[HEADS + h]) + (red2[2 * HEADS + h] + red2[3 * HEADS + h]);
+    }
+  }
+
+};
+
+// =======================================================================================
 // The persistent decode kernel
 // =======================================================================================
 constexpr int kQD = 4;   // depth of the producer -> consumer virtual-CTA queue
@@ -903,14 +1124,26 @@ struct SegInfo {
   int s0;  // ring slot of the segment's first stage
 };
 
+// Engines with tcgen05 state (Tc5Engine) declare TMEM columns, an extra smem region after
+// the ring and fewer fold rows per slot; the others get the neutral values.
+template <class E, class = void>
+struct EngX {
+  static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS;
+};
+template <class E>
+struct EngX<E, std::void_t<decltype(E::TMEM_COLS)>> {
+  static constexpr int TMEM = E::TMEM_COLS, EXTRA = E::EXTRA_BYTES, FW = E::FOLD_WPS;
+};
+
 template <class E>
 struct Smem {
   static constexpr int RING = E::NST * E::STAGE_BYTES;
+  static constexpr int EXTRA = EngX<E>::EXTRA;  // engine state right after the ring
   static constexpr int kFB = E::FOLD_BUFS;  // consumer -> epilogue fold buffers
   static constexpr int FOLD = kFB * E::FOLD_FLOATS * 4;
   static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB + 1) * 8;
   static constexpr int MISC = kQD * 4 + kFB * int(sizeof(SegInfo));
-  static constexpr int BYTES = 1024 + RING + FOLD + BARS + MISC;
+  static constexpr int BYTES = 1024 + RING + EXTRA + FOLD + BARS + MISC;
 };
 
 // The epilogue warp's accumulator for one segment: lane owns dims c = lane + 32 j of every
@@ -924,12 +1157,13 @@ struct EpiAcc {
 template <class E>
 __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeArgs a, const __grid_constant__ TmapPair tm) {
   constexpr int NST = E::NST, WPS = E::WPS, NCW = E::NCW, D = E::D, H = E::HEADS, J = D / 32;
+  constexpr int FW = EngX<E>::FW;  // fold rows per ring slot (WPS, or 1 for a warpgroup engine)
   constexpr int FOLD_FLOATS = E::FOLD_FLOATS;
   constexpr int kFB = E::FOLD_BUFS;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* ring =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* fold = reinterpret_cast<float*>(ring + Smem<E>::RING);
+  float* fold = reinterpret_cast<float*>(ring + Smem<E>::RING + Smem<E>::EXTRA);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(fold) + Smem<E>::FOLD);
   uint64_t* empty = full + NST;
   uint64_t* vq_full = empty + NST;
@@ -967,10 +1201,16 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       mbar_init(&fold_empty[b], 1);
     }
     mbar_init(stage_bar, 1);
+    if constexpr (EngX<E>::TMEM > 0) E::init_barriers();
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (EngX<E>::TMEM > 0) {
+    if (warp == 0) tc5::tmem_alloc(E::tmem_base_ptr(), EngX<E>::TMEM);
+    tc5::fence_before();
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero-fill before TMA writes
   __syncthreads();
+  if constexpr (EngX<E>::TMEM > 0) tc5::fence_after();
 
   if (warp == NCW + 1) {
     // ================================ producer ==========================================
@@ -1245,7 +1485,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       for (int h = 0; h < H; ++h) {
         float mx = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < NCW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 2) + D]);
+        for (int w = 0; w < NST * FW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 2) + D]);
         float l = 0.f, o[J];
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
@@ -1254,8 +1494,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         // is, so the rounding depends only on the segment, never on where the ring stood
         // when it began (dynamic claims need no ring alignment; reading C16).
 #pragma unroll
-        for (int cw = 0; cw < NCW; ++cw) {
-          const int w = ((si.s0 + cw / WPS) % NST) * WPS + cw % WPS;
+        for (int cw = 0; cw < NST * FW; ++cw) {
+          const int w = ((si.s0 + cw / FW) % NST) * FW + cw % FW;
           const float* r = fb + (w * H + h) * (D + 2);
           const float wt = ex2_sub(r[D], mx);  // idle warp / masked row: m = -inf -> 0
           l = fmaf(wt, r[D + 1], l);
@@ -1417,8 +1657,12 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
           if (j % NST == my_slot) {
             mbar_wait(&full[my_slot], (j / NST) & 1);
-            E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
-                     lane, a.box_shift);
+            if constexpr (EngX<E>::TMEM > 0)
+              E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
+                       lane, a.box_shift, uint32_t(j / NST) & 1u);
+            else
+              E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
+                       lane, a.box_shift);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[my_slot]);
           }
@@ -1430,6 +1674,14 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     }
   }
   hand_off(nullptr, -1, -1, 0, 0, 0);  // terminator for the epilogue
+  if constexpr (EngX<E>::TMEM > 0) {  // every consumer's tcgen05 work is done: free TMEM
+    tc5::fence_before();
+    asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+    if (warp == 0) {
+      tc5::fence_after();
+      tc5::tmem_dealloc(*E::tmem_base_ptr(), EngX<E>::TMEM);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1508,7 +1760,13 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
 
 }  // namespace
 
-KernelInfo decode_kernel_info(int dtype, int head_dim, int group) {
+KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine) {
+  if (engine == LA_ENGINE_TCGEN05) {  // 5th-gen tensor cores (bf16 / fp16, d = 128, T_m <= 8, not paged)
+    if (head_dim != 128 || group > 8) return KernelInfo{};
+    if (dtype == LA_BF16) return info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST>>(true);
+    if (dtype == LA_FP16) return info_of<Tc5Engine<__half, LA_TC5_NST>>(true);
+    return KernelInfo{};
+  }
   if (dtype == LA_FP8_E4M3) {  // one tensor-core engine for every T_m <= 8 (MHA included)
     if (head_dim == 128 && group == 1) return info_of<Fp8Engine<128, LA_FP8M_NST, LA_FP8M_WPS, 1>>(true);
     if (head_dim == 128 && group <= 8) return info_of<Fp8Engine<128, LA_FP8_NST, LA_FP8_WPS, 8>>(true);

@@ -156,7 +156,7 @@ struct KernelInfo {
   bool uses_tma_tensor = false;   // K/V TMA tensor maps (encoded per launch)
   const void* fn = nullptr;
 };
-KernelInfo decode_kernel_info(int dtype, int head_dim, int group);
+KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine);
 // Launch the decode kernel (cooperative when a static-schedule CTA waits on a peer).
 int launch_decode(const KernelInfo& ki, const DecodeArgs& a, int64_t kv_rows, int head_dim, int dtype,
                   bool cooperative, void* stream, std::string& err);

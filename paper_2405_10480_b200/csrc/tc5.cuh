@@ -1,0 +1,84 @@
+// tcgen05 (5th-generation tensor core) helpers for sm_100a: TMEM allocation, shared-memory
+// matrix descriptors, instruction descriptors, MMA issue / commit, TMEM loads.  Internal to
+// libleanattn.so (used by the Tc5Engine in decode.cu; scripts/tc5_probe.cu checks the
+// descriptor conventions against a CPU product on the GPU).
+//
+// Descriptor conventions (the SM100 UMMA formats):
+//  * shared-memory descriptor (64 bit): start address >> 4 in bits [0,14), leading byte
+//    offset >> 4 in [16,30), stride byte offset >> 4 in [32,46), version 1 in [46,48),
+//    base offset 0 in [49,52), layout type in [61,64) (2 = 128-B swizzle).
+//    K-major, 128-B swizzle: rows of 128 B, 8-row groups (1024 B swizzle atoms) SBO apart;
+//    a K step inside the 128-B row advances the start address by its byte offset.
+//    MN-major, 128-B swizzle: 64 MN-elements (128 B) contiguous per K row, 8 K rows per
+//    atom; atoms along MN are LBO apart, atoms along K are SBO apart.
+//  * instruction descriptor (32 bit, kind::f16): D format F32 in [4,6), A / B format
+//    (0 = F16, 1 = BF16) in [7,10) / [10,13), A / B major (0 = K, 1 = MN) bits 15 / 16,
+//    N >> 3 in [17,23), M >> 4 in [24,29).
+#pragma once
+
+#include <cstdint>
+
+namespace la {
+namespace tc5 {
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+__host__ __device__ constexpr uint32_t idesc_f16(bool bf16, int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | ((bf16 ? 1u : 0u) << 7) | ((bf16 ? 1u : 0u) << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+// Whole warp: allocate `ncols` TMEM columns (power of 2 >= 32); the address lands in *dst.
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem]; one thread issues for the CTA.
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrive once on `bar` when every tcgen05.mma this thread issued before has completed.
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+
+// Warp: 32 TMEM lanes (this warp's sub-partition) x 16 consecutive 32-bit columns;
+// lane i receives row (lane base + i), columns c0 .. c0 + 15.
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");  // the wait sits in the same asm: no use of r[] can be scheduled before it
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+}  // namespace tc5
+}  // namespace la

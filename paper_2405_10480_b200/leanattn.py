@@ -53,7 +53,7 @@ class la_plan_opts(ctypes.Structure):
                 ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64), ("q_len", ctypes.c_int),
                 ("causal", ctypes.c_int), ("xchg_world", ctypes.c_int), ("xchg_rank", ctypes.c_int),
                 ("q_lens", ctypes.POINTER(ctypes.c_int32)), ("k_scale", ctypes.c_float),
-                ("v_scale", ctypes.c_float)]
+                ("v_scale", ctypes.c_float), ("engine", ctypes.c_int)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -130,6 +130,9 @@ def launch_count() -> int:
     return int(lib().la_launch_count())
 
 
+_ENGINE_CODES = {"mma": 0, "tcgen05": 1}
+
+
 class Plan:
     """``la_plan``: the stream-K schedule (and, unless host_only, its device state)."""
 
@@ -140,7 +143,7 @@ class Plan:
                  dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
                  causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None,
-                 k_scale: float = 0.0, v_scale: float = 0.0):
+                 k_scale: float = 0.0, v_scale: float = 0.0, engine: str = "mma"):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -169,6 +172,8 @@ class Plan:
         opts.xchg_rank = int(xchg_rank)
         opts.k_scale = float(k_scale)  # dtype "fp8": K = codes x k_scale, V = codes x v_scale
         opts.v_scale = float(v_scale)
+        opts.engine = _ENGINE_CODES[engine]  # "mma" (mma.sync) or "tcgen05" (T_m > 1 tiles)
+        self.engine = engine
         if q_lens is not None:  # heterogeneous batch: N_b per request
             ql = np.ascontiguousarray(np.asarray(q_lens, dtype=np.int32))
             self._ql = ql

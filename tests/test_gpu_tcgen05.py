@@ -1,0 +1,97 @@
+"""GPU parity of the tcgen05 engine (LA_ENGINE_TCGEN05: 5th-gen tensor cores, S^T and the
+per-stage O^T in TMEM) against the fp64 oracle -- the same gates and cases as the mma.sync
+GQA engine: groups 2..8, N_q > 1 (causal or full), ragged tails, tile sizes below, at and
+above one 128-token stage, every schedule, packed layout, determinism, c3 at full size."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from _helpers import census_expect, cuda_inputs, gate, oracle_unit, run_cuda, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2405_10480_b200 import build as b
+    b.build()
+    import paper_2405_10480_b200 as la
+    la.lib()
+
+
+TC5 = dict(engine="tcgen05")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("group", [2, 4, 8])
+def test_tcgen05_small_multi_tile_ragged(dtype, group):
+    p = synth.Problem(2, 2 * group, 2, 128, [1000, 777], dtype=dtype, dist="D2", seed=31, max_ctx=1024)
+    O_ref, L_ref = run_oracle(p)
+    inputs = cuda_inputs(p)
+    for schedule in ("streamk", "dynamic", "fixed_split", "sequential"):
+        for tile_n in (64, 128, 256):
+            for grid in (1, 3, 0):
+                O, L, _ = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule, **TC5)
+                gate(O, L, O_ref, L_ref, what=f"tc5 g{group}/{dtype}/T{tile_n}/G{grid}/{schedule}")
+
+
+@pytest.mark.parametrize("dist", ["D0", "D1", "D3", "D4"])
+def test_tcgen05_distributions_packed(dist):
+    p = synth.Problem(3, 16, 2, 128, [700, 1500, 64], dtype="bf16", dist=dist, seed=32, layout="packed")
+    O_ref, L_ref = run_oracle(p)
+    O, L, _ = run_cuda(p, tile_n=128, grid=0, **TC5)
+    gate(O, L, O_ref, L_ref, what=f"tc5 packed {dist}")
+
+
+@pytest.mark.parametrize("group,q_len", [(1, 2), (1, 8), (2, 4), (4, 2)])
+@pytest.mark.parametrize("causal", [True, False])
+def test_tcgen05_multi_token(group, q_len, causal):
+    p = synth.Problem(2, 2 * group, 2, 128, [900, 333], dtype="bf16", dist="D2", seed=61, q_len=q_len)
+    O_ref, L_ref = run_oracle(p, causal=causal)
+    inputs = cuda_inputs(p)
+    for schedule in ("streamk", "dynamic"):
+        for tile_n, grid in ((128, 7), (128, 0)):
+            O, L, _ = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule, causal=causal, **TC5)
+            gate(O, L, O_ref, L_ref, what=f"tc5 Nq{q_len} g{group} causal={causal} G{grid} {schedule}")
+
+
+def test_tcgen05_determinism_and_equivalence():
+    import paper_2405_10480_b200 as la
+    p = synth.Problem(1, 8, 1, 128, [5000], dtype="bf16", dist="D2", seed=33)
+    q, k, v = cuda_inputs(p)
+    for schedule in ("streamk", "dynamic"):
+        plan = la.Plan(1, 8, 1, 128, [5000], grid=11, tile_n=128, schedule=schedule, engine="tcgen05")
+        ref = plan.decode(q, k, v)[0].clone()
+        for _ in range(5):
+            assert torch.equal(plan.decode(q, k, v)[0], ref)
+        mma = la.Plan(1, 8, 1, 128, [5000], grid=11, tile_n=128, schedule=schedule).decode(q, k, v)[0]
+        assert (ref - mma).abs().max().item() <= 2e-5  # both engines: P = P_hi + P_lo, fp32 sums
+
+
+def test_tcgen05_plan_errors():
+    import paper_2405_10480_b200 as la
+    with pytest.raises(la.LaError):  # paged pools stay on the mma.sync engine
+        la.Plan(1, 8, 1, 128, [1000], engine="tcgen05", layout="paged", block_table=np.zeros((1, 63), np.int32),
+                page_size=16, num_pages=63)
+    plan = la.Plan(1, 4, 4, 128, [1000], engine="tcgen05")  # MHA (T_m = 1): CUDA cores, engine ignored
+    assert plan.info.group == 1
+
+
+def test_tcgen05_c3_full_size_sampled():
+    """BASELINE.json config 3 on the tcgen05 engine, sampled units + census closed form."""
+    p = synth.config("c3")
+    inputs = cuda_inputs(p)
+    refs = {(b, h): oracle_unit(p, b, h) for b, h in ((0, 0), (3, 5), (7, 7))}
+    for schedule in ("streamk", "dynamic"):
+        O, L, plan = run_cuda(p, inputs=inputs, schedule=schedule, **TC5)
+        assert plan.info.total_iters == 32768 and plan.info.group == 8
+        for (b, h), (O_ref, L_ref) in refs.items():
+            gate(O[b, 8 * h:8 * h + 8], L[b, 8 * h:8 * h + 8], O_ref, L_ref, what=f"tc5 c3 b{b} h{h} {schedule}")
+    del inputs
+    torch.cuda.empty_cache()
+    p3 = synth.config("c3", dist="D3")
+    O3, L3, _ = run_cuda(p3, **TC5)
+    o_exp, l_exp = census_expect(p3, 0)
+    assert np.max(np.abs(O3 - o_exp[None, None, :])) <= 1e-5
+    assert np.max(np.abs(L3 - l_exp)) <= 1e-5
