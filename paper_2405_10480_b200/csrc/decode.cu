@@ -90,6 +90,9 @@
 #ifndef LA_TC5_NST
 #define LA_TC5_NST 3   // tcgen05 engine: ring stages of 64 KiB (128 tokens), one warpgroup each
 #endif
+#ifndef LA_TC5_BOXH
+#define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
+#endif
 #ifndef LA_FP8_SPLITP
 #define LA_FP8_SPLITP 0  // one f16 P (2^-12 relative, 256x finer than the E4M3 data); 1: P_hi + P_lo
 #endif
@@ -928,6 +931,7 @@ template <typename T, int NST_>
 struct Tc5Engine {
   static constexpr int D = 128, NST = NST_, WPS = 4, NCW = NST * WPS;
   static constexpr int STAGE_TOK = 128;             // = TMA box rows = MMA M
+  static constexpr int BOX_HALVES = LA_TC5_BOXH;    // 128-B row halves per TMA box (16 or 32 KiB boxes)
   static constexpr int KV_BYTES = 2 * STAGE_TOK * 128;  // [half][128 rows][128 B]
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KiB
   static constexpr int HEADS = 8;
@@ -963,16 +967,24 @@ struct Tc5Engine {
   __device__ __forceinline__ static void init_barriers() {  // thread 0, before __syncthreads
     for (int s = 0; s < NST; ++s) {
       uint64_t* b = reinterpret_cast<uint64_t*>(extra() + s * XS + 4096 + 256);
-      mbar_init(&b[0], 1);
-      mbar_init(&b[1], 1);
+      mbar_init(&b[0], 1);  // S^T ready (tcgen05.commit)
+      mbar_init(&b[1], 1);  // O^T tile ready (tcgen05.commit)
+      mbar_init(&b[2], 1);  // V tile landed (producer's expect_tx + TMA bytes)
     }
   }
 
   __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
                                                  int, uint64_t* bar, uint64_t pol) {
-    mbar_arrive_expect_tx(bar, STAGE_BYTES);  // full boxes (rows past the tensor are zero-filled)
-    tma_load_3d(dst, &tm.k, 0, int(row), 0, bar, pol);
-    tma_load_3d(dst + KV_BYTES, &tm.v, 0, int(row), 0, bar, pol);
+    // K on the ring's full barrier, V on the slot's own barrier: S^T, the softmax and P
+    // overlap the V transfer (full boxes; rows past the tensor are zero-filled)
+    const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + 4096 + 256) + 2;
+    mbar_arrive_expect_tx(bar, KV_BYTES);
+    mbar_arrive_expect_tx(vbar, KV_BYTES);
+#pragma unroll
+    for (int h = 0; h < 2 / BOX_HALVES; ++h) tma_load_3d(dst + h * 16384, &tm.k, 0, int(row), h, bar, pol);
+#pragma unroll
+    for (int h = 0; h < 2 / BOX_HALVES; ++h) tma_load_3d(dst + KV_BYTES + h * 16384, &tm.v, 0, int(row), h, vbar, pol);
   }
   __device__ __forceinline__ static void produce_paged(unsigned char*, const DecodeArgs&, const TmapPair&, PageWin&, int,
                                                        int, uint64_t*, uint64_t, int) {}  // not selected when paged
@@ -1001,7 +1013,7 @@ struct Tc5Engine {
   }
 
   __device__ __forceinline__ static void stage(State& s, unsigned char* st, int sub, int ntok, int tok0,
-                                               float scale_log2, int lane, int /*bs*/, uint32_t par) {
+                                               float scale_log2, int lane, int /*bs*/, uint32_t par, uint64_t* empty) {
     const int slot = slot_of_thread(), tid = sub * 32 + lane;
     unsigned char* xs = extra() + slot * XS;
     float* red = reinterpret_cast<float*>(xs + 4096);  // [4][8]
@@ -1020,12 +1032,14 @@ struct Tc5Engine {
       }
       tc5::commit(&bars[0]);
     }
-    if (ntok < STAGE_TOK && tid >= ntok) {  // rows past the stage's tokens: zero V (may be non-finite)
+    if (ntok < STAGE_TOK) {  // rows past the stage's tokens: zero V once it landed (may be non-finite)
+      mbar_wait(&bars[2], par);
+      if (tid >= ntok)
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf)
+        for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(st + KV_BYTES + hf * 16384 + tid * 128 + (c << 4)) = make_uint4(0u, 0u, 0u, 0u);
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(st + KV_BYTES + hf * 16384 + tid * 128 + (c << 4)) = make_uint4(0u, 0u, 0u, 0u);
     }
     mbar_wait(&bars[0], par);
     tc5::fence_after();
@@ -1075,12 +1089,16 @@ struct Tc5Engine {
     wg_bar(slot);
     // ---- O^T_tile = V_f^T P_f^T (Alg1§24) ----------------------------------------------------
     if (tid == 0) {
+      mbar_wait(&bars[2], par);  // V landed
       tc5::fence_after();
 #pragma unroll
       for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
         tc5::mma_f16(tbase + 16, tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
                      tc5::sdesc(kaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), IDESC_O, kk > 0);
+      tc5::commit(empty);     // the slot is free the moment the tensor core is done with it
       tc5::commit(&bars[1]);
+    } else if (sub != 0 && lane == 0) {
+      mbar_arrive(empty);     // this warp no longer touches the slot's shared memory
     }
     mbar_wait(&bars[1], par);
     tc5::fence_after();
@@ -1223,6 +1241,9 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.v)) : "memory");
     }
     int j = 0, k = 0;
+#ifdef LA_PROF
+    long long prof_pwait = 0;  // producer cycles waiting for free slots -> trace field smid
+#endif
     for (bool first = true;; first = false) {
       // Claim the next virtual CTA only once the previous one is fully issued: the ring
       // (NST stages in flight) hides the atomic's latency, and claiming ahead would let a
@@ -1254,7 +1275,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           const int t1 = min(t0 + a.tile_n, u.len);
           for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {  // LoadFragment K, V (Alg1§17-18)
             const int slot = j % NST;
+#ifdef LA_PROF
+            const long long c0 = clock64();
+#endif
             if (lane == 0 && j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
+#ifdef LA_PROF
+            if (lane == 0) prof_pwait += clock64() - c0;
+#endif
             const int ntok = min(a.stage_tokens, t1 - s0);
             if (!a.paged) {
               if (lane == 0) E::produce(ring + slot * E::STAGE_BYTES, a, tm, u.row0 + s0, ntok, &full[slot], pol);
@@ -1267,6 +1294,9 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         ++unit;
       }
     }
+#ifdef LA_PROF
+    if (tr && lane == 0) tr[TR_SMID] = prof_pwait;
+#endif
     return;
   }
 
@@ -1615,6 +1645,9 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   // ================================= consumers ==========================================
   const int my_slot = warp / WPS, sub = warp % WPS;
   int j = 0, k = 0, seg = 0;
+#ifdef LA_PROF  // trace fields reused: (publish, wait0, wait1) = consumer warp 0's cycles waiting
+  long long prof_wait = 0, prof_work = 0, prof_n = 0;  // for data, in stage(), stages
+#endif
   auto hand_off = [&](const typename E::State* st, int v, int unit, int host, int finishing, int s0) {
     // give this warp's segment partial to the epilogue warp (double-buffered)
     const int b = seg % kFB;
@@ -1656,15 +1689,27 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         const int t1 = min(t0 + a.tile_n, u.len);
         for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
           if (j % NST == my_slot) {
+#ifdef LA_PROF
+            const long long c0 = clock64();
+#endif
             mbar_wait(&full[my_slot], (j / NST) & 1);
-            if constexpr (EngX<E>::TMEM > 0)
+#ifdef LA_PROF
+            const long long c1 = clock64();
+            prof_wait += c1 - c0;
+            ++prof_n;
+#endif
+            if constexpr (EngX<E>::TMEM > 0) {  // the engine releases the slot itself
               E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
-                       lane, a.box_shift, uint32_t(j / NST) & 1u);
-            else
+                       lane, a.box_shift, uint32_t(j / NST) & 1u, &empty[my_slot]);
+            } else {
               E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
                        lane, a.box_shift);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[my_slot]);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&empty[my_slot]);
+            }
+#ifdef LA_PROF
+            prof_work += clock64() - c1;
+#endif
           }
           ++j;
         }
@@ -1674,6 +1719,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     }
   }
   hand_off(nullptr, -1, -1, 0, 0, 0);  // terminator for the epilogue
+#ifdef LA_PROF
+  if (tr && threadIdx.x == 0) {
+    tr[TR_PUBLISH] = prof_wait;
+    tr[TR_WAIT0] = prof_work;
+    tr[TR_WAIT1] = prof_n;
+  }
+#endif
   if constexpr (EngX<E>::TMEM > 0) {  // every consumer's tcgen05 work is done: free TMEM
     tc5::fence_before();
     asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
@@ -1716,6 +1768,7 @@ KernelInfo info_of(bool tma) {
   k.stage_tokens_max = E::STAGE_TOK;
   k.uses_tma_tensor = tma;
   k.fn = reinterpret_cast<const void*>(&la_decode<E>);
+  if constexpr (EngX<E>::TMEM > 0) k.box_halves = E::BOX_HALVES;
   return k;
 }
 
@@ -1733,7 +1786,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn(std::string& err) {
   return fn;
 }
 
-bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype, int box_rows, std::string& err) {
+bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype, int box_rows, int box_halves,
+               std::string& err) {
   auto enc = encode_fn(err);
   if (!enc) return false;
   // d = 64: 2-D {element, row}.  d = 128: 3-D {element, row, half} (half stride 128 B), so
@@ -1743,7 +1797,7 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
   const int rank = (d == 64 || fp8) ? 2 : 3;
   cuuint64_t gdim[3] = {cuuint64_t(fp8 ? 128 : 64), cuuint64_t(rows), 2};
   cuuint64_t gstride[2] = {cuuint64_t(d) * (fp8 ? 1 : 2), 128};
-  cuuint32_t box[3] = {cuuint32_t(fp8 ? 128 : 64), cuuint32_t(box_rows), 2};
+  cuuint32_t box[3] = {cuuint32_t(fp8 ? 128 : 64), cuuint32_t(box_rows), cuuint32_t(box_halves)};
   cuuint32_t estr[3] = {1, 1, 1};
   const CUtensorMapDataType ty = fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                      : (dtype == LA_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -1796,8 +1850,8 @@ int launch_decode(const KernelInfo& ki, const DecodeArgs& a_in, int64_t kv_rows,
   std::memset(&tm, 0, sizeof(tm));
   a.uses_tmap = ki.uses_tma_tensor ? 1 : 0;
   if (ki.uses_tma_tensor) {
-    if (!make_tmap(&tm.k, a.k, kv_rows, head_dim, dtype, a.box_rows, err)) return 1;
-    if (!make_tmap(&tm.v, a.v, kv_rows, head_dim, dtype, a.box_rows, err)) return 1;
+    if (!make_tmap(&tm.k, a.k, kv_rows, head_dim, dtype, a.box_rows, ki.box_halves, err)) return 1;
+    if (!make_tmap(&tm.v, a.v, kv_rows, head_dim, dtype, a.box_rows, ki.box_halves, err)) return 1;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.grid);

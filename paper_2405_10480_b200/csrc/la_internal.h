@@ -154,6 +154,7 @@ struct KernelInfo {
   int smem_bytes = 0;
   int stage_tokens_max = 0;
   bool uses_tma_tensor = false;   // K/V TMA tensor maps (encoded per launch)
+  int box_halves = 2;             // d = 128 bf16/fp16 maps: 128-B row halves per TMA box
   const void* fn = nullptr;
 };
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine);
