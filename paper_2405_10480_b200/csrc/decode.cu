@@ -93,6 +93,9 @@
 #ifndef LA_TC5_BOXH
 #define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
 #endif
+#ifndef LA_TC5_SPLIT
+#define LA_TC5_SPLIT 1  // tcgen05 engine: two independent accumulator chains per MMA (4 k-steps each)
+#endif
 #ifndef LA_FP8_SPLITP
 #define LA_FP8_SPLITP 0  // one f16 P (2^-12 relative, 256x finer than the E4M3 data); 1: P_hi + P_lo
 #endif
@@ -915,7 +918,8 @@ struct Fp8Engine {
 //   O^T[128 dim][16] = V_f^T P_f^T    tcgen05.mma M=128 N=16, A = V read MN-major from the
 //                                     same TMA box (no transpose pass), B = P
 //   thread t <- dim t's 16 columns    O_t[h] = alpha_h O_t[h] + O^T[t][h] + O^T[t][8 + h]
-// Each slot owns 32 TMEM columns (S at +0, O-tile at +16).  The per-tile O^T is a fresh
+// Each slot owns 32 TMEM columns (S at +0, O-tile at +16), or 64 with LA_TC5_SPLIT = 2
+// independent accumulator chains per contraction (summed after tcgen05.ld).  The per-tile O^T is a fresh
 // accumulator that is re-scaled and summed in registers (Alg1§24-25), so the tensor core
 // never needs the running max.
 template <typename T>
@@ -939,7 +943,9 @@ struct Tc5Engine {
   static constexpr int FOLD_FLOATS = NST * HEADS * (D + 2);
   static constexpr int FOLD_BUFS = 1;
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
-  static constexpr int TMEM_COLS = NST * 32 <= 32 ? 32 : NST * 32 <= 64 ? 64 : NST * 32 <= 128 ? 128 : 256;
+  static constexpr int SPLIT = LA_TC5_SPLIT;        // accumulator chains per contraction (1 or 2)
+  static constexpr int COLS = 32 * SPLIT;           // TMEM columns per slot: S^T chains, then O^T chains
+  static constexpr int TMEM_COLS = NST * COLS <= 32 ? 32 : NST * COLS <= 64 ? 64 : NST * COLS <= 128 ? 128 : 256;
   // extra smem per slot: Q^T operand [half][16 rows][128 B] (4 KiB, 1024-aligned), the
   // warpgroup's max exchange red[4][8] + l exchange red2[4][8], two MMA-completion barriers
   static constexpr int XS = 5120;
@@ -1018,17 +1024,19 @@ struct Tc5Engine {
     unsigned char* xs = extra() + slot * XS;
     float* red = reinterpret_cast<float*>(xs + 4096);  // [4][8]
     uint64_t* bars = reinterpret_cast<uint64_t*>(xs + 4096 + 256);
-    const uint32_t tbase = *tmem_base_ptr() + uint32_t(32 * slot);
+    const uint32_t tbase = *tmem_base_ptr() + uint32_t(COLS * slot);
+    constexpr uint32_t OC = 16 * SPLIT;  // first O^T column
     const uint32_t tlane = uint32_t(32 * sub) << 16;
     const uint32_t kaddr = smem_u32(st), vaddr = smem_u32(st + KV_BYTES), qaddr = smem_u32(xs);
     // ---- S^T = K_f Q_f^T (Alg1§20) -----------------------------------------------------------
     if (tid == 0) {
       tc5::fence_after();
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
+      for (int kk = 0; kk < D / 16; ++kk) {  // chain c = kk / (8 / SPLIT) accumulates in columns 16 c
         const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-        tc5::mma_f16(tbase, tc5::sdesc(kaddr + off, 16, 1024), tc5::sdesc(qaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024),
-                     IDESC_S, kk > 0);
+        const int c = kk / (8 / SPLIT);
+        tc5::mma_f16(tbase + 16 * c, tc5::sdesc(kaddr + off, 16, 1024),
+                     tc5::sdesc(qaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), IDESC_S, kk % (8 / SPLIT) > 0);
       }
       tc5::commit(&bars[0]);
     }
@@ -1045,6 +1053,12 @@ struct Tc5Engine {
     tc5::fence_after();
     float sc[16];
     tc5::ld16(tbase + tlane, sc);
+    if (SPLIT == 2) {
+      float s2[16];
+      tc5::ld16(tbase + tlane + 16, s2);
+#pragma unroll
+      for (int h = 0; h < HEADS; ++h) sc[h] += s2[h];
+    }
     // ---- scale, mask (C5, causal), running max per row (Alg1§21) ----------------------------
     float mx[HEADS];
 #pragma unroll
@@ -1054,9 +1068,8 @@ struct Tc5Engine {
       mx[h] = sc[h];
     }
 #pragma unroll
-    for (int off = 16; off; off >>= 1)
-#pragma unroll
-      for (int h = 0; h < HEADS; ++h) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], off));
+    for (int h = 0; h < HEADS; ++h)  // warp max: one CREDUX per row (sm_100a f32 redux)
+      asm volatile("redux.sync.max.f32 %0, %0, 0xffffffff;" : "+f"(mx[h]));
     if (lane < HEADS) {
       float v = mx[0];
 #pragma unroll
@@ -1093,8 +1106,8 @@ struct Tc5Engine {
       tc5::fence_after();
 #pragma unroll
       for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
-        tc5::mma_f16(tbase + 16, tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
-                     tc5::sdesc(kaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), IDESC_O, kk > 0);
+        tc5::mma_f16(tbase + OC + 16 * (kk / (8 / SPLIT)), tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
+                     tc5::sdesc(kaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), IDESC_O, kk % (8 / SPLIT) > 0);
       tc5::commit(empty);     // the slot is free the moment the tensor core is done with it
       tc5::commit(&bars[1]);
     } else if (sub != 0 && lane == 0) {
@@ -1103,7 +1116,13 @@ struct Tc5Engine {
     mbar_wait(&bars[1], par);
     tc5::fence_after();
     float ov[16];
-    tc5::ld16(tbase + tlane + 16, ov);
+    tc5::ld16(tbase + tlane + OC, ov);
+    if (SPLIT == 2) {
+      float o2[16];
+      tc5::ld16(tbase + tlane + OC + 16, o2);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) ov[i] += o2[i];
+    }
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) s.o[h] = fmaf(al[h], s.o[h], ov[h] + ov[8 + h]);  // Alg1§25
     tc5::fence_before();
