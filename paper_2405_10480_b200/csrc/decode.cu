@@ -94,7 +94,7 @@
 #define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
 #endif
 #ifndef LA_TC5_SPLIT
-#define LA_TC5_SPLIT 1  // tcgen05 engine: two independent accumulator chains per MMA (4 k-steps each)
+#define LA_TC5_SPLIT 1  // tcgen05 engine: 1 or 2 independent accumulator chains per MMA (4 k-steps each)
 #endif
 #ifndef LA_FP8_SPLITP
 #define LA_FP8_SPLITP 0  // one f16 P (2^-12 relative, 256x finer than the E4M3 data); 1: P_hi + P_lo
@@ -922,6 +922,12 @@ struct Fp8Engine {
 // independent accumulator chains per contraction (summed after tcgen05.ld).  The per-tile O^T is a fresh
 // accumulator that is re-scaled and summed in registers (Alg1§24-25), so the tensor core
 // never needs the running max.
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ T to_kv(float x);
 template <>
@@ -1080,7 +1086,8 @@ struct Tc5Engine {
     float al[HEADS];
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) {
-      const float t = fmaxf(fmaxf(red[h], red[HEADS + h]), fmaxf(red[2 * HEADS + h], red[3 * HEADS + h]));
+      const uint32_t ra = smem_u32(red) + 4 * h;
+      const float t = fmaxf(fmaxf(lds_f32(ra), lds_f32(ra + 4 * HEADS)), fmaxf(lds_f32(ra + 8 * HEADS), lds_f32(ra + 12 * HEADS)));
       const float mn = fmaxf(s.m[h], t);
       al[h] = ex2_sub(s.m[h], mn);  // Alg1§23: e^{m - m_new}; m = -inf -> 0
       s.m[h] = mn;
@@ -1667,11 +1674,15 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #ifdef LA_PROF  // trace fields reused: (publish, wait0, wait1) = consumer warp 0's cycles waiting
   long long prof_wait = 0, prof_work = 0, prof_n = 0;  // for data, in stage(), stages
 #endif
-  auto hand_off = [&](const typename E::State* st, int v, int unit, int host, int finishing, int s0) {
-    // give this warp's segment partial to the epilogue warp (double-buffered)
+  // Give this warp's segment partial to the epilogue warp (double-buffered): wait for a free
+  // fold buffer, E::seg_end writes it (called in the loop body, so the State never has its
+  // address taken and stays in registers), then signal.
+  auto hand_off_wait = [&]() {
     const int b = seg % kFB;
     if (seg >= kFB) mbar_wait(&fold_empty[b], ((seg / kFB) - 1) & 1);
-    if (st) E::seg_end(*const_cast<typename E::State*>(st), fold + b * FOLD_FLOATS, warp, lane);
+    return b;
+  };
+  auto hand_off = [&](int b, int v, int unit, int host, int finishing, int s0) {
     if (warp == 0 && lane == 0) seginfo[b] = SegInfo{v, unit, host, finishing, s0};
     __syncwarp();
     if (lane == 0) mbar_arrive(&fold_full[b]);
@@ -1733,11 +1744,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           ++j;
         }
       }
-      hand_off(&st, v, unit, host, finishing, seg_s0);
+      const int fbuf = hand_off_wait();
+      E::seg_end(st, fold + fbuf * FOLD_FLOATS, warp, lane);
+      hand_off(fbuf, v, unit, host, finishing, seg_s0);
       ++unit;
     }
   }
-  hand_off(nullptr, -1, -1, 0, 0, 0);  // terminator for the epilogue
+  hand_off(hand_off_wait(), -1, -1, 0, 0, 0);  // terminator for the epilogue
 #ifdef LA_PROF
   if (tr && threadIdx.x == 0) {
     tr[TR_PUBLISH] = prof_wait;

@@ -7,5 +7,7 @@ b() {  # label, engine, [lib]
 }
 b tc5 tcgen05
 b mma mma
+timeout 300 python bench.py --steps 200 --warmup 10 --no-cpu --no-e2e > gpurun_out/tc5_bench_c2.json 2>&1
+python -c "import json; d=json.loads(open('gpurun_out/tc5_bench_c2.json').read().strip().splitlines()[-1]); r=d['roofline']; print('c2 mha', round(r['kernel_us'],1), 'us', round(r['achieved']), 'GB/s')"
 for v in paper_2405_10480_b200/lib/v/*.so; do b tc5_$(basename $v .so) tcgen05 $PWD/$v; done
 timeout 120 python scripts/trace_tail.py c3 tcgen05 2>&1 | head -4
