@@ -37,6 +37,24 @@ def test_exports_every_declared_symbol(la):
     assert L.la_status_string(1) == b"LA_ERR_INVALID"
 
 
+def test_plan_opts_struct_matches_the_header(la):
+    """The ctypes mirror of la_plan_opts has the C layout: la_plan_opts_init memsets exactly
+    sizeof(la_plan_opts) bytes, so it must touch the whole ctypes struct and nothing past it,
+    and its defaults must land in the fields of the same names (engine = LA_ENGINE_MMA_SYNC)."""
+    import ctypes
+    from paper_2405_10480_b200.leanattn import la_plan_opts
+    n = ctypes.sizeof(la_plan_opts)
+    buf = (ctypes.c_ubyte * (n + 64))(*([0xAB] * (n + 64)))
+    assert la.lib().la_plan_opts_init(ctypes.cast(buf, ctypes.POINTER(la_plan_opts))) == 0
+    assert all(b == 0xAB for b in bytes(buf)[n:]), "la_plan_opts_init wrote past the ctypes struct"
+    o = la_plan_opts.from_buffer(buf)
+    assert (o.num_sms, o.ctas_per_sm, o.q_len, o.causal, o.dyn_first_permille, o.engine) == (148, 1, 1, 1, 750, 0)
+    header = open(os.path.join(ROOT, "include", "la.h")).read()
+    body = header[header.index("typedef struct {\n  float scale;"):header.index("} la_plan_opts;")]
+    fields = re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(\w+);", body, re.M)
+    assert fields == [f for f, _ in la_plan_opts._fields_]
+
+
 def _oracle_rows(batch, heads_kv, lens, tile_n, grid, layout):
     units = unit_order(batch, heads_kv, layout)
     c_n = [-(-lens[b] // tile_n) for (b, _h) in units]
