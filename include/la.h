@@ -218,6 +218,8 @@ la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t*
  * layout and dtype, contiguous, 16-byte aligned.  out: device (B, H_q, d) fp32.  lse:
  * device (B, H_q) fp32 natural-log logsumexp L, or NULL to skip it.  ctx_lens are the
  * plan's (a serving loop re-plans when they change; planning is O(B*H_kv + G)).
+ * One kernel launch; it may be captured into a CUDA graph and replayed (the Signal/Wait
+ * epoch lives in the plan's device memory), one launch of a plan in flight at a time.
  * Errors: LA_ERR_INVALID (null or misaligned pointer), LA_ERR_STATE (host-only plan),
  * LA_ERR_CUDA (launch failure).
  */

@@ -37,7 +37,6 @@ struct la_plan_s {
   int* d_counters = nullptr;
   int* d_unit_count = nullptr;
   unsigned long long* d_trace = nullptr;
-  uint32_t epoch = 0;
   int64_t workspace = 0;
   // la_decode_host staging
   void* d_stage = nullptr;
@@ -328,7 +327,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     const size_t b_po = align(size_t(G) * 2 * p.rows() * head_dim * sizeof(float));
     const size_t b_pml = align(size_t(G) * 2 * p.rows() * 4 * sizeof(float));
     const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
-    const size_t b_cnt = align((2 + U + size_t(G)) * sizeof(int));
+    const size_t b_cnt = align((4 + U + size_t(G)) * sizeof(int));
     const size_t b_trace = opts.trace ? align(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
     plan->pt_stride = p.layout == LA_KV_PAGED ? (p.pages_per_seq + 31) / 32 * 32 : 0;
     const size_t b_pt = align(size_t(p.batch) * plan->pt_stride * sizeof(int32_t));
@@ -343,7 +342,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     plan->d_part_ml = reinterpret_cast<float*>(base + b_units + b_begin + b_first + b_po);
     plan->d_flags = reinterpret_cast<uint32_t*>(base + b_units + b_begin + b_first + b_po + b_pml);
     plan->d_counters = reinterpret_cast<int*>(base + b_units + b_begin + b_first + b_po + b_pml + b_flags);
-    plan->d_unit_count = plan->d_counters + 2;
+    plan->d_unit_count = plan->d_counters + 4;
     if (opts.trace)
       plan->d_trace = reinterpret_cast<unsigned long long*>(base + b_units + b_begin + b_first + b_po + b_pml +
                                                             b_flags + b_cnt);
@@ -451,11 +450,6 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.part_o = plan->d_part_o;
   a.part_ml = plan->d_part_ml;
   a.flags = plan->d_flags;
-  if (++plan->epoch == 0) {  // epoch wrapped: flags may hold any old value -> reset
-    cudaMemsetAsync(plan->d_flags, 0, plan->sched.grid * sizeof(uint32_t), (cudaStream_t)stream);
-    plan->epoch = 1;
-  }
-  a.epoch = plan->epoch;
   a.trace = plan->d_trace;
   a.counters = plan->d_counters;
   a.unit_count = plan->d_unit_count;

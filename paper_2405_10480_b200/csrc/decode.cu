@@ -1220,6 +1220,12 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int g = blockIdx.x;
+  // This launch's epoch (reading C17): one more than the last launch's, kept ON THE DEVICE
+  // (counters[3], advanced by the last CTA to exit) so a launch captured into a CUDA graph
+  // publishes fresh flag values on every replay.  Launches on one stream never overlap, so
+  // every CTA reads the same value.
+  const uint32_t epoch_prev = *reinterpret_cast<volatile const uint32_t*>(&a.counters[3]);
+  const uint32_t epoch = epoch_prev == 0xFFFFFFFFu ? 1u : epoch_prev + 1u;
   const bool dynamic = a.dynamic != 0;
   const int NV = a.num_v;
   unsigned long long* tr = a.trace ? a.trace + size_t(g) * TR_FIELDS : nullptr;
@@ -1460,7 +1466,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     // on a unit > m, and no CTA is stuck on a unit < m, so every rank completes m's push.
     auto xchg_out = [&](int q_row, int unit) {
       constexpr int RS = D + 4;
-      const int P = a.xw, par = int(a.epoch & 1u);
+      const int P = a.xw, par = int(epoch & 1u);
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         if (h >= nr) continue;
@@ -1477,11 +1483,11 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       __syncwarp();
       if (lane < P) {
         uint32_t* f = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(a.xpeer[lane]) + a.xflag_off);
-        st_release_sys(f + size_t(a.xr) * a.xunits + unit, a.epoch);
+        st_release_sys(f + size_t(a.xr) * a.xunits + unit, epoch);
         const uint32_t* mine = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(a.xpeer[a.xr]) +
                                                                  a.xflag_off) + size_t(lane) * a.xunits + unit;
         const unsigned long long t0 = globaltimer();
-        while (ld_acquire_sys(mine) != a.epoch) {
+        while (ld_acquire_sys(mine) != epoch) {
           // a peer never arrived: flag it and move on (later waits then give up at once)
           if (*reinterpret_cast<volatile int*>(a.xerr) || globaltimer() - t0 > 5000000000ull) {
             atomicExch(a.xerr, 1);
@@ -1584,7 +1590,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           // ---- static, non-host: StorePartials + Signal(flags[g]) (Alg2§19-23) -----------
           store_partial(v);
           if (lane == 0) {
-            st_release_gpu(&a.flags[v], a.epoch);
+            st_release_gpu(&a.flags[v], epoch);
             if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
           }
         } else {
@@ -1593,7 +1599,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           if (tr && lane == 0) tr[TR_WAIT0] = globaltimer();
 #pragma unroll 1
           for (int p = v + 1 + lane; p <= u.last_cta; p += 32)
-            while (ld_acquire_gpu(&a.flags[p]) != a.epoch) __nanosleep(20);
+            while (ld_acquire_gpu(&a.flags[p]) != epoch) __nanosleep(20);
           __syncwarp();
           if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
           fp0 = v + 1;
@@ -1663,6 +1669,12 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           a.counters[0] = 0;
           a.counters[1] = 0;
         }
+      }
+      __threadfence();  // every flag wait of this CTA is over: the last one out advances the epoch
+      if (atomicAdd(&a.counters[2], 1) == int(gridDim.x) - 1) {
+        a.counters[2] = 0;
+        *reinterpret_cast<volatile uint32_t*>(&a.counters[3]) = epoch;
+        __threadfence();
       }
     }
     return;

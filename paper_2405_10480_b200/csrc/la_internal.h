@@ -108,11 +108,11 @@ struct DecodeArgs {
   float* part_o;      // [2][grid][group][d]  Op of Alg2§20 (slot 1: dynamic-mode host partial)
   float* part_ml;     // [2][grid][group][4]  mp, lp, -, - of Alg2§21-22 (m in log2 units; 16 B rows)
   uint32_t* flags;    // [grid]               flags of Alg2§23/§28, epoch-valued (reading C17)
-  int* counters;      // [2] dynamic mode: virtual-CTA claim counter, CTAs done
+  int* counters;      // [4] virtual-CTA claim counter, CTAs done (dynamic mode); CTAs exited,
+                      //     launch epoch (device-side: a captured CUDA graph replays correctly)
   int* unit_count;    // [units] dynamic mode: fold-tree groups completed per unit
   int* grp_count;     // [grid]  dynamic mode: segments published per fold-tree group
   unsigned long long* trace;  // [phys_grid][LA_TRACE_FIELDS] or nullptr
-  uint32_t epoch;
   int dynamic;        // 1: claim virtual CTAs dynamically, last-arriver fold
   int num_v;          // (virtual) CTAs
   int grid;           // CTAs launched

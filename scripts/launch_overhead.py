@@ -2,7 +2,7 @@
 for a few configs (the cooperative-vs-plain comparison in DESIGN.md §6 used a temporary
 LA_EXPERIMENT_NONCOOP switch in launch_decode, since removed).
 
-  python scripts/launch_overhead.py c1 c3:fp8 c2
+  python scripts/launch_overhead.py c1 c3:fp8 c2 c3:tcgen05
 """
 import os
 import sys
@@ -17,12 +17,15 @@ import paper_2405_10480_b200 as la  # noqa: E402
 
 def case(spec):
     cfg, _, dt = spec.partition(":")
+    engine = "mma"
+    if dt == "tcgen05":
+        dt, engine = "", "tcgen05"
     p = synth.config(cfg, **({"dtype": dt} if dt else {}))
     q = synth.gen_q(p, "cuda")
     k = synth.fill_kv_cache(p, "k", "cuda")
     v = synth.fill_kv_cache(p, "v", "cuda")
     kw = dict(k_scale=p.k_scale, v_scale=p.v_scale) if p.dtype == "fp8" else {}
-    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, p.ctx_lens, dtype=p.dtype, trace=True, **kw)
+    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, p.ctx_lens, dtype=p.dtype, trace=True, engine=engine, **kw)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ks, spans, starts = [], [], []
