@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--page-size", type=int, default=0, help="run the config in a paged KV pool (16..256)")
     ap.add_argument("--engine", default="mma", choices=["mma", "tcgen05"],
                     help="tensor-core engine for T_m > 1 tiles (GQA): mma.sync or tcgen05 + TMEM")
+    ap.add_argument("--q-len", type=int, default=1,
+                    help="N_q query tokens per request (speculative decode; single GPU, no e2e / cpu legs)")
     ap.add_argument("--tile-n", type=int, default=0, help="LeanTile size T_n (0 = planner's auto rule)")
     ap.add_argument("--dtype", default=None, choices=["bf16", "fp16", "fp8"],
                     help="KV storage type (default: the config's; fp8 = E4M3 codes + scales, bf16 q; NEXT-4)")
@@ -272,6 +274,11 @@ def bench_ours(args):
             l_all.copy_(lb)
     cfg = args.config or ("c2" if world == 1 else "c5")
     dkw = {"dtype": args.dtype} if args.dtype else {}
+    if args.q_len > 1:
+        if world > 1 or args.page_size:
+            raise SystemExit("--q-len is a single-GPU, non-paged option")
+        dkw["q_len"] = args.q_len
+        args.no_cpu = args.no_e2e = True
     p = synth.config(cfg, **dkw)
     paged_kw = {}
     if p.dtype == "fp8":
@@ -291,7 +298,7 @@ def bench_ours(args):
     v = synth.fill_kv_cache(p, "v", dev, token_range=None if args.page_size else bounds)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
                    schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min,
-                   tile_n=args.tile_n, engine=args.engine, **paged_kw,
+                   tile_n=args.tile_n, engine=args.engine, q_len=args.q_len, **paged_kw,
                    **(dict(xchg_world=world, xchg_rank=rank) if fused else {}))
     xchg_note = None
     if fused:   # collective decision: every rank maps every peer's buffer, or all use NCCL
@@ -305,8 +312,9 @@ def bench_ours(args):
     local_kv = info.kv_bytes
     stream = torch.cuda.current_stream(dev)
     rows = p.batch * p.heads_q
-    out = torch.empty(p.batch, p.heads_q, p.head_dim, dtype=torch.float32, device=dev)
-    lse = torch.empty(p.batch, p.heads_q, dtype=torch.float32, device=dev)
+    nq = (args.q_len,) if args.q_len > 1 else ()
+    out = torch.empty(p.batch, p.heads_q, *nq, p.head_dim, dtype=torch.float32, device=dev)
+    lse = torch.empty(p.batch, p.heads_q, *nq, dtype=torch.float32, device=dev)
     if world > 1:
         o_all = torch.empty(world, rows, p.head_dim, dtype=torch.float32, device=dev)
         l_all = torch.empty(world, rows, dtype=torch.float32, device=dev)
@@ -469,6 +477,8 @@ def bench_ours(args):
                        "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
                        "stage_tokens": info.stage_tokens, "schedule": args.schedule,
                        **({"engine": args.engine} if info.tile_rows > 1 and p.dtype != "fp8" else {}),
+                       **({"q_len": args.q_len, "query_tile_rows": info.tile_rows, "units": info.num_units}
+                          if args.q_len > 1 else {}),
                        "kv_layout": p.layout + (f" (page {args.page_size})" if args.page_size else ""),
                        "virtual_ctas": info.num_vctas,
                        "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),

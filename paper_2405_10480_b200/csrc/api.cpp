@@ -37,6 +37,7 @@ struct la_plan_s {
   int* d_counters = nullptr;
   int* d_unit_count = nullptr;
   unsigned long long* d_trace = nullptr;
+  float* d_gfold = nullptr;  // engine fold buffers in global memory (KernelInfo::global_fold_floats)
   int64_t workspace = 0;
   // la_decode_host staging
   void* d_stage = nullptr;
@@ -186,7 +187,11 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     uniform = uniform && n == p.q_lens[0];
   }
   p.q_len = uniform ? p.q_lens[0] : 0;
-  p.tile_rows = std::min(8, max_rows);   // T_m: 1 -> CUDA-core engine, else tensor-core tiles
+  // T_m: 1 -> CUDA-core engine, else tensor-core tiles of <= 8 rows (mma.sync: N = 8), or
+  // <= 16 on the tcgen05 engine (N = 16 per MMA at no extra cost: one KV pass per 16 rows)
+  const bool wide = opts.engine == LA_ENGINE_TCGEN05 && head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16) &&
+                    opts.layout != LA_KV_PAGED;
+  p.tile_rows = std::min(wide ? 16 : 8, max_rows);
   if (xw && p.causal)
     for (int32_t n : p.q_lens)
       if (n > 1) return fail(LA_ERR_UNSUPPORTED, "sequence-shard exchange needs N_b == 1 or causal == 0");
@@ -254,6 +259,10 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
       return fail(LA_ERR_UNSUPPORTED, "LA_ENGINE_TCGEN05 covers T_m > 1 tiles of a bf16 / fp16, non-paged cache");
     }
     plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows(), p.rows() > 1 ? opts.engine : 0);
+    if (plan->kinfo.global_fold_floats > 0 && (p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT)) {
+      delete plan;  // their fold tree stages peers in the (shared-memory) fold buffer
+      return fail(LA_ERR_UNSUPPORTED, "16-row tcgen05 tiles run the static schedules (streamk, sequential)");
+    }
     if (!plan->kinfo.supported) {
       delete plan;
       return fail(LA_ERR_UNSUPPORTED, "no decode kernel for this (dtype, head_dim, group) in this build");
@@ -331,7 +340,8 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     const size_t b_trace = opts.trace ? align(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
     plan->pt_stride = p.layout == LA_KV_PAGED ? (p.pages_per_seq + 31) / 32 * 32 : 0;
     const size_t b_pt = align(size_t(p.batch) * plan->pt_stride * sizeof(int32_t));
-    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace + b_pt;
+    const size_t b_gf = align(size_t(GP) * plan->kinfo.global_fold_floats * sizeof(float));
+    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace + b_pt + b_gf;
     cudaError_t e = cudaMalloc(&plan->d_tables, bytes);
     if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaMalloc(plan tables)"); }
     char* base = static_cast<char*>(plan->d_tables);
@@ -346,6 +356,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     if (opts.trace)
       plan->d_trace = reinterpret_cast<unsigned long long*>(base + b_units + b_begin + b_first + b_po + b_pml +
                                                             b_flags + b_cnt);
+    if (b_gf) plan->d_gfold = reinterpret_cast<float*>(base + bytes - b_gf);
     plan->workspace = int64_t(bytes);
     e = cudaMemcpy(plan->d_units, s.units.data(), s.units.size() * sizeof(DevUnit), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
@@ -451,6 +462,7 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.part_ml = plan->d_part_ml;
   a.flags = plan->d_flags;
   a.trace = plan->d_trace;
+  a.gfold = plan->d_gfold;
   a.counters = plan->d_counters;
   a.unit_count = plan->d_unit_count;
   a.grp_count = plan->d_unit_count + plan->sched.units.size();

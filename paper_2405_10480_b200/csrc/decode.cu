@@ -937,32 +937,38 @@ __device__ __forceinline__ __half to_kv<__half>(float x) { return __float2half_r
 __device__ __forceinline__ float kv_to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
 __device__ __forceinline__ float kv_to_f(__half x) { return __half2float(x); }
 
-template <typename T, int NST_>
+template <typename T, int NST_, int HEADS_>
 struct Tc5Engine {
   static constexpr int D = 128, NST = NST_, WPS = 4, NCW = NST * WPS;
   static constexpr int STAGE_TOK = 128;             // = TMA box rows = MMA M
   static constexpr int BOX_HALVES = LA_TC5_BOXH;    // 128-B row halves per TMA box (16 or 32 KiB boxes)
   static constexpr int KV_BYTES = 2 * STAGE_TOK * 128;  // [half][128 rows][128 B]
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KiB
-  static constexpr int HEADS = 8;
+  static constexpr int HEADS = HEADS_;              // T_m: 8, or 16 (the wider N of tcgen05: one KV pass
+                                                    // for g * N_b <= 16 rows where mma.sync tiles need two)
+  static_assert(HEADS == 8 || HEADS == 16, "T_m");
+  static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
+  static constexpr int PHS = NO * 128;              // P^T token-half stride [2 HEADS rows][128 B]
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
   static constexpr int FOLD_FLOATS = NST * HEADS * (D + 2);
   static constexpr int FOLD_BUFS = 1;
+  static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
   static constexpr int SPLIT = LA_TC5_SPLIT;        // accumulator chains per contraction (1 or 2)
-  static constexpr int COLS = 32 * SPLIT;           // TMEM columns per slot: S^T chains, then O^T chains
+  static constexpr int OC = 16 * SPLIT;             // first O^T column of a slot (S^T chains before it)
+  static constexpr int COLS = (OC + NO * SPLIT) <= 32 ? 32 : (OC + NO * SPLIT) <= 64 ? 64 : 128;  // per slot
   static constexpr int TMEM_COLS = NST * COLS <= 32 ? 32 : NST * COLS <= 64 ? 64 : NST * COLS <= 128 ? 128 : 256;
   // extra smem per slot: Q^T operand [half][16 rows][128 B] (4 KiB, 1024-aligned), the
   // warpgroup's max exchange red[4][8] + l exchange red2[4][8], two MMA-completion barriers
   static constexpr int XS = 5120;
   static constexpr int EXTRA_BYTES = NST * XS + 1024;  // + the TMEM base address
   static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, 16, false, false);
-  static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, 16, true, false);
+  static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, false);
 
   struct State {
     float m[HEADS], l[HEADS];  // m: the warpgroup's running max (uniform); l: this token lane's share
     float o[HEADS];            // O~ of dim 32 sub + lane, every row
-    int lim[HEADS];            // causal key limit per row (unit-local, exclusive)
+    int lbase, r0, nq;         // causal key limit of row h: lbase + (r0 + h) % nq (unit-local, exclusive)
   };
 
   __device__ __forceinline__ static unsigned char* extra() {
@@ -978,7 +984,7 @@ struct Tc5Engine {
   }
   __device__ __forceinline__ static void init_barriers() {  // thread 0, before __syncthreads
     for (int s = 0; s < NST; ++s) {
-      uint64_t* b = reinterpret_cast<uint64_t*>(extra() + s * XS + 4096 + 256);
+      uint64_t* b = reinterpret_cast<uint64_t*>(extra() + s * XS + 4096 + 512);
       mbar_init(&b[0], 1);  // S^T ready (tcgen05.commit)
       mbar_init(&b[1], 1);  // O^T tile ready (tcgen05.commit)
       mbar_init(&b[2], 1);  // V tile landed (producer's expect_tx + TMA bytes)
@@ -990,7 +996,7 @@ struct Tc5Engine {
     // K on the ring's full barrier, V on the slot's own barrier: S^T, the softmax and P
     // overlap the V transfer (full boxes; rows past the tensor are zero-filled)
     const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
-    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + 4096 + 256) + 2;
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + 4096 + 512) + 2;
     mbar_arrive_expect_tx(bar, KV_BYTES);
     mbar_arrive_expect_tx(vbar, KV_BYTES);
 #pragma unroll
@@ -1018,8 +1024,10 @@ struct Tc5Engine {
       s.m[h] = -INFINITY;
       s.l[h] = 0.f;
       s.o[h] = 0.f;
-      s.lim[h] = a.causal ? u.len - u.nq + ((u.r0 + h) % u.nq) + 1 : u.len;
     }
+    s.lbase = a.causal ? u.len - u.nq + 1 : u.len;  // N_q > 1, causal: query i is token n - N_b + i
+    s.r0 = u.r0;
+    s.nq = a.causal ? u.nq : 1;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // Q writes -> tensor core
     wg_bar(slot);
   }
@@ -1028,10 +1036,9 @@ struct Tc5Engine {
                                                float scale_log2, int lane, int /*bs*/, uint32_t par, uint64_t* empty) {
     const int slot = slot_of_thread(), tid = sub * 32 + lane;
     unsigned char* xs = extra() + slot * XS;
-    float* red = reinterpret_cast<float*>(xs + 4096);  // [4][8]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + 4096 + 256);
+    float* red = reinterpret_cast<float*>(xs + 4096);  // [4][HEADS]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + 4096 + 512);
     const uint32_t tbase = *tmem_base_ptr() + uint32_t(COLS * slot);
-    constexpr uint32_t OC = 16 * SPLIT;  // first O^T column
     const uint32_t tlane = uint32_t(32 * sub) << 16;
     const uint32_t kaddr = smem_u32(st), vaddr = smem_u32(st + KV_BYTES), qaddr = smem_u32(xs);
     // ---- S^T = K_f Q_f^T (Alg1§20) -----------------------------------------------------------
@@ -1069,7 +1076,8 @@ struct Tc5Engine {
     float mx[HEADS];
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) {
-      const bool ok = tid < ntok && tok0 + tid < s.lim[h];
+      // only a stage reaching past the smallest limit needs the per-row causal test
+      const bool ok = tid < ntok && (tok0 + STAGE_TOK <= s.lbase || tok0 + tid < s.lbase + (s.r0 + h) % s.nq);
       sc[h] = ok ? sc[h] * scale_log2 : -INFINITY;
       mx[h] = sc[h];
     }
@@ -1093,7 +1101,7 @@ struct Tc5Engine {
       s.m[h] = mn;
     }
     // ---- P_f = exp(S_f - m) (Alg1§22) into the dead K tile as the PV B operand ---------------
-    unsigned char* pb = st + (tid >> 6) * 2048;  // [token half][16 rows][128 B]
+    unsigned char* pb = st + (tid >> 6) * PHS;  // [token half][2 HEADS rows][128 B]
     const int pc = (tid & 63) >> 3, pe = (tid & 7) * 2;
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) {
@@ -1101,8 +1109,8 @@ struct Tc5Engine {
       s.l[h] = fmaf(al[h], s.l[h], p);
       const T hi = to_kv<T>(p);
       const T lo = to_kv<T>(p - kv_to_f(hi));
-      *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ h) << 4) + pe) = hi;
-      *reinterpret_cast<T*>(pb + (h + 8) * 128 + ((pc ^ h) << 4) + pe) = lo;
+      *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ (h & 7)) << 4) + pe) = hi;
+      *reinterpret_cast<T*>(pb + (h + HEADS) * 128 + ((pc ^ (h & 7)) << 4) + pe) = lo;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (+ zeroed V) -> tensor core
     tc5::fence_before();                                           // S loads done before reuse
@@ -1113,8 +1121,8 @@ struct Tc5Engine {
       tc5::fence_after();
 #pragma unroll
       for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
-        tc5::mma_f16(tbase + OC + 16 * (kk / (8 / SPLIT)), tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
-                     tc5::sdesc(kaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), IDESC_O, kk % (8 / SPLIT) > 0);
+        tc5::mma_f16(tbase + OC + NO * (kk / (8 / SPLIT)), tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
+                     tc5::sdesc(kaddr + (kk >> 2) * PHS + (kk & 3) * 32, 16, 1024), IDESC_O, kk % (8 / SPLIT) > 0);
       tc5::commit(empty);     // the slot is free the moment the tensor core is done with it
       tc5::commit(&bars[1]);
     } else if (sub != 0 && lane == 0) {
@@ -1122,22 +1130,36 @@ struct Tc5Engine {
     }
     mbar_wait(&bars[1], par);
     tc5::fence_after();
-    float ov[16];
-    tc5::ld16(tbase + tlane + OC, ov);
-    if (SPLIT == 2) {
-      float o2[16];
-      tc5::ld16(tbase + tlane + OC + 16, o2);
+    // O^T tile: column h = V^T P_hi row h, column HEADS + h = V^T P_lo row h (per chain)
 #pragma unroll
-      for (int i = 0; i < 16; ++i) ov[i] += o2[i];
+    for (int c0 = 0; c0 < HEADS; c0 += 8) {  // 8 rows at a time: hi columns c0.., lo columns HEADS + c0..
+      float hv[8], lv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) hv[i] = lv[i] = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < SPLIT; ++ch) {
+        float a16[16];
+        if (HEADS == 8) {  // 16 columns: hi 0-7, lo 8-15
+          tc5::ld16(tbase + tlane + OC + NO * ch, a16);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            hv[i] += a16[i];
+            lv[i] += a16[8 + i];
+          }
+        } else {           // 32 columns: hi 0-15, lo 16-31; this pass takes rows c0 .. c0 + 7
+          tc5::ld8(tbase + tlane + OC + NO * ch + c0, hv, ch > 0);
+          tc5::ld8(tbase + tlane + OC + NO * ch + HEADS + c0, lv, ch > 0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s.o[c0 + i] = fmaf(al[c0 + i], s.o[c0 + i], hv[i] + lv[i]);  // Alg1§25
     }
-#pragma unroll
-    for (int h = 0; h < HEADS; ++h) s.o[h] = fmaf(al[h], s.o[h], ov[h] + ov[8 + h]);  // Alg1§25
     tc5::fence_before();
   }
 
   __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
     const int slot = warp / WPS, sub = warp % WPS;
-    float* red2 = reinterpret_cast<float*>(extra() + slot * XS + 4096 + 128);  // [4][8]
+    float* red2 = reinterpret_cast<float*>(extra() + slot * XS + 4096 + 256);  // [4][HEADS]
     float* fb = fold + slot * HEADS * (D + 2);                                  // [row][D + 2]
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) {
@@ -1173,10 +1195,12 @@ struct SegInfo {
 template <class E, class = void>
 struct EngX {
   static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS;
+  static constexpr bool GF = false;  // fold buffers in global scratch (DecodeArgs::gfold)
 };
 template <class E>
 struct EngX<E, std::void_t<decltype(E::TMEM_COLS)>> {
   static constexpr int TMEM = E::TMEM_COLS, EXTRA = E::EXTRA_BYTES, FW = E::FOLD_WPS;
+  static constexpr bool GF = E::GLOBAL_FOLD;
 };
 
 template <class E>
@@ -1184,7 +1208,7 @@ struct Smem {
   static constexpr int RING = E::NST * E::STAGE_BYTES;
   static constexpr int EXTRA = EngX<E>::EXTRA;  // engine state right after the ring
   static constexpr int kFB = E::FOLD_BUFS;  // consumer -> epilogue fold buffers
-  static constexpr int FOLD = kFB * E::FOLD_FLOATS * 4;
+  static constexpr int FOLD = EngX<E>::GF ? 0 : kFB * E::FOLD_FLOATS * 4;
   static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB + 1) * 8;
   static constexpr int MISC = kQD * 4 + kFB * int(sizeof(SegInfo));
   static constexpr int BYTES = 1024 + RING + EXTRA + FOLD + BARS + MISC;
@@ -1207,8 +1231,9 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   extern __shared__ unsigned char smem_raw[];
   unsigned char* ring =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* fold = reinterpret_cast<float*>(ring + Smem<E>::RING + Smem<E>::EXTRA);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(fold) + Smem<E>::FOLD);
+  float* fold = EngX<E>::GF ? a.gfold + size_t(blockIdx.x) * kFB * E::FOLD_FLOATS
+                            : reinterpret_cast<float*>(ring + Smem<E>::RING + Smem<E>::EXTRA);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + Smem<E>::RING + Smem<E>::EXTRA + Smem<E>::FOLD);
   uint64_t* empty = full + NST;
   uint64_t* vq_full = empty + NST;
   uint64_t* vq_empty = vq_full + kQD;
@@ -1813,6 +1838,7 @@ KernelInfo info_of(bool tma) {
   k.uses_tma_tensor = tma;
   k.fn = reinterpret_cast<const void*>(&la_decode<E>);
   if constexpr (EngX<E>::TMEM > 0) k.box_halves = E::BOX_HALVES;
+  if constexpr (EngX<E>::GF) k.global_fold_floats = E::FOLD_BUFS * E::FOLD_FLOATS;
   return k;
 }
 
@@ -1860,9 +1886,12 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
 
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine) {
   if (engine == LA_ENGINE_TCGEN05) {  // 5th-gen tensor cores (bf16 / fp16, d = 128, T_m <= 8, not paged)
-    if (head_dim != 128 || group > 8) return KernelInfo{};
-    if (dtype == LA_BF16) return info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST>>(true);
-    if (dtype == LA_FP16) return info_of<Tc5Engine<__half, LA_TC5_NST>>(true);
+    if (head_dim != 128 || group > 16) return KernelInfo{};
+    if (dtype == LA_BF16)
+      return group <= 8 ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 8>>(true)
+                        : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 16>>(true);
+    if (dtype == LA_FP16)
+      return group <= 8 ? info_of<Tc5Engine<__half, LA_TC5_NST, 8>>(true) : info_of<Tc5Engine<__half, LA_TC5_NST, 16>>(true);
     return KernelInfo{};
   }
   if (dtype == LA_FP8_E4M3) {  // one tensor-core engine for every T_m <= 8 (MHA included)

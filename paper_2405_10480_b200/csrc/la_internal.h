@@ -113,6 +113,7 @@ struct DecodeArgs {
   int* unit_count;    // [units] dynamic mode: fold-tree groups completed per unit
   int* grp_count;     // [grid]  dynamic mode: segments published per fold-tree group
   unsigned long long* trace;  // [phys_grid][LA_TRACE_FIELDS] or nullptr
+  float* gfold;       // [phys_grid][KernelInfo::global_fold_floats] or nullptr
   int dynamic;        // 1: claim virtual CTAs dynamically, last-arriver fold
   int num_v;          // (virtual) CTAs
   int grid;           // CTAs launched
@@ -155,6 +156,8 @@ struct KernelInfo {
   int stage_tokens_max = 0;
   bool uses_tma_tensor = false;   // K/V TMA tensor maps (encoded per launch)
   int box_halves = 2;             // d = 128 bf16/fp16 maps: 128-B row halves per TMA box
+  int global_fold_floats = 0;     // > 0: consumer -> epilogue fold buffers live in plan-owned
+                                  // global scratch (floats per CTA), not shared memory
   const void* fn = nullptr;
 };
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine);

@@ -80,5 +80,18 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Warp: 32 lanes x 8 consecutive columns, into v[] (accumulate = add to v).
+__device__ __forceinline__ void ld8(uint32_t taddr, float (&v)[8], bool accumulate) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = accumulate ? v[i] + __uint_as_float(r[i]) : __uint_as_float(r[i]);
+}
+
 }  // namespace tc5
 }  // namespace la

@@ -95,3 +95,56 @@ def test_tcgen05_c3_full_size_sampled():
     o_exp, l_exp = census_expect(p3, 0)
     assert np.max(np.abs(O3 - o_exp[None, None, :])) <= 1e-5
     assert np.max(np.abs(L3 - l_exp)) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("heads_q,heads_kv,q_len,causal", [(32, 2, 1, True), (16, 1, 1, True), (24, 2, 1, True),
+                                                           (16, 2, 2, True), (16, 2, 2, False), (8, 1, 3, True)])
+def test_tcgen05_wide_tiles(dtype, heads_q, heads_kv, q_len, causal):
+    """16-row query tiles (the tcgen05 engine's N = 16): g * N_q rows of a KV head in ONE
+    pass where mma.sync tiles take two (g = 16, MQA 16, g = 12 -> 16 + 8 rows, g = 8 x N_q 2,
+    g = 8 x N_q 3 -> 16 + 8)."""
+    p = synth.Problem(2, heads_q, heads_kv, 128, [1000, 333], dtype=dtype, dist="D2", seed=71, q_len=q_len)
+    O_ref, L_ref = run_oracle(p, causal=causal)
+    inputs = cuda_inputs(p)
+    for schedule in ("streamk", "sequential"):
+        for tile_n, grid in ((128, 5), (256, 0)):
+            O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule, causal=causal, **TC5)
+            assert plan.info.tile_rows == min(16, p.group * q_len)
+            gate(O, L, O_ref, L_ref, what=f"tc5 wide H{heads_q}/{heads_kv} Nq{q_len} {dtype} {schedule} G{grid}")
+
+
+def test_tcgen05_wide_tiles_one_kv_pass_and_rejects_dynamic():
+    import paper_2405_10480_b200 as la
+    wide = la.Plan(2, 32, 2, 128, [4096, 4096], engine="tcgen05", host_only=True)
+    narrow = la.Plan(2, 32, 2, 128, [4096, 4096], host_only=True)
+    assert wide.info.num_units == 4 and narrow.info.num_units == 8  # C_m = 1 vs 2 query tiles per KV head
+    with pytest.raises(la.LaError):
+        la.Plan(2, 32, 2, 128, [4096, 4096], engine="tcgen05", schedule="dynamic")
+
+
+def test_tcgen05_wide_c3_speculative_full_size():
+    """c3 with N_q = 2 (speculative decode: 16 rows per KV head, ONE pass over the cache) vs the
+    oracle-pinned mma.sync engine (two 8-row passes) at full size, and the census closed form."""
+    p = synth.config("c3", q_len=2)
+    inputs = cuda_inputs(p)
+    O, L, plan = run_cuda(p, inputs=inputs, **TC5)
+    assert plan.info.tile_rows == 16 and plan.info.num_units == 64
+    import oracle
+    q64 = synth.to_f64(synth.gen_q(p))
+    for b, h in ((0, 0), (5, 3)):  # sampled units: 8 heads x 2 queries against the oracle
+        k = synth.to_f64(synth.gen_kv_unit(p, b, h, "k"))[None, None]
+        v = synth.to_f64(synth.gen_kv_unit(p, b, h, "v"))[None, None]
+        O_ref, L_ref = oracle.decode_attention_multi(q64[b:b + 1, 8 * h:8 * h + 8], k, v, [p.ctx_lens[b]], p.scale)
+        gate(O[b:b + 1, 8 * h:8 * h + 8], L[b:b + 1, 8 * h:8 * h + 8], O_ref, L_ref, what=f"tc5 c3 Nq2 b{b} h{h}")
+    O2, L2, plan2 = run_cuda(p, inputs=inputs)
+    assert plan2.info.num_units == 128
+    assert np.abs(O - O2).max() <= 1e-4 and np.abs(L - L2).max() <= 2e-6  # fp32 sums over 64k keys
+    del inputs
+    torch.cuda.empty_cache()
+    p3 = synth.config("c3", q_len=2, dist="D3")
+    O3, L3, _ = run_cuda(p3, causal=False, **TC5)
+    o_exp, l_exp = census_expect(p3, 0)
+    assert np.max(np.abs(O3 - o_exp)) <= 1e-5
+    assert np.max(np.abs(L3 - l_exp)) <= 1e-5
+    torch.cuda.empty_cache()
