@@ -966,10 +966,12 @@ struct Tc5Engine {
   static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, false);
 
   struct State {
-    float m[HEADS], l[HEADS];  // m: the warpgroup's running max (uniform); l: this token lane's share
+    float l[HEADS];            // this token lane's share of the running sums
     float o[HEADS];            // O~ of dim 32 sub + lane, every row
     int lbase, r0, nq;         // causal key limit of row h: lbase + (r0 + h) % nq (unit-local, exclusive)
-  };
+    int mpar;                  // the running max m (uniform over the warpgroup) lives in shared memory,
+  };                           // mb[mpar][row]; a stage writes the new m into mb[mpar ^ 1]
+  static constexpr int MB_OFF = 4096 + 640;  // per-slot extra: Q 0, red 4096, red2 4352, bars 4608, mb 4736
 
   __device__ __forceinline__ static unsigned char* extra() {
     extern __shared__ unsigned char smem_raw[];
@@ -1021,10 +1023,11 @@ struct Tc5Engine {
     }
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) {
-      s.m[h] = -INFINITY;
       s.l[h] = 0.f;
       s.o[h] = 0.f;
     }
+    if (tid < 2 * HEADS) reinterpret_cast<float*>(qs + MB_OFF)[tid] = -INFINITY;
+    s.mpar = 0;
     s.lbase = a.causal ? u.len - u.nq + 1 : u.len;  // N_q > 1, causal: query i is token n - N_b + i
     s.r0 = u.r0;
     s.nq = a.causal ? u.nq : 1;
@@ -1091,22 +1094,27 @@ struct Tc5Engine {
       red[sub * HEADS + lane] = v;
     }
     wg_bar(slot);
-    float al[HEADS];
+    const uint32_t mcur = smem_u32(xs + MB_OFF) + 4 * HEADS * s.mpar, mnext = smem_u32(xs + MB_OFF) + 4 * HEADS * (s.mpar ^ 1);
+    float mn[HEADS];
 #pragma unroll
-    for (int h = 0; h < HEADS; ++h) {
+    for (int h = 0; h < HEADS; ++h) {  // m_new = max(m, tile max) (Alg1§21)
       const uint32_t ra = smem_u32(red) + 4 * h;
       const float t = fmaxf(fmaxf(lds_f32(ra), lds_f32(ra + 4 * HEADS)), fmaxf(lds_f32(ra + 8 * HEADS), lds_f32(ra + 12 * HEADS)));
-      const float mn = fmaxf(s.m[h], t);
-      al[h] = ex2_sub(s.m[h], mn);  // Alg1§23: e^{m - m_new}; m = -inf -> 0
-      s.m[h] = mn;
+      mn[h] = fmaxf(lds_f32(mcur + 4 * h), t);
+    }
+    if (tid < HEADS) {
+      float v = mn[0];
+#pragma unroll
+      for (int h = 1; h < HEADS; ++h) v = tid == h ? mn[h] : v;
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(mnext + 4 * tid), "f"(v) : "memory");
     }
     // ---- P_f = exp(S_f - m) (Alg1§22) into the dead K tile as the PV B operand ---------------
     unsigned char* pb = st + (tid >> 6) * PHS;  // [token half][2 HEADS rows][128 B]
     const int pc = (tid & 63) >> 3, pe = (tid & 7) * 2;
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) {
-      const float p = ex2_sub(sc[h], s.m[h]);
-      s.l[h] = fmaf(al[h], s.l[h], p);
+      const float p = ex2_sub(sc[h], mn[h]);
+      s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23: e^{m - m_new} l + rowsum
       const T hi = to_kv<T>(p);
       const T lo = to_kv<T>(p - kv_to_f(hi));
       *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ (h & 7)) << 4) + pe) = hi;
@@ -1130,6 +1138,9 @@ struct Tc5Engine {
     }
     mbar_wait(&bars[1], par);
     tc5::fence_after();
+    float al[HEADS];  // e^{m - m_new} again from the two shared copies (no registers held across the MMA)
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) al[h] = ex2_sub(lds_f32(mcur + 4 * h), lds_f32(mnext + 4 * h));
     // O^T tile: column h = V^T P_hi row h, column HEADS + h = V^T P_lo row h (per chain)
 #pragma unroll
     for (int c0 = 0; c0 < HEADS; c0 += 8) {  // 8 rows at a time: hi columns c0.., lo columns HEADS + c0..
@@ -1155,6 +1166,7 @@ struct Tc5Engine {
       for (int i = 0; i < 8; ++i) s.o[c0 + i] = fmaf(al[c0 + i], s.o[c0 + i], hv[i] + lv[i]);  // Alg1§25
     }
     tc5::fence_before();
+    s.mpar ^= 1;
   }
 
   __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
@@ -1169,10 +1181,13 @@ struct Tc5Engine {
       for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
       if (lane == h) red2[sub * HEADS + h] = l;
     }
+    // read m before the barrier: past it, the next segment's seg_begin resets mb
+    const float mv = lane < HEADS ? reinterpret_cast<const float*>(extra() + slot * XS + MB_OFF)[HEADS * s.mpar + lane]
+                                  : 0.f;
     wg_bar(slot);
     if (sub == 0 && lane < HEADS) {
       const int h = lane;
-      fb[h * (D + 2) + D] = s.m[h];
+      fb[h * (D + 2) + D] = mv;
       fb[h * (D + 2) + D + 1] = (red2[h] + red2[HEADS + h]) + (red2[2 * HEADS + h] + red2[3 * HEADS + h]);
     }
   }
