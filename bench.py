@@ -54,8 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential", "fixed_split"])
     ap.add_argument("--page-size", type=int, default=0, help="run the config in a paged KV pool (16..256)")
-    ap.add_argument("--engine", default="mma", choices=["mma", "tcgen05"],
-                    help="tensor-core engine for T_m > 1 tiles (GQA): mma.sync or tcgen05 + TMEM")
+    ap.add_argument("--engine", default="auto", choices=["auto", "mma", "tcgen05"],
+                    help="tensor-core engine for T_m > 1 tiles (GQA): auto (the plan's rule), mma.sync or tcgen05 + TMEM")
     ap.add_argument("--q-len", type=int, default=1,
                     help="N_q query tokens per request (speculative decode; single GPU, no e2e / cpu legs)")
     ap.add_argument("--tile-n", type=int, default=0, help="LeanTile size T_n (0 = planner's auto rule)")
@@ -460,8 +460,8 @@ def bench_ours(args):
         peak, peak_src = peaks()
         achieved = local_kv / (kern_ms * 1e-3) / 1e9   # dominant kernel, per launch
         traffic = ncu_traffic(cfg + ("-fp8" if p.dtype == "fp8" else "")
-                              + ("-tc5" if args.engine == "tcgen05" and info.tile_rows > 1 else ""))
-        engine = "Fp8" if p.dtype == "fp8" else (("Tc5" if args.engine == "tcgen05" else "Gqa")
+                              + ("-tc5" if info.engine == 1 and info.tile_rows > 1 else ""))
+        engine = "Fp8" if p.dtype == "fp8" else (("Tc5" if info.engine == 1 else "Gqa")
                                                  if info.tile_rows > 1 else "Mha")
         line = {
             "metric": METRIC, "value": total_kv / (step_ms * 1e-3) / 1e9, "unit": "GB/s",
@@ -476,7 +476,7 @@ def bench_ours(args):
                        "context": p.ctx_lens[0] if len(set(p.ctx_lens)) == 1 else p.ctx_lens,
                        "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
                        "stage_tokens": info.stage_tokens, "schedule": args.schedule,
-                       **({"engine": args.engine} if info.tile_rows > 1 and p.dtype != "fp8" else {}),
+                       **({"engine": {0: "mma.sync", 1: "tcgen05"}[info.engine]} if info.engine >= 0 else {}),
                        **({"q_len": args.q_len, "query_tile_rows": info.tile_rows, "units": info.num_units}
                           if args.q_len > 1 else {}),
                        "kv_layout": p.layout + (f" (page {args.page_size})" if args.page_size else ""),

@@ -138,19 +138,24 @@ typedef struct {
   float k_scale;              /* K = code x k_scale (folded into the score scale)             */
   float v_scale;              /* V = code x v_scale (applied once, at finalize: O x v_scale)  */
   /* Tensor-core engine for T_m > 1 tiles (GQA groups / N_q > 1; MHA always runs on CUDA cores): */
-  int engine;                 /* la_engine, default LA_ENGINE_MMA_SYNC.  LA_ENGINE_TCGEN05
-                                 needs bf16 / fp16, head_dim 128 and a non-paged layout when
-                                 T_m > 1, else la_plan fails with LA_ERR_UNSUPPORTED; it is
-                                 ignored for T_m = 1 (MHA: a GEMV, CUDA cores)               */
+  int engine;                 /* la_engine, default LA_ENGINE_AUTO.  LA_ENGINE_TCGEN05 needs
+                                 bf16 / fp16, head_dim 128 and a non-paged layout when T_m > 1,
+                                 and its 16-row tiles (g * N_q > 8) the static schedules, else
+                                 la_plan fails with LA_ERR_UNSUPPORTED; ignored for T_m = 1
+                                 (MHA: a GEMV, CUDA cores) and FP8 caches                     */
 } la_plan_opts;
 
 /* Which tensor-core instructions contract the T_m x T_n tiles (Alg1§20, §24). */
 typedef enum {
   LA_ENGINE_MMA_SYNC = 0, /* warp-level mma.sync m16n8k16: every consumer warp owns its own
                              32-token rounds and accumulators in registers      */
-  LA_ENGINE_TCGEN05 = 1   /* 5th-gen tensor cores: one warpgroup per 128-token stage, one
-                             thread issues tcgen05.mma (M = 128 tokens / dims, N = 16) with
-                             S^T and the per-stage O^T in TMEM, read back by tcgen05.ld    */
+  LA_ENGINE_TCGEN05 = 1,  /* 5th-gen tensor cores: one warpgroup per 128-token stage, one
+                             thread issues tcgen05.mma (M = 128 tokens / dims, N = 16 / 32)
+                             with S^T and the per-stage O^T in TMEM, read back by
+                             tcgen05.ld; query tiles of up to 16 rows (T_m)                 */
+  LA_ENGINE_AUTO = 2      /* tcgen05 where g * N_q > 8 rows per KV head (one KV pass instead
+                             of two) and it applies (bf16 / fp16, d = 128, not paged, static
+                             schedule); mma.sync otherwise                                   */
 } la_engine;
 
 typedef struct la_plan_s* la_plan_t;
@@ -173,6 +178,8 @@ typedef struct {
   int q_len;               /* N_q (0 when per-request q_lens differ)                      */
   int tile_rows;           /* T_m: query rows per work unit                               */
   int64_t q_rows;          /* query / output rows = sum_b H_q N_b                          */
+  int engine;              /* la_engine chosen for T_m > 1 tiles; -1 for the CUDA-core (MHA)
+                              and FP8 engines                                                */
 } la_plan_info;
 
 /* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */

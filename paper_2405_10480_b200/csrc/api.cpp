@@ -37,7 +37,8 @@ struct la_plan_s {
   int* d_counters = nullptr;
   int* d_unit_count = nullptr;
   unsigned long long* d_trace = nullptr;
-  float* d_gfold = nullptr;  // engine fold buffers in global memory (KernelInfo::global_fold_floats)
+  float* d_gfold = nullptr;
+  int engine = -1;           // la_engine of the T_m > 1 tiles (-1: CUDA cores / FP8 engine)  // engine fold buffers in global memory (KernelInfo::global_fold_floats)
   int64_t workspace = 0;
   // la_decode_host staging
   void* d_stage = nullptr;
@@ -131,6 +132,7 @@ la_status la_plan_opts_init(la_plan_opts* o) {
   o->dyn_min_chunk = 2;
   o->q_len = 1;
   o->causal = 1;
+  o->engine = LA_ENGINE_AUTO;
   return LA_OK;
 }
 
@@ -187,10 +189,18 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     uniform = uniform && n == p.q_lens[0];
   }
   p.q_len = uniform ? p.q_lens[0] : 0;
+  // Engine for T_m > 1 tiles.  AUTO takes tcgen05 exactly where it wins (measured):
+  // more than 8 rows per KV head (g * N_q > 8), which its N = 16 MMAs cover in one pass over
+  // the cache where mma.sync tiles need two; otherwise mma.sync (equal or slightly faster).
+  if (opts.engine != LA_ENGINE_MMA_SYNC && opts.engine != LA_ENGINE_TCGEN05 && opts.engine != LA_ENGINE_AUTO)
+    return fail(LA_ERR_INVALID, "engine must be LA_ENGINE_AUTO, LA_ENGINE_MMA_SYNC or LA_ENGINE_TCGEN05");
+  const bool tc5_ok = head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16) && opts.layout != LA_KV_PAGED;
+  const bool static_sched = opts.schedule == LA_SCHED_STREAMK || opts.schedule == LA_SCHED_SEQUENTIAL;
+  const int engine = opts.engine != LA_ENGINE_AUTO ? opts.engine
+                     : (max_rows > 8 && tc5_ok && static_sched ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
   // T_m: 1 -> CUDA-core engine, else tensor-core tiles of <= 8 rows (mma.sync: N = 8), or
   // <= 16 on the tcgen05 engine (N = 16 per MMA at no extra cost: one KV pass per 16 rows)
-  const bool wide = opts.engine == LA_ENGINE_TCGEN05 && head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16) &&
-                    opts.layout != LA_KV_PAGED;
+  const bool wide = engine == LA_ENGINE_TCGEN05 && tc5_ok;
   p.tile_rows = std::min(wide ? 16 : 8, max_rows);
   if (xw && p.causal)
     for (int32_t n : p.q_lens)
@@ -250,15 +260,12 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (plan->host_only) {
     max_ctas = std::max(1, opts.num_sms) * std::max(1, opts.ctas_per_sm);
   } else {
-    if (opts.engine != LA_ENGINE_MMA_SYNC && opts.engine != LA_ENGINE_TCGEN05) {
-      delete plan;
-      return fail(LA_ERR_INVALID, "engine must be LA_ENGINE_MMA_SYNC or LA_ENGINE_TCGEN05");
-    }
-    if (opts.engine == LA_ENGINE_TCGEN05 && p.rows() > 1 && (p.layout == LA_KV_PAGED || dtype == LA_FP8_E4M3)) {
+    if (engine == LA_ENGINE_TCGEN05 && p.rows() > 1 && (p.layout == LA_KV_PAGED || dtype == LA_FP8_E4M3)) {
       delete plan;
       return fail(LA_ERR_UNSUPPORTED, "LA_ENGINE_TCGEN05 covers T_m > 1 tiles of a bf16 / fp16, non-paged cache");
     }
-    plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows(), p.rows() > 1 ? opts.engine : 0);
+    plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows(), p.rows() > 1 ? engine : 0);
+    plan->engine = p.rows() > 1 && dtype != LA_FP8_E4M3 ? engine : -1;
     if (plan->kinfo.global_fold_floats > 0 && (p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT)) {
       delete plan;  // their fold tree stages peers in the (shared-memory) fold buffer
       return fail(LA_ERR_UNSUPPORTED, "16-row tcgen05 tiles run the static schedules (streamk, sequential)");
@@ -418,6 +425,7 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   info->split = plan->split;
   info->q_len = p.q_len;
   info->tile_rows = p.tile_rows;
+  info->engine = plan->engine;
   info->q_rows = p.q_rows();
   info->num_units = int(s.units.size());
   info->total_iters = s.total_iters;

@@ -63,7 +63,8 @@ class la_plan_info(ctypes.Structure):
                [(n, ctypes.c_int64) for n in ("total_iters", "num_segments", "num_partials",
                                               "workspace_bytes", "kv_bytes")] + \
                [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64), ("split", ctypes.c_int),
-                ("q_len", ctypes.c_int), ("tile_rows", ctypes.c_int), ("q_rows", ctypes.c_int64)]
+                ("q_len", ctypes.c_int), ("tile_rows", ctypes.c_int), ("q_rows", ctypes.c_int64),
+                ("engine", ctypes.c_int)]
 
 
 _lib = None
@@ -130,7 +131,7 @@ def launch_count() -> int:
     return int(lib().la_launch_count())
 
 
-_ENGINE_CODES = {"mma": 0, "tcgen05": 1}
+_ENGINE_CODES = {"mma": 0, "tcgen05": 1, "auto": 2}
 
 
 class Plan:
@@ -143,7 +144,7 @@ class Plan:
                  dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
                  causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None,
-                 k_scale: float = 0.0, v_scale: float = 0.0, engine: str = "mma"):
+                 k_scale: float = 0.0, v_scale: float = 0.0, engine: str = "auto"):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -172,7 +173,7 @@ class Plan:
         opts.xchg_rank = int(xchg_rank)
         opts.k_scale = float(k_scale)  # dtype "fp8": K = codes x k_scale, V = codes x v_scale
         opts.v_scale = float(v_scale)
-        opts.engine = _ENGINE_CODES[engine]  # "mma" (mma.sync) or "tcgen05" (T_m > 1 tiles)
+        opts.engine = _ENGINE_CODES[engine]  # "auto", "mma" (mma.sync) or "tcgen05" (T_m > 1 tiles)
         self.engine = engine
         if q_lens is not None:  # heterogeneous batch: N_b per request
             ql = np.ascontiguousarray(np.asarray(q_lens, dtype=np.int32))

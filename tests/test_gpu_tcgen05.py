@@ -65,7 +65,7 @@ def test_tcgen05_determinism_and_equivalence():
         ref = plan.decode(q, k, v)[0].clone()
         for _ in range(5):
             assert torch.equal(plan.decode(q, k, v)[0], ref)
-        mma = la.Plan(1, 8, 1, 128, [5000], grid=11, tile_n=128, schedule=schedule).decode(q, k, v)[0]
+        mma = la.Plan(1, 8, 1, 128, [5000], grid=11, tile_n=128, schedule=schedule, engine="mma").decode(q, k, v)[0]
         assert (ref - mma).abs().max().item() <= 2e-5  # both engines: P = P_hi + P_lo, fp32 sums
 
 
@@ -117,7 +117,7 @@ def test_tcgen05_wide_tiles(dtype, heads_q, heads_kv, q_len, causal):
 def test_tcgen05_wide_tiles_one_kv_pass_and_rejects_dynamic():
     import paper_2405_10480_b200 as la
     wide = la.Plan(2, 32, 2, 128, [4096, 4096], engine="tcgen05", host_only=True)
-    narrow = la.Plan(2, 32, 2, 128, [4096, 4096], host_only=True)
+    narrow = la.Plan(2, 32, 2, 128, [4096, 4096], host_only=True, engine="mma")
     assert wide.info.num_units == 4 and narrow.info.num_units == 8  # C_m = 1 vs 2 query tiles per KV head
     with pytest.raises(la.LaError):
         la.Plan(2, 32, 2, 128, [4096, 4096], engine="tcgen05", schedule="dynamic")
@@ -137,7 +137,7 @@ def test_tcgen05_wide_c3_speculative_full_size():
         v = synth.to_f64(synth.gen_kv_unit(p, b, h, "v"))[None, None]
         O_ref, L_ref = oracle.decode_attention_multi(q64[b:b + 1, 8 * h:8 * h + 8], k, v, [p.ctx_lens[b]], p.scale)
         gate(O[b:b + 1, 8 * h:8 * h + 8], L[b:b + 1, 8 * h:8 * h + 8], O_ref, L_ref, what=f"tc5 c3 Nq2 b{b} h{h}")
-    O2, L2, plan2 = run_cuda(p, inputs=inputs)
+    O2, L2, plan2 = run_cuda(p, inputs=inputs, engine="mma")
     assert plan2.info.num_units == 128
     assert np.abs(O - O2).max() <= 1e-4 and np.abs(L - L2).max() <= 2e-6  # fp32 sums over 64k keys
     del inputs

@@ -38,22 +38,29 @@ def _cuda(p, causal=True, **kw):
     return out.reshape(-1, p.head_dim).cpu().numpy(), lse.reshape(-1).cpu().numpy(), plan
 
 
+@pytest.mark.parametrize("engine", ["mma", "auto"])
 @pytest.mark.parametrize("hq,hkv,d", [(32, 2, 128), (16, 1, 64), (24, 2, 128)])
-def test_large_groups_mqa(hq, hkv, d):
-    """g = 16, 16, 12 with N_q = 1: C_m = 2 query tiles per KV head (g > 8 was unsupported)."""
+def test_large_groups_mqa(hq, hkv, d, engine):
+    """g = 16, 16, 12 with N_q = 1: C_m = 2 query tiles of 8 rows per KV head on mma.sync
+    (g > 8 was unsupported); "auto" takes the tcgen05 engine's 16-row tiles (C_m = 1) at d = 128."""
     p = synth.Problem(2, hq, hkv, d, [1500, 2777], dtype="bf16", dist="D2", seed=81)
-    O, L, plan = _cuda(p)
-    assert plan.info.tile_rows == 8 and plan.info.num_units == 2 * hkv * 2
-    gate(O, L, *_oracle(p), what=f"g={hq // hkv}")
+    O, L, plan = _cuda(p, engine=engine)
+    tm = 16 if engine == "auto" and d == 128 else 8
+    g = hq // hkv
+    assert plan.info.tile_rows == min(tm, g) and plan.info.num_units == 2 * hkv * -(-g // tm)
+    assert plan.info.engine == (1 if tm == 16 else 0)
+    gate(O, L, *_oracle(p), what=f"g={g} {engine}")
 
 
+@pytest.mark.parametrize("engine", ["mma", "auto"])
 @pytest.mark.parametrize("causal", [True, False])
-def test_query_tiles_multi_token(causal):
-    """g = 8 x N_q = 3 = 24 rows -> 3 tiles; the causal limit follows the row's query index."""
+def test_query_tiles_multi_token(causal, engine):
+    """g = 8 x N_q = 3 = 24 rows -> 3 tiles of 8 (mma.sync) or 16 + 8 (tcgen05 via "auto"); the
+    causal limit follows the row's query index."""
     p = synth.Problem(2, 16, 2, 128, [900, 2000], dtype="bf16", dist="D1", seed=82, q_len=3)
-    O, L, plan = _cuda(p, causal=causal)
-    assert plan.info.num_units == 2 * 2 * 3
-    gate(O, L, *_oracle(p, causal), what=f"tiles causal={causal}")
+    O, L, plan = _cuda(p, causal=causal, engine=engine)
+    assert plan.info.num_units == 2 * 2 * (3 if engine == "mma" else 2)
+    gate(O, L, *_oracle(p, causal), what=f"tiles causal={causal} {engine}")
 
 
 @pytest.mark.parametrize("dtype,d", [("bf16", 128), ("fp16", 64)])

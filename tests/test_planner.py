@@ -40,7 +40,7 @@ def test_exports_every_declared_symbol(la):
 def test_plan_opts_struct_matches_the_header(la):
     """The ctypes mirror of la_plan_opts has the C layout: la_plan_opts_init memsets exactly
     sizeof(la_plan_opts) bytes, so it must touch the whole ctypes struct and nothing past it,
-    and its defaults must land in the fields of the same names (engine = LA_ENGINE_MMA_SYNC)."""
+    and its defaults must land in the fields of the same names (engine = LA_ENGINE_AUTO)."""
     import ctypes
     from paper_2405_10480_b200.leanattn import la_plan_opts
     n = ctypes.sizeof(la_plan_opts)
@@ -48,7 +48,7 @@ def test_plan_opts_struct_matches_the_header(la):
     assert la.lib().la_plan_opts_init(ctypes.cast(buf, ctypes.POINTER(la_plan_opts))) == 0
     assert all(b == 0xAB for b in bytes(buf)[n:]), "la_plan_opts_init wrote past the ctypes struct"
     o = la_plan_opts.from_buffer(buf)
-    assert (o.num_sms, o.ctas_per_sm, o.q_len, o.causal, o.dyn_first_permille, o.engine) == (148, 1, 1, 1, 750, 0)
+    assert (o.num_sms, o.ctas_per_sm, o.q_len, o.causal, o.dyn_first_permille, o.engine) == (148, 1, 1, 1, 750, 2)
     header = open(os.path.join(ROOT, "include", "la.h")).read()
     body = header[header.index("typedef struct {\n  float scale;"):header.index("} la_plan_opts;")]
     fields = re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(\w+);", body, re.M)
@@ -246,9 +246,10 @@ def test_query_tiles_and_heterogeneous_batches_bit_exact(la):
         qls = [int(x) for x in rng.integers(1, 6, size=batch)]
         layout = ["bhsd", "packed"][trial % 2]
         tile = int(rng.choice([32, 64, 128]))
+        engine = ["mma", "tcgen05", "auto"][(trial // 2) % 3]
         p = la.Plan(batch, hkv * g, hkv, 128, lens, tile_n=tile, grid=int(rng.integers(1, 300)), layout=layout,
-                    host_only=True, schedule="streamk", q_lens=qls)
-        tm = min(8, max(g * n for n in qls))
+                    host_only=True, schedule="streamk", q_lens=qls, engine=engine)
+        tm = min(8 if engine == "mma" else 16, max(g * n for n in qls))
         c_n = []
         for (b, _h) in unit_order(batch, hkv, layout):
             c_n += [-(-lens[b] // tile)] * (-(-(g * qls[b]) // tm))
@@ -267,8 +268,14 @@ def test_heterogeneous_validation(la):
     with pytest.raises(la.LaError) as e:   # causal multi-token blocks are not shard-local
         la.Plan(2, 2, 2, 128, [100, 100], host_only=True, q_lens=[1, 2], xchg_world=2)
     assert e.value.status == la.LA_ERR_UNSUPPORTED
-    p = la.Plan(1, 32, 2, 128, [1000], host_only=True)         # MQA-like g = 16: two 8-row tiles
+    p = la.Plan(1, 32, 2, 128, [1000], host_only=True, engine="mma")  # MQA-like g = 16: two 8-row tiles
     assert p.info.tile_rows == 8 and p.info.num_units == 4
+    p = la.Plan(1, 32, 2, 128, [1000], host_only=True)  # auto: tcgen05's 16-row tiles, one per KV head
+    assert p.info.tile_rows == 16 and p.info.num_units == 2
+    p = la.Plan(1, 32, 2, 128, [1000], host_only=True, schedule="dynamic")  # auto, dynamic: mma.sync tiles
+    assert p.info.tile_rows == 8 and p.info.num_units == 4
+    p = la.Plan(1, 16, 2, 128, [1000], host_only=True)  # auto, g = 8: mma.sync
+    assert p.info.tile_rows == 8 and p.info.num_units == 2
 
 
 def test_fp8_plan(la):
