@@ -194,7 +194,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   // the cache where mma.sync tiles need two; otherwise mma.sync (equal or slightly faster).
   if (opts.engine != LA_ENGINE_MMA_SYNC && opts.engine != LA_ENGINE_TCGEN05 && opts.engine != LA_ENGINE_AUTO)
     return fail(LA_ERR_INVALID, "engine must be LA_ENGINE_AUTO, LA_ENGINE_MMA_SYNC or LA_ENGINE_TCGEN05");
-  const bool tc5_ok = head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16) && opts.layout != LA_KV_PAGED;
+  const bool tc5_ok = head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16);
   const bool static_sched = opts.schedule == LA_SCHED_STREAMK || opts.schedule == LA_SCHED_SEQUENTIAL;
   const int engine = opts.engine != LA_ENGINE_AUTO ? opts.engine
                      : (max_rows > 8 && tc5_ok && static_sched ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
@@ -260,9 +260,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (plan->host_only) {
     max_ctas = std::max(1, opts.num_sms) * std::max(1, opts.ctas_per_sm);
   } else {
-    if (engine == LA_ENGINE_TCGEN05 && p.rows() > 1 && (p.layout == LA_KV_PAGED || dtype == LA_FP8_E4M3)) {
+    if (engine == LA_ENGINE_TCGEN05 && p.rows() > 1 && dtype == LA_FP8_E4M3) {
       delete plan;
-      return fail(LA_ERR_UNSUPPORTED, "LA_ENGINE_TCGEN05 covers T_m > 1 tiles of a bf16 / fp16, non-paged cache");
+      return fail(LA_ERR_UNSUPPORTED, "LA_ENGINE_TCGEN05 covers T_m > 1 tiles of a bf16 / fp16 cache");
     }
     plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows(), p.rows() > 1 ? engine : 0);
     plan->engine = p.rows() > 1 && dtype != LA_FP8_E4M3 ? engine : -1;

@@ -1006,8 +1006,28 @@ struct Tc5Engine {
 #pragma unroll
     for (int h = 0; h < 2 / BOX_HALVES; ++h) tma_load_3d(dst + KV_BYTES + h * 16384, &tm.v, 0, int(row), h, vbar, pol);
   }
-  __device__ __forceinline__ static void produce_paged(unsigned char*, const DecodeArgs&, const TmapPair&, PageWin&, int,
-                                                       int, uint64_t*, uint64_t, int) {}  // not selected when paged
+  // Paged KV: boxes of box_rows = min(128, page) rows of ONE 128-B half, each inside one
+  // page, placed so the stage keeps the [half][128 rows][128 B] operand layout; lane r issues
+  // load r = (box i, half, K or V).
+  __device__ __forceinline__ static void produce_paged(unsigned char* dst, const DecodeArgs& a, const TmapPair& tm,
+                                                       PageWin& pw, int s0, int ntok, uint64_t* bar, uint64_t pol,
+                                                       int lane) {
+    const int br = a.box_rows;
+    const int nb = (ntok + br - 1) / br;
+    const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + 4096 + 512) + 2;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * 2));
+      mbar_arrive_expect_tx(vbar, uint32_t(nb * br * 128 * 2));
+    }
+    __syncwarp();
+    for (int task = lane; task < nb * 4; task += 32) {
+      const int i = task >> 2, half = (task >> 1) & 1, is_v = task & 1;
+      const int row = int(pw.row_of(s0 + i * br));
+      tma_load_3d(dst + (is_v ? KV_BYTES : 0) + half * 16384 + i * br * 128, is_v ? &tm.v : &tm.k, 0, row, half,
+                  is_v ? vbar : bar, pol);
+    }
+  }
 
   __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
     const int slot = slot_of_thread(), tid = (int(threadIdx.x >> 5) % WPS) * 32 + lane;

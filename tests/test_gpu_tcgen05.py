@@ -71,9 +71,8 @@ def test_tcgen05_determinism_and_equivalence():
 
 def test_tcgen05_plan_errors():
     import paper_2405_10480_b200 as la
-    with pytest.raises(la.LaError):  # paged pools stay on the mma.sync engine
-        la.Plan(1, 8, 1, 128, [1000], engine="tcgen05", layout="paged", block_table=np.zeros((1, 63), np.int32),
-                page_size=16, num_pages=63)
+    with pytest.raises(la.LaError):  # FP8 caches stay on their f16 mma.sync engine
+        la.Plan(1, 8, 1, 128, [1000], engine="tcgen05", dtype="fp8", k_scale=1.0, v_scale=1.0)
     plan = la.Plan(1, 4, 4, 128, [1000], engine="tcgen05")  # MHA (T_m = 1): CUDA cores, engine ignored
     assert plan.info.group == 1
 
@@ -148,3 +147,19 @@ def test_tcgen05_wide_c3_speculative_full_size():
     assert np.max(np.abs(O3 - o_exp)) <= 1e-5
     assert np.max(np.abs(L3 - l_exp)) <= 1e-5
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("rows", [8, 16])
+@pytest.mark.parametrize("page_size", [16, 32, 64, 128, 256])
+def test_tcgen05_paged(rows, page_size):
+    """Paged pools on the tcgen05 engine: per-half TMA boxes of min(128, page) rows inside one
+    page keep the stage's operand layout; 8-row (g = 8) and 16-row (g = 16) tiles."""
+    p = synth.Problem(3, 2 * rows, 2, 128, [1000, 77, 2500], dtype="bf16", dist="D2", seed=51,
+                      layout="paged", page_size=page_size)
+    O_ref, L_ref = run_oracle(p)
+    inputs = cuda_inputs(p)
+    for schedule in (("streamk", "dynamic") if rows == 8 else ("streamk", "sequential")):
+        for tile_n, grid in ((128, 5), (256, 0)):
+            O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule, **TC5)
+            assert plan.info.engine == 1 and plan.info.tile_rows == rows
+            gate(O, L, O_ref, L_ref, what=f"tc5 paged rows{rows} ps{page_size} T{tile_n} G{grid} {schedule}")
