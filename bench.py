@@ -275,8 +275,8 @@ def bench_ours(args):
     cfg = args.config or ("c2" if world == 1 else "c5")
     dkw = {"dtype": args.dtype} if args.dtype else {}
     if args.q_len > 1:
-        if world > 1 or args.page_size:
-            raise SystemExit("--q-len is a single-GPU, non-paged option")
+        if world > 1:
+            raise SystemExit("--q-len is a single-GPU option")
         dkw["q_len"] = args.q_len
         args.no_cpu = args.no_e2e = True
     p = synth.config(cfg, **dkw)
