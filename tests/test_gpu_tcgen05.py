@@ -163,3 +163,20 @@ def test_tcgen05_paged(rows, page_size):
             O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule, **TC5)
             assert plan.info.engine == 1 and plan.info.tile_rows == rows
             gate(O, L, O_ref, L_ref, what=f"tc5 paged rows{rows} ps{page_size} T{tile_n} G{grid} {schedule}")
+
+
+@pytest.mark.parametrize("rows_per_head", [8, 16])
+def test_tcgen05_tiny_contexts(rows_per_head):
+    """Contexts of 1..129 tokens (one short stage, a stage plus one token) and N_q = 2 blocks
+    whose causal limits cut inside the only stage."""
+    g = rows_per_head
+    p = synth.Problem(4, 2 * g, 2, 128, [1, 3, 128, 129], dtype="bf16", dist="D2", seed=91)
+    O_ref, L_ref = run_oracle(p)
+    for grid in (1, 0):
+        O, L, _ = run_cuda(p, grid=grid, **TC5)
+        gate(O, L, O_ref, L_ref, what=f"tc5 tiny g{g} G{grid}")
+    p2 = synth.Problem(3, g, 2, 128, [2, 9, 200], dtype="bf16", dist="D2", seed=92, q_len=2)
+    O_ref, L_ref = run_oracle(p2, causal=True)
+    O, L, plan = run_cuda(p2, causal=True, **TC5)
+    assert plan.info.tile_rows == g
+    gate(O, L, O_ref, L_ref, what=f"tc5 tiny Nq2 g{g // 2}")
