@@ -151,8 +151,8 @@ typedef enum {
                              32-token rounds and accumulators in registers      */
   LA_ENGINE_TCGEN05 = 1,  /* 5th-gen tensor cores: one warpgroup per 128-token stage, one
                              thread issues tcgen05.mma (M = 128 tokens / dims, N = 16 / 32)
-                             with S^T and the per-stage O^T in TMEM, read back by
-                             tcgen05.ld; query tiles of up to 16 rows (T_m)                 */
+                             with S^T and the per-stage O^T in TMEM (N up to 32 / 64), read back by
+                             tcgen05.ld; query tiles of up to 32 rows (T_m)                 */
   LA_ENGINE_AUTO = 2      /* tcgen05 where g * N_q > 8 rows per KV head (one KV pass instead
                              of two) and it applies (bf16 / fp16, d = 128, static schedule);
                              mma.sync otherwise                                              */

@@ -199,9 +199,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   const int engine = opts.engine != LA_ENGINE_AUTO ? opts.engine
                      : (max_rows > 8 && tc5_ok && static_sched ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
   // T_m: 1 -> CUDA-core engine, else tensor-core tiles of <= 8 rows (mma.sync: N = 8), or
-  // <= 16 on the tcgen05 engine (N = 16 per MMA at no extra cost: one KV pass per 16 rows)
+  // <= 32 on the tcgen05 engine (N = 16 / 32 per MMA at no extra cost: one KV pass per 32 rows)
   const bool wide = engine == LA_ENGINE_TCGEN05 && tc5_ok;
-  p.tile_rows = std::min(wide ? 16 : 8, max_rows);
+  p.tile_rows = std::min(wide ? 32 : 8, max_rows);
   if (xw && p.causal)
     for (int32_t n : p.q_lens)
       if (n > 1) return fail(LA_ERR_UNSUPPORTED, "sequence-shard exchange needs N_b == 1 or causal == 0");

@@ -946,7 +946,10 @@ struct Tc5Engine {
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;  // 64 KiB
   static constexpr int HEADS = HEADS_;              // T_m: 8, or 16 (the wider N of tcgen05: one KV pass
                                                     // for g * N_b <= 16 rows where mma.sync tiles need two)
-  static_assert(HEADS == 8 || HEADS == 16, "T_m");
+  static_assert(HEADS == 8 || HEADS == 16 || HEADS == 32, "T_m");
+  static constexpr int QR = HEADS < 16 ? 16 : HEADS;  // Q^T operand rows = S^T MMA N (>= 16)
+  static constexpr int QHS = QR * 128;               // Q^T dim-half stride
+  static constexpr int LN = HEADS == 32 ? 1 : HEADS;  // running-sum registers per thread
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
   static constexpr int PHS = NO * 128;              // P^T token-half stride [2 HEADS rows][128 B]
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
@@ -955,23 +958,27 @@ struct Tc5Engine {
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
   static constexpr int SPLIT = LA_TC5_SPLIT;        // accumulator chains per contraction (1 or 2)
-  static constexpr int OC = 16 * SPLIT;             // first O^T column of a slot (S^T chains before it)
+  static constexpr int OC = QR * SPLIT;             // first O^T column of a slot (S^T chains before it)
   static constexpr int COLS = (OC + NO * SPLIT) <= 32 ? 32 : (OC + NO * SPLIT) <= 64 ? 64 : 128;  // per slot
+  static_assert(NST * COLS <= 512, "TMEM columns");
   static constexpr int TMEM_COLS = NST * COLS <= 32 ? 32 : NST * COLS <= 64 ? 64 : NST * COLS <= 128 ? 128 : 256;
   // extra smem per slot: Q^T operand [half][16 rows][128 B] (4 KiB, 1024-aligned), the
   // warpgroup's max exchange red[4][8] + l exchange red2[4][8], two MMA-completion barriers
-  static constexpr int XS = 5120;
+  // per-slot extra: Q^T [2][QR][128 B], red [4][HEADS], red2 [4][HEADS], 3 barriers, mb [2][HEADS]
+  static constexpr int RED_OFF = 2 * QHS, RED2_OFF = RED_OFF + 16 * HEADS, BAR_OFF = RED2_OFF + 16 * HEADS;
+  static constexpr int MB_OFF = BAR_OFF + 32;
+  static constexpr int XS = (MB_OFF + 8 * HEADS + 1023) / 1024 * 1024;
   static constexpr int EXTRA_BYTES = NST * XS + 1024;  // + the TMEM base address
-  static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, 16, false, false);
+  static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, QR, false, false);
   static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, false);
 
   struct State {
-    float l[HEADS];            // this token lane's share of the running sums
+    float l[LN];               // HEADS <= 16: this token lane's share of every row's running sum;
+                               // 32: the warp's running sum of row `lane` (transpose-butterfly)
     float o[HEADS];            // O~ of dim 32 sub + lane, every row
     int lbase, r0, nq;         // causal key limit of row h: lbase + (r0 + h) % nq (unit-local, exclusive)
     int mpar;                  // the running max m (uniform over the warpgroup) lives in shared memory,
   };                           // mb[mpar][row]; a stage writes the new m into mb[mpar ^ 1]
-  static constexpr int MB_OFF = 4096 + 640;  // per-slot extra: Q 0, red 4096, red2 4352, bars 4608, mb 4736
 
   __device__ __forceinline__ static unsigned char* extra() {
     extern __shared__ unsigned char smem_raw[];
@@ -986,7 +993,7 @@ struct Tc5Engine {
   }
   __device__ __forceinline__ static void init_barriers() {  // thread 0, before __syncthreads
     for (int s = 0; s < NST; ++s) {
-      uint64_t* b = reinterpret_cast<uint64_t*>(extra() + s * XS + 4096 + 512);
+      uint64_t* b = reinterpret_cast<uint64_t*>(extra() + s * XS + BAR_OFF);
       mbar_init(&b[0], 1);  // S^T ready (tcgen05.commit)
       mbar_init(&b[1], 1);  // O^T tile ready (tcgen05.commit)
       mbar_init(&b[2], 1);  // V tile landed (producer's expect_tx + TMA bytes)
@@ -998,7 +1005,7 @@ struct Tc5Engine {
     // K on the ring's full barrier, V on the slot's own barrier: S^T, the softmax and P
     // overlap the V transfer (full boxes; rows past the tensor are zero-filled)
     const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
-    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + 4096 + 512) + 2;
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + BAR_OFF) + 2;
     mbar_arrive_expect_tx(bar, KV_BYTES);
     mbar_arrive_expect_tx(vbar, KV_BYTES);
 #pragma unroll
@@ -1015,7 +1022,7 @@ struct Tc5Engine {
     const int br = a.box_rows;
     const int nb = (ntok + br - 1) / br;
     const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
-    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + 4096 + 512) + 2;
+    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + BAR_OFF) + 2;
     if (lane == 0) {
       mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * 2));
       mbar_arrive_expect_tx(vbar, uint32_t(nb * br * 128 * 2));
@@ -1033,19 +1040,18 @@ struct Tc5Engine {
     const int slot = slot_of_thread(), tid = (int(threadIdx.x >> 5) % WPS) * 32 + lane;
     unsigned char* qs = extra() + slot * XS;
     // Q^T operand, K-major 128-B swizzle: row r (q-row of the tile, zero past u.rows),
-    // dims 64 half .. 64 half + 63 in the 128-B line (half * 2048 + r * 128)
+    // dims 64 half .. 64 half + 63 in the 128-B line (half * QHS + r * 128)
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QR / 8; ++i) {
       const int c = tid + 128 * i, r = c >> 4, ch = c & 15, half = ch >> 3, cc = ch & 7;
       uint4 w = make_uint4(0u, 0u, 0u, 0u);
       if (r < u.rows) w = *reinterpret_cast<const uint4*>(static_cast<const T*>(a.q) + size_t(u.q_row + r) * D + 8 * ch);
-      *reinterpret_cast<uint4*>(qs + half * 2048 + r * 128 + ((cc ^ (r & 7)) << 4)) = w;
+      *reinterpret_cast<uint4*>(qs + half * QHS + r * 128 + ((cc ^ (r & 7)) << 4)) = w;
     }
 #pragma unroll
-    for (int h = 0; h < HEADS; ++h) {
-      s.l[h] = 0.f;
-      s.o[h] = 0.f;
-    }
+    for (int h = 0; h < HEADS; ++h) s.o[h] = 0.f;
+#pragma unroll
+    for (int h = 0; h < LN; ++h) s.l[h] = 0.f;
     if (tid < 2 * HEADS) reinterpret_cast<float*>(qs + MB_OFF)[tid] = -INFINITY;
     s.mpar = 0;
     s.lbase = a.causal ? u.len - u.nq + 1 : u.len;  // N_q > 1, causal: query i is token n - N_b + i
@@ -1059,8 +1065,8 @@ struct Tc5Engine {
                                                float scale_log2, int lane, int /*bs*/, uint32_t par, uint64_t* empty) {
     const int slot = slot_of_thread(), tid = sub * 32 + lane;
     unsigned char* xs = extra() + slot * XS;
-    float* red = reinterpret_cast<float*>(xs + 4096);  // [4][HEADS]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + 4096 + 512);
+    float* red = reinterpret_cast<float*>(xs + RED_OFF);  // [4][HEADS]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + BAR_OFF);
     const uint32_t tbase = *tmem_base_ptr() + uint32_t(COLS * slot);
     const uint32_t tlane = uint32_t(32 * sub) << 16;
     const uint32_t kaddr = smem_u32(st), vaddr = smem_u32(st + KV_BYTES), qaddr = smem_u32(xs);
@@ -1071,8 +1077,8 @@ struct Tc5Engine {
       for (int kk = 0; kk < D / 16; ++kk) {  // chain c = kk / (8 / SPLIT) accumulates in columns 16 c
         const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
         const int c = kk / (8 / SPLIT);
-        tc5::mma_f16(tbase + 16 * c, tc5::sdesc(kaddr + off, 16, 1024),
-                     tc5::sdesc(qaddr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024), IDESC_S, kk % (8 / SPLIT) > 0);
+        tc5::mma_f16(tbase + QR * c, tc5::sdesc(kaddr + off, 16, 1024),
+                     tc5::sdesc(qaddr + (kk >> 2) * QHS + (kk & 3) * 32, 16, 1024), IDESC_S, kk % (8 / SPLIT) > 0);
       }
       tc5::commit(&bars[0]);
     }
@@ -1087,13 +1093,18 @@ struct Tc5Engine {
     }
     mbar_wait(&bars[0], par);
     tc5::fence_after();
-    float sc[16];
-    tc5::ld16(tbase + tlane, sc);
-    if (SPLIT == 2) {
-      float s2[16];
-      tc5::ld16(tbase + tlane + 16, s2);
+    float sc[QR];
 #pragma unroll
-      for (int h = 0; h < HEADS; ++h) sc[h] += s2[h];
+    for (int c = 0; c < QR; c += 16) {
+      float t16[16];
+      tc5::ld16(tbase + tlane + c, t16);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sc[c + i] = t16[i];
+      if (SPLIT == 2) {
+        tc5::ld16(tbase + tlane + QR + c, t16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sc[c + i] += t16[i];
+      }
     }
     // ---- scale, mask (C5, causal), running max per row (Alg1§21) ----------------------------
     float mx[HEADS];
@@ -1134,11 +1145,25 @@ struct Tc5Engine {
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) {
       const float p = ex2_sub(sc[h], mn[h]);
-      s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23: e^{m - m_new} l + rowsum
+      if constexpr (HEADS < 32) s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23
+      else sc[h] = p;  // summed below
       const T hi = to_kv<T>(p);
       const T lo = to_kv<T>(p - kv_to_f(hi));
       *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ (h & 7)) << 4) + pe) = hi;
       *reinterpret_cast<T*>(pb + (h + HEADS) * 128 + ((pc ^ (h & 7)) << 4) + pe) = lo;
+    }
+    if constexpr (HEADS == 32) {  // Alg1§23 for 32 rows: XOR transpose-butterfly of the 32 p's
+      // (31 shuffles) leaves the warp's sum of row `lane` in sc[0] of lane `lane`
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int j = 0; j < off; ++j) {
+          const float keep = up ? sc[j + off] : sc[j], send = up ? sc[j] : sc[j + off];
+          sc[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      s.l[0] = fmaf(ex2_sub(lds_f32(mcur + 4 * lane), lds_f32(mnext + 4 * lane)), s.l[0], sc[0]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (+ zeroed V) -> tensor core
     tc5::fence_before();                                           // S loads done before reuse
@@ -1191,15 +1216,20 @@ struct Tc5Engine {
 
   __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
     const int slot = warp / WPS, sub = warp % WPS;
-    float* red2 = reinterpret_cast<float*>(extra() + slot * XS + 4096 + 256);  // [4][HEADS]
+    float* red2 = reinterpret_cast<float*>(extra() + slot * XS + RED2_OFF);  // [4][HEADS]
     float* fb = fold + slot * HEADS * (D + 2);                                  // [row][D + 2]
 #pragma unroll
-    for (int h = 0; h < HEADS; ++h) {
-      fb[h * (D + 2) + 32 * sub + lane] = s.o[h];
-      float l = s.l[h];
+    for (int h = 0; h < HEADS; ++h) fb[h * (D + 2) + 32 * sub + lane] = s.o[h];
+    if constexpr (HEADS == 32) {
+      red2[sub * HEADS + lane] = s.l[0];  // lane = row
+    } else {
 #pragma unroll
-      for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-      if (lane == h) red2[sub * HEADS + h] = l;
+      for (int h = 0; h < HEADS; ++h) {
+        float l = s.l[h];
+#pragma unroll
+        for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+        if (lane == h) red2[sub * HEADS + h] = l;
+      }
     }
     // read m before the barrier: past it, the next segment's seg_begin resets mb
     const float mv = lane < HEADS ? reinterpret_cast<const float*>(extra() + slot * XS + MB_OFF)[HEADS * s.mpar + lane]
@@ -1921,12 +1951,15 @@ bool make_tmap(CUtensorMap* tm, const void* base, int64_t rows, int d, int dtype
 
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine) {
   if (engine == LA_ENGINE_TCGEN05) {  // 5th-gen tensor cores (bf16 / fp16, d = 128, T_m <= 8, not paged)
-    if (head_dim != 128 || group > 16) return KernelInfo{};
+    if (head_dim != 128 || group > 32) return KernelInfo{};
     if (dtype == LA_BF16)
-      return group <= 8 ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 8>>(true)
-                        : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 16>>(true);
+      return group <= 8    ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 8>>(true)
+             : group <= 16 ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 16>>(true)
+                           : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 32>>(true);
     if (dtype == LA_FP16)
-      return group <= 8 ? info_of<Tc5Engine<__half, LA_TC5_NST, 8>>(true) : info_of<Tc5Engine<__half, LA_TC5_NST, 16>>(true);
+      return group <= 8    ? info_of<Tc5Engine<__half, LA_TC5_NST, 8>>(true)
+             : group <= 16 ? info_of<Tc5Engine<__half, LA_TC5_NST, 16>>(true)
+                           : info_of<Tc5Engine<__half, LA_TC5_NST, 32>>(true);
     return KernelInfo{};
   }
   if (dtype == LA_FP8_E4M3) {  // one tensor-core engine for every T_m <= 8 (MHA included)

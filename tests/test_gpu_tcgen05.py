@@ -98,18 +98,20 @@ def test_tcgen05_c3_full_size_sampled():
 
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("heads_q,heads_kv,q_len,causal", [(32, 2, 1, True), (16, 1, 1, True), (24, 2, 1, True),
-                                                           (16, 2, 2, True), (16, 2, 2, False), (8, 1, 3, True)])
+                                                           (16, 2, 2, True), (16, 2, 2, False), (8, 1, 3, True),
+                                                           (32, 1, 1, True), (16, 2, 4, True), (24, 1, 2, True),
+                                                           (40, 2, 1, True), (16, 2, 4, False)])
 def test_tcgen05_wide_tiles(dtype, heads_q, heads_kv, q_len, causal):
-    """16-row query tiles (the tcgen05 engine's N = 16): g * N_q rows of a KV head in ONE
-    pass where mma.sync tiles take two (g = 16, MQA 16, g = 12 -> 16 + 8 rows, g = 8 x N_q 2,
-    g = 8 x N_q 3 -> 16 + 8)."""
+    """16- and 32-row query tiles (the tcgen05 engine's N = 16 / 32): g * N_q rows of a KV head
+    in ONE pass where mma.sync tiles take two to four (g = 16, MQA 16 / 32, g = 12, g = 20,
+    g = 8 x N_q 2 / 3 / 4, g = 24 x N_q 2 -> 32 + 16 rows)."""
     p = synth.Problem(2, heads_q, heads_kv, 128, [1000, 333], dtype=dtype, dist="D2", seed=71, q_len=q_len)
     O_ref, L_ref = run_oracle(p, causal=causal)
     inputs = cuda_inputs(p)
     for schedule in ("streamk", "sequential"):
         for tile_n, grid in ((128, 5), (256, 0)):
             O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule, causal=causal, **TC5)
-            assert plan.info.tile_rows == min(16, p.group * q_len)
+            assert plan.info.tile_rows == min(32, p.group * q_len)
             gate(O, L, O_ref, L_ref, what=f"tc5 wide H{heads_q}/{heads_kv} Nq{q_len} {dtype} {schedule} G{grid}")
 
 
@@ -149,7 +151,7 @@ def test_tcgen05_wide_c3_speculative_full_size():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("rows", [8, 16])
+@pytest.mark.parametrize("rows", [8, 16, 32])
 @pytest.mark.parametrize("page_size", [16, 32, 64, 128, 256])
 def test_tcgen05_paged(rows, page_size):
     """Paged pools on the tcgen05 engine: per-half TMA boxes of min(128, page) rows inside one
@@ -165,7 +167,7 @@ def test_tcgen05_paged(rows, page_size):
             gate(O, L, O_ref, L_ref, what=f"tc5 paged rows{rows} ps{page_size} T{tile_n} G{grid} {schedule}")
 
 
-@pytest.mark.parametrize("rows_per_head", [8, 16])
+@pytest.mark.parametrize("rows_per_head", [8, 16, 32])
 def test_tcgen05_tiny_contexts(rows_per_head):
     """Contexts of 1..129 tokens (one short stage, a stage plus one token) and N_q = 2 blocks
     whose causal limits cut inside the only stage."""

@@ -45,21 +45,21 @@ def test_large_groups_mqa(hq, hkv, d, engine):
     (g > 8 was unsupported); "auto" takes the tcgen05 engine's 16-row tiles (C_m = 1) at d = 128."""
     p = synth.Problem(2, hq, hkv, d, [1500, 2777], dtype="bf16", dist="D2", seed=81)
     O, L, plan = _cuda(p, engine=engine)
-    tm = 16 if engine == "auto" and d == 128 else 8
+    tm = 32 if engine == "auto" and d == 128 else 8
     g = hq // hkv
     assert plan.info.tile_rows == min(tm, g) and plan.info.num_units == 2 * hkv * -(-g // tm)
-    assert plan.info.engine == (1 if tm == 16 else 0)
+    assert plan.info.engine == (1 if tm == 32 else 0)
     gate(O, L, *_oracle(p), what=f"g={g} {engine}")
 
 
 @pytest.mark.parametrize("engine", ["mma", "auto"])
 @pytest.mark.parametrize("causal", [True, False])
 def test_query_tiles_multi_token(causal, engine):
-    """g = 8 x N_q = 3 = 24 rows -> 3 tiles of 8 (mma.sync) or 16 + 8 (tcgen05 via "auto"); the
-    causal limit follows the row's query index."""
+    """g = 8 x N_q = 3 = 24 rows -> 3 tiles of 8 (mma.sync) or one of 24 (tcgen05 via "auto");
+    the causal limit follows the row's query index."""
     p = synth.Problem(2, 16, 2, 128, [900, 2000], dtype="bf16", dist="D1", seed=82, q_len=3)
     O, L, plan = _cuda(p, causal=causal, engine=engine)
-    assert plan.info.num_units == 2 * 2 * (3 if engine == "mma" else 2)
+    assert plan.info.num_units == 2 * 2 * (3 if engine == "mma" else 1)
     gate(O, L, *_oracle(p, causal), what=f"tiles causal={causal} {engine}")
 
 

@@ -249,7 +249,7 @@ def test_query_tiles_and_heterogeneous_batches_bit_exact(la):
         engine = ["mma", "tcgen05", "auto"][(trial // 2) % 3]
         p = la.Plan(batch, hkv * g, hkv, 128, lens, tile_n=tile, grid=int(rng.integers(1, 300)), layout=layout,
                     host_only=True, schedule="streamk", q_lens=qls, engine=engine)
-        tm = min(8 if engine == "mma" else 16, max(g * n for n in qls))
+        tm = min(8 if engine == "mma" else 32, max(g * n for n in qls))
         c_n = []
         for (b, _h) in unit_order(batch, hkv, layout):
             c_n += [-(-lens[b] // tile)] * (-(-(g * qls[b]) // tm))
