@@ -928,6 +928,12 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ T to_kv(float x);
 template <>
@@ -970,7 +976,7 @@ struct Tc5Engine {
   static constexpr int XS = (MB_OFF + 8 * HEADS + 1023) / 1024 * 1024;
   static constexpr int EXTRA_BYTES = NST * XS + 1024;  // + the TMEM base address
   static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, QR, false, false);
-  static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, false);
+  static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, HEADS == 32);
 
   struct State {
     float l[LN];               // HEADS <= 16: this token lane's share of every row's running sum;
@@ -1128,10 +1134,14 @@ struct Tc5Engine {
     const uint32_t mcur = smem_u32(xs + MB_OFF) + 4 * HEADS * s.mpar, mnext = smem_u32(xs + MB_OFF) + 4 * HEADS * (s.mpar ^ 1);
     float mn[HEADS];
 #pragma unroll
-    for (int h = 0; h < HEADS; ++h) {  // m_new = max(m, tile max) (Alg1§21)
+    for (int h = 0; h < HEADS; h += 4) {  // m_new = max(m, tile max) (Alg1§21), 4 rows per vector load
       const uint32_t ra = smem_u32(red) + 4 * h;
-      const float t = fmaxf(fmaxf(lds_f32(ra), lds_f32(ra + 4 * HEADS)), fmaxf(lds_f32(ra + 8 * HEADS), lds_f32(ra + 12 * HEADS)));
-      mn[h] = fmaxf(lds_f32(mcur + 4 * h), t);
+      const float4 w0 = lds_f32x4(ra), w1 = lds_f32x4(ra + 4 * HEADS), w2 = lds_f32x4(ra + 8 * HEADS),
+                   w3 = lds_f32x4(ra + 12 * HEADS), mo = lds_f32x4(mcur + 4 * h);
+      mn[h] = fmaxf(mo.x, fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x)));
+      mn[h + 1] = fmaxf(mo.y, fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y)));
+      mn[h + 2] = fmaxf(mo.z, fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z)));
+      mn[h + 3] = fmaxf(mo.w, fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w)));
     }
     if (tid < HEADS) {
       float v = mn[0];
@@ -1140,17 +1150,36 @@ struct Tc5Engine {
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(mnext + 4 * tid), "f"(v) : "memory");
     }
     // ---- P_f = exp(S_f - m) (Alg1§22) into the dead K tile as the PV B operand ---------------
-    unsigned char* pb = st + (tid >> 6) * PHS;  // [token half][2 HEADS rows][128 B]
-    const int pc = (tid & 63) >> 3, pe = (tid & 7) * 2;
+    if constexpr (HEADS < 32) {  // P^T K-major: [token half][2 HEADS rows][128 B], one 2-B store per value
+      unsigned char* pb = st + (tid >> 6) * PHS;
+      const int pc = (tid & 63) >> 3, pe = (tid & 7) * 2;
 #pragma unroll
-    for (int h = 0; h < HEADS; ++h) {
-      const float p = ex2_sub(sc[h], mn[h]);
-      if constexpr (HEADS < 32) s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23
-      else sc[h] = p;  // summed below
-      const T hi = to_kv<T>(p);
-      const T lo = to_kv<T>(p - kv_to_f(hi));
-      *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ (h & 7)) << 4) + pe) = hi;
-      *reinterpret_cast<T*>(pb + (h + HEADS) * 128 + ((pc ^ (h & 7)) << 4) + pe) = lo;
+      for (int h = 0; h < HEADS; ++h) {
+        const float p = ex2_sub(sc[h], mn[h]);
+        s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23
+        const T hi = to_kv<T>(p);
+        const T lo = to_kv<T>(p - kv_to_f(hi));
+        *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ (h & 7)) << 4) + pe) = hi;
+        *reinterpret_cast<T*>(pb + (h + HEADS) * 128 + ((pc ^ (h & 7)) << 4) + pe) = lo;
+      }
+    } else {  // 32 rows: P^T MN-major, token t's 64 columns (P_hi rows, then P_lo rows) in one
+              // 128-B swizzled line -> eight 16-B stores per thread (scripts/tc5_probe.cu checks it)
+#pragma unroll
+      for (int h = 0; h < HEADS; ++h) sc[h] = ex2_sub(sc[h], mn[h]);
+      unsigned char* pl = st + tid * 128;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = sc[8 * j + 2 * e], p1 = sc[8 * j + 2 * e + 1];
+          hw[e] = Mma<T>::pack(p0, p1);
+          const float2 r = Mma<T>::unpack(hw[e]);
+          lw[e] = Mma<T>::pack(p0 - r.x, p1 - r.y);
+        }
+        *reinterpret_cast<uint4*>(pl + ((j ^ (tid & 7)) << 4)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(pl + (((j + 4) ^ (tid & 7)) << 4)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
     }
     if constexpr (HEADS == 32) {  // Alg1§23 for 32 rows: XOR transpose-butterfly of the 32 p's
       // (31 shuffles) leaves the warp's sum of row `lane` in sc[0] of lane `lane`
@@ -1163,7 +1192,13 @@ struct Tc5Engine {
           sc[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
         }
       }
-      s.l[0] = fmaf(ex2_sub(lds_f32(mcur + 4 * lane), lds_f32(mnext + 4 * lane)), s.l[0], sc[0]);
+      // m_new of row `lane` recomputed from red (complete since the first barrier; mnext is
+      // only complete after the second)
+      const uint32_t rl = smem_u32(red) + 4 * lane;
+      const float mo = lds_f32(mcur + 4 * lane);
+      const float mrow = fmaxf(mo, fmaxf(fmaxf(lds_f32(rl), lds_f32(rl + 4 * HEADS)),
+                                         fmaxf(lds_f32(rl + 8 * HEADS), lds_f32(rl + 12 * HEADS))));
+      s.l[0] = fmaf(ex2_sub(mo, mrow), s.l[0], sc[0]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (+ zeroed V) -> tensor core
     tc5::fence_before();                                           // S loads done before reuse
@@ -1175,7 +1210,9 @@ struct Tc5Engine {
 #pragma unroll
       for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
         tc5::mma_f16(tbase + OC + NO * (kk / (8 / SPLIT)), tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
-                     tc5::sdesc(kaddr + (kk >> 2) * PHS + (kk & 3) * 32, 16, 1024), IDESC_O, kk % (8 / SPLIT) > 0);
+                     HEADS == 32 ? tc5::sdesc(kaddr + kk * 2048, 8192, 1024)  // MN-major P^T: 16 token lines
+                                 : tc5::sdesc(kaddr + (kk >> 2) * PHS + (kk & 3) * 32, 16, 1024),
+                     IDESC_O, kk % (8 / SPLIT) > 0);
       tc5::commit(empty);     // the slot is free the moment the tensor core is done with it
       tc5::commit(&bars[1]);
     } else if (sub != 0 && lane == 0) {
