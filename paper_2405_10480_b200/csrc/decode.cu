@@ -914,7 +914,7 @@ struct Fp8Engine {
 //   thread t <- token t's 8 scores    tcgen05.ld 32x32b; mask (C5, causal), per-row max over
 //                                     the warp (shuffles) and the warpgroup (smem, bar.sync)
 //   P^T[16][128 tok] (bf16 / fp16)    rows 0-7 P_hi, rows 8-15 P_lo = p - P_hi (reading C18),
-//                                     written K-major SW128 over the stage's dead K tile
+//                                     written MN-major SW128 over the stage's dead K tile
 //   O^T[128 dim][16] = V_f^T P_f^T    tcgen05.mma M=128 N=16, A = V read MN-major from the
 //                                     same TMA box (no transpose pass), B = P
 //   thread t <- dim t's 16 columns    O_t[h] = alpha_h O_t[h] + O^T[t][h] + O^T[t][8 + h]
@@ -957,7 +957,6 @@ struct Tc5Engine {
   static constexpr int QHS = QR * 128;               // Q^T dim-half stride
   static constexpr int LN = HEADS == 32 ? 1 : HEADS;  // running-sum registers per thread
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
-  static constexpr int PHS = NO * 128;              // P^T token-half stride [2 HEADS rows][128 B]
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
   static constexpr int FOLD_FLOATS = NST * HEADS * (D + 2);
   static constexpr int FOLD_BUFS = 1;
@@ -976,7 +975,7 @@ struct Tc5Engine {
   static constexpr int XS = (MB_OFF + 8 * HEADS + 1023) / 1024 * 1024;
   static constexpr int EXTRA_BYTES = NST * XS + 1024;  // + the TMEM base address
   static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, QR, false, false);
-  static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, HEADS == 32);
+  static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, true);
 
   struct State {
     float l[LN];               // HEADS <= 16: this token lane's share of every row's running sum;
@@ -1150,25 +1149,19 @@ struct Tc5Engine {
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(mnext + 4 * tid), "f"(v) : "memory");
     }
     // ---- P_f = exp(S_f - m) (Alg1§22) into the dead K tile as the PV B operand ---------------
-    if constexpr (HEADS < 32) {  // P^T K-major: [token half][2 HEADS rows][128 B], one 2-B store per value
-      unsigned char* pb = st + (tid >> 6) * PHS;
-      const int pc = (tid & 63) >> 3, pe = (tid & 7) * 2;
+    // P^T MN-major: token t's 2 HEADS columns (P_hi rows, then P_lo rows) in one 128-B swizzled
+    // line over the dead K tile -> 2 HEADS / 8 16-B stores per thread (the B-operand layout
+    // scripts/tc5_probe.cu checks exactly)
 #pragma unroll
-      for (int h = 0; h < HEADS; ++h) {
-        const float p = ex2_sub(sc[h], mn[h]);
-        s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23
-        const T hi = to_kv<T>(p);
-        const T lo = to_kv<T>(p - kv_to_f(hi));
-        *reinterpret_cast<T*>(pb + h * 128 + ((pc ^ (h & 7)) << 4) + pe) = hi;
-        *reinterpret_cast<T*>(pb + (h + HEADS) * 128 + ((pc ^ (h & 7)) << 4) + pe) = lo;
-      }
-    } else {  // 32 rows: P^T MN-major, token t's 64 columns (P_hi rows, then P_lo rows) in one
-              // 128-B swizzled line -> eight 16-B stores per thread (scripts/tc5_probe.cu checks it)
-#pragma unroll
-      for (int h = 0; h < HEADS; ++h) sc[h] = ex2_sub(sc[h], mn[h]);
+    for (int h = 0; h < HEADS; ++h) {
+      const float p = ex2_sub(sc[h], mn[h]);
+      if constexpr (HEADS < 32) s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23
+      sc[h] = p;
+    }
+    {
       unsigned char* pl = st + tid * 128;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < HEADS / 8; ++j) {
         uint32_t hw[4], lw[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -1178,7 +1171,7 @@ struct Tc5Engine {
           lw[e] = Mma<T>::pack(p0 - r.x, p1 - r.y);
         }
         *reinterpret_cast<uint4*>(pl + ((j ^ (tid & 7)) << 4)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(pl + (((j + 4) ^ (tid & 7)) << 4)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        *reinterpret_cast<uint4*>(pl + (((HEADS / 8 + j) ^ (tid & 7)) << 4)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
     }
     if constexpr (HEADS == 32) {  // Alg1§23 for 32 rows: XOR transpose-butterfly of the 32 p's
@@ -1210,8 +1203,7 @@ struct Tc5Engine {
 #pragma unroll
       for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
         tc5::mma_f16(tbase + OC + NO * (kk / (8 / SPLIT)), tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
-                     HEADS == 32 ? tc5::sdesc(kaddr + kk * 2048, 8192, 1024)  // MN-major P^T: 16 token lines
-                                 : tc5::sdesc(kaddr + (kk >> 2) * PHS + (kk & 3) * 32, 16, 1024),
+                     tc5::sdesc(kaddr + kk * 2048, 8192, 1024),  // MN-major P^T: 16 token lines per k-step
                      IDESC_O, kk % (8 / SPLIT) > 0);
       tc5::commit(empty);     // the slot is free the moment the tensor core is done with it
       tc5::commit(&bars[1]);
