@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", f) for f in ("decode.cu", "api.cpp", "planner.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("la_internal.h", "ptx.cuh")] + [os.path.join(ROOT, "include", "la.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("la_internal.h", "ptx.cuh", "tc5.cuh")] + [os.path.join(ROOT, "include", "la.h")]
 OUT = os.path.join(HERE, "lib", "libleanattn.so")
 
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
