@@ -90,6 +90,9 @@
 #ifndef LA_TC5_NST
 #define LA_TC5_NST 3   // tcgen05 engine: ring stages of 64 KiB (128 tokens), one warpgroup each
 #endif
+#ifndef LA_TC5_NST32
+#define LA_TC5_NST32 3  // the same for 32-row query tiles
+#endif
 #ifndef LA_TC5_BOXH
 #define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
 #endif
@@ -972,7 +975,8 @@ struct Tc5Engine {
   // per-slot extra: Q^T [2][QR][128 B], red [4][HEADS], red2 [4][HEADS], 3 barriers, mb [2][HEADS]
   static constexpr int RED_OFF = 2 * QHS, RED2_OFF = RED_OFF + 16 * HEADS, BAR_OFF = RED2_OFF + 16 * HEADS;
   static constexpr int MB_OFF = BAR_OFF + 32;
-  static constexpr int XS = (MB_OFF + 8 * HEADS + 1023) / 1024 * 1024;
+  static constexpr int AL_OFF = MB_OFF + 8 * HEADS;  // alpha_h = e^{m - m_new} of the current stage [HEADS]
+  static constexpr int XS = (AL_OFF + 4 * HEADS + 1023) / 1024 * 1024;
   static constexpr int EXTRA_BYTES = NST * XS + 1024;  // + the TMEM base address
   static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, QR, false, false);
   static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, true);
@@ -1131,33 +1135,36 @@ struct Tc5Engine {
     }
     wg_bar(slot);
     const uint32_t mcur = smem_u32(xs + MB_OFF) + 4 * HEADS * s.mpar, mnext = smem_u32(xs + MB_OFF) + 4 * HEADS * (s.mpar ^ 1);
-    float mn[HEADS];
+    const uint32_t alp = smem_u32(xs + AL_OFF);
+    if (tid < HEADS) {  // row tid: m_new (Alg1§21) and alpha = e^{m - m_new} for every thread's O update
+      const uint32_t rl = smem_u32(red) + 4 * tid;
+      const float mo = lds_f32(mcur + 4 * tid);
+      const float mrow = fmaxf(mo, fmaxf(fmaxf(lds_f32(rl), lds_f32(rl + 4 * HEADS)),
+                                         fmaxf(lds_f32(rl + 8 * HEADS), lds_f32(rl + 12 * HEADS))));
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(mnext + 4 * tid), "f"(mrow) : "memory");
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(alp + 4 * tid), "f"(ex2_sub(mo, mrow)) : "memory");
+    }
+    // ---- P_f = exp(S_f - m_new) (Alg1§22), m_new 4 rows at a time (no per-row register array) --
 #pragma unroll
-    for (int h = 0; h < HEADS; h += 4) {  // m_new = max(m, tile max) (Alg1§21), 4 rows per vector load
+    for (int h = 0; h < HEADS; h += 4) {
       const uint32_t ra = smem_u32(red) + 4 * h;
       const float4 w0 = lds_f32x4(ra), w1 = lds_f32x4(ra + 4 * HEADS), w2 = lds_f32x4(ra + 8 * HEADS),
                    w3 = lds_f32x4(ra + 12 * HEADS), mo = lds_f32x4(mcur + 4 * h);
-      mn[h] = fmaxf(mo.x, fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x)));
-      mn[h + 1] = fmaxf(mo.y, fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y)));
-      mn[h + 2] = fmaxf(mo.z, fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z)));
-      mn[h + 3] = fmaxf(mo.w, fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w)));
-    }
-    if (tid < HEADS) {
-      float v = mn[0];
+      const float mo4[4] = {mo.x, mo.y, mo.z, mo.w};
+      const float mn4[4] = {fmaxf(mo.x, fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x))),
+                            fmaxf(mo.y, fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y))),
+                            fmaxf(mo.z, fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z))),
+                            fmaxf(mo.w, fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w)))};
 #pragma unroll
-      for (int h = 1; h < HEADS; ++h) v = tid == h ? mn[h] : v;
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(mnext + 4 * tid), "f"(v) : "memory");
+      for (int e = 0; e < 4; ++e) {
+        const float p = ex2_sub(sc[h + e], mn4[e]);
+        if constexpr (HEADS < 32) s.l[h + e] = fmaf(ex2_sub(mo4[e], mn4[e]), s.l[h + e], p);  // Alg1§23
+        sc[h + e] = p;
+      }
     }
-    // ---- P_f = exp(S_f - m) (Alg1§22) into the dead K tile as the PV B operand ---------------
     // P^T MN-major: token t's 2 HEADS columns (P_hi rows, then P_lo rows) in one 128-B swizzled
     // line over the dead K tile -> 2 HEADS / 8 16-B stores per thread (the B-operand layout
     // scripts/tc5_probe.cu checks exactly)
-#pragma unroll
-    for (int h = 0; h < HEADS; ++h) {
-      const float p = ex2_sub(sc[h], mn[h]);
-      if constexpr (HEADS < 32) s.l[h] = fmaf(ex2_sub(lds_f32(mcur + 4 * h), mn[h]), s.l[h], p);  // Alg1§23
-      sc[h] = p;
-    }
     {
       unsigned char* pl = st + tid * 128;
 #pragma unroll
@@ -1212,9 +1219,7 @@ struct Tc5Engine {
     }
     mbar_wait(&bars[1], par);
     tc5::fence_after();
-    float al[HEADS];  // e^{m - m_new} again from the two shared copies (no registers held across the MMA)
-#pragma unroll
-    for (int h = 0; h < HEADS; ++h) al[h] = ex2_sub(lds_f32(mcur + 4 * h), lds_f32(mnext + 4 * h));
+    // alpha from shared memory, 8 rows at a time (no registers held across the MMA)
     // O^T tile: column h = V^T P_hi row h, column HEADS + h = V^T P_lo row h (per chain)
 #pragma unroll
     for (int c0 = 0; c0 < HEADS; c0 += 8) {  // 8 rows at a time: hi columns c0.., lo columns HEADS + c0..
@@ -1236,8 +1241,10 @@ struct Tc5Engine {
           tc5::ld8(tbase + tlane + OC + NO * ch + HEADS + c0, lv, ch > 0);
         }
       }
+      const float4 a0 = lds_f32x4(alp + 4 * c0), a1 = lds_f32x4(alp + 4 * c0 + 16);
+      const float al[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s.o[c0 + i] = fmaf(al[c0 + i], s.o[c0 + i], hv[i] + lv[i]);  // Alg1§25
+      for (int i = 0; i < 8; ++i) s.o[c0 + i] = fmaf(al[i], s.o[c0 + i], hv[i] + lv[i]);  // Alg1§25
     }
     tc5::fence_before();
     s.mpar ^= 1;
@@ -1984,11 +1991,11 @@ KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine) {
     if (dtype == LA_BF16)
       return group <= 8    ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 8>>(true)
              : group <= 16 ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 16>>(true)
-                           : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 32>>(true);
+                           : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST32, 32>>(true);
     if (dtype == LA_FP16)
       return group <= 8    ? info_of<Tc5Engine<__half, LA_TC5_NST, 8>>(true)
              : group <= 16 ? info_of<Tc5Engine<__half, LA_TC5_NST, 16>>(true)
-                           : info_of<Tc5Engine<__half, LA_TC5_NST, 32>>(true);
+                           : info_of<Tc5Engine<__half, LA_TC5_NST32, 32>>(true);
     return KernelInfo{};
   }
   if (dtype == LA_FP8_E4M3) {  // one tensor-core engine for every T_m <= 8 (MHA included)
