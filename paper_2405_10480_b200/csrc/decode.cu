@@ -1117,22 +1117,27 @@ struct Tc5Engine {
     }
     // ---- scale, mask (C5, causal), running max per row (Alg1§21) ----------------------------
     float mx[HEADS];
+    if (tid < ntok && tok0 + STAGE_TOK <= s.lbase) {  // the common stage: no key of it is masked
 #pragma unroll
-    for (int h = 0; h < HEADS; ++h) {
-      // only a stage reaching past the smallest limit needs the per-row causal test
-      const bool ok = tid < ntok && (tok0 + STAGE_TOK <= s.lbase || tok0 + tid < s.lbase + (s.r0 + h) % s.nq);
-      sc[h] = ok ? sc[h] * scale_log2 : -INFINITY;
-      mx[h] = sc[h];
+      for (int h = 0; h < HEADS; ++h) mx[h] = sc[h] = sc[h] * scale_log2;
+    } else {  // the stage reaches past the smallest causal limit (or the context end): per-row test,
+              // row h's limit lbase + (r0 + h) mod nq stepped without a division per row
+      const int t = tok0 + tid;
+      int r = s.r0 % s.nq;
+#pragma unroll
+      for (int h = 0; h < HEADS; ++h) {
+        const bool ok = tid < ntok && t < s.lbase + r;
+        mx[h] = sc[h] = ok ? sc[h] * scale_log2 : -INFINITY;
+        r = r + 1 == s.nq ? 0 : r + 1;
+      }
     }
 #pragma unroll
     for (int h = 0; h < HEADS; ++h)  // warp max: one CREDUX per row (sm_100a f32 redux)
       asm volatile("redux.sync.max.f32 %0, %0, 0xffffffff;" : "+f"(mx[h]));
-    if (lane < HEADS) {
-      float v = mx[0];
+    if (lane == 0)  // every lane holds every row's warp max: one lane stores them, 16 B at a time
 #pragma unroll
-      for (int h = 1; h < HEADS; ++h) v = lane == h ? mx[h] : v;
-      red[sub * HEADS + lane] = v;
-    }
+      for (int h = 0; h < HEADS; h += 4)
+        *reinterpret_cast<float4*>(red + sub * HEADS + h) = make_float4(mx[h], mx[h + 1], mx[h + 2], mx[h + 3]);
     wg_bar(slot);
     const uint32_t mcur = smem_u32(xs + MB_OFF) + 4 * HEADS * s.mpar, mnext = smem_u32(xs + MB_OFF) + 4 * HEADS * (s.mpar ^ 1);
     const uint32_t alp = smem_u32(xs + AL_OFF);
