@@ -93,6 +93,12 @@
 #ifndef LA_TC5_NST32
 #define LA_TC5_NST32 3  // the same for 32-row query tiles
 #endif
+#ifndef LA_TC5_NWG32
+#define LA_TC5_NWG32 2  // warpgroups for 32-row tiles (< NST32: the ring prefetches past the warpgroups)
+#endif
+#ifndef LA_TC5_NWG16
+#define LA_TC5_NWG16 LA_TC5_NST  // the same for 16-row tiles
+#endif
 #ifndef LA_TC5_BOXH
 #define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
 #endif
@@ -267,7 +273,7 @@ struct PageWin {
 // =======================================================================================
 template <typename T, int D_, int NST_, int WPS_>
 struct MhaEngine {
-  static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
+  static constexpr int D = D_, NST = NST_, WPS = WPS_, NWG = NST, NCW = NWG * WPS;  // NWG: consumer warp sets
   static constexpr int ROWB = D * int(sizeof(T));          // bytes of one K (or V) row
   static constexpr int LPK = ROWB / 16;                     // lanes per key
   static constexpr int EPL = 16 / int(sizeof(T));           // elements per 16-byte chunk
@@ -473,7 +479,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 
 template <typename T, int D_, int NST_, int WPS_>
 struct GqaEngine {
-  static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
+  static constexpr int D = D_, NST = NST_, WPS = WPS_, NWG = NST, NCW = NWG * WPS;  // NWG: consumer warp sets
   static constexpr int STAGE_TOK = 64;            // = TMA box rows
   static constexpr int NBOX = D / 64;             // 64-element (128-B) boxes per row
   static constexpr int BOX_BYTES = STAGE_TOK * 128;
@@ -715,7 +721,7 @@ __device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t sel) {
 // which frees shared memory for a deeper ring.
 template <int D_, int NST_, int WPS_, int ROWS_>
 struct Fp8Engine {
-  static constexpr int D = D_, NST = NST_, WPS = WPS_, NCW = NST * WPS;
+  static constexpr int D = D_, NST = NST_, WPS = WPS_, NWG = NST, NCW = NWG * WPS;  // NWG: consumer warp sets
   static_assert(ROWS_ == 1 || ROWS_ == 8, "fold rows");
   static_assert(D == 128, "an E4M3 row of d = 128 is exactly one 128-B swizzle span");
   static constexpr int STAGE_TOK = 128;           // = TMA box rows (32 KiB of K+V per stage)
@@ -946,9 +952,12 @@ __device__ __forceinline__ __half to_kv<__half>(float x) { return __float2half_r
 __device__ __forceinline__ float kv_to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
 __device__ __forceinline__ float kv_to_f(__half x) { return __half2float(x); }
 
-template <typename T, int NST_, int HEADS_>
+template <typename T, int NST_, int HEADS_, int NWG_ = NST_>
 struct Tc5Engine {
-  static constexpr int D = 128, NST = NST_, WPS = 4, NCW = NST * WPS;
+  // NST ring slots of 128 tokens; NWG warpgroups take the stages round-robin (NWG < NST: a
+  // warpgroup's next tile is already in flight while it computes)
+  static constexpr int D = 128, NST = NST_, WPS = 4, NWG = NWG_, NCW = NWG * WPS;
+  static_assert(NWG <= NST && NST <= 8, "ring");
   static constexpr int STAGE_TOK = 128;             // = TMA box rows = MMA M
   static constexpr int BOX_HALVES = LA_TC5_BOXH;    // 128-B row halves per TMA box (16 or 32 KiB boxes)
   static constexpr int KV_BYTES = 2 * STAGE_TOK * 128;  // [half][128 rows][128 B]
@@ -961,15 +970,15 @@ struct Tc5Engine {
   static constexpr int LN = HEADS == 32 ? 1 : HEADS;  // running-sum registers per thread
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
-  static constexpr int FOLD_FLOATS = NST * HEADS * (D + 2);
+  static constexpr int FOLD_FLOATS = NWG * HEADS * (D + 2);
   static constexpr int FOLD_BUFS = 1;
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
   static constexpr int SPLIT = LA_TC5_SPLIT;        // accumulator chains per contraction (1 or 2)
   static constexpr int OC = QR * SPLIT;             // first O^T column of a slot (S^T chains before it)
   static constexpr int COLS = (OC + NO * SPLIT) <= 32 ? 32 : (OC + NO * SPLIT) <= 64 ? 64 : 128;  // per slot
-  static_assert(NST * COLS <= 512, "TMEM columns");
-  static constexpr int TMEM_COLS = NST * COLS <= 32 ? 32 : NST * COLS <= 64 ? 64 : NST * COLS <= 128 ? 128 : 256;
+  static_assert(NWG * COLS <= 512, "TMEM columns");
+  static constexpr int TMEM_COLS = NWG * COLS <= 32 ? 32 : NWG * COLS <= 64 ? 64 : NWG * COLS <= 128 ? 128 : NWG * COLS <= 256 ? 256 : 512;
   // extra smem per slot: Q^T operand [half][16 rows][128 B] (4 KiB, 1024-aligned), the
   // warpgroup's max exchange red[4][8] + l exchange red2[4][8], two MMA-completion barriers
   // per-slot extra: Q^T [2][QR][128 B], red [4][HEADS], red2 [4][HEADS], 3 barriers, mb [2][HEADS]
@@ -977,7 +986,7 @@ struct Tc5Engine {
   static constexpr int MB_OFF = BAR_OFF + 32;
   static constexpr int AL_OFF = MB_OFF + 8 * HEADS;  // alpha_h = e^{m - m_new} of the current stage [HEADS]
   static constexpr int XS = (AL_OFF + 4 * HEADS + 1023) / 1024 * 1024;
-  static constexpr int EXTRA_BYTES = NST * XS + 1024;  // + the TMEM base address
+  static constexpr int EXTRA_BYTES = NWG * XS + 1024;  // + the ring slots' V barriers [NST] and the TMEM base address
   static constexpr uint32_t IDESC_S = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, QR, false, false);
   static constexpr uint32_t IDESC_O = tc5::idesc_f16(std::is_same<T, __nv_bfloat16>::value, 128, NO, true, true);
 
@@ -996,17 +1005,20 @@ struct Tc5Engine {
     return ring + NST * STAGE_BYTES;
   }
   __device__ __forceinline__ static int slot_of_thread() { return int(threadIdx.x >> 5) / WPS; }
-  __device__ __forceinline__ static uint32_t* tmem_base_ptr() { return reinterpret_cast<uint32_t*>(extra() + NST * XS); }
+  __device__ __forceinline__ static uint32_t* tmem_base_ptr() { return reinterpret_cast<uint32_t*>(extra() + NWG * XS + 64); }
+  __device__ __forceinline__ static uint64_t* vbar_of(int ring_slot) {  // V tile landed (expect_tx + TMA bytes)
+    return reinterpret_cast<uint64_t*>(extra() + NWG * XS) + ring_slot;
+  }
   __device__ __forceinline__ static void wg_bar(int slot) {  // the slot's 4 warps
     asm volatile("bar.sync %0, 128;" ::"r"(2 + slot) : "memory");
   }
   __device__ __forceinline__ static void init_barriers() {  // thread 0, before __syncthreads
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < NWG; ++s) {
       uint64_t* b = reinterpret_cast<uint64_t*>(extra() + s * XS + BAR_OFF);
       mbar_init(&b[0], 1);  // S^T ready (tcgen05.commit)
       mbar_init(&b[1], 1);  // O^T tile ready (tcgen05.commit)
-      mbar_init(&b[2], 1);  // V tile landed (producer's expect_tx + TMA bytes)
     }
+    for (int s = 0; s < NST; ++s) mbar_init(vbar_of(s), 1);
   }
 
   __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
@@ -1014,7 +1026,7 @@ struct Tc5Engine {
     // K on the ring's full barrier, V on the slot's own barrier: S^T, the softmax and P
     // overlap the V transfer (full boxes; rows past the tensor are zero-filled)
     const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
-    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + BAR_OFF) + 2;
+    uint64_t* vbar = vbar_of(slot);
     mbar_arrive_expect_tx(bar, KV_BYTES);
     mbar_arrive_expect_tx(vbar, KV_BYTES);
 #pragma unroll
@@ -1031,7 +1043,7 @@ struct Tc5Engine {
     const int br = a.box_rows;
     const int nb = (ntok + br - 1) / br;
     const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
-    uint64_t* vbar = reinterpret_cast<uint64_t*>(extra() + slot * XS + BAR_OFF) + 2;
+    uint64_t* vbar = vbar_of(slot);
     if (lane == 0) {
       mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * 2));
       mbar_arrive_expect_tx(vbar, uint32_t(nb * br * 128 * 2));
@@ -1079,6 +1091,8 @@ struct Tc5Engine {
     const uint32_t tbase = *tmem_base_ptr() + uint32_t(COLS * slot);
     const uint32_t tlane = uint32_t(32 * sub) << 16;
     const uint32_t kaddr = smem_u32(st), vaddr = smem_u32(st + KV_BYTES), qaddr = smem_u32(xs);
+    const uint32_t rpar = par & 1u, wpar = par >> 1;  // ring slot's / warpgroup's barrier parity
+    uint64_t* vbar = vbar_of(int((st - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES));
     // ---- S^T = K_f Q_f^T (Alg1§20) -----------------------------------------------------------
     if (tid == 0) {
       tc5::fence_after();
@@ -1092,7 +1106,7 @@ struct Tc5Engine {
       tc5::commit(&bars[0]);
     }
     if (ntok < STAGE_TOK) {  // rows past the stage's tokens: zero V once it landed (may be non-finite)
-      mbar_wait(&bars[2], par);
+      mbar_wait(vbar, rpar);
       if (tid >= ntok)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf)
@@ -1100,7 +1114,7 @@ struct Tc5Engine {
           for (int c = 0; c < 8; ++c)
             *reinterpret_cast<uint4*>(st + KV_BYTES + hf * 16384 + tid * 128 + (c << 4)) = make_uint4(0u, 0u, 0u, 0u);
     }
-    mbar_wait(&bars[0], par);
+    mbar_wait(&bars[0], wpar);
     tc5::fence_after();
     float sc[QR];
 #pragma unroll
@@ -1210,7 +1224,7 @@ struct Tc5Engine {
     wg_bar(slot);
     // ---- O^T_tile = V_f^T P_f^T (Alg1§24) ----------------------------------------------------
     if (tid == 0) {
-      mbar_wait(&bars[2], par);  // V landed
+      mbar_wait(vbar, rpar);  // V landed
       tc5::fence_after();
 #pragma unroll
       for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
@@ -1222,7 +1236,7 @@ struct Tc5Engine {
     } else if (sub != 0 && lane == 0) {
       mbar_arrive(empty);     // this warp no longer touches the slot's shared memory
     }
-    mbar_wait(&bars[1], par);
+    mbar_wait(&bars[1], wpar);
     tc5::fence_after();
     // alpha from shared memory, 8 rows at a time (no registers held across the MMA)
     // O^T tile: column h = V^T P_hi row h, column HEADS + h = V^T P_lo row h (per chain)
@@ -1330,7 +1344,7 @@ struct EpiAcc {
 
 template <class E>
 __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeArgs a, const __grid_constant__ TmapPair tm) {
-  constexpr int NST = E::NST, WPS = E::WPS, NCW = E::NCW, D = E::D, H = E::HEADS, J = D / 32;
+  constexpr int NST = E::NST, NWG = E::NWG, WPS = E::WPS, NCW = E::NCW, D = E::D, H = E::HEADS, J = D / 32;
   constexpr int FW = EngX<E>::FW;  // fold rows per ring slot (WPS, or 1 for a warpgroup engine)
   constexpr int FOLD_FLOATS = E::FOLD_FLOATS;
   constexpr int kFB = E::FOLD_BUFS;
@@ -1678,17 +1692,17 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       for (int h = 0; h < H; ++h) {
         float mx = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < NST * FW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 2) + D]);
+        for (int w = 0; w < NWG * FW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 2) + D]);
         float l = 0.f, o[J];
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
-        // Summed in the order of the slots RELATIVE to the segment's first stage: warp
-        // (slot (s0 + c) % NST, sub) holds the segment's stages c, c + NST, ... whatever s0
+        // Summed in the order of the warp sets RELATIVE to the segment's first stage: warp
+        // (set (s0 + c) % NWG, sub) holds the segment's stages c, c + NWG, ... whatever s0
         // is, so the rounding depends only on the segment, never on where the ring stood
         // when it began (dynamic claims need no ring alignment; reading C16).
 #pragma unroll
-        for (int cw = 0; cw < NST * FW; ++cw) {
-          const int w = ((si.s0 + cw / FW) % NST) * FW + cw % FW;
+        for (int cw = 0; cw < NWG * FW; ++cw) {
+          const int w = ((si.s0 + cw / FW) % NWG) * FW + cw % FW;
           const float* r = fb + (w * H + h) * (D + 2);
           const float wt = ex2_sub(r[D], mx);  // idle warp / masked row: m = -inf -> 0
           l = fmaf(wt, r[D + 1], l);
@@ -1812,7 +1826,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   }
 
   // ================================= consumers ==========================================
-  const int my_slot = warp / WPS, sub = warp % WPS;
+  const int my_wg = warp / WPS, sub = warp % WPS;  // warp set (= ring slot when NWG == NST)
   int j = 0, k = 0, seg = 0;
 #ifdef LA_PROF  // trace fields reused: (publish, wait0, wait1) = consumer warp 0's cycles waiting
   long long prof_wait = 0, prof_work = 0, prof_n = 0;  // for data, in stage(), stages
@@ -1856,29 +1870,33 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       const int finishing = (it1 >= u.iter_end) ? 1 : 0;  // finishing-block (Alg2§18)
       typename E::State st;
       E::seg_begin(st, a, u, lane);
-      const int seg_s0 = j % NST;
+      const int seg_s0 = j % NWG;
       for (; it < seg_end; ++it) {
         const int t0 = (it - u.iter_begin) * a.tile_n;
         const int t1 = min(t0 + a.tile_n, u.len);
         for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
-          if (j % NST == my_slot) {
+          if (j % NWG == my_wg) {
+            const int rs = j % NST;  // ring slot of stage j
 #ifdef LA_PROF
             const long long c0 = clock64();
 #endif
-            mbar_wait(&full[my_slot], (j / NST) & 1);
+            // NWG < NST: slot rs last held stage j - NST of ANOTHER warp set; wait for its
+            // release first, so the full-barrier parity below cannot alias that older phase
+            if (NWG < NST && j >= NST) mbar_wait(&empty[rs], uint32_t((j / NST) - 1) & 1u);
+            mbar_wait(&full[rs], (j / NST) & 1);
 #ifdef LA_PROF
             const long long c1 = clock64();
             prof_wait += c1 - c0;
             ++prof_n;
 #endif
             if constexpr (EngX<E>::TMEM > 0) {  // the engine releases the slot itself
-              E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
-                       lane, a.box_shift, uint32_t(j / NST) & 1u, &empty[my_slot]);
+              E::stage(st, ring + rs * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
+                       lane, a.box_shift, (uint32_t(j / NST) & 1u) | ((uint32_t(j / NWG) & 1u) << 1), &empty[rs]);
             } else {
-              E::stage(st, ring + my_slot * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
+              E::stage(st, ring + rs * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
                        lane, a.box_shift);
               __syncwarp();
-              if (lane == 0) mbar_arrive(&empty[my_slot]);
+              if (lane == 0) mbar_arrive(&empty[rs]);
             }
 #ifdef LA_PROF
             prof_work += clock64() - c1;
@@ -1995,12 +2013,12 @@ KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine) {
     if (head_dim != 128 || group > 32) return KernelInfo{};
     if (dtype == LA_BF16)
       return group <= 8    ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 8>>(true)
-             : group <= 16 ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 16>>(true)
-                           : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST32, 32>>(true);
+             : group <= 16 ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 16, LA_TC5_NWG16>>(true)
+                           : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST32, 32, LA_TC5_NWG32>>(true);
     if (dtype == LA_FP16)
       return group <= 8    ? info_of<Tc5Engine<__half, LA_TC5_NST, 8>>(true)
-             : group <= 16 ? info_of<Tc5Engine<__half, LA_TC5_NST, 16>>(true)
-                           : info_of<Tc5Engine<__half, LA_TC5_NST32, 32>>(true);
+             : group <= 16 ? info_of<Tc5Engine<__half, LA_TC5_NST, 16, LA_TC5_NWG16>>(true)
+                           : info_of<Tc5Engine<__half, LA_TC5_NST32, 32, LA_TC5_NWG32>>(true);
     return KernelInfo{};
   }
   if (dtype == LA_FP8_E4M3) {  // one tensor-core engine for every T_m <= 8 (MHA included)
