@@ -96,6 +96,9 @@
 #ifndef LA_TC5_NWG32
 #define LA_TC5_NWG32 2  // warpgroups for 32-row tiles (< NST32: the ring prefetches past the warpgroups)
 #endif
+#ifndef LA_TC5_LDEFER
+#define LA_TC5_LDEFER 0  // 1: 32 rows, NWG < NST: per-thread running sums updated after the PV MMA (measured 1% slower)
+#endif
 #ifndef LA_TC5_NWG16
 #define LA_TC5_NWG16 LA_TC5_NST  // the same for 16-row tiles
 #endif
@@ -967,7 +970,11 @@ struct Tc5Engine {
   static_assert(HEADS == 8 || HEADS == 16 || HEADS == 32, "T_m");
   static constexpr int QR = HEADS < 16 ? 16 : HEADS;  // Q^T operand rows = S^T MMA N (>= 16)
   static constexpr int QHS = QR * 128;               // Q^T dim-half stride
-  static constexpr int LN = HEADS == 32 ? 1 : HEADS;  // running-sum registers per thread
+  // 32 rows with 168 registers (NWG < NST): every thread keeps its token's share of all 32
+  // running sums and updates them after the PV MMA with the shared alpha (no transpose-butterfly
+  // per stage); 32 rows at 128 registers: the butterfly, lane r keeping row r's sum
+  static constexpr bool LDEFER = LA_TC5_LDEFER && HEADS == 32 && NWG < NST;
+  static constexpr int LN = HEADS == 32 && !LDEFER ? 1 : HEADS;
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
   static constexpr int FOLD_FLOATS = NWG * HEADS * (D + 2);
@@ -1200,7 +1207,7 @@ struct Tc5Engine {
         *reinterpret_cast<uint4*>(pl + (((HEADS / 8 + j) ^ (tid & 7)) << 4)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
     }
-    if constexpr (HEADS == 32) {  // Alg1§23 for 32 rows: XOR transpose-butterfly of the 32 p's
+    if constexpr (HEADS == 32 && !LDEFER) {  // Alg1§23 for 32 rows: XOR transpose-butterfly of the 32 p's
       // (31 shuffles) leaves the warp's sum of row `lane` in sc[0] of lane `lane`
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) {
@@ -1264,6 +1271,9 @@ struct Tc5Engine {
       const float al[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
       for (int i = 0; i < 8; ++i) s.o[c0 + i] = fmaf(al[i], s.o[c0 + i], hv[i] + lv[i]);  // Alg1§25
+      if constexpr (LDEFER)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s.l[c0 + i] = fmaf(al[i], s.l[c0 + i], sc[c0 + i]);  // Alg1§23 (sc = p)
     }
     tc5::fence_before();
     s.mpar ^= 1;
@@ -1275,7 +1285,7 @@ struct Tc5Engine {
     float* fb = fold + slot * HEADS * (D + 2);                                  // [row][D + 2]
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) fb[h * (D + 2) + 32 * sub + lane] = s.o[h];
-    if constexpr (HEADS == 32) {
+    if constexpr (HEADS == 32 && !LDEFER) {
       red2[sub * HEADS + lane] = s.l[0];  // lane = row
     } else {
 #pragma unroll
