@@ -151,6 +151,36 @@ def test_tcgen05_wide_c3_speculative_full_size():
     torch.cuda.empty_cache()
 
 
+def test_tcgen05_wide_c3_q4_full_size():
+    """c3 with N_q = 4 -- the `bench.py --config c3 --q-len 4` launch: 32 rows per KV head in
+    ONE pass on the 2-warpgroup / 3-slot engine (stage j -> warpgroup j mod 2, slot j mod 3),
+    segments of ~220 stages, vs the oracle on sampled units (causal: query i sees n - 4 + i + 1
+    keys) and vs the mma.sync engine (four 8-row passes), plus the census closed form."""
+    p = synth.config("c3", q_len=4)
+    inputs = cuda_inputs(p)
+    O, L, plan = run_cuda(p, inputs=inputs, causal=True, **TC5)
+    assert plan.info.tile_rows == 32 and plan.info.num_units == 64
+    import oracle
+    q64 = synth.to_f64(synth.gen_q(p))
+    for b, h in ((0, 0), (7, 5)):  # sampled units: 8 heads x 4 queries against the oracle
+        k = synth.to_f64(synth.gen_kv_unit(p, b, h, "k"))[None, None]
+        v = synth.to_f64(synth.gen_kv_unit(p, b, h, "v"))[None, None]
+        O_ref, L_ref = oracle.decode_attention_multi(q64[b:b + 1, 8 * h:8 * h + 8], k, v, [p.ctx_lens[b]], p.scale,
+                                                     causal=True)
+        gate(O[b:b + 1, 8 * h:8 * h + 8], L[b:b + 1, 8 * h:8 * h + 8], O_ref, L_ref, what=f"tc5 c3 Nq4 b{b} h{h}")
+    O2, L2, plan2 = run_cuda(p, inputs=inputs, causal=True, engine="mma")
+    assert plan2.info.num_units == 256
+    assert np.abs(O - O2).max() <= 1e-4 and np.abs(L - L2).max() <= 2e-6  # fp32 sums over 64k keys
+    del inputs
+    torch.cuda.empty_cache()
+    p3 = synth.config("c3", q_len=4, dist="D3")
+    O3, L3, _ = run_cuda(p3, causal=False, **TC5)
+    o_exp, l_exp = census_expect(p3, 0)
+    assert np.max(np.abs(O3 - o_exp)) <= 1e-5
+    assert np.max(np.abs(L3 - l_exp)) <= 1e-5
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("rows", [8, 16, 32])
 @pytest.mark.parametrize("page_size", [16, 32, 64, 128, 256])
 def test_tcgen05_paged(rows, page_size):
