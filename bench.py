@@ -459,7 +459,7 @@ def bench_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         achieved = local_kv / (kern_ms * 1e-3) / 1e9   # dominant kernel, per launch
-        traffic = ncu_traffic(cfg + ("-fp8" if p.dtype == "fp8" else "")
+        traffic = ncu_traffic(cfg + (f"-q{p.q_len}" if p.q_len > 1 else "") + ("-fp8" if p.dtype == "fp8" else "")
                               + ("-tc5" if info.engine == 1 and info.tile_rows > 1 else ""))
         engine = "Fp8" if p.dtype == "fp8" else (("Tc5" if info.engine == 1 else "Gqa")
                                                  if info.tile_rows > 1 else "Mha")
