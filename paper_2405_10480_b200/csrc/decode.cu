@@ -981,7 +981,9 @@ struct Tc5Engine {
   static constexpr int FOLD_BUFS = 1;
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
-  static constexpr int SPLIT = LA_TC5_SPLIT;        // accumulator chains per contraction (1 or 2)
+  // accumulator chains per contraction (1 or 2).  LA_TC5_SPLIT = 2 applies to 8-row tiles only:
+  // at 16 / 32 rows it fails a wide-tile parity test and measured slower (32 rows: 383 vs 368 us)
+  static constexpr int SPLIT = HEADS == 8 ? LA_TC5_SPLIT : 1;
   static constexpr int OC = QR * SPLIT;             // first O^T column of a slot (S^T chains before it)
   static constexpr int COLS = (OC + NO * SPLIT) <= 32 ? 32 : (OC + NO * SPLIT) <= 64 ? 64 : 128;  // per slot
   static_assert(NWG * COLS <= 512, "TMEM columns");
