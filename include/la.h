@@ -26,7 +26,8 @@
  *    default stream).  Kernels run asynchronously on `stream`; device-side faults surface
  *    at the caller's next synchronisation.
  *  - A plan owns all device memory it allocates (schedule tables, per-CTA partial slots
- *    Op/mp/lp and flags, Alg2§20-23) until la_plan_destroy().  la_decode never allocates.
+ *    Op/mp/lp and flags, Alg2§20-23) until la_plan_destroy().  la_decode and la_plan_update
+ *    never allocate.
  *  - Not thread-safe on one plan: two la_decode calls on the same plan must be ordered
  *    on one stream (they share the partial slots and flags).
  */
@@ -49,7 +50,8 @@ typedef enum {
   LA_ERR_CUDA = 3,         /* a CUDA runtime call failed (message in la_last_error)     */
   LA_ERR_NOMEM = 4,        /* device or host allocation failed                          */
   LA_ERR_STATE = 5,        /* e.g. la_decode on a host-only plan                         */
-  LA_ERR_TIMEOUT = 6       /* a cross-GPU exchange wait gave up (a peer never arrived)   */
+  LA_ERR_TIMEOUT = 6       /* an in-kernel wait gave up: a peer CTA (10 s) or a peer rank
+                              (5 s) never signalled (reported by la_plan_status)          */
 } la_status;
 
 /* Storage type of Q, K and V ("FP16->32": 16-bit inputs, fp32 arithmetic).
@@ -143,6 +145,9 @@ typedef struct {
                                  tiles (g * N_q > 8) the static schedules, else
                                  la_plan fails with LA_ERR_UNSUPPORTED; ignored for T_m = 1
                                  (MHA: a GEMV, CUDA cores) and FP8 caches                     */
+  void* stream;               /* cudaStream_t for the plan's initial table upload: la_plan then
+                                 returns with the ONE H2D copy of its tables still in flight on
+                                 it (decode on the same stream).  NULL: la_plan waits for it   */
 } la_plan_opts;
 
 /* Which tensor-core instructions contract the T_m x T_n tiles (Alg1§20, §24). */
@@ -180,6 +185,12 @@ typedef struct {
   int64_t q_rows;          /* query / output rows = sum_b H_q N_b                          */
   int engine;              /* la_engine chosen for T_m > 1 tiles; -1 for the CUDA-core (MHA)
                               and FP8 engines                                                */
+  double quantization_efficiency; /* I / (W x max_w LeanTiles of worker w):
+                              W = the ranges of a static schedule (1.0 - 1/ceil(I/G) at worst for
+                              stream-K), the persistent CTAs for dynamic / fixed split (range
+                              j on CTA j mod W, the launch-order wave model)                 */
+  int slot_capacity;       /* (virtual) CTA ranges the plan's device state can hold           */
+  int64_t updates;         /* la_plan_update calls so far                                     */
 } la_plan_info;
 
 /* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */
@@ -205,6 +216,31 @@ la_status la_plan_opts_init(la_plan_opts* opts);
  */
 la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int32_t* ctx_lens,
                   int tile_n, la_dtype dtype, const la_plan_opts* opts, la_plan_t* out);
+
+/*
+ * la_plan_update -- re-plan for the next decode step's context lengths (Lean Ragged
+ * Batching: serving steps change ctx_lens every step) WITHOUT allocating:
+ * Alg2§4-18 is re-run on the host (O(units + G)), the new tables (and block table) are
+ * staged in the plan's pinned buffer and uploaded by ONE cudaMemcpyAsync on `stream`
+ * (cudaStream_t; decode on the same stream, or order it after).  Everything a kernel launch
+ * takes by value is independent of ctx_lens, so a CUDA graph captured around la_decode on
+ * this plan replays correctly after an update (BHSD and paged layouts; a packed cache's
+ * row count changes with sum n_b, so its tensor maps -- and a graph -- are re-made).
+ * The CTA count launched is fixed at la_plan: min(co-resident CTAs, I at the capacity
+ * lengths) -- the capacity is max_ctx for BHSD when opts.max_ctx was given,
+ * pages_per_seq * page_size for paged pools, else the first plan's lengths.
+ *
+ * ctx_lens: HOST [batch], each in [max(1, q_lens[b]), capacity] (BHSD: <= max_ctx; paged:
+ * <= pages_per_seq * page_size).  block_table: HOST [batch][pages_per_seq] for paged plans
+ * (NULL keeps the current table); must be NULL otherwise.  Every other plan parameter
+ * (shape, dtype, layout, schedule options, q_lens) is unchanged.  The staging buffer is
+ * reused: an update first waits for the previous update's copy (long done in a decode loop).
+ * Host-only plans just re-plan (la_plan_export shows the new schedule).
+ * Errors: LA_ERR_INVALID (lengths / table), LA_ERR_STATE (a dynamic or fixed-split schedule
+ * needs more virtual-CTA slots than allocated at la_plan -- create a new plan), LA_ERR_CUDA.
+ * On error the plan is unchanged.
+ */
+la_status la_plan_update(la_plan_t plan, const int32_t* ctx_lens, const int32_t* block_table, void* stream);
 
 /* Scalar facts about a plan (host, synchronous). */
 la_status la_plan_info_get(la_plan_t plan, la_plan_info* info);
@@ -297,8 +333,11 @@ la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* 
  *   for one process driving several GPUs with peer access enabled, or several "ranks"
  *   sharing one GPU (tests).
  * la_decode on an exchange plan needs every peer opened/attached (LA_ERR_STATE otherwise).
- * la_plan_xchg_status: synchronises the device; LA_ERR_TIMEOUT if any wait of a previous
- *   la_decode on this plan gave up after 5 s (its output is then invalid), else LA_OK.
+ * la_plan_xchg_status: la_plan_status on an exchange plan (LA_ERR_STATE without one).
+ * la_plan_xchg_open checks the peer's shape header (batch, heads, head_dim, dtype, rows,
+ *   units, world, rank) written into its buffer at la_plan: LA_ERR_INVALID on a mismatch.
+ * The exchange flags carry an exchange sequence number that only exchange launches
+ *   advance (la_decode_partial on the plan does not), and waits compare wrap-safe.
  * Requires q_len == 1 or causal == 0 (a causal multi-token mask is not shard-local).
  */
 #define LA_XCHG_HANDLE_BYTES 64
@@ -306,6 +345,15 @@ la_status la_plan_xchg_handle(la_plan_t plan, void* handle);
 la_status la_plan_xchg_open(la_plan_t plan, int peer, const void* handle);
 la_status la_plan_xchg_attach(la_plan_t plan, int peer, la_plan_t peer_plan);
 la_status la_plan_xchg_status(la_plan_t plan);
+
+/*
+ * la_plan_status -- synchronises the device and reports whether an in-kernel wait of a
+ * previous launch on this plan gave up: a stream-K host CTA waiting for a peer's partial
+ * (Alg2§28, 10 s) or a cross-GPU exchange wait (5 s).  LA_ERR_TIMEOUT (the output of that
+ * launch is invalid; the error is cleared), LA_ERR_STATE for a host-only plan, else LA_OK.
+ * A protocol failure therefore surfaces as an error instead of hanging the device.
+ */
+la_status la_plan_status(la_plan_t plan);
 
 /* Release a plan and all device memory it owns.  NULL is a no-op. */
 void la_plan_destroy(la_plan_t plan);

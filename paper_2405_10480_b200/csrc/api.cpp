@@ -1,6 +1,6 @@
 // C-ABI layer of libleanattn.so (include/la.h): argument validation, plan ownership of
 // device state, launch configuration.  Every step of the decode path runs in the kernels
-// of kernels.cu; this file only plans (integer work) and marshals.
+// of decode.cu; this file only plans (integer work, planner.cpp) and marshals.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,25 +21,40 @@ struct la_plan_s {
   la::KernelInfo kinfo;
   int stage_tokens = 0;
   bool host_only = true;
-  bool needs_wait = false;   // any non-finishing host -> cooperative launch required
   int split = 0;             // LA_SCHED_FIXED_SPLIT: chunks per unit actually used
   int pt_stride = 0;         // LA_KV_PAGED: padded block-table row stride
-  int32_t* d_block_table = nullptr;
   int device = -1;
-  // device state owned by the plan
+  int engine = -1;           // la_engine of the T_m > 1 tiles (-1: CUDA cores / FP8 engine)
+  // planning options, kept for la_plan_update
+  int opt_grid = 0, opt_dyn_first = 750, opt_dyn_min = 2, opt_split = 0;
+  int max_ctas = 0;          // co-resident CTAs (device) / num_sms x ctas_per_sm (host-only)
+  int slot_cap = 0;          // (virtual) CTA capacity of the range table, partial slots, flags
+  int64_t updates = 0;       // la_plan_update calls
+  // ---- device state, ONE allocation ---------------------------------------------------
+  // upload region (rewritten by la_plan_update with one async copy):
+  //   [hdr 256 B][units U x 48 B][cta_begin cap + 1][cta_first cap][block table B x pt_stride]
+  // then kernel state: partials [2][cap][rows][d] + [2][cap][rows][4], flags [cap],
+  //   counters [kNumCounters] + unit_count [U] + grp_count [2 cap], trace, engine fold scratch
   void* d_tables = nullptr;
+  size_t up_bytes = 0, off_units = 0, off_begin = 0, off_first = 0, off_bt = 0;
+  int32_t* d_hdr = nullptr;
   DevUnit* d_units = nullptr;
   int32_t* d_cta_begin = nullptr;
   int32_t* d_cta_first = nullptr;
+  int32_t* d_block_table = nullptr;
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   uint32_t* d_flags = nullptr;
   int* d_counters = nullptr;
   int* d_unit_count = nullptr;
+  int* d_grp_count = nullptr;
   unsigned long long* d_trace = nullptr;
   float* d_gfold = nullptr;
-  int engine = -1;           // la_engine of the T_m > 1 tiles (-1: CUDA cores / FP8 engine)  // engine fold buffers in global memory (KernelInfo::global_fold_floats)
+  unsigned char* h_stage = nullptr;   // pinned host copy of the upload region
+  cudaEvent_t up_done = nullptr;      // the last upload's copy has left h_stage
+  bool up_pending = false;
   int64_t workspace = 0;
+  la::TmapCache tmaps;                // K / V tensor maps of the last (k, v, rows)
   // la_decode_host staging
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
@@ -68,12 +83,14 @@ la_status cuda_fail(cudaError_t e, const char* what) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int auto_tile_n(const la::Problem& p, int /*max_ctas*/) {
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int auto_tile_n(const la::Problem& p) {
   // 64 KiB of K+V per LeanTile: 128 tokens at d=128 and 256 at d=64 for 16-bit inputs,
   // the sizes the paper's sweep found, whatever the problem size.  Smaller tiles
   // for problems with fewer LeanTiles than SMs were measured never faster on B200 and up to
-  // 18% slower (scripts/sweep_tile.py: a single-unit problem split over more CTAs has its
-  // host fold more peers; the load is latency-, not bandwidth-bound at that size).
+  // 18% slower (a single-unit problem split over more CTAs has its host fold more peers; the
+  // load is latency-, not bandwidth-bound at that size).
   const int row_bytes = p.head_dim * p.elem_bytes();
   return std::max(32, std::min(512, 65536 / (2 * row_bytes)));
 }
@@ -84,18 +101,155 @@ void release_device(la_plan_s* p) {
   if (p->d_xchg) cudaFree(p->d_xchg);
   if (p->d_tables) cudaFree(p->d_tables);
   if (p->d_stage) cudaFree(p->d_stage);
+  if (p->h_stage) cudaFreeHost(p->h_stage);
+  if (p->up_done) cudaEventDestroy(p->up_done);
   p->d_tables = nullptr;
   p->d_stage = nullptr;
   p->d_xchg = nullptr;
+  p->h_stage = nullptr;
+  p->up_done = nullptr;
 }
 
-// Exchange buffer layout (DecodeArgs::xpeer): [2][P][rows][d + 4] fp32, then [P][units]
-// uint32 flags, then one int error word.
+// Exchange buffer layout: a 256-B head -- the error word at +0 and the owner's shape header
+// at +64, at a fixed offset so a peer can read it before it knows the shape (checked by
+// la_plan_xchg_open) -- then the data DecodeArgs::xpeer points at: [2][P][rows][d + 4] fp32
+// and, at xflag_off from there, [P][units] uint32 flags.
+constexpr size_t kXchgHead = 256;
 size_t xchg_flag_off(const la::Problem& p, int P) {
-  return (size_t(2) * P * p.q_rows() * (p.head_dim + 4) * sizeof(float) + 255) & ~size_t(255);
+  return align256(size_t(2) * P * p.q_rows() * (p.head_dim + 4) * sizeof(float));
 }
 size_t xchg_bytes(const la::Problem& p, int P) {
-  return xchg_flag_off(p, P) + ((size_t(P) * p.num_units() * sizeof(uint32_t) + 255) & ~size_t(255)) + 256;
+  return kXchgHead + xchg_flag_off(p, P) + align256(size_t(P) * p.num_units() * sizeof(uint32_t));
+}
+constexpr int kXchgHdrInts = 12;
+void xchg_header(const la_plan_s* pl, int32_t (&h)[kXchgHdrInts]) {
+  const la::Problem& p = pl->prob;
+  const int64_t rows = p.q_rows(), units = p.num_units();
+  const int32_t v[kXchgHdrInts] = {0x4c415848 /* "LAXH" */, p.batch, p.heads_q, p.heads_kv, p.head_dim, p.dtype,
+                                   int32_t(rows), int32_t(units), pl->xw, pl->xr, p.tile_rows, 0};
+  std::memcpy(h, v, sizeof(v));
+}
+
+// I if every request had its capacity length: BHSD with an explicit max_ctx, paged pools
+// (pages_per_seq x page_size).  Sizes the launch grid so that a plan updated to longer
+// contexts keeps one CTA per SM.  Else the current I.
+int64_t capacity_iters(const la::Problem& p, int tile_n, bool explicit_max_ctx, int64_t cur) {
+  int64_t cap_len = 0;
+  if (p.layout == LA_KV_BHSD && explicit_max_ctx) cap_len = p.max_ctx;
+  if (p.layout == LA_KV_PAGED) cap_len = int64_t(p.pages_per_seq) * p.page_size;
+  if (cap_len <= 0) return cur;
+  const int64_t per = (cap_len + tile_n - 1) / tile_n;
+  return std::max(cur, per * (p.num_units()));
+}
+
+// Alg2§4-18 for the plan's current ctx_lens: units in memory order, the (virtual) CTA
+// ranges of the plan's schedule, host / last CTA per unit.  `launch` (CTAs launched) is
+// chosen on the first call and kept: a CUDA graph captured on the plan keeps its grid, and
+// CTAs without a range exit at once.
+la_status plan_schedule(la_plan_s* plan, bool first, int64_t icap_hint) {
+  const la::Problem& p = plan->prob;
+  la::Schedule& s = plan->sched;
+  const int M = plan->max_ctas;
+  la::build_units(p, s.tile_n, s.units, s.total_iters);
+  if (s.total_iters >= (int64_t(1) << 31)) return fail(LA_ERR_INVALID, "too many LeanTiles");
+  const int64_t I = s.total_iters;
+  if (first) {
+    const int64_t icap = std::max(I, icap_hint);
+    int launch;
+    if (p.schedule == LA_SCHED_SEQUENTIAL)
+      launch = int(s.units.size());
+    else if (plan->opt_grid)
+      launch = (plan->host_only && p.schedule == LA_SCHED_STREAMK) ? plan->opt_grid : std::min(plan->opt_grid, M);
+    else
+      launch = int(std::max<int64_t>(1, std::min<int64_t>(M, icap)));
+    s.phys_grid = std::max(1, launch);
+  }
+  const int launch = s.phys_grid;
+  plan->split = 0;
+  if (p.schedule == LA_SCHED_SEQUENTIAL) {
+    la::sequential_ranges(s.units, s.cta_begin);
+  } else if (p.schedule == LA_SCHED_DYNAMIC) {
+    const int G = plan->opt_grid ? launch : int(std::max<int64_t>(1, std::min<int64_t>(launch, I)));
+    la::guided_ranges(I, G, plan->opt_dyn_first, plan->opt_dyn_min, s.cta_begin);
+  } else if (p.schedule == LA_SCHED_FIXED_SPLIT) {
+    int64_t max_cn = 1;
+    for (const DevUnit& u : s.units) max_cn = std::max<int64_t>(max_cn, u.iter_end - u.iter_begin);
+    plan->split = plan->opt_split ? plan->opt_split : la::fa2_num_splits(int64_t(s.units.size()), max_cn, M);
+    la::fixed_split_ranges(s.units, plan->split, s.cta_begin);
+  } else {
+    // stream-K (Eq. 2): G = forced grid, else min(launch, I) equal ranges (reading C15)
+    const int G = plan->opt_grid ? launch : int(std::max<int64_t>(1, std::min<int64_t>(launch, I)));
+    la::streamk_ranges(I, G, s.cta_begin);
+  }
+  la::finish_schedule(s);
+  return LA_OK;
+}
+
+// Quantization efficiency: I / (W x max_w load_w).  Static schedules:
+// W = the ranges (one CTA each); dynamic / fixed split: W = the persistent CTAs, range j on
+// CTA j mod W (the launch-order wave model, as oracle.fixed_split_segments deals chunks).
+double quant_eff(const la_plan_s* plan) {
+  const la::Schedule& s = plan->sched;
+  const bool waves = plan->prob.schedule == LA_SCHED_DYNAMIC || plan->prob.schedule == LA_SCHED_FIXED_SPLIT;
+  const int W = waves ? s.phys_grid : s.grid;
+  if (W < 1 || s.total_iters < 1) return 0.0;
+  std::vector<int64_t> load(size_t(W), 0);
+  for (int v = 0; v < s.grid; ++v) load[size_t(waves ? v % W : v)] += s.cta_begin[v + 1] - s.cta_begin[v];
+  const int64_t mx = *std::max_element(load.begin(), load.end());
+  return mx > 0 ? double(s.total_iters) / (double(W) * double(mx)) : 0.0;
+}
+
+// Copy the current schedule (and block table) into the pinned staging buffer and upload it
+// with ONE async H2D on `stream`.  sync: also wait for it (la_plan without a stream).
+la_status upload_tables(la_plan_s* plan, cudaStream_t stream, bool sync) {
+  const la::Schedule& s = plan->sched;
+  if (plan->up_pending) {  // the previous upload may still be reading the staging buffer
+    cudaError_t e = cudaEventSynchronize(plan->up_done);
+    if (e != cudaSuccess) return cuda_fail(e, "la_plan_update: previous upload");
+    plan->up_pending = false;
+  }
+  unsigned char* h = plan->h_stage;
+  const int32_t hdr[4] = {s.grid, 0, 0, 0};
+  std::memcpy(h, hdr, sizeof(hdr));
+  std::memcpy(h + plan->off_units, s.units.data(), s.units.size() * sizeof(DevUnit));
+  std::memcpy(h + plan->off_begin, s.cta_begin.data(), size_t(s.grid + 1) * sizeof(int32_t));
+  std::memcpy(h + plan->off_first, s.cta_first_unit.data(), size_t(s.grid) * sizeof(int32_t));
+  const la::Problem& p = plan->prob;
+  if (plan->pt_stride) {  // block table, rows padded to pt_stride (the producer reads 32-entry windows)
+    int32_t* bt = reinterpret_cast<int32_t*>(h + plan->off_bt);
+    for (int b = 0; b < p.batch; ++b) {
+      std::copy(p.block_table.begin() + size_t(b) * p.pages_per_seq,
+                p.block_table.begin() + size_t(b + 1) * p.pages_per_seq, bt + size_t(b) * plan->pt_stride);
+      std::fill(bt + size_t(b) * plan->pt_stride + p.pages_per_seq, bt + size_t(b + 1) * plan->pt_stride, 0);
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(plan->d_tables, h, plan->up_bytes, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaEventRecord(plan->up_done, stream);
+  if (e == cudaSuccess && sync) e = cudaEventSynchronize(plan->up_done);
+  if (e != cudaSuccess) return cuda_fail(e, "schedule upload");
+  plan->up_pending = !sync;
+  return LA_OK;
+}
+
+la_status check_lens(const la::Problem& p, const int32_t* ctx_lens, int64_t* maxn_out) {
+  int64_t maxn = 0;
+  for (int b = 0; b < p.batch; ++b) {
+    if (ctx_lens[b] < 1) return fail(LA_ERR_INVALID, "every ctx_lens[b] must be >= 1 (reading C6)");
+    if (ctx_lens[b] < p.q_lens[b])
+      return fail(LA_ERR_INVALID, "ctx_lens[b] must be >= q_lens[b] (the queries are cached tokens)");
+    maxn = std::max<int64_t>(maxn, ctx_lens[b]);
+  }
+  *maxn_out = maxn;
+  return LA_OK;
+}
+
+la_status check_block_table(const la::Problem& p, const int32_t* bt) {
+  for (int b = 0; b < p.batch; ++b)
+    for (int i = 0; i < (p.ctx_lens[b] + p.page_size - 1) / p.page_size; ++i) {
+      const int32_t pg = bt[size_t(b) * p.pages_per_seq + i];
+      if (pg < 0 || pg >= p.num_pages) return fail(LA_ERR_INVALID, "block_table entry out of range");
+    }
+  return LA_OK;
 }
 
 }  // namespace
@@ -229,6 +383,8 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     if (!(p.k_scale > 0.f) || !std::isfinite(p.k_scale) || !(p.v_scale > 0.f) || !std::isfinite(p.v_scale))
       return fail(LA_ERR_INVALID, "k_scale / v_scale must be finite and > 0");
   }
+  if (opts.block_table && p.layout != LA_KV_PAGED)
+    return fail(LA_ERR_INVALID, "block_table given for a non-paged layout");
   if (p.layout == LA_KV_PAGED) {
     const int ps = opts.page_size;
     if (ps != 16 && ps != 32 && ps != 64 && ps != 128 && ps != 256)
@@ -241,11 +397,8 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     p.pages_per_seq = opts.pages_per_seq;
     p.num_pages = opts.num_pages;
     p.block_table.assign(opts.block_table, opts.block_table + size_t(batch) * opts.pages_per_seq);
-    for (int b = 0; b < batch; ++b)
-      for (int i = 0; i < (p.ctx_lens[b] + ps - 1) / ps; ++i) {
-        const int32_t pg = p.block_table[size_t(b) * opts.pages_per_seq + i];
-        if (pg < 0 || pg >= opts.num_pages) return fail(LA_ERR_INVALID, "block_table entry out of range");
-      }
+    la_status st = check_block_table(p, p.block_table.data());
+    if (st != LA_OK) return st;
   }
 
   auto* plan = new (std::nothrow) la_plan_s();
@@ -254,11 +407,14 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   plan->host_only = opts.host_only != 0;
   plan->xw = xw;
   plan->xr = xw ? opts.xchg_rank : 0;
+  plan->opt_grid = opts.grid;
+  plan->opt_dyn_first = opts.dyn_first_permille;
+  plan->opt_dyn_min = opts.dyn_min_chunk;
+  plan->opt_split = opts.split;
 
   // ---- co-resident CTA budget (reading C15) -----------------------------------------
-  int max_ctas = 0;
   if (plan->host_only) {
-    max_ctas = std::max(1, opts.num_sms) * std::max(1, opts.ctas_per_sm);
+    plan->max_ctas = std::max(1, opts.num_sms) * std::max(1, opts.ctas_per_sm);
   } else {
     if (engine == LA_ENGINE_TCGEN05 && p.rows() > 1 && dtype == LA_FP8_E4M3) {
       delete plan;
@@ -290,108 +446,93 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
       delete plan;
       return fail(LA_ERR_UNSUPPORTED, "KV cache rows exceed the TMA int32 coordinate range");
     }
-    max_ctas = sms * occ;
+    plan->max_ctas = sms * occ;
   }
 
   // ---- schedule (Alg2§4-18) -----------------------------------------------------------
-  const int tn = tile_n ? tile_n : auto_tile_n(p, max_ctas);
+  plan->sched.tile_n = tile_n ? tile_n : auto_tile_n(p);
+  {
+    const int64_t icap = capacity_iters(p, plan->sched.tile_n, opts.max_ctx > 0, 0);
+    la_status st = plan_schedule(plan, true, icap);
+    if (st != LA_OK) { delete plan; return st; }
+  }
   la::Schedule& s = plan->sched;
-  s.tile_n = tn;
-  la::build_units(p, tn, s.units, s.total_iters);
-  if (s.total_iters >= (int64_t(1) << 31)) { delete plan; return fail(LA_ERR_INVALID, "too many LeanTiles"); }
-  if (p.schedule == LA_SCHED_SEQUENTIAL) {
-    la::sequential_ranges(s.units, s.cta_begin);
-  } else if (p.schedule == LA_SCHED_DYNAMIC) {
-    // persistent CTAs: one per co-resident slot (or the forced grid), claiming virtual CTAs
-    int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
-    G = std::max(1, std::min(G, max_ctas));
-    la::guided_ranges(s.total_iters, G, opts.dyn_first_permille, opts.dyn_min_chunk, s.cta_begin);
-  } else if (p.schedule == LA_SCHED_FIXED_SPLIT) {
-    int64_t max_cn = 1;
-    for (const DevUnit& u : s.units) max_cn = std::max<int64_t>(max_cn, u.iter_end - u.iter_begin);
-    plan->split = opts.split ? opts.split : la::fa2_num_splits(int64_t(s.units.size()), max_cn, max_ctas);
-    la::fixed_split_ranges(s.units, plan->split, s.cta_begin);
-  } else {
-    int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
-    if (!plan->host_only) G = std::min(G, max_ctas);  // hosts wait on peers: co-residency
-    la::streamk_ranges(s.total_iters, std::max(1, G), s.cta_begin);
-  }
-  la::finish_schedule(s);
-  if (p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT) {
-    // persistent CTAs claim the ranges in order (hardware-wave order for fixed split)
-    int G = opts.grid ? opts.grid : int(std::min<int64_t>(max_ctas, s.total_iters));
-    s.phys_grid = std::max(1, std::min({G, max_ctas, s.grid}));
-  } else {
-    s.phys_grid = s.grid;
-    for (const DevUnit& u : s.units)
-      if (u.last_cta != u.host_cta) plan->needs_wait = true;
-  }
-  if (!plan->host_only && plan->needs_wait && s.grid > max_ctas) {
+  if (!plan->host_only && p.schedule == LA_SCHED_STREAMK && s.phys_grid > plan->max_ctas) {
     delete plan;
     return fail(LA_ERR_INVALID, "grid exceeds the co-resident CTA count");
   }
-  plan->stage_tokens = plan->host_only ? std::min(tn, 64) : std::min(tn, plan->kinfo.stage_tokens_max);
+  plan->stage_tokens = plan->host_only ? std::min(s.tile_n, 64) : std::min(s.tile_n, plan->kinfo.stage_tokens_max);
+  // capacity of (virtual) CTAs: static schedules never exceed the launch grid (stream-K) or the
+  // unit count (sequential); dynamic / fixed-split range counts vary with ctx_lens, so leave room
+  const bool virt = p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT;
+  plan->slot_cap = virt ? 2 * s.grid + s.phys_grid : std::max(s.grid, s.phys_grid);
 
   // ---- device state -------------------------------------------------------------------
   if (!plan->host_only) {
-    const int G = s.grid, GP = s.phys_grid;
+    const int CAP = plan->slot_cap, GP = s.phys_grid;
     const size_t U = s.units.size();
-    auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const size_t b_units = align(U * sizeof(DevUnit));
-    const size_t b_begin = align(size_t(G + 1) * sizeof(int32_t));
-    const size_t b_first = align(size_t(G) * sizeof(int32_t));
-    const size_t b_po = align(size_t(G) * 2 * p.rows() * head_dim * sizeof(float));
-    const size_t b_pml = align(size_t(G) * 2 * p.rows() * 4 * sizeof(float));
-    const size_t b_flags = align(size_t(G) * sizeof(uint32_t));
-    const size_t b_cnt = align((4 + U + size_t(G)) * sizeof(int));
-    const size_t b_trace = opts.trace ? align(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
     plan->pt_stride = p.layout == LA_KV_PAGED ? (p.pages_per_seq + 31) / 32 * 32 : 0;
-    const size_t b_pt = align(size_t(p.batch) * plan->pt_stride * sizeof(int32_t));
-    const size_t b_gf = align(size_t(GP) * plan->kinfo.global_fold_floats * sizeof(float));
-    const size_t bytes = b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace + b_pt + b_gf;
+    plan->off_units = 256;
+    plan->off_begin = plan->off_units + align256(U * sizeof(DevUnit));
+    plan->off_first = plan->off_begin + align256(size_t(CAP + 1) * sizeof(int32_t));
+    plan->off_bt = plan->off_first + align256(size_t(CAP) * sizeof(int32_t));
+    plan->up_bytes = plan->off_bt + align256(size_t(p.batch) * plan->pt_stride * sizeof(int32_t));
+    const size_t b_po = align256(size_t(CAP) * 2 * p.rows() * head_dim * sizeof(float));
+    const size_t b_pml = align256(size_t(CAP) * 2 * p.rows() * 4 * sizeof(float));
+    const size_t b_flags = align256(size_t(CAP) * sizeof(uint32_t));
+    const size_t b_cnt = align256((la::kNumCounters + U + 2 * size_t(CAP)) * sizeof(int));
+    const size_t b_trace = opts.trace ? align256(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
+    const size_t b_gf = align256(size_t(GP) * plan->kinfo.global_fold_floats * sizeof(float));
+    const size_t o_po = plan->up_bytes, o_pml = o_po + b_po, o_flags = o_pml + b_pml, o_cnt = o_flags + b_flags;
+    const size_t o_trace = o_cnt + b_cnt, o_gf = o_trace + b_trace, bytes = o_gf + b_gf;
     cudaError_t e = cudaMalloc(&plan->d_tables, bytes);
     if (e != cudaSuccess) { delete plan; return cuda_fail(e, "cudaMalloc(plan tables)"); }
-    char* base = static_cast<char*>(plan->d_tables);
-    plan->d_units = reinterpret_cast<DevUnit*>(base);
-    plan->d_cta_begin = reinterpret_cast<int32_t*>(base + b_units);
-    plan->d_cta_first = reinterpret_cast<int32_t*>(base + b_units + b_begin);
-    plan->d_part_o = reinterpret_cast<float*>(base + b_units + b_begin + b_first);
-    plan->d_part_ml = reinterpret_cast<float*>(base + b_units + b_begin + b_first + b_po);
-    plan->d_flags = reinterpret_cast<uint32_t*>(base + b_units + b_begin + b_first + b_po + b_pml);
-    plan->d_counters = reinterpret_cast<int*>(base + b_units + b_begin + b_first + b_po + b_pml + b_flags);
-    plan->d_unit_count = plan->d_counters + 4;
-    if (opts.trace)
-      plan->d_trace = reinterpret_cast<unsigned long long*>(base + b_units + b_begin + b_first + b_po + b_pml +
-                                                            b_flags + b_cnt);
-    if (b_gf) plan->d_gfold = reinterpret_cast<float*>(base + bytes - b_gf);
-    plan->workspace = int64_t(bytes);
-    e = cudaMemcpy(plan->d_units, s.units.data(), s.units.size() * sizeof(DevUnit), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-      e = cudaMemcpy(plan->d_cta_begin, s.cta_begin.data(), (G + 1) * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-      e = cudaMemcpy(plan->d_cta_first, s.cta_first_unit.data(), G * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(plan->d_flags, 0, G * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMemset(plan->d_counters, 0, b_cnt);
-    if (e == cudaSuccess && plan->d_trace) e = cudaMemset(plan->d_trace, 0, b_trace);
-    if (e == cudaSuccess && b_pt) {  // block table, rows padded to pt_stride (32-entry windows)
-      plan->d_block_table =
-          reinterpret_cast<int32_t*>(base + b_units + b_begin + b_first + b_po + b_pml + b_flags + b_cnt + b_trace);
-      std::vector<int32_t> padded(size_t(p.batch) * plan->pt_stride, 0);
-      for (int b = 0; b < p.batch; ++b)
-        std::copy(p.block_table.begin() + size_t(b) * p.pages_per_seq,
-                  p.block_table.begin() + size_t(b + 1) * p.pages_per_seq, padded.begin() + size_t(b) * plan->pt_stride);
-      e = cudaMemcpy(plan->d_block_table, padded.data(), padded.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
-    }
+    e = cudaMallocHost(&plan->h_stage, plan->up_bytes);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&plan->up_done, cudaEventDisableTiming);
     if (e != cudaSuccess) {
       release_device(plan);
       delete plan;
-      return cuda_fail(e, "plan upload");
+      return cuda_fail(e, "plan staging");
+    }
+    std::memset(plan->h_stage, 0, plan->up_bytes);
+    char* base = static_cast<char*>(plan->d_tables);
+    plan->d_hdr = reinterpret_cast<int32_t*>(base);
+    plan->d_units = reinterpret_cast<DevUnit*>(base + plan->off_units);
+    plan->d_cta_begin = reinterpret_cast<int32_t*>(base + plan->off_begin);
+    plan->d_cta_first = reinterpret_cast<int32_t*>(base + plan->off_first);
+    plan->d_block_table = plan->pt_stride ? reinterpret_cast<int32_t*>(base + plan->off_bt) : nullptr;
+    plan->d_part_o = reinterpret_cast<float*>(base + o_po);
+    plan->d_part_ml = reinterpret_cast<float*>(base + o_pml);
+    plan->d_flags = reinterpret_cast<uint32_t*>(base + o_flags);
+    plan->d_counters = reinterpret_cast<int*>(base + o_cnt);
+    plan->d_unit_count = plan->d_counters + la::kNumCounters;
+    plan->d_grp_count = plan->d_unit_count + U;
+    if (opts.trace) plan->d_trace = reinterpret_cast<unsigned long long*>(base + o_trace);
+    if (b_gf) plan->d_gfold = reinterpret_cast<float*>(base + o_gf);
+    plan->workspace = int64_t(bytes);
+    // kernel state (flags, counters, trace) starts at zero; then the tables, one async copy
+    cudaStream_t st = static_cast<cudaStream_t>(opts.stream);
+    e = cudaMemsetAsync(base + o_flags, 0, o_gf - o_flags, st);
+    if (e != cudaSuccess) {
+      release_device(plan);
+      delete plan;
+      return cuda_fail(e, "plan state init");
+    }
+    la_status us = upload_tables(plan, st, /*sync=*/opts.stream == nullptr);
+    if (us != LA_OK) {
+      release_device(plan);
+      delete plan;
+      return us;
     }
     if (plan->xw) {
       const size_t xb = xchg_bytes(p, plan->xw);
       plan->xflag_off = xchg_flag_off(p, plan->xw);
       e = cudaMalloc(&plan->d_xchg, xb);
       if (e == cudaSuccess) e = cudaMemset(plan->d_xchg, 0, xb);
+      int32_t hdr[kXchgHdrInts];
+      xchg_header(plan, hdr);
+      if (e == cudaSuccess) e = cudaMemcpy(static_cast<char*>(plan->d_xchg) + 64, hdr, sizeof(hdr),
+                                           cudaMemcpyHostToDevice);
       if (e != cudaSuccess) {
         release_device(plan);
         delete plan;
@@ -402,6 +543,44 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     }
   }
   *out = plan;
+  return LA_OK;
+}
+
+la_status la_plan_update(la_plan_t plan, const int32_t* ctx_lens, const int32_t* block_table, void* stream) {
+  if (!plan || !ctx_lens) return fail(LA_ERR_INVALID, "NULL argument");
+  la::Problem& p = plan->prob;
+  if (block_table && p.layout != LA_KV_PAGED) return fail(LA_ERR_INVALID, "block_table given for a non-paged plan");
+  int64_t maxn = 0;
+  la_status st = check_lens(p, ctx_lens, &maxn);
+  if (st != LA_OK) return st;
+  if (p.layout == LA_KV_BHSD && maxn > p.max_ctx)
+    return fail(LA_ERR_INVALID, "ctx_lens exceed the plan's max_ctx (the BHSD slab stride)");
+  if (p.layout == LA_KV_PAGED && maxn > int64_t(p.pages_per_seq) * p.page_size)
+    return fail(LA_ERR_INVALID, "ctx_lens exceed pages_per_seq * page_size");
+  la::Problem np = p;
+  np.ctx_lens.assign(ctx_lens, ctx_lens + p.batch);
+  if (block_table) np.block_table.assign(block_table, block_table + size_t(p.batch) * p.pages_per_seq);
+  if (p.layout == LA_KV_PAGED) {
+    st = check_block_table(np, np.block_table.data());
+    if (st != LA_OK) return st;
+  }
+  if (!plan->host_only && p.layout == LA_KV_PACKED && plan->kinfo.uses_tma_tensor && np.kv_rows() >= (int64_t(1) << 31))
+    return fail(LA_ERR_UNSUPPORTED, "KV cache rows exceed the TMA int32 coordinate range");
+  const la::Problem old_p = p;
+  const la::Schedule old_s = plan->sched;
+  const int old_split = plan->split;
+  p = np;
+  st = plan_schedule(plan, false, 0);
+  if (st == LA_OK && !plan->host_only && plan->sched.grid > plan->slot_cap)
+    st = fail(LA_ERR_STATE, "the new schedule has more (virtual) CTA ranges than the plan allocated: re-plan");
+  if (st == LA_OK && !plan->host_only) st = upload_tables(plan, static_cast<cudaStream_t>(stream), false);
+  if (st != LA_OK) {  // the plan is left as it was
+    p = old_p;
+    plan->sched = old_s;
+    plan->split = old_split;
+    return st;
+  }
+  ++plan->updates;
   return LA_OK;
 }
 
@@ -427,6 +606,9 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   info->tile_rows = p.tile_rows;
   info->engine = plan->engine;
   info->q_rows = p.q_rows();
+  info->quantization_efficiency = quant_eff(plan);
+  info->slot_capacity = plan->slot_cap;
+  info->updates = plan->updates;
   info->num_units = int(s.units.size());
   info->total_iters = s.total_iters;
   info->num_segments = s.num_segments;
@@ -463,6 +645,7 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.v = v;
   a.out = out;
   a.lse = lse;
+  a.hdr = plan->d_hdr;
   a.units = plan->d_units;
   a.cta_begin = plan->d_cta_begin;
   a.cta_first_unit = plan->d_cta_first;
@@ -473,9 +656,9 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.gfold = plan->d_gfold;
   a.counters = plan->d_counters;
   a.unit_count = plan->d_unit_count;
-  a.grp_count = plan->d_unit_count + plan->sched.units.size();
+  a.grp_count = plan->d_grp_count;
+  a.slot_stride = plan->slot_cap;
   a.dynamic = (plan->prob.schedule == LA_SCHED_DYNAMIC || plan->prob.schedule == LA_SCHED_FIXED_SPLIT) ? 1 : 0;
-  a.num_v = plan->sched.grid;
   a.paged = plan->prob.layout == LA_KV_PAGED ? 1 : 0;
   a.block_table = plan->d_block_table;
   a.pt_stride = plan->pt_stride;
@@ -502,12 +685,15 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
     a.xrows = int(plan->prob.q_rows());
     a.xunits = int(plan->sched.units.size());
     a.xflag_off = plan->xflag_off;
-    for (int r = 0; r < plan->xw; ++r) a.xpeer[r] = plan->xpeer[r];
-    a.xerr = reinterpret_cast<int*>(static_cast<char*>(plan->d_xchg) + xchg_bytes(plan->prob, plan->xw) - 256);
+    for (int r = 0; r < plan->xw; ++r) a.xpeer[r] = reinterpret_cast<float*>(reinterpret_cast<char*>(plan->xpeer[r]) + kXchgHead);
+    a.xerr = static_cast<int*>(plan->d_xchg);
   }
   std::string err;
   const la::Problem& p = plan->prob;
-  const int rc = la::launch_decode(plan->kinfo, a, p.kv_rows(), p.head_dim, p.dtype, plan->needs_wait, stream, err);
+  // stream-K hosts may wait on peers (Alg2§28): co-residency by a cooperative launch (the launch
+  // grid never exceeds the co-resident count; measured no cost vs a plain launch)
+  const bool coop = p.schedule == LA_SCHED_STREAMK;
+  const int rc = la::launch_decode(plan->kinfo, a, p.kv_rows(), p.head_dim, p.dtype, coop, stream, &plan->tmaps, err);
   if (rc != 0) return fail(LA_ERR_CUDA, err);
   return LA_OK;
 }
@@ -611,6 +797,19 @@ la_status la_plan_xchg_open(la_plan_t plan, int peer, const void* handle) {
   void* ptr = nullptr;
   cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  // the peer's shape header (written at its la_plan) must describe the same problem
+  int32_t mine[kXchgHdrInts], theirs[kXchgHdrInts];
+  xchg_header(plan, mine);
+  e = cudaMemcpy(theirs, static_cast<char*>(ptr) + 64, sizeof(theirs), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    cudaIpcCloseMemHandle(ptr);
+    return cuda_fail(e, "reading the peer's exchange header");
+  }
+  mine[9] = peer;  // the peer's rank
+  if (std::memcmp(mine, theirs, sizeof(mine)) != 0) {
+    cudaIpcCloseMemHandle(ptr);
+    return fail(LA_ERR_INVALID, "peer plan has another shape, world or rank (exchange header mismatch)");
+  }
   plan->xpeer[peer] = static_cast<float*>(ptr);
   plan->xpeer_ipc[peer] = true;
   return LA_OK;
@@ -630,17 +829,27 @@ la_status la_plan_xchg_attach(la_plan_t plan, int peer, la_plan_t peer_plan) {
   return LA_OK;
 }
 
+la_status la_plan_status(la_plan_t plan) {
+  if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
+  if (plan->host_only) return fail(LA_ERR_STATE, "host-only plan");
+  int err = 0, xerr = 0;
+  cudaError_t e = cudaDeviceSynchronize();
+  int* d_err = plan->d_counters + la::CTR_ERROR;
+  int* d_xerr = plan->d_xchg ? static_cast<int*>(plan->d_xchg) : nullptr;
+  if (e == cudaSuccess) e = cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && d_xerr) e = cudaMemcpy(&xerr, d_xerr, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && err) e = cudaMemset(d_err, 0, sizeof(int));
+  if (e == cudaSuccess && xerr) e = cudaMemset(d_xerr, 0, sizeof(int));
+  if (e != cudaSuccess) return cuda_fail(e, "la_plan_status");
+  if (xerr) return fail(LA_ERR_TIMEOUT, "a cross-GPU exchange wait timed out (a peer rank never arrived)");
+  if (err) return fail(LA_ERR_TIMEOUT, "a host CTA's wait for a peer partial timed out (Alg2 Wait, reading C17)");
+  return LA_OK;
+}
+
 la_status la_plan_xchg_status(la_plan_t plan) {
   if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
   if (!plan->d_xchg) return fail(LA_ERR_STATE, "plan has no exchange buffer");
-  int err = 0;
-  int* d_err = reinterpret_cast<int*>(static_cast<char*>(plan->d_xchg) + xchg_bytes(plan->prob, plan->xw) - 256);
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && err) e = cudaMemset(d_err, 0, sizeof(int));
-  if (e != cudaSuccess) return cuda_fail(e, "la_plan_xchg_status");
-  if (err) return fail(LA_ERR_TIMEOUT, "a cross-GPU exchange wait timed out (a peer rank never arrived)");
-  return LA_OK;
+  return la_plan_status(plan);
 }
 
 void la_plan_destroy(la_plan_t plan) {

@@ -10,11 +10,10 @@
 
 namespace la {
 
-// One work unit (= output tile): the T_m = g query heads of (b, h_kv) against
-// that KV head's n_b cached rows.  32 bytes, uploaded as-is to the device.
 // A work unit = one output tile: (request b, KV head h_kv, query tile m).  Its rows are
 // r0 .. r0 + rows - 1 of the g * N_b rows of (b, h_kv), row r = q-head j * N_b + query i
-// (Alg2§4's C_m query tiles of T_m rows; C_m = 1 whenever g * N_b <= T_m).
+// (Alg2§4's C_m query tiles of T_m rows; C_m = 1 whenever g * N_b <= T_m).  48 bytes,
+// uploaded as-is to the device.
 struct DevUnit {
   int64_t row0;        // first K/V row of the unit (a row = head_dim elements)
   int32_t len;         // n_b
@@ -102,21 +101,27 @@ struct DecodeArgs {
   const void* v;
   float* out;
   float* lse;
+  // Schedule tables (device; rewritten by la_plan_update, so nothing that depends on ctx_lens
+  // is passed by value -- a CUDA graph captured on the plan replays across updates):
+  const int32_t* hdr;  // [0] = num_v: (virtual) CTA ranges of the current schedule
   const DevUnit* units;
   const int32_t* cta_begin;
   const int32_t* cta_first_unit;
-  float* part_o;      // [2][grid][group][d]  Op of Alg2§20 (slot 1: dynamic-mode host partial)
-  float* part_ml;     // [2][grid][group][4]  mp, lp, -, - of Alg2§21-22 (m in log2 units; 16 B rows)
-  uint32_t* flags;    // [grid]               flags of Alg2§23/§28, epoch-valued (reading C17)
-  int* counters;      // [4] virtual-CTA claim counter, CTAs done (dynamic mode); CTAs exited,
-                      //     launch epoch (device-side: a captured CUDA graph replays correctly)
+  float* part_o;      // [2][slot_stride][group][d]  Op of Alg2§20 (slot 1: host partials that wait
+                      //                              or are folded by the dynamic tree)
+  float* part_ml;     // [2][slot_stride][group][4]  mp, lp, -, - of Alg2§21-22 (m in log2 units)
+  uint32_t* flags;    // [slot_stride]               flags of Alg2§23/§28, epoch-valued (reading C17)
+  int* counters;      // [kNumCounters] see CTR_* (device-side: a captured CUDA graph replays correctly)
   int* unit_count;    // [units] dynamic mode: fold-tree groups completed per unit
-  int* grp_count;     // [grid]  dynamic mode: segments published per fold-tree group
+  int* grp_count;     // [2][slot_stride] dynamic mode: segments published per fold-tree group;
+                      //   a unit's first group (g0 = its host) counts at slot_stride + g0, every
+                      //   other group at g0 -- a virtual CTA can end one unit's group and host
+                      //   the next unit's first group, so one index per CTA would collide
+  int slot_stride;    // capacity of (virtual) CTAs: partial slot 1 of CTA v is slot_stride + v
   unsigned long long* trace;  // [phys_grid][LA_TRACE_FIELDS] or nullptr
   float* gfold;       // [phys_grid][KernelInfo::global_fold_floats] or nullptr
   int dynamic;        // 1: claim virtual CTAs dynamically, last-arriver fold
-  int num_v;          // (virtual) CTAs
-  int grid;           // CTAs launched
+  int grid;           // CTAs launched (fixed for the plan's life)
   int tile_n;
   int stage_tokens;
   int group;          // T_m: rows of a partial slot (a unit's own row count is DevUnit::rows)
@@ -146,6 +151,19 @@ struct DecodeArgs {
   int* xerr;          // own buffer's error word: 1 after a wait timed out
 };
 
+// DecodeArgs::counters
+enum {
+  CTR_CLAIM = 0,   // dynamic: next virtual CTA to claim
+  CTR_DONE = 1,    // dynamic: CTAs done (the last resets CTR_CLAIM)
+  CTR_EXITED = 2,  // CTAs exited (the last one advances CTR_EPOCH / CTR_XEPOCH)
+  CTR_EPOCH = 3,   // launch epoch: value of this launch's Signal flags (reading C17)
+  CTR_XEPOCH = 4,  // cross-GPU exchange sequence: advanced only by exchange launches
+  CTR_ERROR = 5,   // 1: an intra-GPU host wait (Alg2§28) gave up after kWaitTimeoutNs
+  kNumCounters = 8
+};
+constexpr unsigned long long kWaitTimeoutNs = 10000000000ull;  // 10 s: intra-GPU host waits
+constexpr unsigned long long kXchgTimeoutNs = 5000000000ull;   // 5 s: cross-GPU exchange waits
+
 constexpr int kMaxXchgWorld = 8;
 
 // Kernel configuration for (dtype, head_dim, group): threads, dynamic smem, max stage tokens.
@@ -154,16 +172,23 @@ struct KernelInfo {
   int threads = 0;
   int smem_bytes = 0;
   int stage_tokens_max = 0;
-  bool uses_tma_tensor = false;   // K/V TMA tensor maps (encoded per launch)
+  bool uses_tma_tensor = false;   // K/V TMA tensor maps (cached per (k, v, rows) in the plan)
   int box_halves = 2;             // d = 128 bf16/fp16 maps: 128-B row halves per TMA box
   int global_fold_floats = 0;     // > 0: consumer -> epilogue fold buffers live in plan-owned
                                   // global scratch (floats per CTA), not shared memory
   const void* fn = nullptr;
 };
 KernelInfo decode_kernel_info(int dtype, int head_dim, int group, int engine);
-// Launch the decode kernel (cooperative when a static-schedule CTA waits on a peer).
+// The plan's encoded K / V tensor maps and the (k, v, rows) they were encoded for.
+struct TmapCache {
+  const void* k = nullptr;
+  const void* v = nullptr;
+  int64_t rows = -1;
+  alignas(64) unsigned char maps[256];  // CUtensorMap k, v
+};
+// Launch the decode kernel (cooperative when a static-schedule CTA may wait on a peer).
 int launch_decode(const KernelInfo& ki, const DecodeArgs& a, int64_t kv_rows, int head_dim, int dtype,
-                  bool cooperative, void* stream, std::string& err);
+                  bool cooperative, void* stream, TmapCache* cache, std::string& err);
 int launch_combine(const float* o_parts, const float* lse_parts, int parts, int rows,
                    int head_dim, float* out, float* lse, void* stream, std::string& err);
 void note_launch();

@@ -32,8 +32,8 @@ _SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, 
                 "fixed_split": LA_SCHED_FIXED_SPLIT}
 
 # Every symbol include/la.h declares (tests check the library exports all of them).
-EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
-           "la_decode_partial", "la_combine", "la_decode_host", "la_plan_destroy",
+EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_info_get", "la_plan_export", "la_decode",
+           "la_decode_partial", "la_combine", "la_decode_host", "la_plan_status", "la_plan_destroy",
            "la_launch_count", "la_status_string", "la_last_error", "la_version", "la_plan_trace",
            "la_plan_xchg_handle", "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status")
 
@@ -53,7 +53,7 @@ class la_plan_opts(ctypes.Structure):
                 ("page_size", ctypes.c_int), ("num_pages", ctypes.c_int64), ("q_len", ctypes.c_int),
                 ("causal", ctypes.c_int), ("xchg_world", ctypes.c_int), ("xchg_rank", ctypes.c_int),
                 ("q_lens", ctypes.POINTER(ctypes.c_int32)), ("k_scale", ctypes.c_float),
-                ("v_scale", ctypes.c_float), ("engine", ctypes.c_int)]
+                ("v_scale", ctypes.c_float), ("engine", ctypes.c_int), ("stream", ctypes.c_void_p)]
 
 
 class la_plan_info(ctypes.Structure):
@@ -64,7 +64,8 @@ class la_plan_info(ctypes.Structure):
                                               "workspace_bytes", "kv_bytes")] + \
                [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64), ("split", ctypes.c_int),
                 ("q_len", ctypes.c_int), ("tile_rows", ctypes.c_int), ("q_rows", ctypes.c_int64),
-                ("engine", ctypes.c_int)]
+                ("engine", ctypes.c_int), ("quantization_efficiency", ctypes.c_double),
+                ("slot_capacity", ctypes.c_int), ("updates", ctypes.c_int64)]
 
 
 _lib = None
@@ -83,6 +84,8 @@ def lib() -> ctypes.CDLL:
     L.la_plan_opts_init.argtypes = [ctypes.POINTER(la_plan_opts)]
     L.la_plan.argtypes = [i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int32), i32, i32,
                           ctypes.POINTER(la_plan_opts), ctypes.POINTER(vp)]
+    L.la_plan_update.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), vp]
+    L.la_plan_status.argtypes = [vp]
     L.la_plan_info_get.argtypes = [vp, ctypes.POINTER(la_plan_info)]
     L.la_plan_export.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.c_size_t,
                                  ctypes.POINTER(ctypes.c_size_t)]
@@ -102,7 +105,7 @@ def lib() -> ctypes.CDLL:
     L.la_launch_count.restype = i64
     L.la_status_string.restype = ctypes.c_char_p
     L.la_last_error.restype = ctypes.c_char_p
-    for name in ("la_plan_opts_init", "la_plan", "la_plan_info_get", "la_plan_export", "la_decode",
+    for name in ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_status", "la_plan_info_get", "la_plan_export", "la_decode",
                  "la_decode_partial", "la_combine", "la_decode_host", "la_plan_trace", "la_plan_xchg_handle",
                  "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status"):
         if hasattr(L, name):
@@ -144,7 +147,7 @@ class Plan:
                  dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
                  causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None,
-                 k_scale: float = 0.0, v_scale: float = 0.0, engine: str = "auto"):
+                 k_scale: float = 0.0, v_scale: float = 0.0, engine: str = "auto", stream=None):
         L = lib()
         opts = la_plan_opts()
         _check(L.la_plan_opts_init(ctypes.byref(opts)), "la_plan_opts_init")
@@ -174,6 +177,8 @@ class Plan:
         opts.k_scale = float(k_scale)  # dtype "fp8": K = codes x k_scale, V = codes x v_scale
         opts.v_scale = float(v_scale)
         opts.engine = _ENGINE_CODES[engine]  # "auto", "mma" (mma.sync) or "tcgen05" (T_m > 1 tiles)
+        if stream is not None:  # initial table upload left in flight on this stream
+            opts.stream = _stream(stream)
         self.engine = engine
         if q_lens is not None:  # heterogeneous batch: N_b per request
             ql = np.ascontiguousarray(np.asarray(q_lens, dtype=np.int32))
@@ -188,7 +193,38 @@ class Plan:
         self.dtype = dtype
         self.layout = layout
         self.ctx_lens = [int(x) for x in ctx_lens]
+        self.q_lens = None if q_lens is None else [int(x) for x in q_lens]
         self.info = self._info()
+        self._kv_rows = self._cache_rows(max_ctx, num_pages, page_size)
+
+    def _cache_rows(self, max_ctx, num_pages, page_size):
+        """Rows of one K (or V) cache in this plan's layout (binding-side size checks)."""
+        inf = self.info
+        if self.layout == "bhsd":
+            return inf.batch * inf.heads_kv * (int(max_ctx) or max(self.ctx_lens))
+        if self.layout == "packed":
+            return inf.heads_kv * sum(self.ctx_lens)
+        return int(num_pages) * inf.heads_kv * int(page_size)
+
+    def update(self, ctx_lens: Sequence[int], block_table=None, stream=None):
+        """``la_plan_update``: re-plan for new context lengths, one async table upload on
+        ``stream`` (the current stream by default); no allocation, graph-replayable."""
+        lens = (ctypes.c_int32 * len(ctx_lens))(*[int(x) for x in ctx_lens])
+        bt_ptr = None
+        if block_table is not None:
+            bt = np.ascontiguousarray(np.asarray(block_table, dtype=np.int32))
+            self._bt = bt
+            bt_ptr = bt.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        strm = None if _is_host_only(self) else _stream(stream)
+        _check(lib().la_plan_update(self._h, lens, bt_ptr, strm), "la_plan_update")
+        self.ctx_lens = [int(x) for x in ctx_lens]
+        if self.layout == "packed":
+            self._kv_rows = self.info.heads_kv * sum(self.ctx_lens)
+        self.info = self._info()
+
+    def status(self):
+        """``la_plan_status``: synchronises; raises LaError(LA_ERR_TIMEOUT) if an in-kernel wait gave up."""
+        _check(lib().la_plan_status(self._h), "la_plan_status")
 
     def _info(self) -> la_plan_info:
         inf = la_plan_info()
@@ -227,23 +263,48 @@ class Plan:
             lse = torch.empty(rows, dtype=torch.float32, device=q.device)
         return out, lse
 
-    def _check_inputs(self, q, k, v):
-        for name, t in (("q", q), ("k", k), ("v", v)):
+    _KV_DTYPE = {"bf16": ("bfloat16", 2), "fp16": ("float16", 2), "fp32": ("float32", 4), "fp8": (None, 1)}
+
+    def _check_inputs(self, q, k, v, out=None, lse=None):
+        """Marshalling checks only (the C ABI cannot see sizes): dtype, element count and
+        device of every tensor against the plan, so no kernel or TMA descriptor can read or
+        write outside an allocation."""
+        import torch
+        inf = self.info
+        dev = q.device
+        for name, t in (("q", q), ("k", k), ("v", v), ("out", out), ("lse", lse)):
+            if t is None:
+                continue
             if not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous CUDA tensor")
+            if t.device != dev:
+                raise ValueError(f"{name} is on {t.device}, q on {dev}")
+        qdt = torch.bfloat16 if self.dtype == "fp8" else getattr(torch, self._KV_DTYPE[self.dtype][0])
+        if q.dtype != qdt or q.numel() != inf.q_rows * inf.head_dim:
+            raise ValueError(f"q must be {qdt} with {inf.q_rows * inf.head_dim} elements")
+        kv_bytes = self._kv_rows * inf.head_dim * self._KV_DTYPE[self.dtype][1]
+        for name, t in (("k", k), ("v", v)):
+            if self.dtype != "fp8" and t.dtype != qdt:
+                raise ValueError(f"{name} must be {qdt}")
+            if t.element_size() * t.numel() < kv_bytes:
+                raise ValueError(f"{name} holds {t.element_size() * t.numel()} bytes < the plan's {kv_bytes}")
+        if out is not None and (out.dtype != torch.float32 or out.numel() < inf.q_rows * inf.head_dim):
+            raise ValueError(f"out must be float32 with >= {inf.q_rows * inf.head_dim} elements")
+        if lse is not None and (lse.dtype != torch.float32 or lse.numel() < inf.q_rows):
+            raise ValueError(f"lse must be float32 with >= {inf.q_rows} elements")
 
     def decode(self, q, k, v, out=None, lse=None, stream=None, want_lse: bool = True):
         """``la_decode``; returns (out fp32 (B, H_q, d), lse fp32 (B, H_q) or None)."""
-        self._check_inputs(q, k, v)
         out, lse = self._outputs(q, out, lse, want_lse)
+        self._check_inputs(q, k, v, out, lse)
         _check(lib().la_decode(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _stream(stream)),
                "la_decode")
         return out, lse
 
     def decode_partial(self, q, k_shard, v_shard, o_part=None, lse_part=None, stream=None):
         """``la_decode_partial`` on one sequence shard; lse is always produced."""
-        self._check_inputs(q, k_shard, v_shard)
         o_part, lse_part = self._outputs(q, o_part, lse_part, True)
+        self._check_inputs(q, k_shard, v_shard, o_part, lse_part)
         _check(lib().la_decode_partial(self._h, _ptr(q), _ptr(k_shard), _ptr(v_shard), _ptr(o_part),
                                        _ptr(lse_part), _stream(stream)), "la_decode_partial")
         return o_part, lse_part
@@ -284,6 +345,10 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def _is_host_only(plan: "Plan") -> bool:
+    return plan.info.workspace_bytes == 0
 
 
 def la_plan(*args, **kw) -> Plan:

@@ -149,3 +149,36 @@ def test_lean_tile_monotone_max_and_errors():
         oracle.lean_tile(q, k, v, 1.0, 3, 3, 4)
     with pytest.raises(ValueError):
         oracle.lean_tile(q, k, v, 1.0, 0, 11, 4)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_fold_every_order_equals_the_materialised_union(k):
+    """oracle.fold is Alg. 2's host loop (§27-36): a left fold f(f(f(s0, s1), s2) ..).
+    In EVERY order of k <= 5 block partials (m spread +-50) it must equal the materialised
+    partial of the union of the blocks (§4.1's closed form) -- a dropped weight,
+    a wrong sign in an exponent or an unscaled l fails this; finalising it gives Eq. 1."""
+    rng = np.random.default_rng(40 + k)
+    d = 5
+    q = rng.normal(size=(2, d))
+    for trial in range(3):
+        lens = rng.integers(1, 8, size=k)
+        blocks = []
+        for n in lens:
+            kk = rng.normal(size=(n, d)) + rng.uniform(-50, 50) * q[0] / (q[0] @ q[0])
+            blocks.append((kk, rng.normal(size=(n, d))))
+        parts = [oracle.partial(q, kk, vv, 1.0) for kk, vv in blocks]
+        K = np.concatenate([b[0] for b in blocks])
+        V = np.concatenate([b[1] for b in blocks])
+        union = oracle.partial(q, K, V, 1.0)
+        O_ref, L_ref = oracle.decode_attention_unit(q, K, V, 1.0)
+        for perm in itertools.permutations(range(k)):
+            r = oracle.fold(parts[i] for i in perm)
+            assert np.max(np.abs(r.m - union.m)) <= 1e-13 * np.max(np.abs(union.m))
+            assert np.max(np.abs(r.l - union.l) / union.l) <= 1e-12
+            assert np.max(np.abs(r.o - union.o)) <= 1e-12 * np.max(np.abs(union.o))
+            O, L = oracle.finalize(r)
+            assert np.max(np.abs(O - O_ref)) <= 1e-12 and np.max(np.abs(L - L_ref)) <= 1e-12
+    # the neutral element anywhere in the sequence changes nothing, bitwise (Alg1§8-9)
+    a = oracle.fold([parts[0], oracle.neutral(2, d)] + parts[1:])
+    b = oracle.fold(parts)
+    assert np.array_equal(a.o, b.o) and np.array_equal(a.m, b.m) and np.array_equal(a.l, b.l)

@@ -241,7 +241,26 @@ def test_fixed_split_ranges_match_fixed_split_segments():
         ref = oracle.fixed_split_segments(c_n, 10 ** 6, s)
         assert [(x.unit, x.begin, x.end, x.host, x.finishing) for x in segs] == \
                [(x.unit, x.begin, x.end, x.host, x.finishing) for x in ref]
-    # heuristic: efficiency-maximising split, no split once units fill 80% of the SMs
-    assert oracle.fa2_num_splits(1, 10 ** 6, 108) == 108 or oracle.fa2_num_splits(1, 10 ** 6, 108) >= 92
-    assert oracle.fa2_num_splits(200, 64, 148) == 1
-    assert oracle.fa2_num_splits(56, 2, 108) == 1 or oracle.fa2_num_splits(56, 2, 108) == 2
+    # the split heuristic: pinned by exact values below (test_fa2_num_splits_hand_derived)
+
+
+@pytest.mark.parametrize("units,max_cn,sms,expect", [
+    # FlashAttention-2's num_splits heuristic (FlashDecoding's split rule, the paper's FD
+    # baseline P:505; "FD opts not to split ... [when] the total number of heads in the batch
+    # exceeds the number of SMs"), evaluated BY HAND.  With w(s) = units*s/sms waves,
+    # eff(s) = w / ceil(w); no split if units >= 0.8*sms; else the smallest s <= min(128, sms,
+    # max_cn) with eff(s) >= 0.85 * max_s eff(s).
+    (1, 10 ** 6, 108, 92),   # eff(s) = s/108, max 1 at s = 108; 0.85*108 = 91.8 -> s = 92
+    (56, 2, 108, 1),         # s <= 2: eff(1) = 56/108 = .5185, eff(2) = 1.037/2 = .5185 -> 1
+    (56, 2048, 108, 5),      # eff 1:.519 2:.519 3:.778 4:.691 5:2.593/3=.864 >= .85 (max 1 at s=27)
+    (56, 2048, 148, 5),      # eff 1:.378 2:.757 3:.568 4:.757 5:1.892/2=.946 >= .85 (max 1 at s=37)
+    (32, 2048, 148, 4),      # c2: eff 1:.216 2:.432 3:.649 4:.865 >= .85 (max 1 at s=37)
+    (64, 512, 148, 2),       # c3 units: eff 1:.432 2:.865 >= .85 (max 1 at s=37)
+    (10, 3, 148, 3),         # max_cn caps s at 3: eff(3) = .203 is the max -> 3
+    (118, 4, 148, 1),        # 118 < 118.4: every eff(s) = .797 = max -> s = 1
+    (119, 4, 148, 1),        # 119 >= 0.8 * 148: no split at all
+    (200, 64, 148, 1),
+    (128, 2048, 148, 1),     # batch 4 x 32 heads fills 80% of 148 SMs
+])
+def test_fa2_num_splits_hand_derived(units, max_cn, sms, expect):
+    assert oracle.fa2_num_splits(units, max_cn, sms) == expect
