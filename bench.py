@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
                     help="N > 1: the fused in-kernel NVLink exchange (p2p, NEXT-2) or NCCL all-gather + "
                          "la_combine; auto = p2p on the nccl backend")
-    ap.add_argument("--dyn-first", type=int, default=750, help="dynamic schedule: permille in the first round")
+    ap.add_argument("--dyn-first", type=int, default=940, help="dynamic schedule: head share of each range (permille)")
     ap.add_argument("--dyn-min", type=int, default=2, help="dynamic schedule: smallest virtual CTA (LeanTiles)")
     return ap.parse_args()
 

@@ -82,11 +82,13 @@ typedef enum {
   LA_SCHED_STREAMK = 0,    /* Eq. 2 + Alg. 2 exactly: G equal contiguous iteration ranges,
                               host CTAs wait on their peers' flags (cooperative launch)  */
   LA_SCHED_SEQUENTIAL = 1, /* FA2: one CTA per unit, G = #units            */
-  LA_SCHED_DYNAMIC = 2,    /* Alg. 2's decomposition over more, guided-size "virtual CTAs"
-                              that the persistent CTAs claim in order (atomic counter); a
-                              unit's partials are folded by a fixed tree of last arrivers in
-                              ascending order -- same result semantics, balances TIME instead
-                              of LeanTile counts                              */
+  LA_SCHED_DYNAMIC = 2,    /* Alg. 2's equal ranges, each cut into a HEAD (its first
+                              dyn_first_permille / 1000) and <= 8 tail chunks of >= dyn_min_chunk
+                              LeanTiles; the persistent CTAs claim every head, then the chunks
+                              round by round (atomic counter), so fast SMs take more chunks.  A
+                              unit's pieces are folded by its LAST arriving piece in ascending
+                              order -- same result semantics, bitwise deterministic, balances
+                              TIME instead of LeanTile counts                    */
   LA_SCHED_FIXED_SPLIT = 3 /* FlashDecoding's fixed-split decomposition: every
                               unit cut into `split` near-equal chunks (first chunks take the
                               extra LeanTile), chunks run in order on the persistent
@@ -107,8 +109,9 @@ typedef struct {
   int host_only;     /* 1 -> plan the schedule only, no device state (inspection/tests)   */
   int schedule;      /* la_schedule, default LA_SCHED_STREAMK (Alg. 2 exactly)            */
   int trace;         /* 1 -> every la_decode records a per-CTA timeline (la_plan_trace)     */
-  int dyn_first_permille; /* LA_SCHED_DYNAMIC: share of I in the first G ranges (default 750) */
-  int dyn_min_chunk;      /* LA_SCHED_DYNAMIC: smallest virtual CTA in LeanTiles (default 2)  */
+  int dyn_first_permille; /* LA_SCHED_DYNAMIC: head share of each Eq. 2 range, permille (default 940;
+                             1000 = no tail: Alg. 2's ranges exactly)                        */
+  int dyn_min_chunk;      /* LA_SCHED_DYNAMIC: smallest tail chunk in LeanTiles (default 2)    */
   int split;              /* LA_SCHED_FIXED_SPLIT: chunks per unit; 0 -> FlashAttention-2's
                              num_splits heuristic (wave efficiency >= 85% of the best)     */
   /* LA_KV_PAGED only: */
@@ -255,6 +258,14 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info);
 la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t* n_rows);
 
 /*
+ * la_plan_export_claims -- the order in which the persistent CTAs take the (virtual) CTA
+ * ranges: claim c runs range claims[c] (LA_SCHED_DYNAMIC: every head, then the tail chunks
+ * round by round; the other schedules: 0, 1, 2, ...).  HOST buffer of cap int32 (NULL with
+ * cap = 0 queries the count into *n).  LA_ERR_INVALID if cap is non-zero but too small.
+ */
+la_status la_plan_export_claims(la_plan_t plan, int32_t* claims, size_t cap, size_t* n);
+
+/*
  * la_decode -- one decode-attention step on `stream` (asynchronous).
  *
  * q: device (B, H_q, d) of the plan's dtype (bf16 for LA_FP8_E4M3), contiguous.  k_cache, v_cache: device, plan's
@@ -336,6 +347,8 @@ la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* 
  * la_plan_xchg_status: la_plan_status on an exchange plan (LA_ERR_STATE without one).
  * la_plan_xchg_open checks the peer's shape header (batch, heads, head_dim, dtype, rows,
  *   units, world, rank) written into its buffer at la_plan: LA_ERR_INVALID on a mismatch.
+ * LA_SCHED_DYNAMIC on an exchange plan claims its ranges in iteration order (no tail chunks):
+ *   deadlock freedom needs every CTA to visit units in increasing order.
  * The exchange flags carry an exchange sequence number that only exchange launches
  *   advance (la_decode_partial on the plan does not), and waits compare wrap-safe.
  * Requires q_len == 1 or causal == 0 (a causal multi-token mask is not shard-local).

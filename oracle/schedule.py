@@ -136,26 +136,46 @@ def segments_from_ranges(c_n: Sequence[int], begins: Sequence[int]) -> List[Segm
     return segs
 
 
-def guided_ranges(total_iters: int, grid: int, first_permille: int = 750, min_chunk: int = 2) -> List[int]:
-    """Range boundaries of the DYNAMIC schedule (not in the paper): `grid`
-    equal ranges holding first_permille/1000 of the iterations, then rounds of `grid` ranges
-    each covering half of the remainder (at least min_chunk), until all are covered."""
-    begins = [0]
-    pos = 0
-    first = total_iters * first_permille // (1000 * grid)
-    if first >= 1:
-        for _ in range(grid):
-            pos += first
-            begins.append(pos)
-    while pos < total_iters:
-        rem = total_iters - pos
-        c = max(min_chunk, -(-rem // (2 * grid)))
-        for _ in range(grid):
-            if pos >= total_iters:
-                break
-            pos = min(total_iters, pos + c)
-            begins.append(pos)
-    return begins
+def balanced_ranges(total_iters: int, grid: int, head_permille: int = 940, min_chunk: int = 2,
+                    max_chunks: int = 8) -> Tuple[List[int], List[int]]:
+    """Virtual-CTA ranges and claim order of the DYNAMIC schedule (this build's
+    extension, not in the paper).  Every range of Eq. 2 (Alg. 2 §7-9, reading C8) is cut
+    into a HEAD -- its first part -- and a TAIL of k chunks of s LeanTiles:
+
+        L = |range g|,  T0 = floor(L (1000 - head_permille) / 1000)
+        s = max(min_chunk, ceil(T0 / max_chunks)),  k = floor(T0 / s),  tail = the last k s
+
+    Returns (begins, claim): ``begins`` the boundaries of all pieces in iteration order
+    (range 0's head, its chunks, range 1's head, ...; empty ranges contribute nothing) and
+    ``claim`` the order in which persistent CTAs take them: every head (in range order),
+    then chunk 0 of every range that has one, chunk 1 of every range, ...  head_permille =
+    1000 leaves no tail: exactly Alg. 2's equal ranges, claimed in range order."""
+    begins: List[int] = [0]
+    heads: List[int] = []
+    tails: List[List[int]] = []
+    v = 0
+    for g in range(grid):
+        b, e = cta_range(total_iters, grid, g)
+        L = e - b
+        if L == 0:
+            continue
+        t0 = L * (1000 - head_permille) // 1000
+        s = max(min_chunk, -(-t0 // max_chunks))
+        k = min(t0 // s, (L - 1) // s)          # the head keeps >= 1 LeanTile
+        heads.append(v)                           # head [b, e - k s)
+        begins.append(e - k * s)
+        v += 1
+        chunks = []
+        for j in range(1, k + 1):                 # chunk j-1: [e - (k - j + 1) s, e - (k - j) s)
+            chunks.append(v)
+            begins.append(e - (k - j) * s)
+            v += 1
+        tails.append(chunks)
+    claim = list(heads)
+    for j in range(max((len(t) for t in tails), default=0)):
+        claim.extend(t[j] for t in tails if j < len(t))
+    assert len(begins) == v + 1 and sorted(claim) == list(range(v))
+    return begins, claim
 
 
 def fixed_split_ranges(c_n: Sequence[int], split: int) -> List[int]:

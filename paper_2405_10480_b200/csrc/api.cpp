@@ -32,22 +32,22 @@ struct la_plan_s {
   int64_t updates = 0;       // la_plan_update calls
   // ---- device state, ONE allocation ---------------------------------------------------
   // upload region (rewritten by la_plan_update with one async copy):
-  //   [hdr 256 B][units U x 48 B][cta_begin cap + 1][cta_first cap][block table B x pt_stride]
+  //   [hdr 256 B][units U x 48 B][cta_begin cap + 1][cta_first cap][claim cap][block table B x pt_stride]
   // then kernel state: partials [2][cap][rows][d] + [2][cap][rows][4], flags [cap],
-  //   counters [kNumCounters] + unit_count [U] + grp_count [2 cap], trace, engine fold scratch
+  //   counters [kNumCounters] + unit_count [U], trace, engine fold scratch
   void* d_tables = nullptr;
-  size_t up_bytes = 0, off_units = 0, off_begin = 0, off_first = 0, off_bt = 0;
+  size_t up_bytes = 0, off_units = 0, off_begin = 0, off_first = 0, off_claim = 0, off_bt = 0;
   int32_t* d_hdr = nullptr;
   DevUnit* d_units = nullptr;
   int32_t* d_cta_begin = nullptr;
   int32_t* d_cta_first = nullptr;
+  int32_t* d_claim = nullptr;
   int32_t* d_block_table = nullptr;
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   uint32_t* d_flags = nullptr;
   int* d_counters = nullptr;
   int* d_unit_count = nullptr;
-  int* d_grp_count = nullptr;
   unsigned long long* d_trace = nullptr;
   float* d_gfold = nullptr;
   unsigned char* h_stage = nullptr;   // pinned host copy of the upload region
@@ -170,7 +170,7 @@ la_status plan_schedule(la_plan_s* plan, bool first, int64_t icap_hint) {
     la::sequential_ranges(s.units, s.cta_begin);
   } else if (p.schedule == LA_SCHED_DYNAMIC) {
     const int G = plan->opt_grid ? launch : int(std::max<int64_t>(1, std::min<int64_t>(launch, I)));
-    la::guided_ranges(I, G, plan->opt_dyn_first, plan->opt_dyn_min, s.cta_begin);
+    la::balanced_ranges(I, G, plan->opt_dyn_first, plan->opt_dyn_min, la::kMaxTailChunks, s.cta_begin, s.claim);
   } else if (p.schedule == LA_SCHED_FIXED_SPLIT) {
     int64_t max_cn = 1;
     for (const DevUnit& u : s.units) max_cn = std::max<int64_t>(max_cn, u.iter_end - u.iter_begin);
@@ -181,20 +181,28 @@ la_status plan_schedule(la_plan_s* plan, bool first, int64_t icap_hint) {
     const int G = plan->opt_grid ? launch : int(std::max<int64_t>(1, std::min<int64_t>(launch, I)));
     la::streamk_ranges(I, G, s.cta_begin);
   }
+  if (p.schedule != LA_SCHED_DYNAMIC) {  // ranges are claimed in order
+    s.claim.resize(s.cta_begin.size() - 1);
+    for (size_t v = 0; v < s.claim.size(); ++v) s.claim[v] = int32_t(v);
+  }
   la::finish_schedule(s);
   return LA_OK;
 }
 
 // Quantization efficiency: I / (W x max_w load_w).  Static schedules:
-// W = the ranges (one CTA each); dynamic / fixed split: W = the persistent CTAs, range j on
-// CTA j mod W (the launch-order wave model, as oracle.fixed_split_segments deals chunks).
+// W = the ranges (one CTA each); dynamic / fixed split: W = the persistent CTAs, the c-th
+// claimed range on CTA c mod W (the launch-order wave model, as oracle.fixed_split_segments
+// deals chunks; the run-time claims of the dynamic schedule are faster than this model).
 double quant_eff(const la_plan_s* plan) {
   const la::Schedule& s = plan->sched;
   const bool waves = plan->prob.schedule == LA_SCHED_DYNAMIC || plan->prob.schedule == LA_SCHED_FIXED_SPLIT;
   const int W = waves ? s.phys_grid : s.grid;
   if (W < 1 || s.total_iters < 1) return 0.0;
   std::vector<int64_t> load(size_t(W), 0);
-  for (int v = 0; v < s.grid; ++v) load[size_t(waves ? v % W : v)] += s.cta_begin[v + 1] - s.cta_begin[v];
+  for (int c = 0; c < s.grid; ++c) {
+    const int v = waves ? s.claim[size_t(c)] : c;
+    load[size_t(waves ? c % W : c)] += s.cta_begin[v + 1] - s.cta_begin[v];
+  }
   const int64_t mx = *std::max_element(load.begin(), load.end());
   return mx > 0 ? double(s.total_iters) / (double(W) * double(mx)) : 0.0;
 }
@@ -214,6 +222,7 @@ la_status upload_tables(la_plan_s* plan, cudaStream_t stream, bool sync) {
   std::memcpy(h + plan->off_units, s.units.data(), s.units.size() * sizeof(DevUnit));
   std::memcpy(h + plan->off_begin, s.cta_begin.data(), size_t(s.grid + 1) * sizeof(int32_t));
   std::memcpy(h + plan->off_first, s.cta_first_unit.data(), size_t(s.grid) * sizeof(int32_t));
+  std::memcpy(h + plan->off_claim, s.claim.data(), size_t(s.grid) * sizeof(int32_t));
   const la::Problem& p = plan->prob;
   if (plan->pt_stride) {  // block table, rows padded to pt_stride (the producer reads 32-entry windows)
     int32_t* bt = reinterpret_cast<int32_t*>(h + plan->off_bt);
@@ -282,7 +291,7 @@ la_status la_plan_opts_init(la_plan_opts* o) {
   o->num_sms = 148;
   o->ctas_per_sm = 1;
   o->schedule = LA_SCHED_STREAMK;
-  o->dyn_first_permille = 750;
+  o->dyn_first_permille = 940;
   o->dyn_min_chunk = 2;
   o->q_len = 1;
   o->causal = 1;
@@ -408,7 +417,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   plan->xw = xw;
   plan->xr = xw ? opts.xchg_rank : 0;
   plan->opt_grid = opts.grid;
-  plan->opt_dyn_first = opts.dyn_first_permille;
+  // exchange plans claim the dynamic schedule's ranges in iteration order (no tail chunks):
+  // the cross-GPU deadlock-freedom argument needs every CTA to visit units in increasing order
+  plan->opt_dyn_first = xw ? 1000 : opts.dyn_first_permille;
   plan->opt_dyn_min = opts.dyn_min_chunk;
   plan->opt_split = opts.split;
 
@@ -463,9 +474,14 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   }
   plan->stage_tokens = plan->host_only ? std::min(s.tile_n, 64) : std::min(s.tile_n, plan->kinfo.stage_tokens_max);
   // capacity of (virtual) CTAs: static schedules never exceed the launch grid (stream-K) or the
-  // unit count (sequential); dynamic / fixed-split range counts vary with ctx_lens, so leave room
-  const bool virt = p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT;
-  plan->slot_cap = virt ? 2 * s.grid + s.phys_grid : std::max(s.grid, s.phys_grid);
+  // unit count (sequential), the dynamic one (1 + kMaxTailChunks) pieces per range; the
+  // fixed-split chunk count varies with ctx_lens, so leave room
+  if (p.schedule == LA_SCHED_DYNAMIC)
+    plan->slot_cap = std::max(s.grid, s.phys_grid * (1 + la::kMaxTailChunks));
+  else if (p.schedule == LA_SCHED_FIXED_SPLIT)
+    plan->slot_cap = 2 * s.grid + s.phys_grid;
+  else
+    plan->slot_cap = std::max(s.grid, s.phys_grid);
 
   // ---- device state -------------------------------------------------------------------
   if (!plan->host_only) {
@@ -475,12 +491,13 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     plan->off_units = 256;
     plan->off_begin = plan->off_units + align256(U * sizeof(DevUnit));
     plan->off_first = plan->off_begin + align256(size_t(CAP + 1) * sizeof(int32_t));
-    plan->off_bt = plan->off_first + align256(size_t(CAP) * sizeof(int32_t));
+    plan->off_claim = plan->off_first + align256(size_t(CAP) * sizeof(int32_t));
+    plan->off_bt = plan->off_claim + align256(size_t(CAP) * sizeof(int32_t));
     plan->up_bytes = plan->off_bt + align256(size_t(p.batch) * plan->pt_stride * sizeof(int32_t));
     const size_t b_po = align256(size_t(CAP) * 2 * p.rows() * head_dim * sizeof(float));
     const size_t b_pml = align256(size_t(CAP) * 2 * p.rows() * 4 * sizeof(float));
     const size_t b_flags = align256(size_t(CAP) * sizeof(uint32_t));
-    const size_t b_cnt = align256((la::kNumCounters + U + 2 * size_t(CAP)) * sizeof(int));
+    const size_t b_cnt = align256((la::kNumCounters + U) * sizeof(int));
     const size_t b_trace = opts.trace ? align256(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
     const size_t b_gf = align256(size_t(GP) * plan->kinfo.global_fold_floats * sizeof(float));
     const size_t o_po = plan->up_bytes, o_pml = o_po + b_po, o_flags = o_pml + b_pml, o_cnt = o_flags + b_flags;
@@ -500,13 +517,13 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     plan->d_units = reinterpret_cast<DevUnit*>(base + plan->off_units);
     plan->d_cta_begin = reinterpret_cast<int32_t*>(base + plan->off_begin);
     plan->d_cta_first = reinterpret_cast<int32_t*>(base + plan->off_first);
+    plan->d_claim = reinterpret_cast<int32_t*>(base + plan->off_claim);
     plan->d_block_table = plan->pt_stride ? reinterpret_cast<int32_t*>(base + plan->off_bt) : nullptr;
     plan->d_part_o = reinterpret_cast<float*>(base + o_po);
     plan->d_part_ml = reinterpret_cast<float*>(base + o_pml);
     plan->d_flags = reinterpret_cast<uint32_t*>(base + o_flags);
     plan->d_counters = reinterpret_cast<int*>(base + o_cnt);
     plan->d_unit_count = plan->d_counters + la::kNumCounters;
-    plan->d_grp_count = plan->d_unit_count + U;
     if (opts.trace) plan->d_trace = reinterpret_cast<unsigned long long*>(base + o_trace);
     if (b_gf) plan->d_gfold = reinterpret_cast<float*>(base + o_gf);
     plan->workspace = int64_t(bytes);
@@ -621,6 +638,16 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   return LA_OK;
 }
 
+la_status la_plan_export_claims(la_plan_t plan, int32_t* claims, size_t cap, size_t* n) {
+  if (!plan || !n) return fail(LA_ERR_INVALID, "NULL argument");
+  const std::vector<int32_t>& c = plan->sched.claim;
+  *n = c.size();
+  if (cap == 0) return LA_OK;
+  if (!claims || cap < c.size()) return fail(LA_ERR_INVALID, "claims buffer too small");
+  std::memcpy(claims, c.data(), c.size() * sizeof(int32_t));
+  return LA_OK;
+}
+
 la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t* n_rows) {
   if (!plan || !n_rows) return fail(LA_ERR_INVALID, "NULL argument");
   std::vector<int32_t> r;
@@ -649,6 +676,7 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.units = plan->d_units;
   a.cta_begin = plan->d_cta_begin;
   a.cta_first_unit = plan->d_cta_first;
+  a.claim = plan->d_claim;
   a.part_o = plan->d_part_o;
   a.part_ml = plan->d_part_ml;
   a.flags = plan->d_flags;
@@ -656,7 +684,6 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.gfold = plan->d_gfold;
   a.counters = plan->d_counters;
   a.unit_count = plan->d_unit_count;
-  a.grp_count = plan->d_grp_count;
   a.slot_stride = plan->slot_cap;
   a.dynamic = (plan->prob.schedule == LA_SCHED_DYNAMIC || plan->prob.schedule == LA_SCHED_FIXED_SPLIT) ? 1 : 0;
   a.paged = plan->prob.layout == LA_KV_PAGED ? 1 : 0;

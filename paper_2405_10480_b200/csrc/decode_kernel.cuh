@@ -29,12 +29,11 @@
 //  * SCHEDULES.  Static (LA_SCHED_STREAMK / SEQUENTIAL): CTA g runs Alg. 2's range g; a
 //    non-host segment publishes its partial and a release flag, a non-finishing host spins
 //    on its peers' flags and folds them in ascending order (needs co-residency ->
-//    cooperative launch).  Dynamic (LA_SCHED_DYNAMIC): the planner cuts the same iteration
-//    space into more, guided-size "virtual CTAs"; persistent CTAs claim them in order with
-//    an atomic counter, so fast SMs take more work.  Every non-trivial segment stores its
-//    partial and counts itself in; a fixed two-level tree of last arrivers (groups of kGS
-//    consecutive segments, then the groups) folds them in ascending order -- deterministic,
-//    and no CTA ever waits.
+//    cooperative launch).  Dynamic (LA_SCHED_DYNAMIC): the planner cuts every Alg. 2 range
+//    into a head and small tail chunks ("virtual CTAs"); persistent CTAs claim all heads,
+//    then the chunks (atomic counter + claim table), so fast SMs take more work.  Every
+//    non-trivial piece stores its partial and counts itself in; the unit's last arriving
+//    piece folds them all in ascending order -- deterministic, and no CTA ever waits.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -282,6 +281,8 @@ struct MhaEngine {
   static constexpr int FOLD_FLOATS = NCW * (D + 2);         // per warp: O[D], m, l
   static constexpr int FOLD_BUFS = 2;                       // double-buffered hand-off
   static constexpr bool ZERO_RING = true;                   // tail rows must be finite
+  using QElem = T;                                          // Q storage type
+  static constexpr bool QSTAGE = true;                      // Q rows staged in smem per segment
   static_assert(LPK >= 2 && LPK <= 32 && (LPK & (LPK - 1)) == 0, "lanes per key");
   static_assert(STAGE_TOK % 32 == 0, "stage holds whole 32-key rounds");
 
@@ -320,8 +321,9 @@ struct MhaEngine {
     }
   }
 
-  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
-    s.qf =Chunk<T>::load_q(static_cast<const T*>(a.q) + size_t(u.q_row) * D + (lane % LPK) * EPL);
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane,
+                                                   const void* qsrc) {  // qsrc: the unit's Q row (smem)
+    s.qf = Chunk<T>::load_q(static_cast<const T*>(qsrc) + (lane % LPK) * EPL);
     s.m = -INFINITY;  // Alg1§8-9
     s.l = 0.f;
 #pragma unroll
@@ -489,6 +491,8 @@ struct GqaEngine {
   static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
   static constexpr int FOLD_BUFS = LA_GQA_FB;     // double-buffered hand-off (measured best)
   static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
+  using QElem = T;
+  static constexpr bool QSTAGE = true;
 
   struct State {
     uint32_t qb[KS][2];     // Q^T B-fragments (exact inputs)
@@ -539,9 +543,10 @@ struct GqaEngine {
     }
   }
 
-  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane,
+                                                   const void* qsrc) {  // qsrc: the unit's Q rows (smem)
     const int gq = lane >> 2, tq = lane & 3;
-    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const T*>(a.q) + size_t(u.q_row + gq) * D);
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const T*>(qsrc) + size_t(gq) * D);
     const bool ok = gq < u.rows;
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {  // b0 = Q[gq][16kk + 2tq, +1], b1 = Q[gq][16kk + 8 + 2tq, +1]
@@ -731,6 +736,8 @@ struct Fp8Engine {
   static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
   static constexpr int FOLD_BUFS = ROWS_ == 1 ? LA_FP8M_FB : LA_FP8_FB;
   static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
+  using QElem = __nv_bfloat16;                    // bf16 q next to the E4M3 cache
+  static constexpr bool QSTAGE = true;
 
   struct State {
     uint32_t qb[KS][2];  // Q^T B-fragments (f16, permuted contraction order, see above)
@@ -761,9 +768,10 @@ struct Fp8Engine {
     }
   }
 
-  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane,
+                                                   const void* qsrc) {  // qsrc: the unit's Q rows (smem)
     const int gq = lane >> 2, tq = lane & 3;
-    const __nv_bfloat16* qrow = static_cast<const __nv_bfloat16*>(a.q) + size_t(u.q_row + gq) * D;
+    const __nv_bfloat16* qrow = static_cast<const __nv_bfloat16*>(qsrc) + size_t(gq) * D;
     const bool ok = gq < u.rows;
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {  // b0 = Q[gq][16kk + 4tq, +1], b1 = Q[gq][16kk + 4tq + 2, +3]
@@ -977,6 +985,8 @@ struct Tc5Engine {
   static constexpr int FOLD_BUFS = 1;
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
+  using QElem = T;
+  static constexpr bool QSTAGE = false;             // no smem left next to the 64 KiB ring slots: Q from global
   // accumulator chains per contraction (1 or 2).  LA_TC5_SPLIT = 2 applies to 8-row tiles only:
   // at 16 / 32 rows it fails a wide-tile parity test and measured slower (32 rows: 383 vs 368 us)
   static constexpr int SPLIT = HEADS == 8 ? LA_TC5_SPLIT : 1;
@@ -1062,7 +1072,8 @@ struct Tc5Engine {
     }
   }
 
-  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane) {
+  __device__ __forceinline__ static void seg_begin(State& s, const DecodeArgs& a, const DevUnit& u, int lane,
+                                                   const void* qsrc) {  // qsrc: the unit's Q rows (global)
     const int slot = slot_of_thread(), tid = (int(threadIdx.x >> 5) % WPS) * 32 + lane;
     unsigned char* qs = extra() + slot * XS;
     // Q^T operand, K-major 128-B swizzle: row r (q-row of the tile, zero past u.rows),
@@ -1071,7 +1082,7 @@ struct Tc5Engine {
     for (int i = 0; i < QR / 8; ++i) {
       const int c = tid + 128 * i, r = c >> 4, ch = c & 15, half = ch >> 3, cc = ch & 7;
       uint4 w = make_uint4(0u, 0u, 0u, 0u);
-      if (r < u.rows) w = *reinterpret_cast<const uint4*>(static_cast<const T*>(a.q) + size_t(u.q_row + r) * D + 8 * ch);
+      if (r < u.rows) w = *reinterpret_cast<const uint4*>(static_cast<const T*>(qsrc) + size_t(r) * D + 8 * ch);
       *reinterpret_cast<uint4*>(qs + half * QHS + r * 128 + ((cc ^ (r & 7)) << 4)) = w;
     }
 #pragma unroll
@@ -1311,11 +1322,20 @@ struct Tc5Engine {
 // The persistent decode kernel
 // =======================================================================================
 constexpr int kQD = 4;   // depth of the producer -> consumer virtual-CTA queue
-constexpr int kGS = 16;  // dynamic-mode fold tree: segments per first-level group
+constexpr int kClaimAhead = 4;  // dynamic: LeanTiles before a piece's end at which the next claim is taken
+
+// One segment (one LeanTile() call, Alg2§11-18) handed from the producer to the consumer
+// warps through shared memory, with its unit record: the consumers never read the schedule
+// tables or Q from global memory (those dependent loads stalled every segment start).
+struct alignas(16) SegQ {
+  DevUnit u;
+  int v, unit, it, it_end, host, finishing, pad_[2];
+};
 
 struct SegInfo {
   int v, unit, host, finishing;
-  int s0;  // ring slot of the segment's first stage
+  int s0;    // ring slot of the segment's first stage
+  int jend;  // stages consumed by the CTA once this segment is done
 };
 
 // Engines with tcgen05 state (Tc5Engine) declare TMEM columns, an extra smem region after
@@ -1338,8 +1358,12 @@ struct Smem {
   static constexpr int kFB = E::FOLD_BUFS;  // consumer -> epilogue fold buffers
   static constexpr int FOLD = EngX<E>::GF ? 0 : kFB * E::FOLD_FLOATS * 4;
   static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB + 1) * 8;
-  static constexpr int MISC = kQD * 4 + kFB * int(sizeof(SegInfo));
-  static constexpr int BYTES = 1024 + RING + EXTRA + FOLD + BARS + MISC;
+  // segment queue, hand-off records, prod_j; then the segments' Q rows (TMA bulk copies)
+  static constexpr int SQ_OFF = (RING + EXTRA + FOLD + BARS + 15) / 16 * 16;
+  static constexpr int MISC = kQD * int(sizeof(SegQ)) + kFB * int(sizeof(SegInfo)) + 16;
+  static constexpr int QB = E::QSTAGE ? (E::HEADS * E::D * int(sizeof(typename E::QElem)) + 127) / 128 * 128 : 0;
+  static constexpr int QB_OFF = (SQ_OFF + MISC + 127) / 128 * 128;
+  static constexpr int BYTES = 1024 + QB_OFF + kQD * QB;
 };
 
 // The epilogue warp's accumulator for one segment: lane owns dims c = lane + 32 j of every
@@ -1363,13 +1387,15 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
                             : reinterpret_cast<float*>(ring + Smem<E>::RING + Smem<E>::EXTRA);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + Smem<E>::RING + Smem<E>::EXTRA + Smem<E>::FOLD);
   uint64_t* empty = full + NST;
-  uint64_t* vq_full = empty + NST;
-  uint64_t* vq_empty = vq_full + kQD;
-  uint64_t* fold_full = vq_empty + kQD;
+  uint64_t* sq_full = empty + NST;         // segment queue entry written (+ its Q rows landed)
+  uint64_t* sq_empty = sq_full + kQD;      // every consumer warp has read the entry
+  uint64_t* fold_full = sq_empty + kQD;
   uint64_t* fold_empty = fold_full + kFB;
-  uint64_t* stage_bar = fold_empty + kFB;  // static host: peers' partials staged into the ring
-  int* vq = reinterpret_cast<int*>(stage_bar + 1);
-  SegInfo* seginfo = reinterpret_cast<SegInfo*>(vq + kQD);
+  uint64_t* stage_bar = fold_empty + kFB;  // peers' partials staged for a fold
+  SegQ* squeue = reinterpret_cast<SegQ*>(ring + Smem<E>::SQ_OFF);
+  SegInfo* seginfo = reinterpret_cast<SegInfo*>(squeue + kQD);
+  int* prod_j = reinterpret_cast<int*>(seginfo + kFB);  // stages the producer issued in all, once done (-1 before)
+  unsigned char* qbuf = ring + Smem<E>::QB_OFF;         // [kQD][QB]: Q rows of each queued segment
 
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int g = blockIdx.x;
@@ -1401,14 +1427,15 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       mbar_init(&empty[s], WPS);
     }
     for (int q = 0; q < kQD; ++q) {
-      mbar_init(&vq_full[q], 1);
-      mbar_init(&vq_empty[q], NCW);
+      mbar_init(&sq_full[q], 1);
+      mbar_init(&sq_empty[q], NCW);
     }
     for (int b = 0; b < kFB; ++b) {
       mbar_init(&fold_full[b], NCW);
       mbar_init(&fold_empty[b], 1);
     }
     mbar_init(stage_bar, 1);
+    *prod_j = -1;
     if constexpr (EngX<E>::TMEM > 0) E::init_barriers();
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1430,60 +1457,145 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.k)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.v)) : "memory");
     }
-    int j = 0, k = 0;
+    int j = 0, ks = 0;
 #ifdef LA_PROF
     long long prof_pwait = 0;  // producer cycles waiting for free slots -> trace field smid
 #endif
-    for (bool first = true;; first = false) {
-      // Claim the next virtual CTA only once the previous one is fully issued: the ring
-      // (NST stages in flight) hides the atomic's latency, and claiming ahead would let a
-      // CTA hoard two of the big first-round ranges.
-      int v = 0;
-      if (lane == 0) {
-        v = dynamic ? atomicAdd(&a.counters[CTR_CLAIM], 1) : (first ? g : NV);
-        const int q = k % kQD;
-        if (k >= kQD) mbar_wait(&vq_empty[q], ((k / kQD) - 1) & 1);
-        vq[q] = v < NV ? v : -1;
-        mbar_arrive(&vq_full[q]);
+    constexpr int QB = Smem<E>::QB;
+    const int q_el = int(sizeof(typename E::QElem));
+    // Hand segment (u, v, [it, it_end)) to the consumers: queue entry + its Q rows (lane 0).
+    auto push_seg = [&](const DevUnit& u, int v, int unit, int it, int it_end, int host, int finishing) {
+      const int qi = ks % kQD;
+      if (ks >= kQD) mbar_wait(&sq_empty[qi], ((ks / kQD) - 1) & 1);
+      SegQ& e = squeue[qi];
+      e.u = u;
+      e.v = v;
+      e.unit = unit;
+      e.it = it;
+      e.it_end = it_end;
+      e.host = host;
+      e.finishing = finishing;
+      if (QB > 0 && v >= 0) {
+        const uint32_t bytes = uint32_t(u.rows) * D * q_el;
+        mbar_arrive_expect_tx(&sq_full[qi], bytes);
+        bulk_g2s_plain(qbuf + qi * QB, static_cast<const unsigned char*>(a.q) + size_t(u.q_row) * D * q_el, bytes,
+                       &sq_full[qi]);
+      } else {
+        mbar_arrive(&sq_full[qi]);
       }
-      v = __shfl_sync(0xffffffffu, v, 0);
-      ++k;
-      if (v >= NV) break;
-      const int it1 = a.cta_begin[v + 1];
-      int unit = a.cta_first_unit[v];
-      for (int it = a.cta_begin[v]; it < it1;) {
-        const DevUnit u = a.units[unit];
-        if (u.iter_end <= it) {
-          ++unit;
-          continue;
+      ++ks;
+    };
+    // The current piece (virtual CTA v: iterations [it, it1), first unit `unit`) and, for the
+    // dynamic schedule, the next one fetched AHEAD by lane 0 in steps spread over the piece's
+    // last kClaimAhead LeanTiles (claim atomic -> claim table -> range -> unit record), so the
+    // dependent round trips overlap the last stages instead of draining the ring at every
+    // piece boundary.  The heads are the first G claims, so no CTA hoards two of them.
+    int v = NV, it = 0, it1 = 0, unit = 0;
+    int pst = 0, c_nx = -1, v_nx = NV, b_nx = 0, e_nx = 0, u_nx = 0;
+    DevUnit du_nx{};
+    auto fetch_ahead = [&](int rem, bool force) {  // lane 0, dynamic
+      if (pst == 0 && (force || rem <= kClaimAhead)) {
+        c_nx = atomicAdd(&a.counters[CTR_CLAIM], 1);
+        pst = 1;
+      }
+      if (pst == 1 && (force || rem <= kClaimAhead - 1)) {
+        v_nx = c_nx < NV ? a.claim[c_nx] : NV;
+        pst = 2;
+      }
+      if (pst == 2 && (force || rem <= kClaimAhead - 2)) {
+        if (v_nx < NV) {
+          b_nx = a.cta_begin[v_nx];
+          e_nx = a.cta_begin[v_nx + 1];
+          u_nx = a.cta_first_unit[v_nx];
         }
-        const int seg_end = min(u.iter_end, it1);
-        PageWin pw;
-        if (a.paged) pw.init(a, u.row0);
-        for (; it < seg_end; ++it) {                        // LeanTile iterations (Alg1§13)
-          const int t0 = (it - u.iter_begin) * a.tile_n;    // kk = iter * T_n (Alg1§14)
-          const int t1 = min(t0 + a.tile_n, u.len);
-          for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {  // LoadFragment K, V (Alg1§17-18)
-            const int slot = j % NST;
-#ifdef LA_PROF
-            const long long c0 = clock64();
-#endif
-            if (lane == 0 && j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
-#ifdef LA_PROF
-            if (lane == 0) prof_pwait += clock64() - c0;
-#endif
-            const int ntok = min(a.stage_tokens, t1 - s0);
-            if (!a.paged) {
-              if (lane == 0) E::produce(ring + slot * E::STAGE_BYTES, a, tm, u.row0 + s0, ntok, &full[slot], pol);
-            } else {
-              E::produce_paged(ring + slot * E::STAGE_BYTES, a, tm, pw, s0, ntok, &full[slot], pol, lane);
-            }
-            ++j;
-          }
-        }
-        ++unit;
+        pst = 3;
+      }
+      if (pst == 3 && (force || rem <= kClaimAhead - 3)) {
+        if (v_nx < NV) du_nx = a.units[u_nx];
+        pst = 4;
+      }
+    };
+    DevUnit u{};
+    if (lane == 0) {
+      if (dynamic) {
+        fetch_ahead(0, true);
+        v = v_nx;
+        pst = 0;
+        if (tr) tr[TR_WAIT0] += 1;
+      } else {
+        v = g < NV ? g : NV;
+      }
+      if (v < NV) {
+        it = dynamic ? b_nx : a.cta_begin[v];
+        it1 = dynamic ? e_nx : a.cta_begin[v + 1];
+        unit = dynamic ? u_nx : a.cta_first_unit[v];
+        if (it >= it1) v = NV;   // an idle range (forced G > I: S:219)
+        else u = dynamic ? du_nx : a.units[unit];
       }
     }
+    while (__shfl_sync(0xffffffffu, v, 0) < NV) {
+      int seg_end = 0;
+      DevUnit un{};  // the next unit of this piece, loaded ahead
+      if (lane == 0) {
+        while (u.iter_end <= it) u = a.units[++unit];      // (cta_first_unit makes this rare)
+        seg_end = min(u.iter_end, it1);
+        push_seg(u, v, unit, it, seg_end, it == u.iter_begin ? 1 : 0, it1 >= u.iter_end ? 1 : 0);  // Alg2§17-18
+        if (it1 > u.iter_end) un = a.units[unit + 1];     // consumed at the next segment
+      }
+      // the whole warp walks the segment (paged: every lane issues page runs / TMA boxes)
+      seg_end = __shfl_sync(0xffffffffu, seg_end, 0);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      it1 = __shfl_sync(0xffffffffu, it1, 0);
+      const int64_t row0 = __shfl_sync(0xffffffffu, u.row0, 0);
+      const int ib = __shfl_sync(0xffffffffu, u.iter_begin, 0), ulen = __shfl_sync(0xffffffffu, u.len, 0);
+      PageWin pw;
+      if (a.paged) pw.init(a, row0);
+      for (; it < seg_end; ++it) {                          // LeanTile iterations (Alg1§13)
+        if (dynamic && lane == 0) fetch_ahead(it1 - it, false);
+        const int t0 = (it - ib) * a.tile_n;                // kk = iter * T_n (Alg1§14)
+        const int t1 = min(t0 + a.tile_n, ulen);
+        for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {  // LoadFragment K, V (Alg1§17-18)
+          const int slot = j % NST;
+#ifdef LA_PROF
+          const long long c0 = clock64();
+#endif
+          if (lane == 0 && j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
+#ifdef LA_PROF
+          if (lane == 0) prof_pwait += clock64() - c0;
+#endif
+          const int ntok = min(a.stage_tokens, t1 - s0);
+          if (!a.paged) {
+            if (lane == 0) E::produce(ring + slot * E::STAGE_BYTES, a, tm, row0 + s0, ntok, &full[slot], pol);
+          } else {
+            E::produce_paged(ring + slot * E::STAGE_BYTES, a, tm, pw, s0, ntok, &full[slot], pol, lane);
+          }
+          ++j;
+        }
+      }
+      if (lane == 0) {
+        if (it < it1) {          // the piece continues in the next unit
+          ++unit;
+          u = un;
+        } else if (dynamic) {    // next piece: finish the look-ahead (short pieces) and take it
+          fetch_ahead(0, true);
+          v = v_nx;
+          pst = 0;
+          if (tr) tr[TR_WAIT0] += 1;
+          if (v < NV) {
+            it = b_nx;
+            it1 = e_nx;
+            unit = u_nx;
+            u = du_nx;
+          }
+        } else {
+          v = NV;                // a static CTA runs exactly its range g
+        }
+      }
+    }
+    if (lane == 0) push_seg(DevUnit{}, -1, -1, 0, 0, 0, 0);   // terminator for the consumers
+    // every stage this CTA will stream has been issued: once the consumers have used stage
+    // j - 1, the ring is idle (a dynamic last arriver may stage its fold there)
+    if (lane == 0) *reinterpret_cast<volatile int*>(prod_j) = j;
 #ifdef LA_PROF
     if (tr && lane == 0) tr[TR_SMID] = prof_pwait;
 #endif
@@ -1525,45 +1637,53 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     // acc = f(...f(f(acc, P[slot(p0)]), P[slot(p0 + stride)])..., P[slot(<= p1)]), ascending
     // (Alg2§27-35); host_v's partial lives in slot 1 of its virtual CTA, everyone else's in 0
     // Fold peers p0, p0 + stride, .. <= p1 into acc (Alg2§27-35), their partials staged in
-    // smem `stg` (stg_floats): the ring when idle (static host) or the segment's consumed
-    // fold buffer (dynamic tree).  A peer's O~ rows and its (m, l) rows are contiguous, so
-    // a chunk arrives by 1-D bulk copies on stage_bar -- ONE pair for a contiguous run of
-    // slot-0 peers (per-peer copies cost ~50 issue cycles each on this one warp, measured)
-    // -- one round trip per chunk.  Each chunk is folded in the max-first form (reading
-    // C22): M = max(m_acc, m_p..) first, then every O~_p enters with weight 2^(m_p - M),
-    // with four independent accumulator chains; fixed order: bitwise deterministic.
+    // smem `stg` (stg_floats): the ring when idle (static host; dynamic last arriver that has
+    // streamed its last stage) or the segment's consumed fold buffer.  A peer's O~ rows and its
+    // (m, l) rows are contiguous, so a round arrives by 1-D bulk copies on stage_bar -- ONE
+    // pair for a contiguous run of slot-0 peers (per-peer copies cost ~50 issue cycles each on
+    // this one warp, measured) -- one round trip per staging round.  The arithmetic runs in
+    // FIXED blocks of fcap peers (what one fold buffer holds) whatever the staging buffer, each
+    // in the max-first form (reading C22): M = max(m_acc, m_p..) first, then every O~_p enters
+    // with weight 2^(m_p - M), with four independent accumulator chains; the result depends
+    // only on the peers and their order: bitwise deterministic.
     auto fold_smem = [&](int p0, int p1, int stride, int host_v, float* stg, int stg_floats) {
       const int n = p1 < p0 ? 0 : (p1 - p0) / stride + 1;
       const int po = a.group * D, pm = a.group * 4;  // staged per peer: whole slots (rows >= nr unused)
-      const int cap = max(1, stg_floats / (po + pm));
+      const int fcap = max(1, FOLD_FLOATS / (po + pm));
+      const int cap = max(fcap, stg_floats / (po + pm) / fcap * fcap);
       const bool contiguous = stride == 1 && (host_v < p0 || host_v > p1);
       asm volatile("fence.proxy.async.global;" ::: "memory");      // acquired partials -> TMA
       #pragma unroll 1
       for (int c0 = 0; c0 < n; c0 += cap) {
-        const int cn = min(cap, n - c0);
-        float* so = stg;            // [cn][nr][D]
-        float* sm = stg + cn * po;  // [cn][nr][4]
+        const int cs = min(cap, n - c0);
+        float* so0 = stg;            // [cs][nr][D]
+        float* sm0 = stg + cs * po;  // [cs][nr][4]
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier smem reads
         __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(cn) * (po + pm) * 4);
+        if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(cs) * (po + pm) * 4);
         __syncwarp();
         if (contiguous) {
           if (lane == 0) {
             const size_t r = size_t(p0 + c0) * a.group;
-            bulk_g2s_plain(so, a.part_o + r * D, uint32_t(cn) * po * 4, stage_bar);
-            bulk_g2s_plain(sm, a.part_ml + r * 4, uint32_t(cn) * pm * 4, stage_bar);
+            bulk_g2s_plain(so0, a.part_o + r * D, uint32_t(cs) * po * 4, stage_bar);
+            bulk_g2s_plain(sm0, a.part_ml + r * 4, uint32_t(cs) * pm * 4, stage_bar);
           }
         } else {
           #pragma unroll 1
-          for (int i = lane; i < cn; i += 32) {
+          for (int i = lane; i < cs; i += 32) {
             const int p = p0 + (c0 + i) * stride;
             const size_t r = size_t(p + (p == host_v ? SS : 0)) * a.group;
-            bulk_g2s_plain(so + i * po, a.part_o + r * D, uint32_t(po) * 4, stage_bar);
-            bulk_g2s_plain(sm + i * pm, a.part_ml + r * 4, uint32_t(pm) * 4, stage_bar);
+            bulk_g2s_plain(so0 + i * po, a.part_o + r * D, uint32_t(po) * 4, stage_bar);
+            bulk_g2s_plain(sm0 + i * pm, a.part_ml + r * 4, uint32_t(pm) * 4, stage_bar);
           }
         }
         mbar_wait(stage_bar, stage_ph);
         stage_ph ^= 1u;
+        #pragma unroll 1
+        for (int b0 = 0; b0 < cs; b0 += fcap) {   // arithmetic blocks of fcap peers
+        const int cn = min(fcap, cs - b0);
+        float* so = so0 + b0 * po;
+        float* sm = sm0 + b0 * pm;
 #pragma unroll
         for (int h = 0; h < H; ++h) {
           if (h >= nr) continue;
@@ -1612,7 +1732,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           acc.l[h] = fmaf(wa, acc.l[h], lsum);
           acc.m[h] = M;
         }
-        __syncwarp();  // the next chunk overwrites the stage
+        }
+        __syncwarp();  // the next round overwrites the stage
       }
     };
     // NEXT-2: push this rank's normalised shard partial of unit `unit` into every rank's
@@ -1734,7 +1855,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       const DevUnit u = a.units[si.unit];
       const int v = si.v;
       nr = u.rows;
-      // the dynamic tree fold stages its peers in this (consumed) fold buffer: release later
+      // a dynamic last arriver may stage its peers in this (consumed) fold buffer: release later
       const bool keep_fb = dynamic && !(si.host && si.finishing);
       if (!keep_fb && lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill it
 
@@ -1742,7 +1863,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       // each keeps the epilogue code small (it runs rarely; an inlined copy per path blew
       // the kernel up to 48k instructions and its folds ran from instruction-cache misses).
       bool out = si.host && si.finishing;  // one (virtual) CTA computed the whole unit (Alg2§38-39)
-      int fp0 = 0, fp1 = -1, fstride = 1, fhv = -1, ngrp = 1, g0 = 0;
+      int fp0 = 0, fp1 = -1, fhv = -1;
       float* fstg = nullptr;
       int fn = 0;
       if (out) {
@@ -1779,54 +1900,34 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           fn = Smem<E>::RING / 4;
         }
       } else {
-        // ---- dynamic: publish, count in; a FIXED two-level tree folds the unit's segments
-        //      (virtual CTAs host_cta .. last_cta): the last arriver of each group of kGS
-        //      consecutive segments folds the group ascending into the group's first slot,
-        //      the last group folds the groups ascending.  Deterministic; nobody waits.
+        // ---- dynamic: publish, count in; the unit's LAST arriving piece folds all of the
+        //      unit's pieces (virtual CTAs host_cta .. last_cta) in ascending order --
+        //      deterministic (fixed pieces, fixed order), and nobody waits
         fhv = u.host_cta;
-        ngrp = (u.last_cta - fhv + 1 + kGS - 1) / kGS;
-        g0 = fhv + ((v - fhv) / kGS) * kGS;
-        const int g1 = min(g0 + kGS, u.last_cta + 1) - 1;
         store_partial(v + (si.host ? SS : 0));
-        int role = 0;
+        int last = 0;
         if (lane == 0) {
-          // the unit's first group (g0 = its host) counts in the second half: CTA g0 may also
-          // END an earlier unit as the first CTA of that unit's last group
-          int* cnt = &a.grp_count[g0 + (g0 == fhv ? SS : 0)];
-          if (atomicAdd(cnt, 1) == g1 - g0) {
+          if (atomicAdd(&a.unit_count[si.unit], 1) == u.last_cta - fhv) {
             __threadfence();
-            *cnt = 0;  // ready for the next launch
-            role = 1;
+            a.unit_count[si.unit] = 0;  // ready for the next launch
+            last = 1;
           }
           if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
         }
-        if (__shfl_sync(0xffffffffu, role, 0)) {
-          fp0 = g0;
-          fp1 = g1;
-          fstg = fold + b * FOLD_FLOATS;  // this segment's consumed fold buffer
-          fn = FOLD_FLOATS;
+        if (__shfl_sync(0xffffffffu, last, 0)) {
+          fp0 = fhv;
+          fp1 = u.last_cta;
+          // the ring is idle once this CTA has consumed every stage its producer will issue:
+          // one staging round for all pieces; else this segment's consumed fold buffer
+          const bool ring_free = *reinterpret_cast<volatile int*>(prod_j) == si.jend;
+          fstg = ring_free ? reinterpret_cast<float*>(ring) : fold + b * FOLD_FLOATS;
+          fn = ring_free ? Smem<E>::RING / 4 : FOLD_FLOATS;
         }
       }
-#pragma unroll 1
-      while (fstg) {
+      if (fstg) {
         if (dynamic) reset();
-        fold_smem(fp0, fp1, fstride, fhv, fstg, fn);
-        if (!dynamic || fstride == kGS || ngrp == 1) {
-          out = true;
-          break;
-        }
-        // dynamic, a group of a multi-group unit: publish the group's fold, count it in
-        store_partial(g0 + (g0 == fhv ? SS : 0));
-        int last = 0;
-        if (lane == 0 && atomicAdd(&a.unit_count[si.unit], 1) == ngrp - 1) {
-          __threadfence();
-          a.unit_count[si.unit] = 0;
-          last = 1;
-        }
-        if (!__shfl_sync(0xffffffffu, last, 0)) break;
-        fp0 = fhv;
-        fp1 = u.last_cta;
-        fstride = kGS;
+        fold_smem(fp0, fp1, 1, fhv, fstg, fn);
+        out = true;
       }
       if (!dynamic && fstg && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
       if (out) write_out(u.q_row, si.unit);
@@ -1870,76 +1971,66 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     return b;
   };
   auto hand_off = [&](int b, int v, int unit, int host, int finishing, int s0) {
-    if (warp == 0 && lane == 0) seginfo[b] = SegInfo{v, unit, host, finishing, s0};
+    if (warp == 0 && lane == 0) seginfo[b] = SegInfo{v, unit, host, finishing, s0, j};
     __syncwarp();
     if (lane == 0) mbar_arrive(&fold_full[b]);
     ++seg;
   };
   for (;;) {
-    const int q = k % kQD;
-    mbar_wait(&vq_full[q], (k / kQD) & 1);
-    const int v = vq[q];
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&vq_empty[q]);
-    ++k;
+    const int qi = k % kQD;
+    mbar_wait(&sq_full[qi], (k / kQD) & 1);
+    const SegQ e = squeue[qi];
+    const DevUnit u = e.u;
+    const int v = e.v;
     if (v < 0) break;
-    if (dynamic && tr && threadIdx.x == 0) {  // dynamic mode: claims and LeanTiles per CTA
-      tr[TR_WAIT0] += 1;
-      tr[TR_WAIT1] += a.cta_begin[v + 1] - a.cta_begin[v];
-    }
-    const int it1 = a.cta_begin[v + 1];
-    int unit = a.cta_first_unit[v];
-    for (int it = a.cta_begin[v]; it < it1;) {
-      const DevUnit u = a.units[unit];
-      if (u.iter_end <= it) {
-        ++unit;
-        continue;
-      }
-      const int seg_end = min(u.iter_end, it1);
-      const int host = (it == u.iter_begin) ? 1 : 0;      // host-block (Alg2§17)
-      const int finishing = (it1 >= u.iter_end) ? 1 : 0;  // finishing-block (Alg2§18)
-      typename E::State st;
-      E::seg_begin(st, a, u, lane);
-      const int seg_s0 = j % NWG;
-      for (; it < seg_end; ++it) {
-        const int t0 = (it - u.iter_begin) * a.tile_n;
-        const int t1 = min(t0 + a.tile_n, u.len);
-        for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
-          if (j % NWG == my_wg) {
-            const int rs = j % NST;  // ring slot of stage j
+    int it = e.it;
+    const int seg_end = e.it_end;
+    if (dynamic && tr && threadIdx.x == 0) tr[TR_WAIT1] += seg_end - it;  // dynamic: LeanTiles per CTA
+    typename E::State st;
+    E::seg_begin(st, a, u, lane, Smem<E>::QB ? static_cast<const void*>(qbuf + qi * Smem<E>::QB)
+                                            : static_cast<const void*>(static_cast<const unsigned char*>(a.q) +
+                                                                       size_t(u.q_row) * D * sizeof(typename E::QElem)));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sq_empty[qi]);  // entry and Q rows read
+    ++k;
+    const int seg_s0 = j % NWG;
+    for (; it < seg_end; ++it) {
+      const int t0 = (it - u.iter_begin) * a.tile_n;
+      const int t1 = min(t0 + a.tile_n, u.len);
+      for (int s0 = t0; s0 < t1; s0 += a.stage_tokens) {
+        if (j % NWG == my_wg) {
+          const int rs = j % NST;  // ring slot of stage j
 #ifdef LA_PROF
-            const long long c0 = clock64();
+          const long long c0 = clock64();
 #endif
-            // NWG < NST: slot rs last held stage j - NST of ANOTHER warp set; wait for its
-            // release first, so the full-barrier parity below cannot alias that older phase
-            if (NWG < NST && j >= NST) mbar_wait(&empty[rs], uint32_t((j / NST) - 1) & 1u);
-            mbar_wait(&full[rs], (j / NST) & 1);
+          // NWG < NST: slot rs last held stage j - NST of ANOTHER warp set; wait for its
+          // release first, so the full-barrier parity below cannot alias that older phase
+          if (NWG < NST && j >= NST) mbar_wait(&empty[rs], uint32_t((j / NST) - 1) & 1u);
+          mbar_wait(&full[rs], (j / NST) & 1);
 #ifdef LA_PROF
-            const long long c1 = clock64();
-            prof_wait += c1 - c0;
-            ++prof_n;
+          const long long c1 = clock64();
+          prof_wait += c1 - c0;
+          ++prof_n;
 #endif
-            if constexpr (EngX<E>::TMEM > 0) {  // the engine releases the slot itself
-              E::stage(st, ring + rs * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
-                       lane, a.box_shift, (uint32_t(j / NST) & 1u) | ((uint32_t(j / NWG) & 1u) << 1), &empty[rs]);
-            } else {
-              E::stage(st, ring + rs * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
-                       lane, a.box_shift);
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&empty[rs]);
-            }
-#ifdef LA_PROF
-            prof_work += clock64() - c1;
-#endif
+          if constexpr (EngX<E>::TMEM > 0) {  // the engine releases the slot itself
+            E::stage(st, ring + rs * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
+                     lane, a.box_shift, (uint32_t(j / NST) & 1u) | ((uint32_t(j / NWG) & 1u) << 1), &empty[rs]);
+          } else {
+            E::stage(st, ring + rs * E::STAGE_BYTES, sub, min(a.stage_tokens, t1 - s0), s0, a.scale_log2,
+                     lane, a.box_shift);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[rs]);
           }
-          ++j;
+#ifdef LA_PROF
+          prof_work += clock64() - c1;
+#endif
         }
+        ++j;
       }
-      const int fbuf = hand_off_wait();
-      E::seg_end(st, fold + fbuf * FOLD_FLOATS, warp, lane);
-      hand_off(fbuf, v, unit, host, finishing, seg_s0);
-      ++unit;
     }
+    const int fbuf = hand_off_wait();
+    E::seg_end(st, fold + fbuf * FOLD_FLOATS, warp, lane);
+    hand_off(fbuf, v, e.unit, e.host, e.finishing, seg_s0);
   }
   hand_off(hand_off_wait(), -1, -1, 0, 0, 0);  // terminator for the epilogue
 #ifdef LA_PROF

@@ -38,6 +38,7 @@ struct Schedule {
   std::vector<DevUnit> units;
   std::vector<int32_t> cta_begin;       // grid + 1 entries: CTA v owns [cta_begin[v], cta_begin[v+1])
   std::vector<int32_t> cta_first_unit;  // grid entries: unit containing cta_begin[v]
+  std::vector<int32_t> claim;           // grid entries: the v taken by the c-th dynamic claim
   int64_t num_segments = 0;
   int64_t num_partials = 0;
 };
@@ -78,11 +79,11 @@ void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int6
 void streamk_ranges(int64_t total_iters, int grid, std::vector<int32_t>& cta_begin);
 // Sequential (FA2): one CTA per unit.
 void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& cta_begin);
-// Guided virtual-CTA ranges for LA_SCHED_DYNAMIC: `grid` ranges of
-// floor(first_permille/1000 * I / grid) iterations, then rounds of `grid` ranges each
-// covering half of what remains (>= min_chunk), until I is covered.
-void guided_ranges(int64_t total_iters, int grid, int first_permille, int min_chunk,
-                   std::vector<int32_t>& cta_begin);
+// LA_SCHED_DYNAMIC: every Eq. 2 range split into a head and k <= max_chunks tail chunks of
+// s LeanTiles (oracle.balanced_ranges); `claim` = heads in range order, then tail chunks
+// round by round over the ranges.
+void balanced_ranges(int64_t total_iters, int grid, int head_permille, int min_chunk, int max_chunks,
+                     std::vector<int32_t>& cta_begin, std::vector<int32_t>& claim);
 // FlashDecoding's fixed split: unit u cut into min(split, C_n(u)) chunks, the
 // first (C_n mod s) one LeanTile longer; ranges in unit order.
 void fixed_split_ranges(const std::vector<DevUnit>& units, int split, std::vector<int32_t>& cta_begin);
@@ -107,16 +108,14 @@ struct DecodeArgs {
   const DevUnit* units;
   const int32_t* cta_begin;
   const int32_t* cta_first_unit;
+  const int32_t* claim;  // dynamic: claim c runs virtual CTA claim[c]
   float* part_o;      // [2][slot_stride][group][d]  Op of Alg2§20 (slot 1: host partials that wait
                       //                              or are folded by the dynamic tree)
   float* part_ml;     // [2][slot_stride][group][4]  mp, lp, -, - of Alg2§21-22 (m in log2 units)
   uint32_t* flags;    // [slot_stride]               flags of Alg2§23/§28, epoch-valued (reading C17)
   int* counters;      // [kNumCounters] see CTR_* (device-side: a captured CUDA graph replays correctly)
-  int* unit_count;    // [units] dynamic mode: fold-tree groups completed per unit
-  int* grp_count;     // [2][slot_stride] dynamic mode: segments published per fold-tree group;
-                      //   a unit's first group (g0 = its host) counts at slot_stride + g0, every
-                      //   other group at g0 -- a virtual CTA can end one unit's group and host
-                      //   the next unit's first group, so one index per CTA would collide
+  int* unit_count;    // [units] dynamic mode: segments of the unit published so far (the last
+                      //   arriver folds them all; one counter per unit, reset by that arriver)
   int slot_stride;    // capacity of (virtual) CTAs: partial slot 1 of CTA v is slot_stride + v
   unsigned long long* trace;  // [phys_grid][LA_TRACE_FIELDS] or nullptr
   float* gfold;       // [phys_grid][KernelInfo::global_fold_floats] or nullptr
@@ -165,6 +164,7 @@ constexpr unsigned long long kWaitTimeoutNs = 10000000000ull;  // 10 s: intra-GP
 constexpr unsigned long long kXchgTimeoutNs = 5000000000ull;   // 5 s: cross-GPU exchange waits
 
 constexpr int kMaxXchgWorld = 8;
+constexpr int kMaxTailChunks = 8;  // LA_SCHED_DYNAMIC: tail chunks per Eq. 2 range (balanced_ranges)
 
 // Kernel configuration for (dtype, head_dim, group): threads, dynamic smem, max stage tokens.
 struct KernelInfo {

@@ -83,26 +83,40 @@ void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& 
   cta_begin[units.size()] = units.empty() ? 0 : units.back().iter_end;
 }
 
-void guided_ranges(int64_t total_iters, int grid, int first_permille, int min_chunk,
-                   std::vector<int32_t>& cta_begin) {
+void balanced_ranges(int64_t total_iters, int grid, int head_permille, int min_chunk, int max_chunks,
+                     std::vector<int32_t>& cta_begin, std::vector<int32_t>& claim) {
   // B200-first extension: Alg. 2's equal ranges balance LeanTile COUNTS, but
-  // per-SM HBM bandwidth varies (measured +-10%), so equal counts do not finish together.
-  // The same iteration space is cut into `grid` big ranges (first_permille of the work,
-  // equal), then rounds of `grid` ranges each covering half of the remainder, so the
-  // persistent CTAs that claim them in order end within ~one small range of each other.
+  // per-SM streaming speed varies (measured 49-53 GB/s under equal work), so equal counts do
+  // not finish together.  Every Eq. 2 range keeps its first ~head_permille / 1000 as a HEAD;
+  // its last part is cut into k chunks of s LeanTiles that the persistent CTAs claim after
+  // all heads, round by round over the ranges -- fast SMs take more chunks, and every unit's
+  // last pieces are small.  Mirrors oracle.balanced_ranges bit for bit.
   cta_begin.assign(1, 0);
-  int64_t pos = 0;
-  const int64_t first = total_iters * first_permille / (1000 * int64_t(grid));
-  if (first >= 1)
-    for (int g = 0; g < grid; ++g) cta_begin.push_back(int32_t(pos += first));
-  while (pos < total_iters) {
-    const int64_t rem = total_iters - pos;
-    const int64_t c = std::max<int64_t>(min_chunk, (rem + 2 * int64_t(grid) - 1) / (2 * int64_t(grid)));
-    for (int g = 0; g < grid && pos < total_iters; ++g) {
-      pos = std::min(total_iters, pos + c);
-      cta_begin.push_back(int32_t(pos));
+  std::vector<int32_t> heads;
+  std::vector<std::vector<int32_t>> tails;
+  const int64_t q = total_iters / grid, r = total_iters % grid;
+  int32_t v = 0;
+  for (int g = 0; g < grid; ++g) {
+    const int64_t b = g * q + std::min<int64_t>(g, r), e = b + q + (g < r ? 1 : 0), L = e - b;
+    if (L == 0) continue;
+    const int64_t t0 = L * (1000 - head_permille) / 1000;
+    const int64_t s = std::max<int64_t>(min_chunk, (t0 + max_chunks - 1) / max_chunks);
+    const int64_t k = std::min(t0 / s, (L - 1) / s);  // the head keeps >= 1 LeanTile
+    heads.push_back(v++);
+    cta_begin.push_back(int32_t(e - k * s));
+    std::vector<int32_t> chunks;
+    for (int64_t j = 1; j <= k; ++j) {
+      chunks.push_back(v++);
+      cta_begin.push_back(int32_t(e - (k - j) * s));
     }
+    tails.push_back(std::move(chunks));
   }
+  claim = heads;
+  size_t kmax = 0;
+  for (const auto& t : tails) kmax = std::max(kmax, t.size());
+  for (size_t j = 0; j < kmax; ++j)
+    for (const auto& t : tails)
+      if (j < t.size()) claim.push_back(t[j]);
 }
 
 void fixed_split_ranges(const std::vector<DevUnit>& units, int split, std::vector<int32_t>& cta_begin) {

@@ -32,7 +32,8 @@ _SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, 
                 "fixed_split": LA_SCHED_FIXED_SPLIT}
 
 # Every symbol include/la.h declares (tests check the library exports all of them).
-EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_info_get", "la_plan_export", "la_decode",
+EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_info_get", "la_plan_export",
+           "la_plan_export_claims", "la_decode",
            "la_decode_partial", "la_combine", "la_decode_host", "la_plan_status", "la_plan_destroy",
            "la_launch_count", "la_status_string", "la_last_error", "la_version", "la_plan_trace",
            "la_plan_xchg_handle", "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status")
@@ -84,11 +85,15 @@ def lib() -> ctypes.CDLL:
     L.la_plan_opts_init.argtypes = [ctypes.POINTER(la_plan_opts)]
     L.la_plan.argtypes = [i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int32), i32, i32,
                           ctypes.POINTER(la_plan_opts), ctypes.POINTER(vp)]
-    L.la_plan_update.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), vp]
-    L.la_plan_status.argtypes = [vp]
+    if hasattr(L, "la_plan_update"):  # (older builds, e.g. LEANATTN_LIB A/B variants, lack these)
+        L.la_plan_update.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), vp]
+        L.la_plan_status.argtypes = [vp]
     L.la_plan_info_get.argtypes = [vp, ctypes.POINTER(la_plan_info)]
     L.la_plan_export.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.c_size_t,
                                  ctypes.POINTER(ctypes.c_size_t)]
+    if hasattr(L, "la_plan_export_claims"):
+        L.la_plan_export_claims.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.c_size_t,
+                                            ctypes.POINTER(ctypes.c_size_t)]
     L.la_decode.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.la_decode_partial.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.la_combine.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
@@ -105,7 +110,8 @@ def lib() -> ctypes.CDLL:
     L.la_launch_count.restype = i64
     L.la_status_string.restype = ctypes.c_char_p
     L.la_last_error.restype = ctypes.c_char_p
-    for name in ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_status", "la_plan_info_get", "la_plan_export", "la_decode",
+    for name in ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_status", "la_plan_info_get", "la_plan_export",
+                 "la_plan_export_claims", "la_decode",
                  "la_decode_partial", "la_combine", "la_decode_host", "la_plan_trace", "la_plan_xchg_handle",
                  "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status"):
         if hasattr(L, name):
@@ -144,7 +150,7 @@ class Plan:
                  tile_n: int = 0, dtype: str = "bf16", scale: float = 0.0, layout: str = "bhsd",
                  max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
                  ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
-                 dyn_first_permille: int = 750, dyn_min_chunk: int = 2, split: int = 0,
+                 dyn_first_permille: int = 940, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
                  causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None,
                  k_scale: float = 0.0, v_scale: float = 0.0, engine: str = "auto", stream=None):
@@ -239,6 +245,15 @@ class Plan:
         buf = np.zeros((n.value, 7), dtype=np.int32)
         _check(lib().la_plan_export(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n.value,
                                     ctypes.byref(n)), "la_plan_export")
+        return buf
+
+    def claims(self) -> np.ndarray:
+        """``la_plan_export_claims``: claim c runs (virtual) CTA range claims[c]."""
+        n = ctypes.c_size_t()
+        _check(lib().la_plan_export_claims(self._h, None, 0, ctypes.byref(n)), "la_plan_export_claims")
+        buf = np.zeros(n.value, dtype=np.int32)
+        _check(lib().la_plan_export_claims(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n.value,
+                                           ctypes.byref(n)), "la_plan_export_claims")
         return buf
 
     def trace(self) -> np.ndarray:

@@ -36,14 +36,10 @@ def test_dynamic_fold_tree_on_a_colliding_shape():
     schedule a virtual CTA ends one unit's last fold group and hosts the next unit's first
     group (the r01 counter index collided there -- checked here on the plan's own export)."""
     import paper_2405_10480_b200 as la
-    from test_plan_update import _dynamic_counter_keys
     p = synth.Problem(3, 8, 4, 128, [32544, 5404, 6961], dtype="bf16", dist="D2", seed=31)
     q, k, v = cuda_inputs(p)
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, p.ctx_lens, schedule="dynamic", engine="mma")
-    rows = plan.export()
-    old = _dynamic_counter_keys(rows, plan.info.slot_capacity, fixed=False)
-    assert any(len(s) > 1 for s in old.values()), "shape no longer collides under the r01 indexing"
-    assert all(len(s) == 1 for s in _dynamic_counter_keys(rows, plan.info.slot_capacity).values())
+    # (r02 folds each unit by its last arriving piece; the shape stays as a regression case)
     O_ref, L_ref = run_oracle(p)
     first = None
     for it in range(4):   # counters must come back clean for every next launch

@@ -204,19 +204,43 @@ def test_segments_from_ranges_generalises_alg2():
         assert sorted(segs, key=lambda s: (s.cta, s.unit)) == sorted(brute, key=lambda s: (s.cta, s.unit))
 
 
-def test_guided_ranges_properties():
-    for I, G in [(65536, 148), (32768, 148), (245056, 148), (10, 4), (7, 10), (1000, 1), (149, 148)]:
-        b = oracle.guided_ranges(I, G)
-        sizes = np.diff(b)
-        assert b[0] == 0 and b[-1] == I and np.all(sizes >= 1)
-        first = I * 750 // (1000 * G)
-        if first >= 1:
-            assert np.all(sizes[:G] == first)                       # the static 75% part
-            tail = sizes[G:]
-            assert np.all(tail[:-1][: len(tail) - 1] >= 1)
-        # later ranges never grow (guided self-scheduling), last ones >= min chunk except the clip
-        rest = sizes[G:] if first >= 1 else sizes
-        assert all(rest[i] >= rest[i + 1] or i + 1 == len(rest) - 1 for i in range(len(rest) - 1))
+def test_balanced_ranges_properties():
+    """The dynamic schedule's layout (oracle.balanced_ranges): each Eq. 2 range (reading C8)
+    is its head followed by k equal chunks; the pieces tile [0, I) in order; claims are every
+    head in range order, then chunk j of every range, j = 0, 1, ..."""
+    for I, G, hp, mc in [(65536, 148, 940, 2), (32768, 148, 940, 2), (245056, 148, 940, 2), (10, 4, 500, 1),
+                         (7, 10, 940, 2), (1000, 1, 900, 3), (149, 148, 500, 1), (5000, 37, 800, 4)]:
+        begins, claim = oracle.balanced_ranges(I, G, hp, mc)
+        sizes = np.diff(begins)
+        assert begins[0] == 0 and begins[-1] == I and np.all(sizes >= 1)
+        assert sorted(claim) == list(range(len(begins) - 1))
+        bset = set(begins)
+        heads = []
+        for g in range(G):
+            lo, hi = oracle.cta_range(I, G, g)
+            if lo == hi:
+                continue
+            assert lo in bset and hi in bset                    # every Eq. 2 range is a union of pieces
+            inner = [x for x in begins if lo <= x <= hi]
+            pieces = np.diff(inner)
+            L = hi - lo
+            t0 = L * (1000 - hp) // 1000
+            s = max(mc, -(-t0 // 8))
+            k = len(pieces) - 1
+            assert k == min(t0 // s, (L - 1) // s) and k <= 8   # k chunks of s, head >= 1
+            assert np.all(pieces[1:] == s) and pieces[0] == L - k * s
+            heads.append(begins.index(lo))
+        assert claim[:len(heads)] == heads                      # heads first, in range order
+        rest = claim[len(heads):]
+        rounds = [begins[v + 1] - begins[v] for v in rest]
+        assert all(r >= 1 for r in rounds)
+    # head share 1000: no tail -- exactly Alg. 2's equal ranges, claimed in order
+    for I, G in [(65536, 148), (10, 4), (7, 10)]:
+        begins, claim = oracle.balanced_ranges(I, G, 1000, 2)
+        exp = sorted({oracle.cta_range(I, G, g)[0] for g in range(G)} | {I})
+        assert begins == exp and claim == list(range(len(begins) - 1))
+    # hand example: I = 10, G = 4 (ranges 3, 3, 2, 2), half tails of 1 LeanTile
+    assert oracle.balanced_ranges(10, 4, 500, 1) == ([0, 2, 3, 5, 6, 7, 8, 9, 10], [0, 2, 4, 6, 1, 3, 5, 7])
 
 
 def test_alg2_with_virtual_ctas_equals_eq1():
@@ -228,7 +252,7 @@ def test_alg2_with_virtual_ctas_equals_eq1():
     O_ref, L_ref = oracle.decode_attention(q, k, v, lens, 0.35)
     c_n = [-(-n // 16) for n in lens for _ in range(3)]
     for G in (1, 3, 7, 40):
-        begins = oracle.guided_ranges(sum(c_n), G)
+        begins, _ = oracle.balanced_ranges(sum(c_n), G, 700, 1)
         O, L = oracle.lean_attention(q, k, v, lens, 0.35, 16, G, begins=begins)
         assert np.max(np.abs(O - O_ref)) <= 1e-12 and np.max(np.abs(L - L_ref)) <= 1e-12
 

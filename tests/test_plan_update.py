@@ -115,9 +115,11 @@ def test_update_validation(la):
 
 
 def _dynamic_counter_keys(rows, slot_stride, fixed=True):
-    """The kernel's fold-tree counter index of every counted segment (decode.cu, dynamic
-    branch): group g0 = host + 16 * floor((v - host) / 16); index g0 (+ slot_stride for a
-    unit's first group when `fixed`).  Returns {index: {(unit, g0), ...}}."""
+    """The r01 kernel's fold-tree counter index of every counted segment (groups of 16
+    segments from the unit's host; index g0, plus slot_stride for a unit's first group when
+    `fixed`).  Returns {index: {(unit, g0), ...}} -- kept to show the shapes where the r01
+    indexing collided; r02 folds each unit by its last arriving piece, with ONE
+    counter per unit."""
     host = {int(r[1]): int(r[0]) for r in rows if r[4] == 1}
     keys = {}
     for r in rows:
@@ -131,22 +133,22 @@ def _dynamic_counter_keys(rows, slot_stride, fixed=True):
     return keys
 
 
-def test_dynamic_fold_counters_are_distinct(la):
+def test_dynamic_pieces_of_a_unit_are_contiguous(la):
+    """The kernel's dynamic fold counts a unit's pieces in ONE per-unit counter and expects
+    last_cta - host_cta + 1 of them: every virtual CTA from the unit's host to its last CTA
+    holds exactly one segment of the unit."""
     rng = np.random.default_rng(5)
-    collided_before = 0
-    for trial in range(300):
+    for trial in range(200):
         batch = int(rng.integers(1, 5))
         hkv = int(rng.choice([1, 2, 4, 8]))
         g = int(rng.choice([1, 2, 4, 8]))
         p = la.Plan(batch, hkv * g, hkv, 128, _lens(rng, batch, 1000, 40000), host_only=True, schedule="dynamic",
-                    engine="mma")
+                    engine="mma", dyn_first_permille=int(rng.integers(500, 1001)))
         rows = p.export()
-        keys = _dynamic_counter_keys(rows, p.info.slot_capacity)
-        assert all(len(s) == 1 for s in keys.values()), trial
-        assert max(keys) < 2 * p.info.slot_capacity          # inside the allocated [2][capacity]
-        old = _dynamic_counter_keys(rows, p.info.slot_capacity, fixed=False)
-        collided_before += any(len(s) > 1 for s in old.values())
-    assert collided_before > 0   # the r01 indexing did collide on some of these shapes
+        for u in np.unique(rows[:, 1]):
+            r = rows[rows[:, 1] == u]
+            host = int(r[r[:, 4] == 1][0, 0])
+            assert sorted(r[:, 0].tolist()) == list(range(host, int(r[0, 6]) + 1))
 
 
 def test_quantization_efficiency_matches_oracle(la):

@@ -48,7 +48,7 @@ def test_plan_opts_struct_matches_the_header(la):
     assert la.lib().la_plan_opts_init(ctypes.cast(buf, ctypes.POINTER(la_plan_opts))) == 0
     assert all(b == 0xAB for b in bytes(buf)[n:]), "la_plan_opts_init wrote past the ctypes struct"
     o = la_plan_opts.from_buffer(buf)
-    assert (o.num_sms, o.ctas_per_sm, o.q_len, o.causal, o.dyn_first_permille, o.engine) == (148, 1, 1, 1, 750, 2)
+    assert (o.num_sms, o.ctas_per_sm, o.q_len, o.causal, o.dyn_first_permille, o.engine) == (148, 1, 1, 1, 940, 2)
     header = open(os.path.join(ROOT, "include", "la.h")).read()
     body = header[header.index("typedef struct {\n  float scale;"):header.index("} la_plan_opts;")]
     fields = re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(\w+);", body, re.M)
@@ -147,27 +147,31 @@ def test_validation(la, args, status):
 
 
 def test_dynamic_schedule_bit_exact(la):
-    """LA_SCHED_DYNAMIC: Alg. 2's walk over the guided virtual-CTA ranges, bit-exact."""
+    """LA_SCHED_DYNAMIC: Alg. 2's walk over the balanced virtual-CTA ranges (heads + tail
+    chunks), bit-exact against the oracle's layout, incl. the claim order (la_plan_export's
+    rows are per virtual CTA; the claim order is checked through la_plan_info + the oracle)."""
     rng = np.random.default_rng(1)
     import synth
-    cases = [(synth.config(c), 148) for c in ("c2", "c3", "c4", "c5")]
+    cases = [(synth.config(c), 148, 940, 2) for c in ("c2", "c3", "c4", "c5")]
     for trial in range(25):
         batch = int(rng.integers(1, 9))
         heads = int(rng.integers(1, 17))
         lens = [int(x) for x in rng.integers(1, 30000, size=batch)]
         cases.append((synth.Problem(batch, heads, heads, 128, lens, layout=["bhsd", "packed"][trial % 2]),
-                      int(rng.integers(1, 200))))
-    for pr, sms in cases:
+                      int(rng.integers(1, 200)), int(rng.integers(500, 1001)), int(rng.integers(1, 6))))
+    for pr, sms, hp, mc in cases:
         p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
-                    num_sms=sms, layout=pr.layout, schedule="dynamic")
+                    num_sms=sms, layout=pr.layout, schedule="dynamic", dyn_first_permille=hp, dyn_min_chunk=mc)
         units = unit_order(pr.batch, pr.heads_kv, pr.layout)
         c_n = [-(-pr.ctx_lens[b] // 128) for (b, _h) in units]
         I = sum(c_n)
         G = min(sms, I)
-        begins = oracle.guided_ranges(I, G, 750, 2)
+        begins, claim = oracle.balanced_ranges(I, G, hp, mc)
         exp = np.array([s.row() for s in oracle.segments_from_ranges(c_n, begins)], dtype=np.int32).reshape(-1, 7)
         assert np.array_equal(p.export(), exp)
-        assert p.info.num_vctas == len(begins) - 1 and p.info.grid == min(G, len(begins) - 1)
+        assert p.info.num_vctas == len(begins) - 1 and p.info.grid == G
+        assert p.info.num_vctas <= p.info.slot_capacity
+        assert p.claims().tolist() == claim
         # partial slots: <= 1 non-host and <= 1 non-finishing-host segment per virtual CTA
         rows = p.export()
         assert np.bincount(rows[rows[:, 4] == 0][:, 0], minlength=p.info.num_vctas).max() <= 1
