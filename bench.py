@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--cpu-heads", type=int, default=32, help="heads in the oracle cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--schedule", default="streamk", choices=["streamk", "dynamic", "sequential", "fixed_split"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "streamk", "dynamic", "sequential", "fixed_split"])
     ap.add_argument("--page-size", type=int, default=0, help="run the config in a paged KV pool (16..256)")
     ap.add_argument("--engine", default="auto", choices=["auto", "mma", "tcgen05"],
                     help="tensor-core engine for T_m > 1 tiles (GQA): auto (the plan's rule), mma.sync or tcgen05 + TMEM")
@@ -246,6 +246,7 @@ def bench_ours(args):
     import torch.distributed as dist
     import synth
     import paper_2405_10480_b200 as la
+    from paper_2405_10480_b200.leanattn import SCHEDULE_NAMES
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -475,7 +476,9 @@ def bench_ours(args):
                        "heads_kv": p.heads_kv, "head_dim": p.head_dim,
                        "context": p.ctx_lens[0] if len(set(p.ctx_lens)) == 1 else p.ctx_lens,
                        "kv_bytes": total_kv, "tile_n": info.tile_n, "grid": info.grid,
-                       "stage_tokens": info.stage_tokens, "schedule": args.schedule,
+                       "stage_tokens": info.stage_tokens,
+                       "schedule": SCHEDULE_NAMES[info.schedule] + (" (auto)" if args.schedule == "auto" else ""),
+                       "quantization_efficiency": info.quantization_efficiency,
                        **({"engine": {0: "mma.sync", 1: "tcgen05"}[info.engine]} if info.engine >= 0 else {}),
                        **({"q_len": args.q_len, "query_tile_rows": info.tile_rows, "units": info.num_units}
                           if args.q_len > 1 else {}),

@@ -89,11 +89,15 @@ typedef enum {
                               unit's pieces are folded by its LAST arriving piece in ascending
                               order -- same result semantics, bitwise deterministic, balances
                               TIME instead of LeanTile counts                    */
-  LA_SCHED_FIXED_SPLIT = 3 /* FlashDecoding's fixed-split decomposition: every
+  LA_SCHED_FIXED_SPLIT = 3,/* FlashDecoding's fixed-split decomposition: every
                               unit cut into `split` near-equal chunks (first chunks take the
                               extra LeanTile), chunks run in order on the persistent
                               CTAs like hardware waves, folded in-kernel (the comparison
                               baseline of the paper's evaluation, NEXT-1)                 */
+  LA_SCHED_AUTO = 4        /* (default) LA_SCHED_DYNAMIC for one-row tiles (MHA, T_m = 1) whose
+                              Eq. 2 ranges hold >= 64 LeanTiles, LA_SCHED_STREAMK otherwise and
+                              for exchange plans -- the faster of the two as measured on B200
+                              (DESIGN §6); la_plan_info.schedule reports the choice          */
 } la_schedule;
 
 typedef struct {
@@ -107,7 +111,7 @@ typedef struct {
   int num_sms;       /* host-only plans: SM count assumed when grid == 0 (default 148)    */
   int ctas_per_sm;   /* host-only plans: occupancy assumed when grid == 0 (default 1)     */
   int host_only;     /* 1 -> plan the schedule only, no device state (inspection/tests)   */
-  int schedule;      /* la_schedule, default LA_SCHED_STREAMK (Alg. 2 exactly)            */
+  int schedule;      /* la_schedule, default LA_SCHED_AUTO (resolved at la_plan)          */
   int trace;         /* 1 -> every la_decode records a per-CTA timeline (la_plan_trace)     */
   int dyn_first_permille; /* LA_SCHED_DYNAMIC: head share of each Eq. 2 range, permille (default 940;
                              1000 = no tail: Alg. 2's ranges exactly)                        */
@@ -318,6 +322,8 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
  * smid, t_start, t_publish (non-host partial signalled, Alg2§23; for a static waiting host:
  * its peers' partials folded; 0 if none), t_wait_begin,
  * t_wait_end (host fold wait, Alg2§28; 0 if none), t_end -- %globaltimer nanoseconds.
+ * LA_SCHED_DYNAMIC / FIXED_SPLIT: t_publish = when the epilogue took the CTA's last segment,
+ * t_wait_begin / t_wait_end = claims taken / LeanTiles streamed (counts, not times).
  * *n_ctas receives G.  LA_ERR_STATE if the plan has no trace buffer.
  */
 #define LA_TRACE_FIELDS 6

@@ -220,9 +220,19 @@ la_status upload_tables(la_plan_s* plan, cudaStream_t stream, bool sync) {
   const int32_t hdr[4] = {s.grid, 0, 0, 0};
   std::memcpy(h, hdr, sizeof(hdr));
   std::memcpy(h + plan->off_units, s.units.data(), s.units.size() * sizeof(DevUnit));
-  std::memcpy(h + plan->off_begin, s.cta_begin.data(), size_t(s.grid + 1) * sizeof(int32_t));
-  std::memcpy(h + plan->off_first, s.cta_first_unit.data(), size_t(s.grid) * sizeof(int32_t));
-  std::memcpy(h + plan->off_claim, s.claim.data(), size_t(s.grid) * sizeof(int32_t));
+  // the kernel reads no range count: the tables are padded to the plan's capacity with empty
+  // ranges [I, I) (static CTAs past the schedule idle) and claims of -1 (a dynamic CTA that
+  // draws one has no more work; every CTA draws exactly one, so cap + launch entries)
+  const int CAP = plan->slot_cap;
+  int32_t* cb = reinterpret_cast<int32_t*>(h + plan->off_begin);
+  int32_t* cf = reinterpret_cast<int32_t*>(h + plan->off_first);
+  int32_t* cl = reinterpret_cast<int32_t*>(h + plan->off_claim);
+  std::memcpy(cb, s.cta_begin.data(), size_t(s.grid + 1) * sizeof(int32_t));
+  std::fill(cb + s.grid + 1, cb + CAP + 1, int32_t(s.total_iters));
+  std::memcpy(cf, s.cta_first_unit.data(), size_t(s.grid) * sizeof(int32_t));
+  std::fill(cf + s.grid, cf + CAP, int32_t(s.units.empty() ? 0 : s.units.size() - 1));
+  std::memcpy(cl, s.claim.data(), size_t(s.grid) * sizeof(int32_t));
+  std::fill(cl + s.grid, cl + CAP + s.phys_grid, int32_t(-1));
   const la::Problem& p = plan->prob;
   if (plan->pt_stride) {  // block table, rows padded to pt_stride (the producer reads 32-entry windows)
     int32_t* bt = reinterpret_cast<int32_t*>(h + plan->off_bt);
@@ -290,7 +300,7 @@ la_status la_plan_opts_init(la_plan_opts* o) {
   o->layout = LA_KV_BHSD;
   o->num_sms = 148;
   o->ctas_per_sm = 1;
-  o->schedule = LA_SCHED_STREAMK;
+  o->schedule = LA_SCHED_AUTO;
   o->dyn_first_permille = 940;
   o->dyn_min_chunk = 2;
   o->q_len = 1;
@@ -316,7 +326,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (opts.layout != LA_KV_BHSD && opts.layout != LA_KV_PACKED && opts.layout != LA_KV_PAGED)
     return fail(LA_ERR_INVALID, "bad layout");
   if (opts.schedule != LA_SCHED_STREAMK && opts.schedule != LA_SCHED_SEQUENTIAL &&
-      opts.schedule != LA_SCHED_DYNAMIC && opts.schedule != LA_SCHED_FIXED_SPLIT)
+      opts.schedule != LA_SCHED_DYNAMIC && opts.schedule != LA_SCHED_FIXED_SPLIT && opts.schedule != LA_SCHED_AUTO)
     return fail(LA_ERR_INVALID, "bad schedule");
   if (opts.split < 0) return fail(LA_ERR_INVALID, "split must be >= 0");
   if (opts.dyn_first_permille < 0 || opts.dyn_first_permille > 1000 || opts.dyn_min_chunk < 1)
@@ -358,7 +368,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   if (opts.engine != LA_ENGINE_MMA_SYNC && opts.engine != LA_ENGINE_TCGEN05 && opts.engine != LA_ENGINE_AUTO)
     return fail(LA_ERR_INVALID, "engine must be LA_ENGINE_AUTO, LA_ENGINE_MMA_SYNC or LA_ENGINE_TCGEN05");
   const bool tc5_ok = head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16);
-  const bool static_sched = opts.schedule == LA_SCHED_STREAMK || opts.schedule == LA_SCHED_SEQUENTIAL;
+  // AUTO resolves to stream-K for multi-row tiles (below), so it admits the wide tcgen05 tiles
+  const bool static_sched = opts.schedule == LA_SCHED_STREAMK || opts.schedule == LA_SCHED_SEQUENTIAL ||
+                            opts.schedule == LA_SCHED_AUTO;
   const int engine = opts.engine != LA_ENGINE_AUTO ? opts.engine
                      : (max_rows > 8 && tc5_ok && static_sched ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
   // T_m: 1 -> CUDA-core engine, else tensor-core tiles of <= 8 rows (mma.sync: N = 8), or
@@ -462,6 +474,17 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
 
   // ---- schedule (Alg2§4-18) -----------------------------------------------------------
   plan->sched.tile_n = tile_n ? tile_n : auto_tile_n(p);
+  if (p.schedule == LA_SCHED_AUTO) {
+    // the balanced dynamic schedule for one-row tiles whose Eq. 2 ranges are long enough for a
+    // tail to matter (measured faster on B200: c2 -1%, c4 -1%); stream-K for multi-row tiles
+    // (whose 8-32-row folds cost more per piece than the balance gains) and exchange plans
+    std::vector<DevUnit> tmp;
+    int64_t I = 0;
+    la::build_units(p, plan->sched.tile_n, tmp, I);
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(plan->opt_grid ? plan->opt_grid : plan->max_ctas, I));
+    p.schedule = (p.rows() == 1 && !xw && I / G >= 64) ? LA_SCHED_DYNAMIC : LA_SCHED_STREAMK;
+    plan->prob.schedule = p.schedule;
+  }
   {
     const int64_t icap = capacity_iters(p, plan->sched.tile_n, opts.max_ctx > 0, 0);
     la_status st = plan_schedule(plan, true, icap);
@@ -492,7 +515,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     plan->off_begin = plan->off_units + align256(U * sizeof(DevUnit));
     plan->off_first = plan->off_begin + align256(size_t(CAP + 1) * sizeof(int32_t));
     plan->off_claim = plan->off_first + align256(size_t(CAP) * sizeof(int32_t));
-    plan->off_bt = plan->off_claim + align256(size_t(CAP) * sizeof(int32_t));
+    plan->off_bt = plan->off_claim + align256(size_t(CAP + GP) * sizeof(int32_t));
     plan->up_bytes = plan->off_bt + align256(size_t(p.batch) * plan->pt_stride * sizeof(int32_t));
     const size_t b_po = align256(size_t(CAP) * 2 * p.rows() * head_dim * sizeof(float));
     const size_t b_pml = align256(size_t(CAP) * 2 * p.rows() * 4 * sizeof(float));
@@ -672,7 +695,6 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   a.v = v;
   a.out = out;
   a.lse = lse;
-  a.hdr = plan->d_hdr;
   a.units = plan->d_units;
   a.cta_begin = plan->d_cta_begin;
   a.cta_first_unit = plan->d_cta_first;

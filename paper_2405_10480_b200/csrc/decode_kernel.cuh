@@ -278,7 +278,7 @@ struct MhaEngine {
   static constexpr int STAGE_TOK = 32768 / (2 * ROWB);      // 32 KiB of K+V per stage
   static constexpr int STAGE_BYTES = 2 * STAGE_TOK * ROWB;
   static constexpr int HEADS = 1;                           // q-heads per unit
-  static constexpr int FOLD_FLOATS = NCW * (D + 2);         // per warp: O[D], m, l
+  static constexpr int FOLD_FLOATS = NCW * (D + 4);         // per warp: O[D], m, l, pad (16-B rows)
   static constexpr int FOLD_BUFS = 2;                       // double-buffered hand-off
   static constexpr bool ZERO_RING = true;                   // tail rows must be finite
   using QElem = T;                                          // Q storage type
@@ -383,7 +383,7 @@ struct MhaEngine {
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) s.l += __shfl_xor_sync(0xffffffffu, s.l, off);
-    float* fb = fold + warp * (D + 2);
+    float* fb = fold + warp * (D + 4);
     if (kg == 0) {
 #pragma unroll
       for (int e = 0; e < EPL / 2; ++e) {
@@ -488,7 +488,7 @@ struct GqaEngine {
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;
   static constexpr int HEADS = 8;                 // MMA N: q-heads per unit (padded to 8)
   static constexpr int KS = D / 16;               // k-steps of QK^T = m-tiles of PV
-  static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
+  static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 4);
   static constexpr int FOLD_BUFS = LA_GQA_FB;     // double-buffered hand-off (measured best)
   static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
   using QElem = T;
@@ -670,21 +670,21 @@ struct GqaEngine {
       s.l[0] += __shfl_xor_sync(0xffffffffu, s.l[0], off);
       s.l[1] += __shfl_xor_sync(0xffffffffu, s.l[1], off);
     }
-    float* fb = fold + warp * HEADS * (D + 2);  // [head][D + 2]
+    float* fb = fold + warp * HEADS * (D + 4);  // [head][D + 4]
     const int h0 = 2 * tq, h1 = 2 * tq + 1;
 #pragma unroll
     for (int mm = 0; mm < KS; ++mm) {
       const int c = 16 * mm + gq;
-      fb[h0 * (D + 2) + c] = s.o[mm][0];
-      fb[h1 * (D + 2) + c] = s.o[mm][1];
-      fb[h0 * (D + 2) + c + 8] = s.o[mm][2];
-      fb[h1 * (D + 2) + c + 8] = s.o[mm][3];
+      fb[h0 * (D + 4) + c] = s.o[mm][0];
+      fb[h1 * (D + 4) + c] = s.o[mm][1];
+      fb[h0 * (D + 4) + c + 8] = s.o[mm][2];
+      fb[h1 * (D + 4) + c + 8] = s.o[mm][3];
     }
     if (gq == 0) {
-      fb[h0 * (D + 2) + D] = s.m[0];
-      fb[h0 * (D + 2) + D + 1] = s.l[0];
-      fb[h1 * (D + 2) + D] = s.m[1];
-      fb[h1 * (D + 2) + D + 1] = s.l[1];
+      fb[h0 * (D + 4) + D] = s.m[0];
+      fb[h0 * (D + 4) + D + 1] = s.l[0];
+      fb[h1 * (D + 4) + D] = s.m[1];
+      fb[h1 * (D + 4) + D + 1] = s.l[1];
     }
   }
 };
@@ -733,7 +733,7 @@ struct Fp8Engine {
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;
   static constexpr int HEADS = ROWS_;             // fold-buffer rows (MMA N is 8 regardless)
   static constexpr int KS = D / 16;
-  static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 2);
+  static constexpr int FOLD_FLOATS = NCW * HEADS * (D + 4);
   static constexpr int FOLD_BUFS = ROWS_ == 1 ? LA_FP8M_FB : LA_FP8_FB;
   static constexpr bool ZERO_RING = false;        // tail V rows are zeroed per warp
   using QElem = __nv_bfloat16;                    // bf16 q next to the E4M3 cache
@@ -896,24 +896,24 @@ struct Fp8Engine {
       s.l[0] += __shfl_xor_sync(0xffffffffu, s.l[0], off);
       s.l[1] += __shfl_xor_sync(0xffffffffu, s.l[1], off);
     }
-    float* fb = fold + warp * HEADS * (D + 2);  // [head][D + 2]
+    float* fb = fold + warp * HEADS * (D + 4);  // [head][D + 4]
     const int h0 = 2 * tq, h1 = 2 * tq + 1;
     if (h0 < HEADS) {
 #pragma unroll
       for (int mm = 0; mm < KS; ++mm)  // accumulator rows gq / gq + 8 = dims c / c + 1
-        *reinterpret_cast<float2*>(fb + h0 * (D + 2) + 16 * mm + 2 * gq) = make_float2(s.o[mm][0], s.o[mm][2]);
+        *reinterpret_cast<float2*>(fb + h0 * (D + 4) + 16 * mm + 2 * gq) = make_float2(s.o[mm][0], s.o[mm][2]);
       if (gq == 0) {
-        fb[h0 * (D + 2) + D] = s.m[0];
-        fb[h0 * (D + 2) + D + 1] = s.l[0];
+        fb[h0 * (D + 4) + D] = s.m[0];
+        fb[h0 * (D + 4) + D + 1] = s.l[0];
       }
     }
     if (h1 < HEADS) {
 #pragma unroll
       for (int mm = 0; mm < KS; ++mm)
-        *reinterpret_cast<float2*>(fb + h1 * (D + 2) + 16 * mm + 2 * gq) = make_float2(s.o[mm][1], s.o[mm][3]);
+        *reinterpret_cast<float2*>(fb + h1 * (D + 4) + 16 * mm + 2 * gq) = make_float2(s.o[mm][1], s.o[mm][3]);
       if (gq == 0) {
-        fb[h1 * (D + 2) + D] = s.m[1];
-        fb[h1 * (D + 2) + D + 1] = s.l[1];
+        fb[h1 * (D + 4) + D] = s.m[1];
+        fb[h1 * (D + 4) + D + 1] = s.l[1];
       }
     }
   }
@@ -981,7 +981,7 @@ struct Tc5Engine {
   static constexpr int LN = HEADS == 32 && !LDEFER ? 1 : HEADS;
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
-  static constexpr int FOLD_FLOATS = NWG * HEADS * (D + 2);
+  static constexpr int FOLD_FLOATS = NWG * HEADS * (D + 4);
   static constexpr int FOLD_BUFS = 1;
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
@@ -1291,9 +1291,9 @@ struct Tc5Engine {
   __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
     const int slot = warp / WPS, sub = warp % WPS;
     float* red2 = reinterpret_cast<float*>(extra() + slot * XS + RED2_OFF);  // [4][HEADS]
-    float* fb = fold + slot * HEADS * (D + 2);                                  // [row][D + 2]
+    float* fb = fold + slot * HEADS * (D + 4);                                  // [row][D + 4]
 #pragma unroll
-    for (int h = 0; h < HEADS; ++h) fb[h * (D + 2) + 32 * sub + lane] = s.o[h];
+    for (int h = 0; h < HEADS; ++h) fb[h * (D + 4) + 32 * sub + lane] = s.o[h];
     if constexpr (HEADS == 32 && !LDEFER) {
       red2[sub * HEADS + lane] = s.l[0];  // lane = row
     } else {
@@ -1311,8 +1311,8 @@ struct Tc5Engine {
     wg_bar(slot);
     if (sub == 0 && lane < HEADS) {
       const int h = lane;
-      fb[h * (D + 2) + D] = mv;
-      fb[h * (D + 2) + D + 1] = (red2[h] + red2[HEADS + h]) + (red2[2 * HEADS + h] + red2[3 * HEADS + h]);
+      fb[h * (D + 4) + D] = mv;
+      fb[h * (D + 4) + D + 1] = (red2[h] + red2[HEADS + h]) + (red2[2 * HEADS + h] + red2[3 * HEADS + h]);
     }
   }
 
@@ -1357,17 +1357,46 @@ struct Smem {
   static constexpr int EXTRA = EngX<E>::EXTRA;  // engine state right after the ring
   static constexpr int kFB = E::FOLD_BUFS;  // consumer -> epilogue fold buffers
   static constexpr int FOLD = EngX<E>::GF ? 0 : kFB * E::FOLD_FLOATS * 4;
-  static constexpr int BARS = (2 * E::NST + 2 * kQD + 2 * kFB + 1) * 8;
+  static constexpr int BARS = (2 * E::NST + 2 * kQD + 4 * kFB + 1) * 8;
   // segment queue, hand-off records, prod_j; then the segments' Q rows (TMA bulk copies)
   static constexpr int SQ_OFF = (RING + EXTRA + FOLD + BARS + 15) / 16 * 16;
-  static constexpr int MISC = kQD * int(sizeof(SegQ)) + kFB * int(sizeof(SegInfo)) + 16;
+  static constexpr int MISC = kQD * int(sizeof(SegQ)) + kFB * int(sizeof(SegInfo)) + 32 + 32 * 8 * 4;  // + prod_j, fold weights (16-B aligned)
   static constexpr int QB = E::QSTAGE ? (E::HEADS * E::D * int(sizeof(typename E::QElem)) + 127) / 128 * 128 : 0;
   static constexpr int QB_OFF = (SQ_OFF + MISC + 127) / 128 * 128;
   static constexpr int BYTES = 1024 + QB_OFF + kQD * QB;
 };
 
-// The epilogue warp's accumulator for one segment: lane owns dims c = lane + 32 j of every
-// head h (the fold buffer layout is [warp][head][D + 2] = O[D], m, l for both engines).
+// The epilogue warp's accumulator for one segment: lane owns dims J lane .. J lane + J - 1 of
+// every head h (one 16-B / 8-B vector per row); the fold buffer layout is [warp][head][D + 4]
+// = O[D], m, l, pad for every engine.
+template <int J>
+__device__ __forceinline__ void ldv(const float* p, float (&x)[J]) {
+  if constexpr (J == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+  } else {
+    static_assert(J == 2, "J");
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    x[0] = t.x; x[1] = t.y;
+  }
+}
+template <int J>
+__device__ __forceinline__ void ldv_cg(const float* p, float (&x)[J]) {  // L1-bypassing (acquired data)
+  if constexpr (J == 4) {
+    const float4 t = __ldcg(reinterpret_cast<const float4*>(p));
+    x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+  } else {
+    const float2 t = __ldcg(reinterpret_cast<const float2*>(p));
+    x[0] = t.x; x[1] = t.y;
+  }
+}
+template <int J>
+__device__ __forceinline__ void stv(float* p, const float (&x)[J], float scale = 1.f) {
+  if constexpr (J == 4)
+    *reinterpret_cast<float4*>(p) = make_float4(x[0] * scale, x[1] * scale, x[2] * scale, x[3] * scale);
+  else
+    *reinterpret_cast<float2*>(p) = make_float2(x[0] * scale, x[1] * scale);
+}
 template <class E>
 struct EpiAcc {
   static constexpr int H = E::HEADS, D = E::D, J = E::D / 32;
@@ -1395,6 +1424,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   SegQ* squeue = reinterpret_cast<SegQ*>(ring + Smem<E>::SQ_OFF);
   SegInfo* seginfo = reinterpret_cast<SegInfo*>(squeue + kQD);
   int* prod_j = reinterpret_cast<int*>(seginfo + kFB);  // stages the producer issued in all, once done (-1 before)
+  float* wscr = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(prod_j + 4) + 15) & ~uintptr_t(15));  // [32][<= 8] fold weights
   unsigned char* qbuf = ring + Smem<E>::QB_OFF;         // [kQD][QB]: Q rows of each queued segment
 
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -1410,7 +1440,6 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   const uint32_t xepoch_prev = *reinterpret_cast<volatile const uint32_t*>(&a.counters[CTR_XEPOCH]);
   const uint32_t xepoch = xepoch_prev == 0xFFFFFFFFu ? 1u : xepoch_prev + 1u;
   const bool dynamic = a.dynamic != 0;
-  const int NV = a.hdr[0];          // ranges of the current schedule (la_plan_update rewrites it)
   const int SS = a.slot_stride;     // partial slot 1 of (virtual) CTA v is SS + v
   unsigned long long* tr = a.trace ? a.trace + size_t(g) * TR_FIELDS : nullptr;
   if (tr && threadIdx.x == 0) {
@@ -1490,8 +1519,8 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     // last kClaimAhead LeanTiles (claim atomic -> claim table -> range -> unit record), so the
     // dependent round trips overlap the last stages instead of draining the ring at every
     // piece boundary.  The heads are the first G claims, so no CTA hoards two of them.
-    int v = NV, it = 0, it1 = 0, unit = 0;
-    int pst = 0, c_nx = -1, v_nx = NV, b_nx = 0, e_nx = 0, u_nx = 0;
+    int v = -1, it = 0, it1 = 0, unit = 0;
+    int pst = 0, c_nx = -1, v_nx = -1, b_nx = 0, e_nx = 0, u_nx = 0;
     DevUnit du_nx{};
     auto fetch_ahead = [&](int rem, bool force) {  // lane 0, dynamic
       if (pst == 0 && (force || rem <= kClaimAhead)) {
@@ -1499,11 +1528,11 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         pst = 1;
       }
       if (pst == 1 && (force || rem <= kClaimAhead - 1)) {
-        v_nx = c_nx < NV ? a.claim[c_nx] : NV;
+        v_nx = a.claim[c_nx];   // padded with -1 past the schedule's ranges: no more work
         pst = 2;
       }
       if (pst == 2 && (force || rem <= kClaimAhead - 2)) {
-        if (v_nx < NV) {
+        if (v_nx >= 0) {
           b_nx = a.cta_begin[v_nx];
           e_nx = a.cta_begin[v_nx + 1];
           u_nx = a.cta_first_unit[v_nx];
@@ -1511,7 +1540,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         pst = 3;
       }
       if (pst == 3 && (force || rem <= kClaimAhead - 3)) {
-        if (v_nx < NV) du_nx = a.units[u_nx];
+        if (v_nx >= 0) du_nx = a.units[u_nx];
         pst = 4;
       }
     };
@@ -1521,19 +1550,21 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         fetch_ahead(0, true);
         v = v_nx;
         pst = 0;
+#ifndef LA_EPI_TRACE
         if (tr) tr[TR_WAIT0] += 1;
+#endif
       } else {
-        v = g < NV ? g : NV;
+        v = g;   // static: CTA g runs range g (the range table is padded with empty ranges)
       }
-      if (v < NV) {
+      if (v >= 0) {
         it = dynamic ? b_nx : a.cta_begin[v];
         it1 = dynamic ? e_nx : a.cta_begin[v + 1];
         unit = dynamic ? u_nx : a.cta_first_unit[v];
-        if (it >= it1) v = NV;   // an idle range (forced G > I: S:219)
+        if (it >= it1) v = -1;   // an idle range (forced G > I: S:219; or a grid wider than the schedule)
         else u = dynamic ? du_nx : a.units[unit];
       }
     }
-    while (__shfl_sync(0xffffffffu, v, 0) < NV) {
+    while (__shfl_sync(0xffffffffu, v, 0) >= 0) {
       int seg_end = 0;
       DevUnit un{};  // the next unit of this piece, loaded ahead
       if (lane == 0) {
@@ -1580,15 +1611,17 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           fetch_ahead(0, true);
           v = v_nx;
           pst = 0;
+#ifndef LA_EPI_TRACE
           if (tr) tr[TR_WAIT0] += 1;
-          if (v < NV) {
+#endif
+          if (v >= 0) {
             it = b_nx;
             it1 = e_nx;
             unit = u_nx;
             u = du_nx;
           }
         } else {
-          v = NV;                // a static CTA runs exactly its range g
+          v = -1;                // a static CTA runs exactly its range g
         }
       }
     }
@@ -1624,8 +1657,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       for (int h = 0; h < H; ++h) {
         if (h >= nr) continue;
         const size_t row = size_t(slot) * a.group + h;
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) a.part_o[row * D + lane + 32 * jj] = acc.o[h][jj];
+        stv<J>(a.part_o + row * D + J * lane, acc.o[h]);
         if (lane == 0) {
           a.part_ml[row * 4] = acc.m[h];
           a.part_ml[row * 4 + 1] = acc.l[h];
@@ -1634,107 +1666,149 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       __threadfence();  // every lane: its stores are visible GPU-wide before the signal
       __syncwarp();
     };
-    // acc = f(...f(f(acc, P[slot(p0)]), P[slot(p0 + stride)])..., P[slot(<= p1)]), ascending
-    // (Alg2§27-35); host_v's partial lives in slot 1 of its virtual CTA, everyone else's in 0
-    // Fold peers p0, p0 + stride, .. <= p1 into acc (Alg2§27-35), their partials staged in
-    // smem `stg` (stg_floats): the ring when idle (static host; dynamic last arriver that has
-    // streamed its last stage) or the segment's consumed fold buffer.  A peer's O~ rows and its
-    // (m, l) rows are contiguous, so a round arrives by 1-D bulk copies on stage_bar -- ONE
-    // pair for a contiguous run of slot-0 peers (per-peer copies cost ~50 issue cycles each on
-    // this one warp, measured) -- one round trip per staging round.  The arithmetic runs in
-    // FIXED blocks of fcap peers (what one fold buffer holds) whatever the staging buffer, each
-    // in the max-first form (reading C22): M = max(m_acc, m_p..) first, then every O~_p enters
-    // with weight 2^(m_p - M), with four independent accumulator chains; the result depends
-    // only on the peers and their order: bitwise deterministic.
-    auto fold_smem = [&](int p0, int p1, int stride, int host_v, float* stg, int stg_floats) {
-      const int n = p1 < p0 ? 0 : (p1 - p0) / stride + 1;
-      const int po = a.group * D, pm = a.group * 4;  // staged per peer: whole slots (rows >= nr unused)
-      const int fcap = max(1, FOLD_FLOATS / (po + pm));
-      const int cap = max(fcap, stg_floats / (po + pm) / fcap * fcap);
-      const bool contiguous = stride == 1 && (host_v < p0 || host_v > p1);
-      asm volatile("fence.proxy.async.global;" ::: "memory");      // acquired partials -> TMA
-      #pragma unroll 1
-      for (int c0 = 0; c0 < n; c0 += cap) {
-        const int cs = min(cap, n - c0);
-        float* so0 = stg;            // [cs][nr][D]
-        float* sm0 = stg + cs * po;  // [cs][nr][4]
+    // Fold peers p0 .. p1 (ascending) into acc (Alg2§27-35, reading C22's max-first form): in
+    // blocks of 32 peers (lane i <-> peer i of the block),
+    //   A: every lane reads its peer's (m, l) of each row from L2; M = max(m_acc, m_p..) by a
+    //      warp reduction, w_p = 2^(m_p - M), l = 2^(m_acc - M) l_acc + sum_p w_p l_p;
+    //   B: the peers' O~ rows are staged in smem `stg` (stg_floats: the ring when idle, else a
+    //      consumed fold buffer) by 1-D bulk copies -- ONE copy for a contiguous run of slot-0
+    //      peers -- in as many rounds as the buffer needs, and O = 2^(m_acc - M) O_acc +
+    //      sum_p w_p O~_p accumulates in NCH fixed chains (peer k of the block -> chain k % NCH).
+    // The arithmetic depends only on the peers and their order -- never on the staging buffer
+    // -- so the result is bitwise deterministic.  host_v's partial lives in slot 1 (SS + v).
+    auto fold_smem = [&](int p0, int p1, int host_v, float* stg, int stg_floats) {
+      constexpr int NCH = H == 1 ? 4 : 1;  // independent accumulator chains per row
+      constexpr int RG = H < 8 ? H : 8;    // rows folded together (wide tcgen05 tiles: groups of 8)
+      const int n = p1 < p0 ? 0 : p1 - p0 + 1;
+      const int po = RG * D;               // staged per peer and row group: RG O~ rows
+      const int cap = max(NCH, stg_floats / po / NCH * NCH);  // a multiple of NCH: peer k -> chain k % NCH
+      auto slot_of = [&](int p) { return p + (p == host_v ? SS : 0); };
+      // stage the O~ rows (row group r0) of peers q0 .. q0 + cs - 1 into stg, asynchronously
+      auto stage = [&](int r0, int q0, int cs) {
+        // one copy for a run of slot-0 peers whose RG rows are all of their rows
+        const bool contiguous = RG == a.group && (host_v < q0 || host_v >= q0 + cs);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier smem reads
         __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(cs) * (po + pm) * 4);
+        const int rows = min(RG, a.group - r0);  // the slot's rows in this group
+        if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(cs) * rows * D * 4);
         __syncwarp();
         if (contiguous) {
-          if (lane == 0) {
-            const size_t r = size_t(p0 + c0) * a.group;
-            bulk_g2s_plain(so0, a.part_o + r * D, uint32_t(cs) * po * 4, stage_bar);
-            bulk_g2s_plain(sm0, a.part_ml + r * 4, uint32_t(cs) * pm * 4, stage_bar);
-          }
+          if (lane == 0) bulk_g2s_plain(stg, a.part_o + size_t(q0) * a.group * D, uint32_t(cs) * po * 4, stage_bar);
         } else {
           #pragma unroll 1
-          for (int i = lane; i < cs; i += 32) {
-            const int p = p0 + (c0 + i) * stride;
-            const size_t r = size_t(p + (p == host_v ? SS : 0)) * a.group;
-            bulk_g2s_plain(so0 + i * po, a.part_o + r * D, uint32_t(po) * 4, stage_bar);
-            bulk_g2s_plain(sm0 + i * pm, a.part_ml + r * 4, uint32_t(pm) * 4, stage_bar);
-          }
+          for (int i = lane; i < cs; i += 32)
+            bulk_g2s_plain(stg + i * po, a.part_o + (size_t(slot_of(q0 + i)) * a.group + r0) * D, uint32_t(rows) * D * 4,
+                           stage_bar);
         }
-        mbar_wait(stage_bar, stage_ph);
-        stage_ph ^= 1u;
-        #pragma unroll 1
-        for (int b0 = 0; b0 < cs; b0 += fcap) {   // arithmetic blocks of fcap peers
-        const int cn = min(fcap, cs - b0);
-        float* so = so0 + b0 * po;
-        float* sm = sm0 + b0 * pm;
+      };
+#ifdef LA_FOLD_PRINT
+      const unsigned long long ft0 = globaltimer();
+      unsigned long long ftA = 0, ftW = 0;
+#endif
+      asm volatile("fence.proxy.async.global;" ::: "memory");      // acquired partials -> TMA
+      #pragma unroll 1
+      for (int r0 = 0; r0 < nr; r0 += RG) {
+      #pragma unroll 1
+      for (int b0 = 0; b0 < n; b0 += 32) {
+        const int bn = min(32, n - b0);
+        stage(r0, p0 + b0, min(cap, bn));  // the first round flies while A reads the (m, l)s
+        // ---- A: max-first weights and l, every row at once (independent shuffle chains) --------
+        const size_t mlrow = size_t(slot_of(p0 + b0 + min(lane, bn - 1))) * a.group + r0;
+        float mp[RG], lp[RG], M[RG], wa[RG];
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
+        for (int hh = 0; hh < RG; ++hh) {  // every row's (m, l) first: ONE L2 round trip
+          const float2 ml = r0 + hh < nr ? __ldcg(reinterpret_cast<const float2*>(a.part_ml + (mlrow + hh) * 4))
+                                         : make_float2(-INFINITY, 0.f);
+          mp[hh] = lane < bn ? ml.x : -INFINITY;
+          lp[hh] = lane < bn ? ml.y : 0.f;
+          M[hh] = fmaxf(r0 + hh < nr ? acc.m[r0 + hh] : -INFINITY, mp[hh]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+          for (int hh = 0; hh < RG; ++hh) M[hh] = fmaxf(M[hh], __shfl_xor_sync(0xffffffffu, M[hh], o));
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh) {
+          mp[hh] = ex2_sub(mp[hh], M[hh]);  // w_p; 0 for lanes past the block / masked rows
+          lp[hh] *= mp[hh];
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+          for (int hh = 0; hh < RG; ++hh) lp[hh] += __shfl_xor_sync(0xffffffffu, lp[hh], o);
+        __syncwarp();  // the previous block's reads of wscr are done
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh) {
+          wscr[lane * RG + hh] = mp[hh];  // peer lane's weights, read back as broadcasts in B
+          const int h = r0 + hh;
+          wa[hh] = 0.f;
           if (h >= nr) continue;
-          float M = acc.m[h], lsum = 0.f;
+          wa[hh] = ex2_sub(acc.m[h], M[hh]);  // idle / masked accumulator: -inf -> 0
+          acc.l[h] = fmaf(wa[hh], acc.l[h], lp[hh]);
+          acc.m[h] = M[hh];
+        }
+        __syncwarp();
+        // ---- B: O~ rows, round by round ----------------------------------------------------
+#ifdef LA_FOLD_PRINT
+        ftA += globaltimer() - ft0;
+#endif
+        float oc[NCH][RG][J];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int hh = 0; hh < RG; ++hh)
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) oc[c][hh][jj] = c == 0 ? acc.o[r0 + hh][jj] * wa[hh] : 0.f;
+        #pragma unroll 1
+        for (int c0 = 0; c0 < bn; c0 += cap) {
+          const int cs = min(cap, bn - c0);
+          if (c0 > 0) stage(r0, p0 + b0 + c0, cs);
+          mbar_wait(stage_bar, stage_ph);
+          stage_ph ^= 1u;
+#ifdef LA_FOLD_PRINT
+          ftW += globaltimer() - ft0;
+#endif
           #pragma unroll 1
-          for (int i = lane; i < cn; i += 32) M = fmaxf(M, sm[i * pm + 4 * h]);
+          for (int i0 = 0; i0 < cs; i0 += NCH) {
 #pragma unroll
-          for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-          #pragma unroll 1
-          for (int i = lane; i < cn; i += 32) {
-            float* ml = sm + i * pm + 4 * h;
-            const float w = ex2_sub(ml[0], M);
-            lsum = fmaf(w, ml[1], lsum);
-            ml[2] = w;
-          }
-          __syncwarp();
-          const float wa = ex2_sub(acc.m[h], M);  // idle / masked accumulator: -inf -> 0
-          float o4[4][J];
+            for (int c = 0; c < NCH; ++c) {
+              const int i = i0 + c;  // block peer c0 + i is on chain c (c0 and i0 are multiples of NCH)
+              if (i >= cs) break;
+              float wk[RG];
 #pragma unroll
-          for (int jj = 0; jj < J; ++jj) {
-            o4[0][jj] = acc.o[h][jj] * wa;
-            o4[1][jj] = o4[2][jj] = o4[3][jj] = 0.f;
-          }
-          int i = 0;
-          #pragma unroll 1
-          for (; i + 4 <= cn; i += 4) {
+              for (int hh = 0; hh < RG; hh += (RG % 4 == 0 ? 4 : 1)) {  // broadcast reads of the weights
+                if constexpr (RG % 4 == 0) {
+                  const float4 t = *reinterpret_cast<const float4*>(wscr + (c0 + i) * RG + hh);
+                  wk[hh] = t.x; wk[hh + 1] = t.y; wk[hh + 2] = t.z; wk[hh + 3] = t.w;
+                } else {
+                  wk[hh] = wscr[(c0 + i) * RG + hh];
+                }
+              }
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const float w = sm[(i + c) * pm + 4 * h + 2];
-              const float* r = so + (i + c) * po + h * D;
+              for (int hh = 0; hh < RG; ++hh) {
+                if (r0 + hh >= nr) continue;
+                float rv[J];
+                ldv<J>(stg + i * po + hh * D + J * lane, rv);
 #pragma unroll
-              for (int jj = 0; jj < J; ++jj) o4[c][jj] = fmaf(w, r[lane + 32 * jj], o4[c][jj]);
+                for (int jj = 0; jj < J; ++jj) oc[c][hh][jj] = fmaf(wk[hh], rv[jj], oc[c][hh][jj]);
+              }
             }
           }
-          #pragma unroll 1
-          for (; i < cn; ++i) {
-            const float w = sm[i * pm + 4 * h + 2];
-            const float* r = so + i * po + h * D;
-#pragma unroll
-            for (int jj = 0; jj < J; ++jj) o4[0][jj] = fmaf(w, r[lane + 32 * jj], o4[0][jj]);
-          }
-#pragma unroll
-          for (int jj = 0; jj < J; ++jj) acc.o[h][jj] = (o4[0][jj] + o4[1][jj]) + (o4[2][jj] + o4[3][jj]);
-#pragma unroll
-          for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-          acc.l[h] = fmaf(wa, acc.l[h], lsum);
-          acc.m[h] = M;
+          __syncwarp();  // the next round overwrites the stage
         }
-        }
-        __syncwarp();  // the next round overwrites the stage
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh)
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj)
+            acc.o[r0 + hh][jj] = NCH == 4 ? (oc[0][hh][jj] + oc[1 % NCH][hh][jj]) + (oc[2 % NCH][hh][jj] + oc[3 % NCH][hh][jj])
+                                          : oc[0][hh][jj];
       }
+      }
+#ifdef LA_FOLD_PRINT
+      if (lane == 0 && n > 1)
+        printf("FOLD cta %d n %d nr %d cap %d ring %d: A-done %llu wait-done %llu total %llu ns\n", int(blockIdx.x), n, nr,
+               cap, int(stg == reinterpret_cast<float*>(ring)), ftA, ftW, globaltimer() - ft0);
+#endif
     };
     // NEXT-2: push this rank's normalised shard partial of unit `unit` into every rank's
     // exchange buffer, release flag [xr][unit] there, acquire the P flags of the unit here
@@ -1753,8 +1827,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         #pragma unroll 1
         for (int d = 0; d < P; ++d) {
           float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + q_row + h) * RS;
-#pragma unroll
-          for (int jj = 0; jj < J; ++jj) dst[lane + 32 * jj] = acc.o[h][jj] * inv;
+          stv<J>(dst + J * lane, acc.o[h], inv);
           if (lane == 0) dst[D] = l2;
         }
       }
@@ -1794,12 +1867,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           const float* src = xb + (size_t(r) * a.xrows + q_row + h) * RS;
           const float w = ex2_sub(ld_cg(src + D), M);
           l += w;
+          float rv[J];
+          ldv_cg<J>(src + J * lane, rv);
 #pragma unroll
-          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(w, ld_cg(src + lane + 32 * jj), o[jj]);
+          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(w, rv[jj], o[jj]);
         }
         const float inv = 1.f / l;
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) a.out[size_t(q_row + h) * D + lane + 32 * jj] = o[jj] * inv;
+        stv<J>(a.out + size_t(q_row + h) * D + J * lane, o, inv);
         if (lane == 0 && a.lse) a.lse[q_row + h] = (M + log2f(l)) * kLn2;
       }
     };
@@ -1812,8 +1886,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       for (int h = 0; h < H; ++h) {
         if (h >= nr) continue;
         const float inv = a.out_scale / acc.l[h];  // V = codes x v_scale (FP8 KV; 1 otherwise)
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) a.out[size_t(q_row + h) * D + lane + 32 * jj] = acc.o[h][jj] * inv;
+        stv<J>(a.out + size_t(q_row + h) * D + J * lane, acc.o[h], inv);
         if (lane == 0 && a.lse) a.lse[q_row + h] = (acc.m[h] + log2f(acc.l[h])) * kLn2;
       }
     };
@@ -1823,13 +1896,14 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       mbar_wait(&fold_full[b], (seg / kFB) & 1);
       const SegInfo si = seginfo[b];
       if (si.unit < 0) break;
+      if (dynamic && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // dynamic: the last segment taken
       // ---- fold the consumer warps' partials of this segment ------------------------------
       const float* fb = fold + b * FOLD_FLOATS;
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         float mx = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < NWG * FW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 2) + D]);
+        for (int w = 0; w < NWG * FW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 4) + D]);
         float l = 0.f, o[J];
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
@@ -1840,11 +1914,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #pragma unroll
         for (int cw = 0; cw < NWG * FW; ++cw) {
           const int w = ((si.s0 + cw / FW) % NWG) * FW + cw % FW;
-          const float* r = fb + (w * H + h) * (D + 2);
+          const float* r = fb + (w * H + h) * (D + 4);
           const float wt = ex2_sub(r[D], mx);  // idle warp / masked row: m = -inf -> 0
           l = fmaf(wt, r[D + 1], l);
+          float rv[J];
+          ldv<J>(r + J * lane, rv);
 #pragma unroll
-          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(wt, r[lane + 32 * jj], o[jj]);
+          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(wt, rv[jj], o[jj]);
         }
         acc.m[h] = mx;
         acc.l[h] = l;
@@ -1912,7 +1988,9 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
             a.unit_count[si.unit] = 0;  // ready for the next launch
             last = 1;
           }
-          if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
+#ifdef LA_EPI_TRACE  // debug builds: when the last segment's publish + count-in completed
+          if (tr) tr[TR_WAIT0] = globaltimer();
+#endif
         }
         if (__shfl_sync(0xffffffffu, last, 0)) {
           fp0 = fhv;
@@ -1926,8 +2004,11 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       }
       if (fstg) {
         if (dynamic) reset();
-        fold_smem(fp0, fp1, 1, fhv, fstg, fn);
+        fold_smem(fp0, fp1, fhv, fstg, fn);
         out = true;
+#ifdef LA_EPI_TRACE  // debug builds: when the last fold completed
+        if (dynamic && tr && lane == 0) tr[TR_WAIT1] = globaltimer();
+#endif
       }
       if (!dynamic && fstg && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
       if (out) write_out(u.q_row, si.unit);
@@ -1985,7 +2066,9 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     if (v < 0) break;
     int it = e.it;
     const int seg_end = e.it_end;
+#ifndef LA_EPI_TRACE
     if (dynamic && tr && threadIdx.x == 0) tr[TR_WAIT1] += seg_end - it;  // dynamic: LeanTiles per CTA
+#endif
     typename E::State st;
     E::seg_begin(st, a, u, lane, Smem<E>::QB ? static_cast<const void*>(qbuf + qi * Smem<E>::QB)
                                             : static_cast<const void*>(static_cast<const unsigned char*>(a.q) +

@@ -103,12 +103,12 @@ struct DecodeArgs {
   float* out;
   float* lse;
   // Schedule tables (device; rewritten by la_plan_update, so nothing that depends on ctx_lens
-  // is passed by value -- a CUDA graph captured on the plan replays across updates):
-  const int32_t* hdr;  // [0] = num_v: (virtual) CTA ranges of the current schedule
+  // is passed by value -- a CUDA graph captured on the plan replays across updates; padded
+  // to the plan's capacity so the kernel needs no range count):
   const DevUnit* units;
-  const int32_t* cta_begin;
-  const int32_t* cta_first_unit;
-  const int32_t* claim;  // dynamic: claim c runs virtual CTA claim[c]
+  const int32_t* cta_begin;       // [cap + 1]: ranges past the schedule's are empty [I, I)
+  const int32_t* cta_first_unit;  // [cap]
+  const int32_t* claim;           // [cap + grid] dynamic: claim c runs virtual CTA claim[c] (-1: no more)
   float* part_o;      // [2][slot_stride][group][d]  Op of Alg2§20 (slot 1: host partials that wait
                       //                              or are folded by the dynamic tree)
   float* part_ml;     // [2][slot_stride][group][4]  mp, lp, -, - of Alg2§21-22 (m in log2 units)

@@ -24,12 +24,13 @@ LA_OK, LA_ERR_INVALID, LA_ERR_UNSUPPORTED, LA_ERR_CUDA, LA_ERR_NOMEM, LA_ERR_STA
 LA_XCHG_HANDLE_BYTES = 64
 LA_BF16, LA_FP16, LA_FP32, LA_FP8_E4M3 = 0, 1, 2, 3
 LA_KV_BHSD, LA_KV_PACKED, LA_KV_PAGED = 0, 1, 2
-LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC, LA_SCHED_FIXED_SPLIT = 0, 1, 2, 3
+LA_SCHED_STREAMK, LA_SCHED_SEQUENTIAL, LA_SCHED_DYNAMIC, LA_SCHED_FIXED_SPLIT, LA_SCHED_AUTO = 0, 1, 2, 3, 4
 
 _DTYPE_CODES = {"bf16": LA_BF16, "fp16": LA_FP16, "fp32": LA_FP32, "fp8": LA_FP8_E4M3}  # fp8: E4M3 K/V, bf16 q
 _LAYOUT_CODES = {"bhsd": LA_KV_BHSD, "packed": LA_KV_PACKED, "paged": LA_KV_PAGED}
 _SCHED_CODES = {"streamk": LA_SCHED_STREAMK, "sequential": LA_SCHED_SEQUENTIAL, "dynamic": LA_SCHED_DYNAMIC,
-                "fixed_split": LA_SCHED_FIXED_SPLIT}
+                "fixed_split": LA_SCHED_FIXED_SPLIT, "auto": LA_SCHED_AUTO}
+SCHEDULE_NAMES = {v: k for k, v in _SCHED_CODES.items()}
 
 # Every symbol include/la.h declares (tests check the library exports all of them).
 EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_info_get", "la_plan_export",
@@ -149,7 +150,7 @@ class Plan:
     def __init__(self, batch: int, heads_q: int, heads_kv: int, head_dim: int, ctx_lens: Sequence[int],
                  tile_n: int = 0, dtype: str = "bf16", scale: float = 0.0, layout: str = "bhsd",
                  max_ctx: int = 0, grid: int = 0, host_only: bool = False, num_sms: int = 148,
-                 ctas_per_sm: int = 1, schedule: str = "streamk", trace: bool = False,
+                 ctas_per_sm: int = 1, schedule: str = "auto", trace: bool = False,
                  dyn_first_permille: int = 940, dyn_min_chunk: int = 2, split: int = 0,
                  block_table=None, page_size: int = 0, num_pages: int = 0, q_len: int = 1,
                  causal: bool = True, xchg_world: int = 0, xchg_rank: int = 0, q_lens=None,

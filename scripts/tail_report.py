@@ -71,5 +71,15 @@ if a.schedule in ("streamk", "sequential"):
     print(f"  host wait us: max {w.max():.2f}  mean(>0) {w[w > 0].mean() if (w > 0).any() else 0:.2f}")
 else:
     print(f"  claims per CTA min/max {tr[:, 3].min()}/{tr[:, 3].max()}, LeanTiles per CTA min/max {tr[:, 4].min()}/{tr[:, 4].max()}")
+    if os.environ.get("LA_EPI_TRACE"):  # a -DLA_EPI_TRACE build: fields 3, 4 are times (count-in done, fold done)
+        ci = np.where(tr[:, 3] > 0, (tr[:, 3] - tr[:, 2]) / 1e3, np.nan)
+        fo = np.where(tr[:, 4] > 0, (tr[:, 4] - tr[:, 3]) / 1e3, np.nan)
+        print(f"  last segment -> count-in done: med {np.nanmedian(ci):.2f} p90 {np.nanpercentile(ci, 90):.2f} max {np.nanmax(ci):.2f} us;"
+              f" fold: n {np.sum(~np.isnan(fo))} med {np.nanmedian(fo):.2f} max {np.nanmax(fo):.2f} us")
+    lastseg = (tr[:, 2] - t0) / 1e3
+    epi = en - lastseg
+    print(f"  last segment taken by the epilogue: med {np.median(lastseg):.1f} max {lastseg.max():.1f}; "
+          f"epilogue tail after it: med {np.median(epi):.2f} p90 {np.percentile(epi, 90):.2f} max {epi.max():.2f} us")
 for g in np.argsort(en)[-5:]:
-    print(f"  late CTA {g} smid {tr[g, 0]}: start {st[g]:.2f} end {en[g]:.1f}")
+    extra = f" last seg {(tr[g, 2] - t0) / 1e3:.1f} claims {tr[g, 3]} tiles {tr[g, 4]}" if a.schedule in ("dynamic", "fixed_split") else ""
+    print(f"  late CTA {g} smid {tr[g, 0]}: start {st[g]:.2f} end {en[g]:.1f}{extra}")
