@@ -241,12 +241,28 @@ def _has_cuda():
 
 
 # --------------------------------------------------------------------------------------
+def _timed_loop(step, steps, stream, sync):
+    """K steps between two events (no other work in between); per-launch kernel events from
+    the step's own (ev0, ev1) pair.  Returns (total_ms / K, sorted per-launch ms)."""
+    import torch
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sync()
+    t0.record(stream)
+    for i in range(steps):
+        step(ev0[i], ev1[i])
+    t1.record(stream)
+    sync()
+    return t0.elapsed_time(t1) / steps, sorted(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+
+
 def bench_ours(args):
     import torch
     import torch.distributed as dist
     import synth
     import paper_2405_10480_b200 as la
-    from paper_2405_10480_b200.leanattn import SCHEDULE_NAMES
+    from paper_2405_10480_b200.leanattn import SCHEDULE_NAMES, la_combine_packed
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,15 +280,6 @@ def bench_ours(args):
             dist.init_process_group(args.backend)
     from paper_2405_10480_b200 import sharded
 
-    def gather(o_part, l_part, o_all, l_all):
-        """The one exchange step of the sequence-sharded path (NCCL all-gather)."""
-        if args.backend == "nccl":
-            dist.all_gather_into_tensor(o_all, o_part)
-            dist.all_gather_into_tensor(l_all, l_part)
-        else:
-            oa, lb = sharded.gather_partials(o_part, l_part)
-            o_all.copy_(oa)
-            l_all.copy_(lb)
     cfg = args.config or ("c2" if world == 1 else "c5")
     dkw = {"dtype": args.dtype} if args.dtype else {}
     if args.q_len > 1:
@@ -297,9 +304,9 @@ def bench_ours(args):
     q = synth.gen_q(p, dev)
     k = synth.fill_kv_cache(p, "k", dev, token_range=None if args.page_size else bounds)
     v = synth.fill_kv_cache(p, "v", dev, token_range=None if args.page_size else bounds)
-    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, dtype=p.dtype, layout=p.layout,
-                   schedule=args.schedule, dyn_first_permille=args.dyn_first, dyn_min_chunk=args.dyn_min,
-                   tile_n=args.tile_n, engine=args.engine, q_len=args.q_len, **paged_kw,
+    plan_kw = dict(dtype=p.dtype, layout=p.layout, schedule=args.schedule, dyn_first_permille=args.dyn_first,
+                   dyn_min_chunk=args.dyn_min, tile_n=args.tile_n, engine=args.engine, q_len=args.q_len, **paged_kw)
+    plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, lens, **plan_kw,
                    **(dict(xchg_world=world, xchg_rank=rank) if fused else {}))
     xchg_note = None
     if fused:   # collective decision: every rank maps every peer's buffer, or all use NCCL
@@ -312,79 +319,102 @@ def bench_ours(args):
     total_kv = p.kv_bytes                       # whole job
     local_kv = info.kv_bytes
     stream = torch.cuda.current_stream(dev)
-    rows = p.batch * p.heads_q
+    rows, d = p.batch * p.heads_q, p.head_dim
     nq = (args.q_len,) if args.q_len > 1 else ()
-    out = torch.empty(p.batch, p.heads_q, *nq, p.head_dim, dtype=torch.float32, device=dev)
+    out = torch.empty(p.batch, p.heads_q, *nq, d, dtype=torch.float32, device=dev)
     lse = torch.empty(p.batch, p.heads_q, *nq, dtype=torch.float32, device=dev)
-    if world > 1:
-        o_all = torch.empty(world, rows, p.head_dim, dtype=torch.float32, device=dev)
-        l_all = torch.empty(world, rows, dtype=torch.float32, device=dev)
-        fin_o = torch.empty(rows, p.head_dim, dtype=torch.float32, device=dev)
+    if world > 1:   # the NCCL path: O_r and L_r written into ONE packed buffer, ONE all-gather
+        packed = torch.empty(rows * (d + 1), dtype=torch.float32, device=dev)
+        po, pl = packed[:rows * d].view(rows, d), packed[rows * d:]
+        allp = torch.empty(world, rows * (d + 1), dtype=torch.float32, device=dev)
+        fin_o = torch.empty(rows, d, dtype=torch.float32, device=dev)
         fin_l = torch.empty(rows, dtype=torch.float32, device=dev)
+
+        def gather_packed():
+            if args.backend == "nccl":
+                dist.all_gather_into_tensor(allp, packed)
+            else:
+                allp.copy_(sharded.gather_packed(packed))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if total_kv < 2 * L2_BYTES else None
 
-    def step(ev0=None, ev1=None):
+    def step_single(ev0=None, ev1=None):
         if flush is not None:
             flush.zero_()
         if ev0 is not None:
             ev0.record(stream)
-        if world == 1 or fused:   # fused: the exchange and the fold run inside this launch
-            plan.decode(q, k, v, out, lse, stream=stream)
-        else:
-            plan.decode_partial(q, k, v, out, lse, stream=stream)
+        plan.decode(q, k, v, out, lse, stream=stream)   # fused: the exchange + fold run inside
         if ev1 is not None:
             ev1.record(stream)
-        if world > 1 and not fused:   # sharded.sequence_sharded_decode with preallocated buffers
-            gather(out.view(rows, p.head_dim), lse.view(rows), o_all, l_all)
-            la.la_combine(o_all, l_all, fin_o, fin_l, stream=stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    if fused:   # the fused exchange must agree with partial + all-gather + la_combine
-        bad = 0.0
-        try:
-            plan.xchg_status()
-        except la.LaError:
-            bad = 1.0
-        plan.decode_partial(q, k, v, out, lse, stream=stream)
-        gather(out.view(rows, p.head_dim), lse.view(rows), o_all, l_all)
-        ref_o, ref_l = la.la_combine(o_all, l_all, stream=stream)
-        plan.decode(q, k, v, out, lse, stream=stream)
-        try:
-            plan.xchg_status()
-        except la.LaError:
-            bad = 1.0
-        chk = torch.tensor([bad, (out.view(rows, -1) - ref_o).abs().max().item(),
-                            (lse.view(rows) - ref_l).abs().max().item()], dtype=torch.float64, device=dev)
-        dist.all_reduce(chk, op=dist.ReduceOp.MAX)   # one collective decision for all ranks
-        bad, do, dl = chk.tolist()
-        xchg_note = {"max_abs_diff_vs_nccl_combine": [do, dl]}
-        if bad or max(do, dl) > 1e-5:
-            fused = False
-            xchg_note["p2p_rejected"] = "exchange wait timed out" if bad else "disagrees with the NCCL combine"
+    def step_nccl(ev0=None, ev1=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        plan.decode_partial(q, k, v, po, pl, stream=stream)
+        if ev1 is not None:
+            ev1.record(stream)
+        gather_packed()
+        la_combine_packed(allp, world, rows, d, fin_o, fin_l, stream=stream)
+
+    def sync():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(*vals):
+        if world == 1:
+            return list(vals)
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    paths = {}
     if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+        for _ in range(args.warmup):
+            step_nccl()
+        if fused:   # the fused exchange must agree with partial + all-gather + la_combine
+            for _ in range(args.warmup):
+                step_single()
+            sync()
+            bad = 0.0
+            try:
+                plan.xchg_status()
+            except la.LaError:
+                bad = 1.0
+            step_nccl()
+            step_single()
+            try:
+                plan.xchg_status()
+            except la.LaError:
+                bad = 1.0
+            chk = torch.tensor([bad, (out.view(rows, -1) - fin_o).abs().max().item(),
+                                (lse.view(rows) - fin_l).abs().max().item()], dtype=torch.float64, device=dev)
+            dist.all_reduce(chk, op=dist.ReduceOp.MAX)   # one collective decision for all ranks
+            bad, do, dl = chk.tolist()
+            xchg_note = {"max_abs_diff_vs_nccl_combine": [do, dl]}
+            if bad or max(do, dl) > 1e-5:
+                fused = False
+                xchg_note["p2p_rejected"] = "exchange wait timed out" if bad else "disagrees with the NCCL combine"
+        # time BOTH exchange paths (the north star's NCCL combine and the fused NVLink fixup)
+        ms, kern = _timed_loop(step_nccl, args.steps, stream, sync)
+        ms, kmean = max_over_ranks(ms, sum(kern) / len(kern))
+        paths["nccl_allgather_combine"] = {"step_us": ms * 1e3, "kernel_us": kmean * 1e3}
+        if fused:
+            ms_f, kern_f = _timed_loop(step_single, args.steps, stream, sync)
+            ms_f, kmean_f = max_over_ranks(ms_f, sum(kern_f) / len(kern_f))
+            paths["fused_p2p"] = {"step_us": ms_f * 1e3, "kernel_us": kmean_f * 1e3}
+    else:
+        for _ in range(args.warmup):
+            step_single()
+    # ---- the timed region of the reported line ------------------------------------------
+    main_step = step_single if (world == 1 or fused) else step_nccl
+    sync()
     launches0 = la.launch_count()
     with ClockSampler(local) as clk:
-        t_start.record(stream)
-        for i in range(args.steps):
-            step(ev0[i], ev1[i])
-        t_end.record(stream)
-        torch.cuda.synchronize(dev)
+        step_ms, kern_each = _timed_loop(main_step, args.steps, stream, sync)
     launches = la.launch_count() - launches0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    total_ms = t_start.elapsed_time(t_end)
-    kern_each = sorted(a.elapsed_time(b) for a, b in zip(ev0, ev1))
     kern_ms = sum(kern_each) / args.steps
-    pct = {f"p{q}": kern_each[min(len(kern_each) - 1, int(q / 100 * len(kern_each)))] * 1e3 for q in (10, 50, 90)}
+    pct = {f"p{q_}": kern_each[min(len(kern_each) - 1, int(q_ / 100 * len(kern_each)))] * 1e3 for q_ in (10, 50, 90)}
     unflushed_us = None
     if flush is not None and world == 1:   # L2-resident config: also the warm-L2 kernel time
         u0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -395,13 +425,39 @@ def bench_ours(args):
             u1[i].record(stream)
         torch.cuda.synchronize(dev)
         unflushed_us = sorted(a.elapsed_time(b) for a, b in zip(u0, u1))[args.steps // 2] * 1e3
-    step_ms = total_ms / args.steps
-    if flush is not None:   # the flush is not part of the step: report the kernel time
-        step_ms = kern_ms if world == 1 else step_ms
+    if flush is not None and world == 1:   # the flush is not part of the step: report the kernel time
+        step_ms = kern_ms
+    step_ms, kern_ms = max_over_ranks(step_ms, kern_ms)
+
+    # ---- N > 1: the same workload unsharded on rank 0's GPU (T_1) -------------------------
+    scaling = None
     if world > 1:
-        t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms, kern_ms = t.tolist()
+        t1_ms = 0.0
+        if rank == 0:
+            k1 = synth.fill_kv_cache(p, "k", dev)
+            v1 = synth.fill_kv_cache(p, "v", dev)
+            plan1 = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, p.ctx_lens, **plan_kw)
+            o1 = torch.empty_like(out)
+            l1 = torch.empty_like(lse)
+
+            def step1(ev0=None, ev1=None):
+                if ev0 is not None:
+                    ev0.record(stream)
+                plan1.decode(q, k1, v1, o1, l1, stream=stream)
+                if ev1 is not None:
+                    ev1.record(stream)
+            for _ in range(args.warmup):
+                step1()
+            torch.cuda.synchronize(dev)
+            t1_ms, _ = _timed_loop(step1, max(3, min(args.steps, 20)), stream, lambda: torch.cuda.synchronize(dev))
+            del k1, v1
+        (t1_ms,) = max_over_ranks(t1_ms)   # only rank 0 measured: the max is its value
+        peak, _ = peaks()
+        per_gpu = local_kv / (kern_ms * 1e-3) / 1e9
+        scaling = {"t1_us": t1_ms * 1e3, "tp_us": step_ms * 1e3, "scaling_efficiency": t1_ms / (world * step_ms),
+                   "per_gpu_gbs": per_gpu, "per_gpu_frac": per_gpu / peak,
+                   "per_gpu_kv_bytes": local_kv, "exchange_paths": paths,
+                   "note": "T_1 = the unsharded workload on rank 0's GPU in this run; efficiency = T_1 / (P T_P)"}
 
     # ---- end to end through the C ABI with host buffers ---------------------------------
     e2e = None
@@ -409,35 +465,27 @@ def bench_ours(args):
         qh = q.cpu().pin_memory()
         kh = k.cpu().pin_memory()
         vh = v.cpu().pin_memory()
-        oh = torch.empty(p.batch, p.heads_q, p.head_dim, dtype=torch.float32).pin_memory()
-        lh = torch.empty(p.batch, p.heads_q, dtype=torch.float32).pin_memory()
-        plan.decode_host(qh, kh, vh, oh, lh, stream=stream)   # warm-up (allocates staging)
-        if world > 1:
-            oh_all = torch.empty(world, rows, p.head_dim, dtype=torch.float32, device=dev)
-            lh_all = torch.empty(world, rows, dtype=torch.float32, device=dev)
-            dist.barrier()
-        torch.cuda.synchronize(dev)
+        oh = torch.empty(rows * (d + 1), dtype=torch.float32).pin_memory()   # O rows then L (packed)
+        ohv, lhv = oh[:rows * d].view(p.batch, p.heads_q, d), oh[rows * d:].view(p.batch, p.heads_q)
+        plan.decode_host(qh, kh, vh, ohv, lhv, stream=stream)   # warm-up (allocates staging)
+        fin_h = torch.empty(rows, d, dtype=torch.float32).pin_memory()
+        sync()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            plan.decode_host(qh, kh, vh, oh, lh, stream=stream)
-            if world > 1 and not fused:
-                o_dev = oh.to(dev, non_blocking=True).view(rows, p.head_dim)
-                l_dev = lh.to(dev, non_blocking=True).view(rows)
-                gather(o_dev, l_dev, oh_all, lh_all)
-                fo, fl = la.la_combine(oh_all, lh_all, stream=stream)
-                fo.cpu()
+            plan.decode_host(qh, kh, vh, ohv, lhv, stream=stream)
+            if world > 1 and not fused:   # the shard result goes through the exchange and the combine
+                packed.copy_(oh, non_blocking=True)
+                gather_packed()
+                la_combine_packed(allp, world, rows, d, fin_o, fin_l, stream=stream)
+                fin_h.copy_(fin_o, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = t.item()
+        (e2e_ms,) = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps)
         e2e = {"value": total_kv / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(qh.numel() * qh.element_size() + 2 * kh.numel() * kh.element_size()),
-               "d2h_bytes_per_step": int(oh.numel() * 4 + lh.numel() * 4)}
+               "d2h_bytes_per_step": int(rows * (d + 1) * 4)}
 
     # ---- oracle cpu_baseline (rank 0, N = 1 only) -----------------------------------------
     cpu = None
@@ -445,8 +493,9 @@ def bench_ours(args):
         units = oracle_sample(p, min(args.cpu_heads, p.batch * p.heads_kv), device=dev)
         secs = run_oracle_sample(units, p.scale)
         cpu = {"value": sample_bytes(units, synth.DTYPE_BYTES[p.dtype]) / secs / 1e9, "unit": "GB/s",
-               "cores": blas_threads(), "kind": "oracle", "seconds": secs,
-               "sample": f"{len(units)} of {p.batch * p.heads_kv} (b, h_kv) units of {cfg} (full context each)"}
+               "cores": blas_threads(), "host_cores": os.cpu_count(), "kind": "oracle", "seconds": secs,
+               "sample": f"{len(units)} of {p.batch * p.heads_kv} (b, h_kv) units of {cfg} (full context each); "
+                         f"cores = the numpy/BLAS threads the oracle used, host_cores = the box's logical CPUs"}
         try:   # the same oracle on ONE core, on a smaller bounded sample
             from threadpoolctl import threadpool_limits
             one = units[:max(1, len(units) // 8)]
@@ -487,7 +536,8 @@ def bench_ours(args):
                        "l2": ("inputs > L2 (no flush)" if flush is None else "L2 flushed (512 MB memset) before every step"),
                        "parallelism": "single GPU" if world == 1 else
                        (f"sequence-sharded x{world}, fused in-kernel NVLink exchange (NEXT-2)" if fused else
-                        f"sequence-sharded x{world} + {args.backend.upper()} all-gather + la_combine"),
+                        f"sequence-sharded x{world} + {args.backend.upper()} all-gather (one packed O||L message) "
+                        f"+ la_combine_strided"),
                        **({"exchange_check": xchg_note} if xchg_note else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -496,6 +546,7 @@ def bench_ours(args):
                          "algorithmic_bytes_per_launch": local_kv,
                          "read_probe_gbs": read_probe_gbs(),
                          "frac_of_read_probe": (achieved / read_probe_gbs()) if read_probe_gbs() else None},
+            **({"multi_gpu": scaling} if scaling else {}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

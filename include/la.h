@@ -305,6 +305,17 @@ la_status la_combine(const float* o_parts, const float* lse_parts, int parts, in
                      int head_dim, float* out, float* lse, void* stream);
 
 /*
+ * la_combine_strided -- la_combine with part p's O at o_parts + p * o_part_stride and its L
+ * at lse_parts + p * lse_part_stride (floats): a rank's (O_r, L_r) packed in ONE buffer
+ * [rows * head_dim + rows] is exchanged by ONE all-gather and combined in place
+ * (o_part_stride = lse_part_stride = rows * (head_dim + 1), lse_parts = o_parts + rows * head_dim).
+ * Strides must be >= one part (LA_ERR_INVALID).
+ */
+la_status la_combine_strided(const float* o_parts, int64_t o_part_stride, const float* lse_parts,
+                             int64_t lse_part_stride, int parts, int rows, int head_dim, float* out, float* lse,
+                             void* stream);
+
+/*
  * la_decode_host -- la_decode through HOST buffers (end-to-end path): copies q, k, v
  * (plan's layout; sizes from the plan) host->device into plan-owned staging buffers
  * (allocated on first use, kept until la_plan_destroy), decodes, copies out (and lse if

@@ -758,15 +758,25 @@ la_status la_decode_partial(la_plan_t plan, const void* q, const void* k_shard, 
   return decode_impl(plan, q, k_shard, v_shard, o_part, lse_part, stream, /*xchg=*/false);
 }
 
-la_status la_combine(const float* o_parts, const float* lse_parts, int parts, int rows, int head_dim,
-                     float* out, float* lse, void* stream) {
+la_status la_combine_strided(const float* o_parts, int64_t o_part_stride, const float* lse_parts,
+                             int64_t lse_part_stride, int parts, int rows, int head_dim, float* out, float* lse,
+                             void* stream) {
   if (!o_parts || !lse_parts || !out) return fail(LA_ERR_INVALID, "NULL tensor pointer");
   if (parts < 1 || rows < 1) return fail(LA_ERR_INVALID, "parts and rows must be >= 1");
   if (head_dim != 64 && head_dim != 128) return fail(LA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (o_part_stride < int64_t(rows) * head_dim || lse_part_stride < rows)
+    return fail(LA_ERR_INVALID, "part strides smaller than one part");
   std::string err;
-  if (la::launch_combine(o_parts, lse_parts, parts, rows, head_dim, out, lse, stream, err) != 0)
+  if (la::launch_combine(o_parts, size_t(o_part_stride), lse_parts, size_t(lse_part_stride), parts, rows, head_dim,
+                         out, lse, stream, err) != 0)
     return fail(LA_ERR_CUDA, err);
   return LA_OK;
+}
+
+la_status la_combine(const float* o_parts, const float* lse_parts, int parts, int rows, int head_dim,
+                     float* out, float* lse, void* stream) {
+  return la_combine_strided(o_parts, int64_t(rows) * head_dim, lse_parts, rows, parts, rows, head_dim, out, lse,
+                            stream);
 }
 
 la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache,

@@ -24,17 +24,18 @@ namespace {
 // Sequence-shard combine: L = ln sum_r e^{L_r}, O = sum_r e^{L_r - L} O_r  (ascending r)
 // ---------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(D) la_combine_kernel(const float* __restrict__ o_parts,
-                                                       const float* __restrict__ lse_parts, int parts, int rows,
+__global__ void __launch_bounds__(D) la_combine_kernel(const float* __restrict__ o_parts, size_t o_stride,
+                                                       const float* __restrict__ lse_parts, size_t l_stride, int parts,
                                                        float* __restrict__ out, float* __restrict__ lse) {
+  // part p's row r: o_parts[p * o_stride + r * D + c], lse_parts[p * l_stride + r]
   const int r = blockIdx.x, c = threadIdx.x;
   float mx = -INFINITY;
-  for (int p = 0; p < parts; ++p) mx = fmaxf(mx, lse_parts[size_t(p) * rows + r]);
+  for (int p = 0; p < parts; ++p) mx = fmaxf(mx, lse_parts[p * l_stride + r]);
   float s = 0.f, acc = 0.f;
   for (int p = 0; p < parts; ++p) {
-    const float w = expf(lse_parts[size_t(p) * rows + r] - mx);
+    const float w = expf(lse_parts[p * l_stride + r] - mx);
     s += w;
-    acc = fmaf(w, o_parts[(size_t(p) * rows + r) * D + c], acc);
+    acc = fmaf(w, o_parts[p * o_stride + size_t(r) * D + c], acc);
   }
   out[size_t(r) * D + c] = acc / s;
   if (c == 0 && lse) lse[r] = mx + logf(s);
@@ -137,13 +138,13 @@ int launch_decode(const KernelInfo& ki, const DecodeArgs& a_in, int64_t kv_rows,
   return 0;
 }
 
-int launch_combine(const float* o_parts, const float* lse_parts, int parts, int rows, int head_dim, float* out,
-                   float* lse, void* stream, std::string& err) {
+int launch_combine(const float* o_parts, size_t o_stride, const float* lse_parts, size_t l_stride, int parts, int rows,
+                   int head_dim, float* out, float* lse, void* stream, std::string& err) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (head_dim == 128)
-    la_combine_kernel<128><<<rows, 128, 0, st>>>(o_parts, lse_parts, parts, rows, out, lse);
+    la_combine_kernel<128><<<rows, 128, 0, st>>>(o_parts, o_stride, lse_parts, l_stride, parts, out, lse);
   else
-    la_combine_kernel<64><<<rows, 64, 0, st>>>(o_parts, lse_parts, parts, rows, out, lse);
+    la_combine_kernel<64><<<rows, 64, 0, st>>>(o_parts, o_stride, lse_parts, l_stride, parts, out, lse);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("combine launch: ") + cudaGetErrorString(e);

@@ -189,8 +189,8 @@ struct TmapCache {
 // Launch the decode kernel (cooperative when a static-schedule CTA may wait on a peer).
 int launch_decode(const KernelInfo& ki, const DecodeArgs& a, int64_t kv_rows, int head_dim, int dtype,
                   bool cooperative, void* stream, TmapCache* cache, std::string& err);
-int launch_combine(const float* o_parts, const float* lse_parts, int parts, int rows,
-                   int head_dim, float* out, float* lse, void* stream, std::string& err);
+int launch_combine(const float* o_parts, size_t o_stride, const float* lse_parts, size_t l_stride, int parts,
+                   int rows, int head_dim, float* out, float* lse, void* stream, std::string& err);
 void note_launch();
 int64_t launch_count();
 

@@ -35,7 +35,7 @@ SCHEDULE_NAMES = {v: k for k, v in _SCHED_CODES.items()}
 # Every symbol include/la.h declares (tests check the library exports all of them).
 EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_info_get", "la_plan_export",
            "la_plan_export_claims", "la_decode",
-           "la_decode_partial", "la_combine", "la_decode_host", "la_plan_status", "la_plan_destroy",
+           "la_decode_partial", "la_combine", "la_combine_strided", "la_decode_host", "la_plan_status", "la_plan_destroy",
            "la_launch_count", "la_status_string", "la_last_error", "la_version", "la_plan_trace",
            "la_plan_xchg_handle", "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status")
 
@@ -98,6 +98,8 @@ def lib() -> ctypes.CDLL:
     L.la_decode.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.la_decode_partial.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.la_combine.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
+    if hasattr(L, "la_combine_strided"):
+        L.la_combine_strided.argtypes = [vp, i64, vp, i64, i32, i32, i32, vp, vp, vp]
     L.la_decode_host.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
     L.la_plan_trace.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
                                 ctypes.POINTER(ctypes.c_size_t)]
@@ -113,7 +115,7 @@ def lib() -> ctypes.CDLL:
     L.la_last_error.restype = ctypes.c_char_p
     for name in ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_status", "la_plan_info_get", "la_plan_export",
                  "la_plan_export_claims", "la_decode",
-                 "la_decode_partial", "la_combine", "la_decode_host", "la_plan_trace", "la_plan_xchg_handle",
+                 "la_decode_partial", "la_combine", "la_combine_strided", "la_decode_host", "la_plan_trace", "la_plan_xchg_handle",
                  "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status"):
         if hasattr(L, name):
             getattr(L, name).restype = ctypes.c_int
@@ -385,4 +387,22 @@ def la_combine(o_parts, lse_parts, out=None, lse=None, stream=None):
         raise ValueError("o_parts / lse_parts must be contiguous")
     _check(lib().la_combine(_ptr(o_parts), _ptr(lse_parts), int(P), int(rows), int(d), _ptr(out), _ptr(lse),
                             _stream(stream)), "la_combine")
+    return out, lse
+
+
+def la_combine_packed(packed, parts: int, rows: int, head_dim: int, out=None, lse=None, stream=None):
+    """``la_combine_strided`` over ``packed`` = (parts, rows * (head_dim + 1)) fp32: part p holds
+    its O (rows, head_dim) then its L (rows) -- the layout one all-gather of a rank's packed
+    (O_r, L_r) produces."""
+    import torch
+    if not packed.is_contiguous() or packed.numel() != parts * rows * (head_dim + 1):
+        raise ValueError("packed must be contiguous (parts, rows * (head_dim + 1)) fp32")
+    if out is None:
+        out = torch.empty(rows, head_dim, dtype=torch.float32, device=packed.device)
+    if lse is None:
+        lse = torch.empty(rows, dtype=torch.float32, device=packed.device)
+    stride = rows * (head_dim + 1)
+    _check(lib().la_combine_strided(_ptr(packed), stride, packed.data_ptr() + rows * head_dim * 4, stride, int(parts),
+                                    int(rows), int(head_dim), _ptr(out), _ptr(lse), _stream(stream)),
+           "la_combine_strided")
     return out, lse

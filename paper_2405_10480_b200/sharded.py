@@ -2,9 +2,9 @@
 
 Each rank (one process per GPU, ``torch.distributed`` over NCCL/NVLink) holds a contiguous
 1/P slice of every head's context, runs the SAME single-GPU kernel on it
-(``la_decode_partial`` -> normalised O_r and logsumexp L_r), one all-gather exchanges the
-per-head (O_r, L_r) pairs (B*H_q*(d+1)*4 bytes per rank: 16.5 KB at c5), and ``la_combine``
-folds them with the softmax re-scaling operator (§4.1; exact for any split by
+(``la_decode_partial`` -> normalised O_r and logsumexp L_r, written into ONE packed buffer),
+one all-gather exchanges the per-head (O_r, L_r) pairs (B*H_q*(d+1)*4 bytes per rank: 16.5 KB
+at c5), and ``la_combine_strided`` folds them with the softmax re-scaling operator (§4.1; exact for any split by
 associativity).  Head- or batch-sharded layouts (the paper's tensor parallelism,
 P:511) need no collective at all: every rank simply plans and decodes its own units.
 
@@ -26,39 +26,55 @@ def shard_bounds(ctx_lens: Sequence[int], rank: int, world: int) -> List[Tuple[i
     return [((rank * n) // world, ((rank + 1) * n) // world) for n in ctx_lens]
 
 
-def gather_partials(o_part, lse_part, group=None):
-    """All-gather the per-rank (O_r, L_r): returns ([P, rows, d], [P, rows]) in rank order.
-
-    NCCL: one ``all_gather_into_tensor`` per tensor into preallocated buffers.  Other
-    backends (gloo, used by the CPU tests) go through ``all_gather`` lists.
-    """
+def gather_packed(packed, group=None):
+    """All-gather every rank's packed (O_r, L_r) buffer (rows * (d + 1) fp32: O then L) in
+    ONE collective: returns (P, rows * (d + 1)) in rank order.  NCCL: all_gather_into_tensor
+    into a preallocated buffer; other backends (gloo, the CPU tests) via all_gather lists."""
     import torch
     import torch.distributed as dist
     P = dist.get_world_size(group)
-    d = o_part.shape[-1]
-    o = o_part.reshape(-1, d).contiguous()
-    l = lse_part.reshape(-1).contiguous()
+    packed = packed.reshape(-1).contiguous()
     if dist.get_backend(group) == "nccl":
-        o_all = torch.empty((P,) + o.shape, dtype=o.dtype, device=o.device)
-        l_all = torch.empty((P,) + l.shape, dtype=l.dtype, device=l.device)
-        dist.all_gather_into_tensor(o_all, o, group=group)
-        dist.all_gather_into_tensor(l_all, l, group=group)
-        return o_all, l_all
-    os_ = [torch.empty_like(o) for _ in range(P)]
-    ls_ = [torch.empty_like(l) for _ in range(P)]
-    dist.all_gather(os_, o, group=group)
-    dist.all_gather(ls_, l, group=group)
-    return torch.stack(os_), torch.stack(ls_)
+        out = torch.empty((P, packed.numel()), dtype=packed.dtype, device=packed.device)
+        dist.all_gather_into_tensor(out, packed, group=group)
+        return out
+    parts = [torch.empty_like(packed) for _ in range(P)]
+    dist.all_gather(parts, packed, group=group)
+    return torch.stack(parts)
+
+
+def pack_partials(o_part, lse_part):
+    """(O_r, L_r) -> one contiguous rows * (d + 1) buffer (O rows, then the L column)."""
+    import torch
+    d = o_part.shape[-1]
+    return torch.cat([o_part.reshape(-1, d).reshape(-1), lse_part.reshape(-1)])
+
+
+def gather_partials(o_part, lse_part, group=None):
+    """All-gather the per-rank (O_r, L_r) with ONE collective on their packed form: returns
+    ([P, rows, d], [P, rows]) in rank order."""
+    d = o_part.shape[-1]
+    rows = lse_part.numel()
+    allp = gather_packed(pack_partials(o_part, lse_part), group)
+    return allp[:, :rows * d].reshape(-1, rows, d), allp[:, rows * d:]
 
 
 def sequence_sharded_decode(plan, q, k_shard, v_shard, group=None, stream=None):
     """One decode step of the sequence-sharded path on this rank; returns the full (O, L)
-    (replicated on every rank).  ``plan`` must be built for this rank's shard lengths."""
-    from .leanattn import la_combine
-    o, l = plan.decode_partial(q, k_shard, v_shard, stream=stream)
-    o_all, l_all = gather_partials(o, l, group)
-    out, lse = la_combine(o_all, l_all, stream=stream)
-    return out.view_as(o), lse.view_as(l)
+    (replicated on every rank).  ``plan`` must be built for this rank's shard lengths.  The
+    kernel writes O_r and L_r straight into ONE packed buffer, one all-gather exchanges it
+    (B*H_q*(d+1)*4 bytes per rank), la_combine_strided folds the P parts in place."""
+    import torch
+    import torch.distributed as dist
+    from .leanattn import la_combine_packed
+    rows, d = int(plan.info.q_rows), plan.info.head_dim
+    packed = torch.empty(rows * (d + 1), dtype=torch.float32, device=q.device)
+    o = packed[:rows * d].view(rows, d)
+    l = packed[rows * d:]
+    plan.decode_partial(q, k_shard, v_shard, o, l, stream=stream)
+    allp = gather_packed(packed, group)
+    out, lse = la_combine_packed(allp, dist.get_world_size(group), rows, d, stream=stream)
+    return out, lse
 
 
 def exchange_handles(handle: bytes, group=None) -> List[bytes]:
