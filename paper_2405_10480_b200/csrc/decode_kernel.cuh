@@ -1902,25 +1902,33 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         float mx = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < NWG * FW; ++w) mx = fmaxf(mx, fb[(w * H + h) * (D + 4) + D]);
         float l = 0.f, o[J];
 #pragma unroll
         for (int jj = 0; jj < J; ++jj) o[jj] = 0.f;
-        // Summed in the order of the warp sets RELATIVE to the segment's first stage: warp
-        // (set (s0 + c) % NWG, sub) holds the segment's stages c, c + NWG, ... whatever s0
-        // is, so the rounding depends only on the segment, never on where the ring stood
-        // when it began (dynamic claims need no ring alignment; reading C16).
+        // every load of the row first (with global fold buffers -- wide tiles -- a dependent
+        // max -> weights -> rows chain cost two L2 round trips per row)
+        float mw[NWG * FW], lw[NWG * FW], ow[NWG * FW][J];
 #pragma unroll
         for (int cw = 0; cw < NWG * FW; ++cw) {
+          // Summed in the order of the warp sets RELATIVE to the segment's first stage: warp
+          // (set (s0 + c) % NWG, sub) holds the segment's stages c, c + NWG, ... whatever s0
+          // is, so the rounding depends only on the segment, never on where the ring stood
+          // when it began (dynamic claims need no ring alignment; reading C16).
           const int w = ((si.s0 + cw / FW) % NWG) * FW + cw % FW;
           const float* r = fb + (w * H + h) * (D + 4);
-          const float wt = ex2_sub(r[D], mx);  // idle warp / masked row: m = -inf -> 0
-          l = fmaf(wt, r[D + 1], l);
-          float rv[J];
-          ldv<J>(r + J * lane, rv);
+          const float2 ml = *reinterpret_cast<const float2*>(r + D);
+          mw[cw] = ml.x;
+          lw[cw] = ml.y;
+          ldv<J>(r + J * lane, ow[cw]);
+        }
 #pragma unroll
-          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(wt, rv[jj], o[jj]);
+        for (int cw = 0; cw < NWG * FW; ++cw) mx = fmaxf(mx, mw[cw]);
+#pragma unroll
+        for (int cw = 0; cw < NWG * FW; ++cw) {
+          const float wt = ex2_sub(mw[cw], mx);  // idle warp / masked row: m = -inf -> 0
+          l = fmaf(wt, lw[cw], l);
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) o[jj] = fmaf(wt, ow[cw][jj], o[jj]);
         }
         acc.m[h] = mx;
         acc.l[h] = l;

@@ -1,18 +1,36 @@
-# Full evaluation pass on one B200: build, smoke, GPU tests, bench (+e2e, +cpu baseline),
-# reference arm, other configs / engines, ncu launch list + full captures.
-set -x
-mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; tail -n 5 gpurun_out/smoke.log
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -n 3 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 2500 gpurun_out/bench_default.json
-timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_reference.json 2>&1; tail -c 600 gpurun_out/bench_reference.json
-for c in c3 c4; do timeout 300 python bench.py --config $c --no-cpu --no-e2e > gpurun_out/bench_$c.json 2>&1; done
-timeout 300 python bench.py --config c3 --engine tcgen05 --no-cpu --no-e2e > gpurun_out/bench_c3_tc5.json 2>&1
-for ql in 2 4; do for e in auto mma; do timeout 300 python bench.py --config c3 --q-len $ql --engine $e --no-cpu --no-e2e > gpurun_out/bench_c3_q${ql}_$e.json 2>&1; done; done
-for c in c2 c3; do timeout 300 python bench.py --config $c --dtype fp8 --no-cpu --no-e2e > gpurun_out/bench_${c}_fp8.json 2>&1; done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:la_decode -s 3 -c 1 -o gpurun_out/prof_c2 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/prof_c2.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:la_decode -s 3 -c 1 -o gpurun_out/prof_c3 python bench.py --config c3 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/prof_c3.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:la_decode -s 3 -c 1 -o gpurun_out/prof_c3_tc5 python bench.py --config c3 --engine tcgen05 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/prof_c3_tc5.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:la_decode -s 3 -c 1 -o gpurun_out/prof_c3_q2_tc5 python bench.py --config c3 --q-len 2 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/prof_c3_q2_tc5.log 2>&1
-ls -la gpurun_out
+#!/bin/bash
+# Full evaluation pass on one B200 (run under gpurun): smoke, the GPU test suite, the default
+# bench line (+ e2e + cpu baseline), the reference arm, every config / engine / schedule
+# variant, and ncu evidence (launch list + one full capture) for the main configs.
+# Everything lands in gpurun_out/$R/ (R = round tag, default r02).
+R=${R:-r02}
+O=gpurun_out/$R
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -n 3 $O/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; tail -n 2 $O/pytest_gpu.log
+timeout 900 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err; tail -c 400 $O/bench_c2.json
+timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > $O/bench_reference.json 2>&1
+run() {  # name, bench args
+  timeout 600 python bench.py $2 --no-cpu --no-e2e > $O/bench_$1.json 2> $O/bench_$1.err
+  python -c "import json,sys; d=json.loads(open('$O/bench_$1.json').read().strip().splitlines()[-1]); r=d['roofline']; print('%-14s %8.1f us/step  kernel p50 %7.1f  %6.0f GB/s  frac %.3f  %s' % ('$1', d['ms_per_step']*1e3, r['kernel_us_pct']['p50'], r['achieved'], r['frac'], d['config'].get('schedule')))" 2>/dev/null || echo "$1 failed"
+}
+run c1 "--config c1"
+run c2_streamk "--config c2 --schedule streamk"
+run c3 "--config c3"
+run c3_tc5 "--config c3 --engine tcgen05"
+run c3_q2 "--config c3 --q-len 2"
+run c3_q4 "--config c3 --q-len 4"
+run c4 "--config c4"
+run c4_streamk "--config c4 --schedule streamk"
+
+run c5 "--config c5"
+run c2_fp8 "--config c2 --dtype fp8"
+run c3_fp8 "--config c3 --dtype fp8"
+run c2_paged16 "--config c2 --page-size 16"
+run c3_paged16 "--config c3 --page-size 16"
+for cfg in "c2|--config c2|c2" "c3|--config c3|c3" "c4|--config c4|c4" "c1|--config c1|c1" "c3_q4|--config c3 --q-len 4|c3-q4-tc5"; do
+  IFS='|' read -r name args key <<< "$cfg"
+  bash scripts/profile.sh ${R}_$name "$args" $key > $O/profile_$name.log 2>&1
+  mv gpurun_out/${R}_${name}* $O/ 2>/dev/null
+done
+ls -la $O | tail -40
