@@ -94,10 +94,11 @@ typedef enum {
                               extra LeanTile), chunks run in order on the persistent
                               CTAs like hardware waves, folded in-kernel (the comparison
                               baseline of the paper's evaluation, NEXT-1)                 */
-  LA_SCHED_AUTO = 4        /* (default) LA_SCHED_DYNAMIC for one-row tiles (MHA, T_m = 1) whose
-                              Eq. 2 ranges hold >= 64 LeanTiles, LA_SCHED_STREAMK otherwise and
-                              for exchange plans -- the faster of the two as measured on B200
-                              (DESIGN §6); la_plan_info.schedule reports the choice          */
+  LA_SCHED_AUTO = 4        /* (default) LA_SCHED_DYNAMIC for one-row tiles (MHA, T_m = 1) of a
+                              bf16 / fp16 / fp32 BHSD or packed cache whose Eq. 2 ranges hold
+                              >= 64 LeanTiles, LA_SCHED_STREAMK otherwise (multi-row tiles, FP8,
+                              paged pools, exchange plans) -- the faster of the two as measured
+                              on B200; la_plan_info.schedule reports the choice   */
 } la_schedule;
 
 typedef struct {

@@ -476,13 +476,16 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   plan->sched.tile_n = tile_n ? tile_n : auto_tile_n(p);
   if (p.schedule == LA_SCHED_AUTO) {
     // the balanced dynamic schedule for one-row tiles whose Eq. 2 ranges are long enough for a
-    // tail to matter (measured faster on B200: c2 -1%, c4 -1%); stream-K for multi-row tiles
-    // (whose 8-32-row folds cost more per piece than the balance gains) and exchange plans
+    // tail to matter (measured faster on B200: c2 -1%, c4 -1%, c5 -1%); stream-K for multi-row
+    // tiles (whose 8-32-row folds cost more per piece than the balance gains) and exchange plans
     std::vector<DevUnit> tmp;
     int64_t I = 0;
     la::build_units(p, plan->sched.tile_n, tmp, I);
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>(plan->opt_grid ? plan->opt_grid : plan->max_ctas, I));
-    p.schedule = (p.rows() == 1 && !xw && I / G >= 64) ? LA_SCHED_DYNAMIC : LA_SCHED_STREAMK;
+    // (measured slower with dynamic, r02: the FP8 engine -- c2 314 vs 309 us -- and paged pools,
+    // whose producer refills a page window at every piece -- c2 page 16: 650 vs 622 us)
+    p.schedule = (p.rows() == 1 && !xw && I / G >= 64 && p.dtype != LA_FP8_E4M3 && p.layout != LA_KV_PAGED)
+                     ? LA_SCHED_DYNAMIC : LA_SCHED_STREAMK;
     plan->prob.schedule = p.schedule;
   }
   {

@@ -280,7 +280,7 @@ struct MhaEngine {
   static constexpr int HEADS = 1;                           // q-heads per unit
   static constexpr int FOLD_FLOATS = NCW * (D + 4);         // per warp: O[D], m, l, pad (16-B rows)
   static constexpr int FOLD_BUFS = 2;                       // double-buffered hand-off
-  static constexpr bool ZERO_RING = true;                   // tail rows must be finite
+  static constexpr bool ZERO_RING = false;                  // tail V rows are zeroed per warp
   using QElem = T;                                          // Q storage type
   static constexpr bool QSTAGE = true;                      // Q rows staged in smem per segment
   static_assert(LPK >= 2 && LPK <= 32 && (LPK & (LPK - 1)) == 0, "lanes per key");
@@ -337,6 +337,14 @@ struct MhaEngine {
     const unsigned char* ks = st;
     const unsigned char* vs = st + STAGE_TOK * ROWB;
     for (int r = sub * 32; r < ntok; r += 32 * WPS) {
+      if (r + 32 > ntok) {
+        // keys ntok .. r + 31 of this round are past the stage (the next unit's rows, or stale
+        // smem that may not be finite): their scores are masked, and their V rows zeroed so
+        // that 0 * V stays 0 (reading C5) -- only a unit's short last stage gets here
+        uint4* vz = reinterpret_cast<uint4*>(st + STAGE_TOK * ROWB + ntok * ROWB);
+        for (int i = lane; i < (r + 32 - ntok) * (ROWB / 16); i += 32) vz[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+      }
       const int kb = r + kg * LPK;
       // S_f = Q_f K_f^T (Alg1§20): lane li accumulates key (jj ^ li) over its chunk li
       float acc[LPK];
@@ -367,6 +375,7 @@ struct MhaEngine {
       for (int jj = 0; jj < LPK; ++jj)  // O_acc += P_f V_f (Alg1§24); lane li owns chunk li
         Chunk<T>::axpy(__shfl_sync(0xffffffffu, p, jj, LPK),
                        *reinterpret_cast<const uint4*>(vs + (kb + jj) * ROWB + li * 16), s.o);
+      if (r + 32 > ntok) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> TMA WAR
     }
   }
 
