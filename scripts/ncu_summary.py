@@ -102,8 +102,9 @@ def main():
         for n, v in sorted(per.items(), key=lambda x: -sum(x[1]))[:8]:
             lines.append(f"| `{n[:80]}` | {len(v)} | {sum(v):.1f} | {100 * sum(v) / tot:.1f}% | {sum(v) / len(v):.1f} |")
         lines.append("")
-        lines.append("Inside a bench step the decode kernel is the only launch at N=1 (one la_decode per step); "
-                     "the other kernels are torch's synthetic-input generation before the timed region.")
+        lines.append("The list is filtered to the library's kernels (ncu -k la_decode|la_combine): a bench step at "
+                     "N=1 is exactly one la_decode launch, so the decode kernel is 100% of the step's GPU time "
+                     "(torch's synthetic-input generation runs before the timed region).")
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     data[cfg] = summary
