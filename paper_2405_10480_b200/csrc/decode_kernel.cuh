@@ -1412,6 +1412,230 @@ struct EpiAcc {
   float o[H][J], m[H], l[H];
 };
 
+// =======================================================================================
+// Epilogue of the 16 / 32-row tcgen05 tiles (static schedules): the same fixup as the kernel's
+// epilogue below, but every step runs in groups of 8 rows whose accumulator lives in
+// registers.  A 32-row accumulator does not fit the register file; spilled to local memory it
+// thrashes the L1 (nearly all carved out as shared memory), and the last segment's fold +
+// write at a CTA's end took ~25 us (r02 trace).
+// =======================================================================================
+template <class E>
+__device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPair&, unsigned char* ring, float* fold,
+                                              uint64_t* fold_full, uint64_t* fold_empty, uint64_t* stage_bar,
+                                              const SegInfo* seginfo, uint32_t epoch, uint32_t xepoch,
+                                              unsigned long long* tr, int lane) {
+  constexpr int NWG = E::NWG, D = E::D, H = E::HEADS, J = D / 32, RG = 8, RS = D + 4;
+  constexpr int FW = EngX<E>::FW, kFB = E::FOLD_BUFS, FOLD_FLOATS = E::FOLD_FLOATS;
+  static_assert(H % RG == 0, "row groups");
+  float o[RG][J], m[RG], l[RG];
+  uint32_t stage_ph = 0;
+  int nr = 0;
+  #pragma unroll 1
+  for (int seg = 0;; ++seg) {
+    const int b = seg % kFB;
+    mbar_wait(&fold_full[b], (seg / kFB) & 1);
+    const SegInfo si = seginfo[b];
+    if (si.unit < 0) break;
+    const float* fb = fold + b * FOLD_FLOATS;
+    const DevUnit u = a.units[si.unit];
+    const int v = si.v;
+    nr = u.rows;
+    const bool out = si.host && si.finishing;  // one CTA computed the whole unit (Alg2§38-39)
+    const bool host_wait = si.host && !si.finishing;
+    if (host_wait) {  // Wait(flags[cta]) for cta = g+1 .. last_cta (Alg2§26-28, reading C9)
+      if (tr && lane == 0) tr[TR_WAIT0] = globaltimer();
+      #pragma unroll 1
+      for (int p = v + 1 + lane; p <= u.last_cta; p += 32) {
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_gpu(&a.flags[p]) != epoch) {
+          __nanosleep(20);
+          if (globaltimer() - t0 > kWaitTimeoutNs || *reinterpret_cast<volatile int*>(&a.counters[CTR_ERROR])) {
+            atomicExch(&a.counters[CTR_ERROR], 1);
+            break;
+          }
+        }
+      }
+      __syncwarp();
+      if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired partials -> TMA
+    }
+    #pragma unroll 1
+    for (int r0 = 0; r0 < nr; r0 += RG) {
+      // ---- rows r0 .. r0 + 7 of the NWG x FW warp partials (branch-free: loads issue together)
+#pragma unroll
+      for (int hh = 0; hh < RG; ++hh) {
+        const int h = r0 + hh;
+        float mw[NWG * FW], lw[NWG * FW], ow[NWG * FW][J], mx = -INFINITY, ls = 0.f;
+#pragma unroll
+        for (int cw = 0; cw < NWG * FW; ++cw) {  // warp sets relative to the segment's first stage (C16)
+          const int w = ((si.s0 + cw / FW) % NWG) * FW + cw % FW;
+          const float* r = fb + (w * H + h) * (D + 4);
+          const float2 ml = *reinterpret_cast<const float2*>(r + D);
+          mw[cw] = ml.x;
+          lw[cw] = ml.y;
+          ldv<J>(r + J * lane, ow[cw]);
+        }
+#pragma unroll
+        for (int cw = 0; cw < NWG * FW; ++cw) mx = fmaxf(mx, mw[cw]);
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) o[hh][jj] = 0.f;
+#pragma unroll
+        for (int cw = 0; cw < NWG * FW; ++cw) {
+          const float wt = ex2_sub(mw[cw], mx);
+          ls = fmaf(wt, lw[cw], ls);
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) o[hh][jj] = fmaf(wt, ow[cw][jj], o[hh][jj]);
+        }
+        m[hh] = mx;
+        l[hh] = ls;
+      }
+      __syncwarp();
+      if (r0 + RG >= nr && lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill it
+      if (!out && !host_wait) {  // StorePartials (Alg2§20-22)
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh) {
+          if (r0 + hh >= nr) continue;
+          const size_t row = size_t(v) * a.group + r0 + hh;
+          stv<J>(a.part_o + row * D + J * lane, o[hh]);
+          if (lane == 0) *reinterpret_cast<float2*>(a.part_ml + row * 4) = make_float2(m[hh], l[hh]);
+        }
+        continue;
+      }
+      if (host_wait) {
+        // ---- fold the peers v+1 .. last_cta (ascending, max-first, reading C22), their rows
+        //      r0 .. r0 + 7 staged in the idle ring (this is the CTA's last segment)
+        const int p0 = v + 1, n = u.last_cta - v;
+        float* stg = reinterpret_cast<float*>(ring);
+        #pragma unroll 1
+        for (int b0 = 0; b0 < n; b0 += 32) {  // (a 16 / 32-row unit spans few CTAs: one block)
+          const int bn = min(32, n - b0);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(bn) * RG * D * 4);
+          __syncwarp();
+          if (lane < bn)
+            bulk_g2s_plain(stg + lane * RG * D, a.part_o + (size_t(p0 + b0 + lane) * a.group + r0) * D, RG * D * 4,
+                           stage_bar);
+          float2 ml[RG];
+          const size_t mlrow = size_t(p0 + b0 + min(lane, bn - 1)) * a.group + r0;
+#pragma unroll
+          for (int hh = 0; hh < RG; ++hh) ml[hh] = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (mlrow + hh) * 4));
+          float w[RG];
+#pragma unroll
+          for (int hh = 0; hh < RG; ++hh) {
+            float M = fmaxf(m[hh], lane < bn ? ml[hh].x : -INFINITY);
+#pragma unroll
+            for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            w[hh] = lane < bn ? ex2_sub(ml[hh].x, M) : 0.f;
+            float lsum = w[hh] * (lane < bn ? ml[hh].y : 0.f);
+#pragma unroll
+            for (int off = 16; off; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+            const float wa = ex2_sub(m[hh], M);
+            l[hh] = fmaf(wa, l[hh], lsum);
+            m[hh] = M;
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) o[hh][jj] *= wa;
+          }
+          mbar_wait(stage_bar, stage_ph);
+          stage_ph ^= 1u;
+          #pragma unroll 1
+          for (int i = 0; i < bn; ++i) {  // ascending peers
+#pragma unroll
+            for (int hh = 0; hh < RG; ++hh) {
+              const float wk = __shfl_sync(0xffffffffu, w[hh], i);
+              float rv[J];
+              ldv<J>(stg + (i * RG + hh) * D + J * lane, rv);
+#pragma unroll
+              for (int jj = 0; jj < J; ++jj) o[hh][jj] = fmaf(wk, rv[jj], o[hh][jj]);
+            }
+          }
+          __syncwarp();
+        }
+      }
+      // ---- O = diag(l)^-1 O, L = m + log(l) (Alg2§38-39) -- or this rank's normalised shard
+      //      partial pushed into every rank's exchange buffer (NEXT-2)
+#pragma unroll
+      for (int hh = 0; hh < RG; ++hh) {
+        const int h = r0 + hh;
+        if (h >= nr) continue;
+        const float inv = a.out_scale / l[hh];
+        if (a.xw > 1) {
+          const int P = a.xw, par = int(xepoch & 1u);
+          const float l2 = m[hh] + log2f(l[hh]);
+          #pragma unroll 1
+          for (int d = 0; d < P; ++d) {
+            float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + u.q_row + h) * RS;
+            stv<J>(dst + J * lane, o[hh], inv);
+            if (lane == 0) dst[D] = l2;
+          }
+        } else {
+          stv<J>(a.out + size_t(u.q_row + h) * D + J * lane, o[hh], inv);
+          if (lane == 0 && a.lse) a.lse[u.q_row + h] = (m[hh] + log2f(l[hh])) * kLn2;
+        }
+      }
+    }
+    if (!out && !host_wait) {  // Signal (Alg2§23)
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        st_release_gpu(&a.flags[v], epoch);
+        if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
+      }
+    } else if (a.xw > 1) {  // NEXT-2: release, wait for the P ranks, fold their partials
+      const int P = a.xw, par = int(xepoch & 1u);
+      __threadfence_system();
+      __syncwarp();
+      if (lane < P) {
+        uint32_t* f = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(a.xpeer[lane]) + a.xflag_off);
+        st_release_sys(f + size_t(a.xr) * a.xunits + si.unit, xepoch);
+        const uint32_t* mine = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(a.xpeer[a.xr]) +
+                                                                 a.xflag_off) + size_t(lane) * a.xunits + si.unit;
+        const unsigned long long t0 = globaltimer();
+        while (int32_t(ld_acquire_sys(mine) - xepoch) < 0) {
+          if (*reinterpret_cast<volatile int*>(a.xerr) || globaltimer() - t0 > kXchgTimeoutNs) {
+            atomicExch(a.xerr, 1);
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      __syncwarp();
+      const float* xb = a.xpeer[a.xr] + size_t(par) * P * a.xrows * RS;
+      #pragma unroll 1
+      for (int h = 0; h < nr; ++h) {
+        float M = -INFINITY, lsum = 0.f, acc[J];
+        #pragma unroll 1
+        for (int r = 0; r < P; ++r) M = fmaxf(M, ld_cg(xb + (size_t(r) * a.xrows + u.q_row + h) * RS + D));
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) acc[jj] = 0.f;
+        #pragma unroll 1
+        for (int r = 0; r < P; ++r) {
+          const float* src = xb + (size_t(r) * a.xrows + u.q_row + h) * RS;
+          const float w = ex2_sub(ld_cg(src + D), M);
+          lsum += w;
+          float rv[J];
+          ldv_cg<J>(src + J * lane, rv);
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) acc[jj] = fmaf(w, rv[jj], acc[jj]);
+        }
+        stv<J>(a.out + size_t(u.q_row + h) * D + J * lane, acc, 1.f / lsum);
+        if (lane == 0 && a.lse) a.lse[u.q_row + h] = (M + log2f(lsum)) * kLn2;
+      }
+    }
+    if (host_wait && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
+  }
+  if (lane == 0) {
+    if (tr) tr[TR_END] = globaltimer();
+    __threadfence();  // every flag wait of this CTA is over: the last one out advances the epoch
+    if (atomicAdd(&a.counters[CTR_EXITED], 1) == int(gridDim.x) - 1) {
+      a.counters[CTR_EXITED] = 0;
+      *reinterpret_cast<volatile uint32_t*>(&a.counters[CTR_EPOCH]) = epoch;
+      if (a.xw > 1) *reinterpret_cast<volatile uint32_t*>(&a.counters[CTR_XEPOCH]) = xepoch;
+      __threadfence();
+    }
+  }
+}
+
 template <class E>
 __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeArgs a, const __grid_constant__ TmapPair tm) {
   constexpr int NST = E::NST, NWG = E::NWG, WPS = E::WPS, NCW = E::NCW, D = E::D, H = E::HEADS, J = D / 32;
@@ -1644,7 +1868,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     return;
   }
 
-  if (warp == NCW) {
+  if constexpr (H > 8) {
+    if (warp == NCW) {
+      wide_epilogue<E>(a, tm, ring, fold, fold_full, fold_empty, stage_bar, seginfo, epoch, xepoch, tr, lane);
+      return;
+    }
+  }
+  if constexpr (H <= 8) if (warp == NCW) {
     // ================================ epilogue ==========================================
     // Folds the NCW per-warp partials of each finished segment (§4.1 operator) and runs the
     // fixup -- partial stores, flags / counters, peer folds, finalize -- off the consumers'
