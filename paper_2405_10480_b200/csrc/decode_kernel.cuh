@@ -101,6 +101,12 @@
 #ifndef LA_TC5_NWG16
 #define LA_TC5_NWG16 LA_TC5_NST  // the same for 16-row tiles
 #endif
+#ifndef LA_TC5_NWG8
+#define LA_TC5_NWG8 LA_TC5_NST   // the same for 8-row tiles
+#endif
+#ifndef LA_TC5_FB8
+#define LA_TC5_FB8 1             // 8-row tiles: consumer -> epilogue fold buffers (2 fit with NWG8 = 2)
+#endif
 #ifndef LA_TC5_BOXH
 #define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
 #endif
@@ -991,7 +997,7 @@ struct Tc5Engine {
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
   static constexpr int FOLD_FLOATS = NWG * HEADS * (D + 4);
-  static constexpr int FOLD_BUFS = 1;
+  static constexpr int FOLD_BUFS = HEADS > 8 ? 1 : LA_TC5_FB8;
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
   using QElem = T;

@@ -4,7 +4,7 @@
 namespace la {
 
 KernelInfo info_tc5_bf16(int group) {
-  return group <= 8    ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 8>>(true)
+  return group <= 8    ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 8, LA_TC5_NWG8>>(true)
          : group <= 16 ? info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST, 16, LA_TC5_NWG16>>(true)
                        : info_of<Tc5Engine<__nv_bfloat16, LA_TC5_NST32, 32, LA_TC5_NWG32>>(true);
 }
