@@ -36,6 +36,19 @@ def test_c1_fp32_d64(dist, schedule):
     assert plan.info.grid > 1 and plan.info.num_partials > 0     # the fixup path is exercised
 
 
+@pytest.mark.parametrize("schedule", SCHEDULES + ("fixed_split",))
+def test_fp32_d128_ragged(schedule):
+    """MhaEngine<float, 128>: fp32 cache at head_dim 128 (c1 covers d = 64 only), ragged tails,
+    several CTAs per unit and a grid that does not divide the work."""
+    p = synth.Problem(3, 4, 4, 128, [4096, 1000, 77], dtype="fp32", dist="D2", seed=17, max_ctx=4096)
+    O_ref, L_ref = run_oracle(p)
+    inputs = cuda_inputs(p)
+    for tile_n, grid in ((32, 7), (128, 0), (64, 148)):
+        O, L, plan = run_cuda(p, inputs=inputs, tile_n=tile_n, grid=grid, schedule=schedule)
+        gate(O, L, O_ref, L_ref, what=f"fp32/d128/T{tile_n}/G{grid}/{schedule}")
+        assert plan.info.num_partials > 0
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("dist", ["D1", "D2", "D4"])
