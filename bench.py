@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
                     help="N > 1: the fused in-kernel NVLink exchange (p2p, NEXT-2) or NCCL all-gather + "
                          "la_combine; auto = p2p on the nccl backend")
+    ap.add_argument("--sm-weights", default="off", choices=["off", "calibrate"],
+                    help="stream-K plans: SM-rate-weighted ranges from la_plan_calibrate (before the warm-up)")
     ap.add_argument("--dyn-first", type=int, default=940, help="dynamic schedule: head share of each range (permille)")
     ap.add_argument("--dyn-min", type=int, default=2, help="dynamic schedule: smallest virtual CTA (LeanTiles)")
     return ap.parse_args()
@@ -371,6 +373,16 @@ def bench_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist()
 
+    # SM-rate-weighted stream-K (la_plan_calibrate): a plan-setup step, outside the
+    # timed region; single GPU, inputs larger than L2 (a flushed config would calibrate warm)
+    weights_note = "equal (Eq. 2)" if SCHEDULE_NAMES[plan.info.schedule] == "streamk" else None
+    if args.sm_weights == "calibrate" and SCHEDULE_NAMES[plan.info.schedule] == "streamk" and world == 1 \
+            and flush is None:
+        plan.calibrate(q, k, v, launches=6, rounds=2, stream=stream)
+        rl = plan.range_lengths()
+        weights_note = (f"calibrated (la_plan_calibrate: 2 rounds x 6 launches; LeanTiles per CTA "
+                        f"{int(rl.min())}..{int(rl.max())})")
+    info = plan.info
     paths = {}
     if world > 1:
         for _ in range(args.warmup):
@@ -539,6 +551,7 @@ def bench_ours(args):
                        "stage_tokens": info.stage_tokens,
                        "schedule": SCHEDULE_NAMES[info.schedule] + (" (auto)" if args.schedule == "auto" else ""),
                        "quantization_efficiency": info.quantization_efficiency,
+                       **({"sm_weights": weights_note} if weights_note else {}),
                        **({"engine": {0: "mma.sync", 1: "tcgen05"}[info.engine]} if info.engine >= 0 else {}),
                        **({"q_len": args.q_len, "query_tile_rows": info.tile_rows, "units": info.num_units}
                           if args.q_len > 1 else {}),

@@ -199,6 +199,7 @@ typedef struct {
                               j on CTA j mod W, the launch-order wave model)                 */
   int slot_capacity;       /* (virtual) CTA ranges the plan's device state can hold           */
   int64_t updates;         /* la_plan_update calls so far                                     */
+  int sm_weighted;         /* 1: stream-K ranges follow la_plan_set_weights / la_plan_calibrate */
 } la_plan_info;
 
 /* Fill *opts with defaults.  Always LA_OK for a non-null pointer. */
@@ -249,6 +250,38 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
  * On error the plan is unchanged.
  */
 la_status la_plan_update(la_plan_t plan, const int32_t* ctx_lens, const int32_t* block_table, void* stream);
+
+/*
+ * la_plan_set_weights -- SM-rate-weighted stream-K (B200 extension of Eq. 2).
+ * Eq. 2 gives every CTA I/G LeanTiles, which balances TIME only if every SM streams at the
+ * same rate; on B200 the per-SM share of HBM bandwidth under full load is not uniform (a
+ * stable property of the SM: DESIGN §6), so the slowest SMs set the kernel's end.  With
+ * weights w_0 .. w_{G-1} (one per CTA of the plan's LA_SCHED_STREAMK grid; blockIdx g) the
+ * ranges become contiguous with boundaries
+ *     cta_begin[g] = floor(I * (w_0 + .. + w_{g-1}) / (w_0 + .. + w_{G-1}))
+ * (integer arithmetic; equal weights give sizes differing by at most one) -- still Alg. 2's
+ * contiguous ranges, hosts and fixup, so the result is exact for any weights and
+ * bitwise reproducible for fixed weights.  The weights persist across la_plan_update.
+ * weights: HOST [n] int32 in [1, 2^20], n == la_plan_info.grid; NULL restores equal ranges.
+ * The new tables are uploaded on `stream` (as la_plan_update).
+ * Errors: LA_ERR_INVALID (n, range), LA_ERR_STATE (the plan's schedule is not
+ * LA_SCHED_STREAMK), LA_ERR_CUDA.
+ */
+la_status la_plan_set_weights(la_plan_t plan, const int32_t* weights, int n, void* stream);
+
+/*
+ * la_plan_calibrate -- measure each CTA's streaming rate and set the weights from it
+ * (la_plan_set_weights).  Per round, `launches` + 1 samples of 3 back-to-back la_decode
+ * calls on the given (device) tensors on `stream`, the last of each traced (a temporary
+ * device buffer if the plan has none; the first sample is a warm-up): time_g =
+ * t_stream_end - t_start of CTA g summed over the samples, then w_g <- w_g * (mean time /
+ * time_g) (rate-proportional shares), so the CTAs finish streaming together.  out / lse receive the last launch's (correct) result.
+ * Synchronises the device.  LA_SCHED_STREAMK plans only (LA_ERR_STATE otherwise);
+ * launches, rounds >= 1.  Weights are a property of the GPU's SMs: calibrate once per plan
+ * (la_plan_update keeps them).
+ */
+la_status la_plan_calibrate(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache, float* out,
+                            float* lse, int launches, int rounds, void* stream);
 
 /* Scalar facts about a plan (host, synchronous). */
 la_status la_plan_info_get(la_plan_t plan, la_plan_info* info);
@@ -336,9 +369,12 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
  * t_wait_end (host fold wait, Alg2§28; 0 if none), t_end -- %globaltimer nanoseconds.
  * LA_SCHED_DYNAMIC / FIXED_SPLIT: t_publish = when the epilogue took the CTA's last segment,
  * t_wait_begin / t_wait_end = claims taken / LeanTiles streamed (counts, not times).
+ * Field 6, every schedule: t_stream_end = when the epilogue took the CTA's last segment
+ * (its consumers had streamed every LeanTile of its range(s); 0 if it had none) -- the
+ * per-CTA streaming time t_stream_end - t_start is what la_plan_calibrate measures.
  * *n_ctas receives G.  LA_ERR_STATE if the plan has no trace buffer.
  */
-#define LA_TRACE_FIELDS 6
+#define LA_TRACE_FIELDS 7
 la_status la_plan_trace(la_plan_t plan, uint64_t* out, size_t cap_ctas, size_t* n_ctas);
 
 /*

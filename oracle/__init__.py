@@ -32,7 +32,7 @@ from .leantile import lean_tile
 from .schedule import (Segment, iters_per_cta, cta_range, owner, stream_k_segments,
                        owner_table, segments_from_owner_table, last_cta_literal,
                        fixed_split_segments, quantization_efficiency, segments_from_ranges,
-                       balanced_ranges, fixed_split_ranges, fa2_num_splits)
+                       balanced_ranges, fixed_split_ranges, fa2_num_splits, weighted_ranges)
 from .lean_attention import lean_attention
 from .shard_combine import combine_shards
 from .fp8 import e4m3_decode, dequantize

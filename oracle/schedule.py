@@ -178,6 +178,28 @@ def balanced_ranges(total_iters: int, grid: int, head_permille: int = 940, min_c
     return begins, claim
 
 
+def weighted_ranges(total_iters: int, weights: Sequence[int]) -> List[int]:
+    """Range boundaries of the SM-rate-weighted stream-K schedule (this
+    build's extension of Eq. 2, not in the paper): Eq. 2 hands every CTA I / G
+    LeanTiles; here CTA g's share is proportional to its weight w_g (its SM's measured
+    streaming rate) on top of one LeanTile each,
+
+        R = max(I - G, 0),  begins[g] = min(g, I) + floor(R * (w_0 + ... + w_{g-1}) / W),
+
+    W = w_0 + ... + w_{G-1}, in exact integer arithmetic.  Every CTA g < I gets >= 1
+    LeanTile (an empty range inside a unit would leave its host waiting for a partial
+    nobody writes; with I < G the trailing CTAs idle, as Alg. 2's).  The ranges stay
+    contiguous, so Alg. 2 §10-18 runs over them unchanged (``segments_from_ranges``)."""
+    assert len(weights) >= 1 and all(1 <= int(w) <= (1 << 20) for w in weights)
+    G, W = len(weights), sum(int(w) for w in weights)
+    R = max(total_iters - G, 0)
+    begins, acc = [], 0
+    for g, w in enumerate(list(weights) + [0]):
+        begins.append(min(g, total_iters) + R * acc // W)
+        acc += int(w)
+    return begins
+
+
 def fixed_split_ranges(c_n: Sequence[int], split: int) -> List[int]:
     """Range boundaries of FlashDecoding's fixed split: unit u cut into
     s = min(split, C_n(u)) chunks, the first C_n mod s of them one LeanTile longer."""

@@ -30,6 +30,7 @@ struct la_plan_s {
   int max_ctas = 0;          // co-resident CTAs (device) / num_sms x ctas_per_sm (host-only)
   int slot_cap = 0;          // (virtual) CTA capacity of the range table, partial slots, flags
   int64_t updates = 0;       // la_plan_update calls
+  std::vector<int32_t> weights;  // la_plan_set_weights: per-CTA stream-K weights (empty: Eq. 2's equal ranges)
   // ---- device state, ONE allocation ---------------------------------------------------
   // upload region (rewritten by la_plan_update with one async copy):
   //   [hdr 256 B][units U x 48 B][cta_begin cap + 1][cta_first cap][claim cap][block table B x pt_stride]
@@ -179,7 +180,12 @@ la_status plan_schedule(la_plan_s* plan, bool first, int64_t icap_hint) {
   } else {
     // stream-K (Eq. 2): G = forced grid, else min(launch, I) equal ranges (reading C15)
     const int G = plan->opt_grid ? launch : int(std::max<int64_t>(1, std::min<int64_t>(launch, I)));
-    la::streamk_ranges(I, G, s.cta_begin);
+    if (plan->weights.empty()) {
+      la::streamk_ranges(I, G, s.cta_begin);
+    } else {  // SM-rate-weighted ranges (la_plan_set_weights): CTA g keeps weight g
+      const std::vector<int32_t> w(plan->weights.begin(), plan->weights.begin() + G);
+      la::weighted_ranges(I, w, s.cta_begin);
+    }
   }
   if (p.schedule != LA_SCHED_DYNAMIC) {  // ranges are claimed in order
     s.claim.resize(s.cta_begin.size() - 1);
@@ -627,6 +633,100 @@ la_status la_plan_update(la_plan_t plan, const int32_t* ctx_lens, const int32_t*
   return LA_OK;
 }
 
+la_status la_plan_set_weights(la_plan_t plan, const int32_t* weights, int n, void* stream) {
+  if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
+  if (plan->prob.schedule != LA_SCHED_STREAMK) return fail(LA_ERR_STATE, "weights apply to LA_SCHED_STREAMK plans");
+  if (weights) {
+    if (n != plan->sched.phys_grid) return fail(LA_ERR_INVALID, "n must equal la_plan_info.grid");
+    for (int g = 0; g < n; ++g)
+      if (weights[g] < 1 || weights[g] > (1 << 20)) return fail(LA_ERR_INVALID, "weights must be in [1, 2^20]");
+  }
+  std::vector<int32_t> old_w = plan->weights;
+  const la::Schedule old_s = plan->sched;
+  if (weights)
+    plan->weights.assign(weights, weights + n);
+  else
+    plan->weights.clear();
+  la_status st = plan_schedule(plan, false, 0);
+  if (st == LA_OK && !plan->host_only) st = upload_tables(plan, static_cast<cudaStream_t>(stream), false);
+  if (st != LA_OK) {
+    plan->weights = old_w;
+    plan->sched = old_s;
+  }
+  return st;
+}
+
+static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const void* v, float* out,
+                             float* lse, void* stream, bool xchg = true);
+
+la_status la_plan_calibrate(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache, float* out,
+                            float* lse, int launches, int rounds, void* stream) {
+  if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
+  if (plan->host_only) return fail(LA_ERR_STATE, "host-only plan cannot decode");
+  if (plan->prob.schedule != LA_SCHED_STREAMK) return fail(LA_ERR_STATE, "calibration applies to LA_SCHED_STREAMK plans");
+  if (launches < 1 || rounds < 1) return fail(LA_ERR_INVALID, "launches and rounds must be >= 1");
+  const int GP = plan->sched.phys_grid;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* own_trace = plan->d_trace;
+  unsigned long long* tmp = nullptr;
+  if (!own_trace) {
+    cudaError_t e = cudaMalloc(&tmp, size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(calibration trace)");
+    plan->d_trace = tmp;
+  }
+  std::vector<int32_t> w = plan->weights.empty() ? std::vector<int32_t>(size_t(GP), 1 << 16) : plan->weights;
+  std::vector<uint64_t> tr(size_t(GP) * LA_TRACE_FIELDS);
+  la_status rs = LA_OK;
+  for (int r = 0; r < rounds && rs == LA_OK; ++r) {
+    rs = la_plan_set_weights(plan, w.data(), GP, stream);
+    std::vector<double> t(size_t(GP), 0.0);
+    for (int i = 0; i <= launches && rs == LA_OK; ++i) {  // sample 0 warms the new tables up
+      // each sample: kSteady launches back to back, the trace is the last one's -- a launch
+      // that starts on an idle GPU (after a host sync) streams differently from the steady
+      // state a decode loop runs in
+      constexpr int kSteady = 3;
+      for (int j = 0; j < kSteady && rs == LA_OK; ++j) rs = decode_impl(plan, q, k_cache, v_cache, out, lse, stream);
+      if (rs != LA_OK) break;
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(tr.data(), plan->d_trace, tr.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) { rs = cuda_fail(e, "la_plan_calibrate"); break; }
+      if (i == 0) continue;
+      for (int g = 0; g < GP; ++g) {
+        const uint64_t* x = &tr[size_t(g) * LA_TRACE_FIELDS];
+        if (x[6] > x[1]) t[size_t(g)] += double(x[6] - x[1]);
+      }
+    }
+    if (rs != LA_OK) break;
+    // rate-proportional shares: w_g <- w_g * mean(t) / t_g over the CTAs that streamed
+    const la::Schedule& s = plan->sched;
+    double tsum = 0.0;
+    int cnt = 0;
+    for (int g = 0; g < s.grid; ++g)
+      if (s.cta_begin[g + 1] > s.cta_begin[g] && t[size_t(g)] > 0.0) {
+        tsum += t[size_t(g)];
+        ++cnt;
+      }
+    if (cnt == 0) break;
+    const double tm = tsum / cnt;
+    for (int g = 0; g < s.grid; ++g)
+      if (s.cta_begin[g + 1] > s.cta_begin[g] && t[size_t(g)] > 0.0) {
+        const double nw = std::round(double(w[size_t(g)]) * tm / t[size_t(g)]);
+        w[size_t(g)] = int32_t(std::min(double(1 << 20), std::max(1.0, nw)));
+      }
+  }
+  if (rs == LA_OK) rs = la_plan_set_weights(plan, w.data(), GP, stream);
+  if (rs == LA_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rs = cuda_fail(e, "la_plan_calibrate");
+  }
+  if (tmp) {
+    plan->d_trace = own_trace;
+    cudaFree(tmp);
+  }
+  return rs;
+}
+
 la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   if (!plan || !info) return fail(LA_ERR_INVALID, "NULL argument");
   const la::Problem& p = plan->prob;
@@ -652,6 +752,7 @@ la_status la_plan_info_get(la_plan_t plan, la_plan_info* info) {
   info->quantization_efficiency = quant_eff(plan);
   info->slot_capacity = plan->slot_cap;
   info->updates = plan->updates;
+  info->sm_weighted = plan->weights.empty() ? 0 : 1;
   info->num_units = int(s.units.size());
   info->total_iters = s.total_iters;
   info->num_segments = s.num_segments;
@@ -686,7 +787,7 @@ la_status la_plan_export(la_plan_t plan, int32_t* rows, size_t cap_rows, size_t*
 }
 
 static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const void* v, float* out,
-                             float* lse, void* stream, bool xchg = true) {
+                             float* lse, void* stream, bool xchg) {
   if (!plan) return fail(LA_ERR_INVALID, "plan is NULL");
   if (plan->host_only) return fail(LA_ERR_STATE, "host-only plan cannot decode");
   if (!q || !k || !v || !out) return fail(LA_ERR_INVALID, "NULL tensor pointer");
@@ -752,7 +853,7 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
 
 la_status la_decode(la_plan_t plan, const void* q, const void* k_cache, const void* v_cache, float* out,
                     float* lse, void* stream) {
-  return decode_impl(plan, q, k_cache, v_cache, out, lse, stream);
+  return decode_impl(plan, q, k_cache, v_cache, out, lse, stream, true);
 }
 
 la_status la_decode_partial(la_plan_t plan, const void* q, const void* k_shard, const void* v_shard,
@@ -815,7 +916,7 @@ la_status la_decode_host(la_plan_t plan, const void* q, const void* k_cache, con
   if (e == cudaSuccess) e = cudaMemcpyAsync(dk, k_cache, kv_bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dv, v_cache, kv_bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  la_status s = decode_impl(plan, dq, dk, dv, dout, lse ? dlse : nullptr, stream);
+  la_status s = decode_impl(plan, dq, dk, dv, dout, lse ? dlse : nullptr, stream, true);
   if (s != LA_OK) return s;
   e = cudaMemcpyAsync(out, dout, o_bytes, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess && lse) e = cudaMemcpyAsync(lse, dlse, l_bytes, cudaMemcpyDeviceToHost, st);

@@ -1428,11 +1428,12 @@ struct EpiAcc {
 template <class E>
 __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPair&, unsigned char* ring, float* fold,
                                               uint64_t* fold_full, uint64_t* fold_empty, uint64_t* stage_bar,
-                                              const SegInfo* seginfo, uint32_t epoch, uint32_t xepoch,
-                                              unsigned long long* tr, int lane) {
+                                              const SegInfo* seginfo, const int* prod_j, uint32_t epoch,
+                                              uint32_t xepoch, unsigned long long* tr, int lane) {
   constexpr int NWG = E::NWG, D = E::D, H = E::HEADS, J = D / 32, RG = 8, RS = D + 4;
   constexpr int FW = EngX<E>::FW, kFB = E::FOLD_BUFS, FOLD_FLOATS = E::FOLD_FLOATS;
   static_assert(H % RG == 0, "row groups");
+  static_assert((FOLD_FLOATS * 4) % 16 == 0, "fold buffer: whole 16-B units for one bulk copy");
   float o[RG][J], m[RG], l[RG];
   uint32_t stage_ph = 0;
   int nr = 0;
@@ -1442,12 +1443,35 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
     mbar_wait(&fold_full[b], (seg / kFB) & 1);
     const SegInfo si = seginfo[b];
     if (si.unit < 0) break;
+    if (tr && lane == 0) tr[TR_STREAM] = globaltimer();  // the consumers finished this segment
     const float* fb = fold + b * FOLD_FLOATS;
     const DevUnit u = a.units[si.unit];
     const int v = si.v;
     nr = u.rows;
     const bool out = si.host && si.finishing;  // one CTA computed the whole unit (Alg2§38-39)
     const bool host_wait = si.host && !si.finishing;
+    // The CTA's last segment (its producer has issued every stage, all consumed): the ring is
+    // idle, so the segment's warp partials (global fold buffer) and, for a waiting host, all
+    // of its peers' partial rows and (m, l) are staged there by bulk copies -- ONE L2 round
+    // trip each instead of three dependent ones per 8-row group (the 32-row host fold took
+    // ~13 us that way, on the kernel's critical path).  The arithmetic is unchanged: only
+    // where the operands are read from differs, so results stay bitwise identical.
+    const int np = host_wait ? u.last_cta - v : 0;
+    const bool idle = *reinterpret_cast<volatile const int*>(prod_j) == si.jend;
+    const bool stage_peers = idle && host_wait &&
+                             FOLD_FLOATS * 4 + size_t(np) * nr * (D + 4) * 4 <= size_t(Smem<E>::RING);
+    float* fstg = reinterpret_cast<float*>(ring);         // [FOLD_FLOATS]
+    float* pml = fstg + FOLD_FLOATS;                       // [np][nr][4]  peers' (m, l, -, -)
+    float* prow = pml + size_t(np) * nr * 4;               // [np][nr][D]  peers' O~ rows
+    if (idle) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");      // consumers' fold-buffer stores -> TMA
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring's last generic reads
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(stage_bar, uint32_t(FOLD_FLOATS) * 4);
+        bulk_g2s_plain(fstg, fb, uint32_t(FOLD_FLOATS) * 4, stage_bar);
+      }
+    }
     if (host_wait) {  // Wait(flags[cta]) for cta = g+1 .. last_cta (Alg2§26-28, reading C9)
       if (tr && lane == 0) tr[TR_WAIT0] = globaltimer();
       #pragma unroll 1
@@ -1465,8 +1489,32 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
       if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
       asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired partials -> TMA
     }
+    if (idle) {  // the fold buffer has landed (issued before the peer wait)
+      mbar_wait(stage_bar, stage_ph);
+      stage_ph ^= 1u;
+      fb = fstg;
+    }
+    if (stage_peers) {  // every peer's rows [0, nr) and (m, l): contiguous runs of its slot
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(np) * nr * (D + 4) * 4);
+      __syncwarp();
+      #pragma unroll 1
+      for (int i = lane; i < np; i += 32) {
+        const size_t row = size_t(v + 1 + i) * a.group;
+        bulk_g2s_plain(prow + size_t(i) * nr * D, a.part_o + row * D, uint32_t(nr) * D * 4, stage_bar);
+        bulk_g2s_plain(pml + size_t(i) * nr * 4, a.part_ml + row * 4, uint32_t(nr) * 16, stage_bar);
+      }
+      mbar_wait(stage_bar, stage_ph);
+      stage_ph ^= 1u;
+    }
+#ifdef LA_WIDE_PRINT
+    unsigned long long wt[8] = {globaltimer(), 0, 0, 0, 0, 0, 0, 0};
+#endif
     #pragma unroll 1
     for (int r0 = 0; r0 < nr; r0 += RG) {
+#ifdef LA_WIDE_PRINT
+      if (r0 / RG < 6) wt[1 + r0 / RG] = globaltimer();
+#endif
       // ---- rows r0 .. r0 + 7 of the NWG x FW warp partials (branch-free: loads issue together)
 #pragma unroll
       for (int hh = 0; hh < RG; ++hh) {
@@ -1497,6 +1545,9 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
       }
       __syncwarp();
       if (r0 + RG >= nr && lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill it
+#ifdef LA_WIDE_PRINT
+      if (r0 == 0) wt[5] = globaltimer();
+#endif
       if (!out && !host_wait) {  // StorePartials (Alg2§20-22)
 #pragma unroll
         for (int hh = 0; hh < RG; ++hh) {
@@ -1508,24 +1559,32 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
         continue;
       }
       if (host_wait) {
-        // ---- fold the peers v+1 .. last_cta (ascending, max-first, reading C22), their rows
-        //      r0 .. r0 + 7 staged in the idle ring (this is the CTA's last segment)
-        const int p0 = v + 1, n = u.last_cta - v;
-        float* stg = reinterpret_cast<float*>(ring);
+        // ---- fold the peers v+1 .. last_cta (ascending, max-first, reading C22): all staged
+        //      above (stage_peers), else their rows r0 .. r0 + 7 staged per group in the ring
+        //      (past the staged fold buffer when it is there)
+        const int p0 = v + 1, n = np;
+        float* stg = idle ? fstg + FOLD_FLOATS : reinterpret_cast<float*>(ring);  // <= 33 + 128 KiB
         #pragma unroll 1
         for (int b0 = 0; b0 < n; b0 += 32) {  // (a 16 / 32-row unit spans few CTAs: one block)
           const int bn = min(32, n - b0);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(bn) * RG * D * 4);
-          __syncwarp();
-          if (lane < bn)
-            bulk_g2s_plain(stg + lane * RG * D, a.part_o + (size_t(p0 + b0 + lane) * a.group + r0) * D, RG * D * 4,
-                           stage_bar);
           float2 ml[RG];
-          const size_t mlrow = size_t(p0 + b0 + min(lane, bn - 1)) * a.group + r0;
+          if (!stage_peers) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(bn) * RG * D * 4);
+            __syncwarp();
+            if (lane < bn)
+              bulk_g2s_plain(stg + lane * RG * D, a.part_o + (size_t(p0 + b0 + lane) * a.group + r0) * D, RG * D * 4,
+                             stage_bar);
+            const size_t mlrow = size_t(p0 + b0 + min(lane, bn - 1)) * a.group + r0;
 #pragma unroll
-          for (int hh = 0; hh < RG; ++hh) ml[hh] = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (mlrow + hh) * 4));
+            for (int hh = 0; hh < RG; ++hh) ml[hh] = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (mlrow + hh) * 4));
+          } else {
+            const float* mls = pml + (size_t(b0 + min(lane, bn - 1)) * nr + r0) * 4;
+#pragma unroll
+            for (int hh = 0; hh < RG; ++hh)
+              ml[hh] = r0 + hh < nr ? *reinterpret_cast<const float2*>(mls + hh * 4) : make_float2(-INFINITY, 0.f);
+          }
           float w[RG];
 #pragma unroll
           for (int hh = 0; hh < RG; ++hh) {
@@ -1542,15 +1601,18 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
 #pragma unroll
             for (int jj = 0; jj < J; ++jj) o[hh][jj] *= wa;
           }
-          mbar_wait(stage_bar, stage_ph);
-          stage_ph ^= 1u;
+          if (!stage_peers) {
+            mbar_wait(stage_bar, stage_ph);
+            stage_ph ^= 1u;
+          }
           #pragma unroll 1
           for (int i = 0; i < bn; ++i) {  // ascending peers
 #pragma unroll
             for (int hh = 0; hh < RG; ++hh) {
               const float wk = __shfl_sync(0xffffffffu, w[hh], i);
               float rv[J];
-              ldv<J>(stg + (i * RG + hh) * D + J * lane, rv);
+              ldv<J>(stage_peers ? prow + ((size_t(b0 + i) * nr + r0 + hh) * D + J * lane)
+                                 : stg + (i * RG + hh) * D + J * lane, rv);
 #pragma unroll
               for (int jj = 0; jj < J; ++jj) o[hh][jj] = fmaf(wk, rv[jj], o[hh][jj]);
             }
@@ -1558,26 +1620,42 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
           __syncwarp();
         }
       }
+#ifdef LA_WIDE_PRINT
+      if (r0 == 0) wt[6] = globaltimer();
+#endif
       // ---- O = diag(l)^-1 O, L = m + log(l) (Alg2§38-39) -- or this rank's normalised shard
-      //      partial pushed into every rank's exchange buffer (NEXT-2)
+      //      partial pushed into every rank's exchange buffer (NEXT-2).  Lane hh computes row
+      //      hh's 1 / l and log2 l (the same operations as a per-row loop, so the same bits):
+      //      one division and one logarithm of latency instead of RG serial ones.
+      float lsel = l[0], msel = m[0];
 #pragma unroll
-      for (int hh = 0; hh < RG; ++hh) {
-        const int h = r0 + hh;
-        if (h >= nr) continue;
-        const float inv = a.out_scale / l[hh];
-        if (a.xw > 1) {
-          const int P = a.xw, par = int(xepoch & 1u);
-          const float l2 = m[hh] + log2f(l[hh]);
+      for (int hh = 1; hh < RG; ++hh)
+        if (lane == hh) {
+          lsel = l[hh];
+          msel = m[hh];
+        }
+      const float inv_lane = a.out_scale / lsel, l2_lane = msel + log2f(lsel);
+      if (a.xw > 1) {
+        const int P = a.xw, par = int(xepoch & 1u);
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh) {
+          const float inv = __shfl_sync(0xffffffffu, inv_lane, hh), l2 = __shfl_sync(0xffffffffu, l2_lane, hh);
+          if (r0 + hh >= nr) continue;
           #pragma unroll 1
           for (int d = 0; d < P; ++d) {
-            float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + u.q_row + h) * RS;
+            float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + u.q_row + r0 + hh) * RS;
             stv<J>(dst + J * lane, o[hh], inv);
             if (lane == 0) dst[D] = l2;
           }
-        } else {
-          stv<J>(a.out + size_t(u.q_row + h) * D + J * lane, o[hh], inv);
-          if (lane == 0 && a.lse) a.lse[u.q_row + h] = (m[hh] + log2f(l[hh])) * kLn2;
         }
+      } else {
+        float* dst = a.out + size_t(u.q_row + r0) * D + J * lane;
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh) {
+          const float inv = __shfl_sync(0xffffffffu, inv_lane, hh);
+          if (r0 + hh < nr) stv<J>(dst + hh * D, o[hh], inv);
+        }
+        if (a.lse && lane < RG && r0 + lane < nr) a.lse[u.q_row + r0 + lane] = l2_lane * kLn2;
       }
     }
     if (!out && !host_wait) {  // Signal (Alg2§23)
@@ -1629,6 +1707,13 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
       }
     }
     if (host_wait && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
+#ifdef LA_WIDE_PRINT
+    if (lane == 0 && host_wait && blockIdx.x % 16 == 0)
+      printf("WIDE cta %d np %d nr %d idle %d sp %d: w1->loop %llu, rg %llu %llu %llu %llu, end %llu ns; rg0: cfold %llu peers %llu write %llu\n",
+             int(blockIdx.x), np, nr, int(idle), int(stage_peers), wt[0] - (tr ? tr[TR_WAIT1] : wt[0]), wt[1] - wt[0],
+             wt[2] - wt[1], wt[3] - wt[2], wt[4] - wt[3], globaltimer() - wt[0], wt[5] - wt[1], wt[6] - wt[5],
+             wt[2] - wt[6]);
+#endif
   }
   if (lane == 0) {
     if (tr) tr[TR_END] = globaltimer();
@@ -1684,7 +1769,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   if (tr && threadIdx.x == 0) {
     tr[TR_SMID] = smid();
     tr[TR_START] = globaltimer();
-    tr[TR_PUBLISH] = tr[TR_WAIT0] = tr[TR_WAIT1] = 0;
+    tr[TR_PUBLISH] = tr[TR_WAIT0] = tr[TR_WAIT1] = tr[TR_STREAM] = 0;
   }
   if (E::ZERO_RING)  // rows past a short stage must be finite (masked p = 0; 0 * finite = 0)
     for (int i = threadIdx.x; i < Smem<E>::RING / 16; i += blockDim.x)
@@ -1876,7 +1961,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 
   if constexpr (H > 8) {
     if (warp == NCW) {
-      wide_epilogue<E>(a, tm, ring, fold, fold_full, fold_empty, stage_bar, seginfo, epoch, xepoch, tr, lane);
+      wide_epilogue<E>(a, tm, ring, fold, fold_full, fold_empty, stage_bar, seginfo, prod_j, epoch, xepoch, tr, lane);
       return;
     }
   }
@@ -2127,13 +2212,24 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
         xchg_out(q_row, unit);
         return;
       }
+      // lane h computes row h's 1 / l and log2 l (the same operations as a per-row loop, so
+      // the same bits): one division and one logarithm of latency instead of H serial ones
+      float lsel = acc.l[0], msel = acc.m[0];
+#pragma unroll
+      for (int h = 1; h < H; ++h)
+        if (lane == h) {
+          lsel = acc.l[h];
+          msel = acc.m[h];
+        }
+      const float inv_lane = a.out_scale / lsel;  // V = codes x v_scale (FP8 KV; 1 otherwise)
+      const float l2_lane = msel + log2f(lsel);
+      float* dst = a.out + size_t(q_row) * D + J * lane;
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        if (h >= nr) continue;
-        const float inv = a.out_scale / acc.l[h];  // V = codes x v_scale (FP8 KV; 1 otherwise)
-        stv<J>(a.out + size_t(q_row + h) * D + J * lane, acc.o[h], inv);
-        if (lane == 0 && a.lse) a.lse[q_row + h] = (acc.m[h] + log2f(acc.l[h])) * kLn2;
+        const float inv = H == 1 ? inv_lane : __shfl_sync(0xffffffffu, inv_lane, h);
+        if (h < nr) stv<J>(dst + h * D, acc.o[h], inv);
       }
+      if (a.lse && lane < H && lane < nr) a.lse[q_row + lane] = l2_lane * kLn2;
     };
 
     for (int seg = 0;; ++seg) {
@@ -2141,7 +2237,10 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       mbar_wait(&fold_full[b], (seg / kFB) & 1);
       const SegInfo si = seginfo[b];
       if (si.unit < 0) break;
-      if (dynamic && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // dynamic: the last segment taken
+      if (tr && lane == 0) {
+        tr[TR_STREAM] = globaltimer();                 // the consumers finished this segment
+        if (dynamic) tr[TR_PUBLISH] = tr[TR_STREAM];   // dynamic: the last segment taken
+      }
       // ---- fold the consumer warps' partials of this segment ------------------------------
       const float* fb = fold + b * FOLD_FLOATS;
 #pragma unroll

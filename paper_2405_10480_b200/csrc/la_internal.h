@@ -77,6 +77,9 @@ struct Problem {
 void build_units(const Problem& p, int tile_n, std::vector<DevUnit>& units, int64_t& total_iters);
 // Eq. 2 / Alg2§7-9 with the remainder rule (reading C8); grid >= 1.
 void streamk_ranges(int64_t total_iters, int grid, std::vector<int32_t>& cta_begin);
+// SM-rate-weighted Eq. 2 (la_plan_set_weights): cta_begin[g] = min(g, I) + floor((I - G)+ *
+// sum_{i<g} w_i / sum w), w_i in [1, 2^20] (oracle.weighted_ranges).
+void weighted_ranges(int64_t total_iters, const std::vector<int32_t>& w, std::vector<int32_t>& cta_begin);
 // Sequential (FA2): one CTA per unit.
 void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& cta_begin);
 // LA_SCHED_DYNAMIC: every Eq. 2 range split into a head and k <= max_chunks tail chunks of

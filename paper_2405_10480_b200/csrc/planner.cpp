@@ -77,6 +77,23 @@ void streamk_ranges(int64_t total_iters, int grid, std::vector<int32_t>& cta_beg
   for (int g = 0; g <= grid; ++g) cta_begin[g] = int32_t(g * q + std::min<int64_t>(g, r));
 }
 
+void weighted_ranges(int64_t total_iters, const std::vector<int32_t>& w, std::vector<int32_t>& cta_begin) {
+  // SM-rate-weighted Eq. 2: one LeanTile per CTA plus a share of the other
+  // R = I - G proportional to its weight, boundary g = min(g, I) + floor(R * W_{<g} / W) --
+  // no empty range inside a unit (its host would wait for a partial nobody writes).  Integers
+  // only (R < 2^31, W <= G * 2^20), so the oracle reproduces it exactly.
+  const int64_t G = int64_t(w.size());
+  int64_t W = 0;
+  for (int32_t x : w) W += x;
+  const int64_t R = std::max<int64_t>(total_iters - G, 0);
+  cta_begin.resize(size_t(G) + 1);
+  int64_t acc = 0;
+  for (int64_t g = 0; g <= G; ++g) {
+    cta_begin[size_t(g)] = int32_t(std::min(g, total_iters) + R * acc / W);
+    if (g < G) acc += w[size_t(g)];
+  }
+}
+
 void sequential_ranges(const std::vector<DevUnit>& units, std::vector<int32_t>& cta_begin) {
   cta_begin.resize(units.size() + 1);
   for (size_t u = 0; u < units.size(); ++u) cta_begin[u] = units[u].iter_begin;

@@ -106,7 +106,7 @@ __device__ __forceinline__ unsigned smid() {
 }
 
 // LA_TRACE record fields (include/la.h la_plan_trace)
-enum { TR_SMID = 0, TR_START, TR_PUBLISH, TR_WAIT0, TR_WAIT1, TR_END, TR_FIELDS };
+enum { TR_SMID = 0, TR_START, TR_PUBLISH, TR_WAIT0, TR_WAIT1, TR_END, TR_STREAM, TR_FIELDS };  // = LA_TRACE_FIELDS
 
 __device__ __forceinline__ void consumer_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");

@@ -37,7 +37,8 @@ EXPORTS = ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_info_get",
            "la_plan_export_claims", "la_decode",
            "la_decode_partial", "la_combine", "la_combine_strided", "la_decode_host", "la_plan_status", "la_plan_destroy",
            "la_launch_count", "la_status_string", "la_last_error", "la_version", "la_plan_trace",
-           "la_plan_xchg_handle", "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status")
+           "la_plan_xchg_handle", "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status",
+           "la_plan_set_weights", "la_plan_calibrate")
 
 
 class LaError(RuntimeError):
@@ -67,7 +68,7 @@ class la_plan_info(ctypes.Structure):
                [("scale", ctypes.c_float), ("num_vctas", ctypes.c_int64), ("split", ctypes.c_int),
                 ("q_len", ctypes.c_int), ("tile_rows", ctypes.c_int), ("q_rows", ctypes.c_int64),
                 ("engine", ctypes.c_int), ("quantization_efficiency", ctypes.c_double),
-                ("slot_capacity", ctypes.c_int), ("updates", ctypes.c_int64)]
+                ("slot_capacity", ctypes.c_int), ("updates", ctypes.c_int64), ("sm_weighted", ctypes.c_int)]
 
 
 _lib = None
@@ -108,6 +109,9 @@ def lib() -> ctypes.CDLL:
         L.la_plan_xchg_open.argtypes = [vp, i32, ctypes.c_char_p]
         L.la_plan_xchg_attach.argtypes = [vp, i32, vp]
         L.la_plan_xchg_status.argtypes = [vp]
+    if hasattr(L, "la_plan_set_weights"):
+        L.la_plan_set_weights.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), i32, vp]
+        L.la_plan_calibrate.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.la_plan_destroy.argtypes = [vp]
     L.la_plan_destroy.restype = None
     L.la_launch_count.restype = i64
@@ -116,7 +120,8 @@ def lib() -> ctypes.CDLL:
     for name in ("la_plan_opts_init", "la_plan", "la_plan_update", "la_plan_status", "la_plan_info_get", "la_plan_export",
                  "la_plan_export_claims", "la_decode",
                  "la_decode_partial", "la_combine", "la_combine_strided", "la_decode_host", "la_plan_trace", "la_plan_xchg_handle",
-                 "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status"):
+                 "la_plan_xchg_open", "la_plan_xchg_attach", "la_plan_xchg_status", "la_plan_set_weights",
+                 "la_plan_calibrate"):
         if hasattr(L, name):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
@@ -259,12 +264,42 @@ class Plan:
                                            ctypes.byref(n)), "la_plan_export_claims")
         return buf
 
+    def set_weights(self, weights=None, stream=None):
+        """``la_plan_set_weights``: per-CTA stream-K weights (int32 in [1, 2^20], one per CTA of
+        the launch grid), ranges floor(I * W_<g / W); None restores Eq. 2's equal ranges."""
+        if weights is None:
+            ptr, n = None, 0
+        else:
+            w = np.ascontiguousarray(np.asarray(weights, dtype=np.int32))
+            self._w = w
+            ptr, n = w.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), int(w.size)
+        strm = None if _is_host_only(self) else _stream(stream)
+        _check(lib().la_plan_set_weights(self._h, ptr, n, strm), "la_plan_set_weights")
+        self.info = self._info()
+
+    def calibrate(self, q, k, v, launches: int = 6, rounds: int = 2, stream=None):
+        """``la_plan_calibrate``: measure each CTA's streaming rate on (q, k, v) and set
+        rate-proportional stream-K weights (synchronises); returns the weights."""
+        self._check_inputs(q, k, v)
+        out, lse = self._outputs(q, None, None, True)
+        _check(lib().la_plan_calibrate(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), int(launches),
+                                       int(rounds), _stream(stream)), "la_plan_calibrate")
+        self.info = self._info()
+        return self.range_lengths()
+
+    def range_lengths(self) -> np.ndarray:
+        """LeanTiles per (virtual) CTA range of the current schedule (weighted or not)."""
+        seg = self.export()
+        return np.bincount(seg[:, 0], weights=seg[:, 3] - seg[:, 2], minlength=self.info.num_vctas).astype(np.int64)
+
+    TRACE_FIELDS = 7
+
     def trace(self) -> np.ndarray:
-        """``la_plan_trace``: (G, 6) uint64 per-CTA timeline of the last decode
-        (smid, t_start, t_publish, t_wait_begin, t_wait_end, t_end) in ns."""
+        """``la_plan_trace``: (G, 7) uint64 per-CTA timeline of the last decode
+        (smid, t_start, t_publish, t_wait_begin, t_wait_end, t_end, t_stream_end) in ns."""
         n = ctypes.c_size_t()
         _check(lib().la_plan_trace(self._h, None, 0, ctypes.byref(n)), "la_plan_trace")
-        buf = np.zeros((n.value, 6), dtype=np.uint64)
+        buf = np.zeros((n.value, self.TRACE_FIELDS), dtype=np.uint64)
         _check(lib().la_plan_trace(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n.value,
                                    ctypes.byref(n)), "la_plan_trace")
         return buf

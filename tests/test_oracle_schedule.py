@@ -257,6 +257,54 @@ def test_alg2_with_virtual_ctas_equals_eq1():
         assert np.max(np.abs(O - O_ref)) <= 1e-12 and np.max(np.abs(L - L_ref)) <= 1e-12
 
 
+def test_weighted_ranges_properties_and_hand_values():
+    """oracle.weighted_ranges (SM-rate-weighted Eq. 2): pinned by hand values,
+    brute force and the properties the formula fixes."""
+    # hand values: I = 10, w = (1, 2, 2): R = 7, begins = (0, 1 + 7/5, 2 + 21/5, 3 + 7) floored
+    assert oracle.weighted_ranges(10, [1, 2, 2]) == [0, 2, 6, 10]
+    assert oracle.weighted_ranges(7, [3, 1]) == [0, 4, 7]          # 1 + floor(5 * 3 / 4) = 4
+    assert oracle.weighted_ranges(3, [1, 1, 1, 1, 1]) == [0, 1, 2, 3, 3, 3]   # I < G: trailing CTAs idle
+    assert oracle.weighted_ranges(5, [1 << 20, 1]) == [0, 3, 5]    # 1 + floor(3 * 2^20 / (2^20 + 1)); the tiny weight keeps 2
+    rng = np.random.default_rng(7)
+    for trial in range(300):
+        G = int(rng.integers(1, 200))
+        I = int(rng.integers(0, 300000))
+        w = [int(x) for x in rng.integers(1, 1 << 20, size=G)]
+        if trial % 3 == 0:
+            w = [int(x) for x in rng.integers(60000, 70000, size=G)]   # calibrated weights: +-8%
+        b = oracle.weighted_ranges(I, w)
+        W, R = sum(w), max(I - G, 0)
+        sizes = np.diff(b)
+        assert b[0] == 0 and b[-1] == I and np.all(sizes[:min(I, G)] >= 1) and np.all(sizes[min(I, G):] == 0)
+        # each range within one LeanTile of 1 + its exact share R w_g / W (brute force, fractions)
+        from fractions import Fraction
+        for g in range(0, min(I, G), max(1, G // 20)):
+            assert abs(Fraction(int(sizes[g])) - 1 - Fraction(R * w[g], W)) < 1
+    # equal weights: sizes differ by at most one and sum to I (Eq. 2's balance, reading C8's
+    # multiset of sizes, though the longer ranges are spread rather than first)
+    for I, G in [(65536, 148), (32768, 148), (245056, 148), (10, 4), (7, 10), (149, 148)]:
+        sizes = np.diff(oracle.weighted_ranges(I, [5] * G))
+        assert sizes.sum() == I and sizes.max() - sizes.min() <= 1
+        assert sorted(sizes.tolist()) == sorted(oracle.iters_per_cta(I, G))
+    # scale invariance: multiplying every weight by c changes nothing
+    assert oracle.weighted_ranges(12345, [3, 7, 11]) == oracle.weighted_ranges(12345, [300, 700, 1100])
+
+
+def test_alg2_over_weighted_ranges_equals_eq1():
+    rng = np.random.default_rng(5)
+    q = rng.normal(size=(2, 4, 8)) * 2
+    lens = [333, 91]
+    k = rng.normal(size=(2, 2, 333, 8))
+    v = rng.normal(size=(2, 2, 333, 8))
+    O_ref, L_ref = oracle.decode_attention(q, k, v, lens, 0.4)
+    c_n = [-(-n // 16) for n in lens for _ in range(2)]
+    for G in (1, 2, 5, 13, 60):
+        w = [int(x) for x in rng.integers(1, 1000, size=G)]
+        begins = oracle.weighted_ranges(sum(c_n), w)
+        O, L = oracle.lean_attention(q, k, v, lens, 0.4, 16, G, begins=begins)
+        assert np.max(np.abs(O - O_ref)) <= 1e-12 and np.max(np.abs(L - L_ref)) <= 1e-12
+
+
 def test_fixed_split_ranges_match_fixed_split_segments():
     # the range form of FD's split == the chunk list of fixed_split_segments (S:225-233)
     for c_n, s in [([5, 5], 2), ([7, 3, 9], 3), ([1, 2, 3], 4), ([16] * 5, 4)]:

@@ -179,6 +179,61 @@ def test_dynamic_schedule_bit_exact(la):
         assert np.bincount(wait_hosts[:, 0], minlength=p.info.num_vctas).max() <= 1
 
 
+def test_weighted_streamk_bit_exact(la):
+    """la_plan_set_weights: the SM-rate-weighted stream-K ranges and Alg. 2's walk over them,
+    bit-exact against oracle.weighted_ranges + oracle.segments_from_ranges; the weights
+    persist across la_plan_update; NULL restores Eq. 2."""
+    rng = np.random.default_rng(3)
+    import synth
+    cases = [synth.config(c) for c in ("c2", "c3", "c4")]
+    for trial in range(20):
+        batch = int(rng.integers(1, 9))
+        hkv = int(rng.integers(1, 9))
+        lens = [int(x) for x in rng.integers(1, 30000, size=batch)]
+        cases.append(synth.Problem(batch, hkv * int(rng.integers(1, 3)), hkv, 128, lens,
+                                   layout=["bhsd", "packed"][trial % 2]))
+    for i, pr in enumerate(cases):
+        sms = [148, 37, 200, 5][i % 4]
+        p = la.Plan(pr.batch, pr.heads_q, pr.heads_kv, pr.head_dim, pr.ctx_lens, tile_n=128, host_only=True,
+                    num_sms=sms, layout=pr.layout, schedule="streamk")
+        G = p.info.grid
+        w = [int(x) for x in rng.integers(1, 1 << 20, size=G)] if i % 2 else \
+            [int(x) for x in rng.integers(60000, 70000, size=G)]
+        p.set_weights(w)
+        assert p.info.sm_weighted == 1
+        units = unit_order(pr.batch, pr.heads_kv, pr.layout)
+        c_n = [-(-pr.ctx_lens[b] // 128) for (b, _h) in units for _ in range(-(-pr.group // 8))]
+        begins = oracle.weighted_ranges(sum(c_n), w)
+        exp = np.array([s.row() for s in oracle.segments_from_ranges(c_n, begins)], dtype=np.int32).reshape(-1, 7)
+        assert np.array_equal(p.export(), exp)
+        rows = p.export()   # <= 1 non-host and <= 1 waiting-host segment per CTA (any contiguous ranges)
+        assert np.bincount(rows[rows[:, 4] == 0][:, 0], minlength=G).max(initial=0) <= 1
+        wait_hosts = rows[(rows[:, 4] == 1) & (rows[:, 5] == 0)]
+        assert np.bincount(wait_hosts[:, 0], minlength=G).max(initial=0) <= 1
+        # the weights stay with the plan across an update (per CTA, independent of ctx_lens)
+        lens2 = [max(1, n // 2 + 7) for n in pr.ctx_lens]
+        p.update(lens2)
+        c_n2 = [-(-n // 128) for (b, _h) in units for n in [lens2[b]] for _ in range(-(-pr.group // 8))]
+        begins2 = oracle.weighted_ranges(sum(c_n2), w[:min(G, sum(c_n2))])
+        exp2 = np.array([s.row() for s in oracle.segments_from_ranges(c_n2, begins2)], dtype=np.int32).reshape(-1, 7)
+        assert np.array_equal(p.export(), exp2)
+        p.set_weights(None)
+        assert p.info.sm_weighted == 0
+        exp3 = np.array([s.row() for s in oracle.stream_k_segments(c_n2, min(G, sum(c_n2)))],
+                        dtype=np.int32).reshape(-1, 7)
+        assert np.array_equal(p.export(), exp3)
+    # validation: wrong count, out-of-range weight, non-stream-K plan
+    p = la.Plan(1, 2, 2, 128, [5000], host_only=True, schedule="streamk")
+    for bad in ([1] * (p.info.grid + 1), [0] * p.info.grid, [(1 << 20) + 1] * p.info.grid):
+        with pytest.raises(la.LaError) as e:
+            p.set_weights(bad)
+        assert e.value.status == la.LA_ERR_INVALID
+    pd = la.Plan(1, 2, 2, 128, [5000], host_only=True, schedule="dynamic")
+    with pytest.raises(la.LaError) as e:
+        pd.set_weights([1] * pd.info.grid)
+    assert e.value.status == la.LA_ERR_STATE
+
+
 def test_fixed_split_schedule_bit_exact(la):
     """LA_SCHED_FIXED_SPLIT (NEXT-1, FlashDecoding's decomposition): chunk ranges and the
     FA2 split heuristic, bit-exact against the oracle."""
