@@ -2036,8 +2036,13 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       unsigned long long ftA = 0, ftW = 0;
 #endif
       asm volatile("fence.proxy.async.global;" ::: "memory");      // acquired partials -> TMA
-      #pragma unroll 1
-      for (int r0 = 0; r0 < nr; r0 += RG) {
+      // this epilogue serves tiles of H <= 8 rows: ONE row group (RG = H), r0 a compile-time 0,
+      // so every acc index below is static and the accumulator stays in registers (a runtime
+      // row-group loop made them dynamic and put acc in local memory: every epilogue step
+      // then paid dependent L1 round trips)
+      static_assert(RG == H, "one row group");
+      {
+      constexpr int r0 = 0;
       #pragma unroll 1
       for (int b0 = 0; b0 < n; b0 += 32) {
         const int bn = min(32, n - b0);
