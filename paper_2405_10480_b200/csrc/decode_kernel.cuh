@@ -95,9 +95,6 @@
 #ifndef LA_TC5_NWG32
 #define LA_TC5_NWG32 2  // warpgroups for 32-row tiles (< NST32: the ring prefetches past the warpgroups)
 #endif
-#ifndef LA_TC5_LDEFER
-#define LA_TC5_LDEFER 0  // 1: 32 rows, NWG < NST: per-thread running sums updated after the PV MMA (measured 1% slower)
-#endif
 #ifndef LA_TC5_NWG16
 #define LA_TC5_NWG16 LA_TC5_NST  // the same for 16-row tiles
 #endif
@@ -109,6 +106,9 @@
 #endif
 #ifndef LA_TC5_BOXH
 #define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
+#endif
+#ifndef LA_TC5_MMA8
+#define LA_TC5_MMA8 1  // tcgen05 engine: each stage's 8 k-step MMAs of one product in one asm statement
 #endif
 #ifndef LA_TC5_SPLIT
 #define LA_TC5_SPLIT 1  // tcgen05 engine: 1 or 2 independent accumulator chains per MMA (4 k-steps each)
@@ -989,11 +989,16 @@ struct Tc5Engine {
   static_assert(HEADS == 8 || HEADS == 16 || HEADS == 32, "T_m");
   static constexpr int QR = HEADS < 16 ? 16 : HEADS;  // Q^T operand rows = S^T MMA N (>= 16)
   static constexpr int QHS = QR * 128;               // Q^T dim-half stride
-  // 32 rows with 168 registers (NWG < NST): every thread keeps its token's share of all 32
-  // running sums and updates them after the PV MMA with the shared alpha (no transpose-butterfly
-  // per stage); 32 rows at 128 registers: the butterfly, lane r keeping row r's sum
-  static constexpr bool LDEFER = LA_TC5_LDEFER && HEADS == 32 && NWG < NST;
-  static constexpr int LN = HEADS == 32 && !LDEFER ? 1 : HEADS;
+  // 32 rows: the warp's running sum of row `lane` (a transpose-butterfly per stage); <= 16
+  // rows: every thread keeps its token's share of each row's sum (r01 also tried per-thread
+  // 32-row sums updated after the PV MMA: 1% slower, removed)
+  // NWG < NST: a warpgroup's next stage sits in ANOTHER ring slot, so its PV MMA need not be
+  // waited for at the end of a stage -- the warpgroup moves on, issues the next stage's S^T
+  // MMA, and only then folds the previous O^T tile (both tensor-core round trips overlap the
+  // other's work instead of adding up).  With NWG == NST the next stage's data cannot land
+  // before this PV completes (same slot), so there is nothing to overlap.
+  static constexpr bool OVERLAP = NWG < NST;
+  static constexpr int LN = HEADS == 32 ? 1 : HEADS;
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
   static constexpr int FOLD_FLOATS = NWG * HEADS * (D + 4);
@@ -1026,7 +1031,13 @@ struct Tc5Engine {
     float o[HEADS];            // O~ of dim 32 sub + lane, every row
     int lbase, r0, nq;         // causal key limit of row h: lbase + (r0 + h) % nq (unit-local, exclusive)
     int mpar;                  // the running max m (uniform over the warpgroup) lives in shared memory,
-  };                           // mb[mpar][row]; a stage writes the new m into mb[mpar ^ 1]
+                               // mb[mpar][row]; a stage writes the new m into mb[mpar ^ 1]
+    int pend;                  // OVERLAP: barrier parity of this warpgroup's PV MMA still in flight (-1: none)
+#ifdef LA_TC5_PROF
+    long long pt[6];           // debug: cycles per stage phase, summed
+    int pn;
+#endif
+  };
 
   __device__ __forceinline__ static unsigned char* extra() {
     extern __shared__ unsigned char smem_raw[];
@@ -1106,6 +1117,11 @@ struct Tc5Engine {
     for (int h = 0; h < LN; ++h) s.l[h] = 0.f;
     if (tid < 2 * HEADS) reinterpret_cast<float*>(qs + MB_OFF)[tid] = -INFINITY;
     s.mpar = 0;
+    s.pend = -1;
+#ifdef LA_TC5_PROF
+    for (int i = 0; i < 6; ++i) s.pt[i] = 0;
+    s.pn = 0;
+#endif
     s.lbase = a.causal ? u.len - u.nq + 1 : u.len;  // N_q > 1, causal: query i is token n - N_b + i
     s.r0 = u.r0;
     s.nq = a.causal ? u.nq : 1;
@@ -1124,15 +1140,32 @@ struct Tc5Engine {
     const uint32_t kaddr = smem_u32(st), vaddr = smem_u32(st + KV_BYTES), qaddr = smem_u32(xs);
     const uint32_t rpar = par & 1u, wpar = par >> 1;  // ring slot's / warpgroup's barrier parity
     uint64_t* vbar = vbar_of(int((st - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES));
+#ifdef LA_TC5_PROF
+    long long ck[6];
+    ck[0] = clock64();
+#define TC5_CK(i) ck[i] = clock64()
+#else
+#define TC5_CK(i)
+#endif
     // ---- S^T = K_f Q_f^T (Alg1§20) -----------------------------------------------------------
-    if (tid == 0) {
+    if (SPLIT == 1 && LA_TC5_MMA8) {
+      if (sub == 0) {  // warp 0, converged: one elected lane issues (operands stay warp-uniform)
+        tc5::fence_after();
+        constexpr int Q = QHS / 16;  // k-step kk: K at (kk >> 2) 16 KiB + (kk & 3) 32 B, Q^T likewise
+        tc5::mma8_f16<2, 4, 6, 1024, 1026, 1028, 1030, 2, 4, 6, Q, Q + 2, Q + 4, Q + 6>(
+            tbase, tc5::sdesc(kaddr, 16, 1024), tc5::sdesc(qaddr, 16, 1024), IDESC_S);
+        tc5::commit_elect(&bars[0]);
+      }
+    } else if (tid == 0) {
       tc5::fence_after();
+      {
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {  // chain c = kk / (8 / SPLIT) accumulates in columns 16 c
-        const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-        const int c = kk / (8 / SPLIT);
-        tc5::mma_f16(tbase + QR * c, tc5::sdesc(kaddr + off, 16, 1024),
-                     tc5::sdesc(qaddr + (kk >> 2) * QHS + (kk & 3) * 32, 16, 1024), IDESC_S, kk % (8 / SPLIT) > 0);
+        for (int kk = 0; kk < D / 16; ++kk) {  // chain c = kk / (8 / SPLIT) accumulates in columns 16 c
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const int c = kk / (8 / SPLIT);
+          tc5::mma_f16(tbase + QR * c, tc5::sdesc(kaddr + off, 16, 1024),
+                       tc5::sdesc(qaddr + (kk >> 2) * QHS + (kk & 3) * 32, 16, 1024), IDESC_S, kk % (8 / SPLIT) > 0);
+        }
       }
       tc5::commit(&bars[0]);
     }
@@ -1145,8 +1178,13 @@ struct Tc5Engine {
           for (int c = 0; c < 8; ++c)
             *reinterpret_cast<uint4*>(st + KV_BYTES + hf * 16384 + tid * 128 + (c << 4)) = make_uint4(0u, 0u, 0u, 0u);
     }
+    if constexpr (OVERLAP) {  // the previous stage's O^T tile, while this stage's S^T MMA runs
+      if (s.pend >= 0) finish_o(s, sub, lane, uint32_t(s.pend));
+    }
+    TC5_CK(1);
     mbar_wait(&bars[0], wpar);
     tc5::fence_after();
+    TC5_CK(2);
     float sc[QR];
 #pragma unroll
     for (int c = 0; c < QR; c += 16) {
@@ -1184,6 +1222,7 @@ struct Tc5Engine {
       for (int h = 0; h < HEADS; h += 4)
         *reinterpret_cast<float4*>(red + sub * HEADS + h) = make_float4(mx[h], mx[h + 1], mx[h + 2], mx[h + 3]);
     wg_bar(slot);
+    TC5_CK(3);
     const uint32_t mcur = smem_u32(xs + MB_OFF) + 4 * HEADS * s.mpar, mnext = smem_u32(xs + MB_OFF) + 4 * HEADS * (s.mpar ^ 1);
     const uint32_t alp = smem_u32(xs + AL_OFF);
     if (tid < HEADS) {  // row tid: m_new (Alg1§21) and alpha = e^{m - m_new} for every thread's O update
@@ -1231,7 +1270,7 @@ struct Tc5Engine {
         *reinterpret_cast<uint4*>(pl + (((HEADS / 8 + j) ^ (tid & 7)) << 4)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
     }
-    if constexpr (HEADS == 32 && !LDEFER) {  // Alg1§23 for 32 rows: XOR transpose-butterfly of the 32 p's
+    if constexpr (HEADS == 32) {  // Alg1§23 for 32 rows: XOR transpose-butterfly of the 32 p's
       // (31 shuffles) leaves the warp's sum of row `lane` in sc[0] of lane `lane`
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) {
@@ -1253,20 +1292,57 @@ struct Tc5Engine {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (+ zeroed V) -> tensor core
     tc5::fence_before();                                           // S loads done before reuse
     wg_bar(slot);
+    TC5_CK(4);
     // ---- O^T_tile = V_f^T P_f^T (Alg1§24) ----------------------------------------------------
-    if (tid == 0) {
+    if (SPLIT == 1 && LA_TC5_MMA8) {
+      if (sub == 0) {  // warp 0, converged: one elected lane issues
+        mbar_wait(vbar, rpar);  // V landed
+        tc5::fence_after();     // k-step kk: 16 tokens = 2 KiB further in V and in P^T
+        tc5::mma8_f16<128, 256, 384, 512, 640, 768, 896, 128, 256, 384, 512, 640, 768, 896>(
+            tbase + OC, tc5::sdesc(vaddr, 16384, 1024), tc5::sdesc(kaddr, 8192, 1024), IDESC_O);
+        tc5::commit_elect(empty);     // the slot is free the moment the tensor core is done with it
+        tc5::commit_elect(&bars[1]);
+      } else if (lane == 0) {
+        mbar_arrive(empty);     // this warp no longer touches the slot's shared memory
+      }
+    } else if (tid == 0) {
       mbar_wait(vbar, rpar);  // V landed
       tc5::fence_after();
+      {
 #pragma unroll
-      for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
-        tc5::mma_f16(tbase + OC + NO * (kk / (8 / SPLIT)), tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
-                     tc5::sdesc(kaddr + kk * 2048, 8192, 1024),  // MN-major P^T: 16 token lines per k-step
-                     IDESC_O, kk % (8 / SPLIT) > 0);
+        for (int kk = 0; kk < STAGE_TOK / 16; ++kk)
+          tc5::mma_f16(tbase + OC + NO * (kk / (8 / SPLIT)), tc5::sdesc(vaddr + kk * 2048, 16384, 1024),
+                       tc5::sdesc(kaddr + kk * 2048, 8192, 1024),  // MN-major P^T: 16 token lines per k-step
+                       IDESC_O, kk % (8 / SPLIT) > 0);
+      }
       tc5::commit(empty);     // the slot is free the moment the tensor core is done with it
       tc5::commit(&bars[1]);
     } else if (sub != 0 && lane == 0) {
       mbar_arrive(empty);     // this warp no longer touches the slot's shared memory
     }
+    if constexpr (OVERLAP) {
+      s.pend = int(wpar);     // folded by the next stage (or seg_end)
+    } else {
+      finish_o(s, sub, lane, wpar);
+    }
+    s.mpar ^= 1;
+#ifdef LA_TC5_PROF
+    ck[5] = clock64();
+    for (int i = 0; i < 5; ++i) s.pt[i] += ck[i + 1] - ck[i];
+    ++s.pn;
+#endif
+#undef TC5_CK
+  }
+
+  // O~ += the stage's O^T tile with the stage's alpha (Alg1§24-25): wait for its PV MMA (barrier
+  // parity wpar), read the tile from TMEM, fold.  Must precede the next softmax's alpha writes.
+  __device__ __forceinline__ static void finish_o(State& s, int sub, int lane, uint32_t wpar) {
+    const int slot = slot_of_thread();
+    unsigned char* xs = extra() + slot * XS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + BAR_OFF);
+    const uint32_t tbase = *tmem_base_ptr() + uint32_t(COLS * slot);
+    const uint32_t tlane = uint32_t(32 * sub) << 16;
+    const uint32_t alp = smem_u32(xs + AL_OFF);
     mbar_wait(&bars[1], wpar);
     tc5::fence_after();
     // alpha from shared memory, 8 rows at a time (no registers held across the MMA)
@@ -1295,21 +1371,27 @@ struct Tc5Engine {
       const float al[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
       for (int i = 0; i < 8; ++i) s.o[c0 + i] = fmaf(al[i], s.o[c0 + i], hv[i] + lv[i]);  // Alg1§25
-      if constexpr (LDEFER)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s.l[c0 + i] = fmaf(al[i], s.l[c0 + i], sc[c0 + i]);  // Alg1§23 (sc = p)
     }
     tc5::fence_before();
-    s.mpar ^= 1;
   }
 
   __device__ __forceinline__ static void seg_end(State& s, float* fold, int warp, int lane) {
     const int slot = warp / WPS, sub = warp % WPS;
+    if constexpr (OVERLAP) {  // the segment's last O^T tile
+      if (s.pend >= 0) finish_o(s, sub, lane, uint32_t(s.pend));
+      s.pend = -1;
+    }
+#ifdef LA_TC5_PROF
+    if (sub == 0 && lane == 0 && blockIdx.x % 37 == 0 && s.pn > 8)
+      printf("TC5PROF cta %d wg %d H %d stages %d: [S-issue..finish_o] %lld [S wait] %lld [ld+mask+redux+bar] %lld "
+             "[alpha+P+bar] %lld [PV issue..end] %lld cycles/stage\n", int(blockIdx.x), slot, HEADS, s.pn,
+             s.pt[0] / s.pn, s.pt[1] / s.pn, s.pt[2] / s.pn, s.pt[3] / s.pn, s.pt[4] / s.pn);
+#endif
     float* red2 = reinterpret_cast<float*>(extra() + slot * XS + RED2_OFF);  // [4][HEADS]
     float* fb = fold + slot * HEADS * (D + 4);                                  // [row][D + 4]
 #pragma unroll
     for (int h = 0; h < HEADS; ++h) fb[h * (D + 4) + 32 * sub + lane] = s.o[h];
-    if constexpr (HEADS == 32 && !LDEFER) {
+    if constexpr (HEADS == 32) {
       red2[sub * HEADS + lane] = s.l[0];  // lane = row
     } else {
 #pragma unroll

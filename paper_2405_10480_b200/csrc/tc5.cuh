@@ -57,6 +57,44 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_
       : "memory");
 }
 
+// Eight chained k-steps in ONE asm statement, called by a whole (converged) warp: one elected
+// lane issues them (elect.sync -- the same lane as commit_elect's).  D = sum_k A_k B_k, the
+// first overwriting D.
+// Descriptor k is the base descriptor plus a constant start-address step (16-B units, no carry
+// out of the 14-bit field for any shared-memory address), added inside the statement -- so
+// only the two base descriptors cross from ordinary to uniform registers instead of sixteen
+// (one waterfall loop of the compiler for the whole chain instead of one per MMA).
+template <int A1, int A2, int A3, int A4, int A5, int A6, int A7, int B1, int B2, int B3, int B4, int B5, int B6, int B7>
+__device__ __forceinline__ void mma8_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred pf, pt, pe;\n\t.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n\t"
+      "setp.ne.b32 pf, 0, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\telect.sync _|pe, 0xffffffff;\n\t"
+      "add.s64 a1, %1, %4;\n\tadd.s64 a2, %1, %5;\n\tadd.s64 a3, %1, %6;\n\tadd.s64 a4, %1, %7;\n\t"
+      "add.s64 a5, %1, %8;\n\tadd.s64 a6, %1, %9;\n\tadd.s64 a7, %1, %10;\n\t"
+      "add.s64 b1, %2, %11;\n\tadd.s64 b2, %2, %12;\n\tadd.s64 b3, %2, %13;\n\tadd.s64 b4, %2, %14;\n\t"
+      "add.s64 b5, %2, %15;\n\tadd.s64 b6, %2, %16;\n\tadd.s64 b7, %2, %17;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pf;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, pt;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "n"(A1), "n"(A2), "n"(A3), "n"(A4), "n"(A5), "n"(A6), "n"(A7), "n"(B1),
+      "n"(B2), "n"(B3), "n"(B4), "n"(B5), "n"(B6), "n"(B7)
+      : "memory");
+}
+
+// commit() by the warp's elected lane (the one that issued mma8_f16's MMAs); whole warp.
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+      "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
 // Arrive once on `bar` when every tcgen05.mma this thread issued before has completed.
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -14,13 +14,13 @@ import synth  # noqa: E402
 import paper_2405_10480_b200 as la  # noqa: E402
 
 
-def main(cfg, engine):
-    p = synth.config(cfg)
+def main(cfg, engine, q_len=1):
+    p = synth.config(cfg, **(dict(q_len=q_len) if q_len > 1 else {}))
     q = synth.gen_q(p, "cuda")
     k = synth.fill_kv_cache(p, "k", "cuda")
     v = synth.fill_kv_cache(p, "v", "cuda")
     plan = la.Plan(p.batch, p.heads_q, p.heads_kv, p.head_dim, p.ctx_lens, dtype=p.dtype, layout=p.layout,
-                   trace=True, engine=engine)
+                   trace=True, engine=engine, q_len=q_len)
     for _ in range(5):
         plan.decode(q, k, v)
     import torch
@@ -42,4 +42,4 @@ def main(cfg, engine):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "mma")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "mma", int(sys.argv[3]) if len(sys.argv) > 3 else 1)
