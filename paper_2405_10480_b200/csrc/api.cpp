@@ -846,6 +846,7 @@ static la_status decode_impl(la_plan_t plan, const void* q, const void* k, const
   // stream-K hosts may wait on peers (Alg2§28): co-residency by a cooperative launch (the launch
   // grid never exceeds the co-resident count; measured no cost vs a plain launch)
   const bool coop = p.schedule == LA_SCHED_STREAMK;
+
   const int rc = la::launch_decode(plan->kinfo, a, p.kv_rows(), p.head_dim, p.dtype, coop, stream, &plan->tmaps, err);
   if (rc != 0) return fail(LA_ERR_CUDA, err);
   return LA_OK;

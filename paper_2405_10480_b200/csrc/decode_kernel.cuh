@@ -107,6 +107,26 @@
 #ifndef LA_TC5_BOXH
 #define LA_TC5_BOXH 1  // tcgen05 engine: one 128-B half of 128 rows per TMA box (16 KiB)
 #endif
+#ifndef LA_TC5_WIN8
+#define LA_TC5_WIN8 0   // tcgen05 engine, 8-row tiles: stages in flight (0: the whole ring; measured: the
+                        // full ring scatters the CTAs' rates, 2 stages 311 -> 305 us, 3 with V at 2: 306 -> 304)
+#endif
+#ifndef LA_TC5_VWIN8
+#define LA_TC5_VWIN8 2  // tcgen05 engine, 8-row tiles: V of stage j after stage j - VWIN8 is consumed (0: off)
+#endif
+#ifndef LA_TC5_WIN16
+#define LA_TC5_WIN16 2  // ... 16-row tiles (measured: c3 N_q = 2 317 -> 313 us)
+#endif
+#ifndef LA_TC5_WIN32
+#define LA_TC5_WIN32 0  // ... 32-row tiles (compute-bound: 2 stages measured 314 -> 355 us)
+#endif
+#ifndef LA_MHA_WIN
+#define LA_MHA_WIN 0    // MHA engine: stages in flight (0: the whole ring; 4 measured within noise for
+                        // c2 stream-K, slower for the dynamic schedule and paged pools; 3: 630 us)
+#endif
+#ifndef LA_GQA_WIN
+#define LA_GQA_WIN 0    // mma.sync GQA engine: stages in flight (0: the whole ring)
+#endif
 #ifndef LA_TC5_MMA8
 #define LA_TC5_MMA8 1  // tcgen05 engine: each stage's 8 k-step MMAs of one product in one asm statement
 #endif
@@ -278,6 +298,7 @@ struct PageWin {
 template <typename T, int D_, int NST_, int WPS_>
 struct MhaEngine {
   static constexpr int D = D_, NST = NST_, WPS = WPS_, NWG = NST, NCW = NWG * WPS;  // NWG: consumer warp sets
+  static constexpr int WIN = LA_MHA_WIN > 0 ? LA_MHA_WIN : NST;  // stages in flight
   static constexpr int ROWB = D * int(sizeof(T));          // bytes of one K (or V) row
   static constexpr int LPK = ROWB / 16;                     // lanes per key
   static constexpr int EPL = 16 / int(sizeof(T));           // elements per 16-byte chunk
@@ -496,6 +517,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 template <typename T, int D_, int NST_, int WPS_>
 struct GqaEngine {
   static constexpr int D = D_, NST = NST_, WPS = WPS_, NWG = NST, NCW = NWG * WPS;  // NWG: consumer warp sets
+  static constexpr int WIN = LA_GQA_WIN > 0 ? LA_GQA_WIN : NST;  // stages in flight
   static constexpr int STAGE_TOK = 64;            // = TMA box rows
   static constexpr int NBOX = D / 64;             // 64-element (128-B) boxes per row
   static constexpr int BOX_BYTES = STAGE_TOK * 128;
@@ -741,6 +763,7 @@ __device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t sel) {
 template <int D_, int NST_, int WPS_, int ROWS_>
 struct Fp8Engine {
   static constexpr int D = D_, NST = NST_, WPS = WPS_, NWG = NST, NCW = NWG * WPS;  // NWG: consumer warp sets
+  static constexpr int WIN = NST;                 // stages in flight: the whole ring
   static_assert(ROWS_ == 1 || ROWS_ == 8, "fold rows");
   static_assert(D == 128, "an E4M3 row of d = 128 is exactly one 128-B swizzle span");
   static constexpr int STAGE_TOK = 128;           // = TMA box rows (32 KiB of K+V per stage)
@@ -979,6 +1002,11 @@ struct Tc5Engine {
   // NST ring slots of 128 tokens; NWG warpgroups take the stages round-robin (NWG < NST: a
   // warpgroup's next tile is already in flight while it computes)
   static constexpr int D = 128, NST = NST_, WPS = 4, NWG = NWG_, NCW = NWG * WPS;
+  static constexpr int WIN_ = HEADS_ == 8 ? LA_TC5_WIN8 : HEADS_ == 16 ? LA_TC5_WIN16 : LA_TC5_WIN32;
+  static constexpr int WIN = WIN_ > 0 ? WIN_ : NST;  // stages in flight
+  // V of stage j waits until stage j - VWIN is consumed (VWIN < WIN: ~WIN - 1/2 stages in flight)
+  static constexpr int VWIN_ = HEADS_ == 8 ? LA_TC5_VWIN8 : 0;
+  static constexpr int VWIN = VWIN_ > 0 ? VWIN_ : WIN;
   static_assert(NWG <= NST && NST <= 8, "ring");
   static constexpr int STAGE_TOK = 128;             // = TMA box rows = MMA M
   static constexpr int BOX_HALVES = LA_TC5_BOXH;    // 128-B row halves per TMA box (16 or 32 KiB boxes)
@@ -1062,6 +1090,19 @@ struct Tc5Engine {
     for (int s = 0; s < NST; ++s) mbar_init(vbar_of(s), 1);
   }
 
+  __device__ __forceinline__ static void produce_k(unsigned char* dst, const TmapPair& tm, int64_t row, uint64_t* bar,
+                                                   uint64_t pol) {
+    mbar_arrive_expect_tx(bar, KV_BYTES);
+#pragma unroll
+    for (int h = 0; h < 2 / BOX_HALVES; ++h) tma_load_3d(dst + h * 16384, &tm.k, 0, int(row), h, bar, pol);
+  }
+  __device__ __forceinline__ static void produce_v(unsigned char* dst, const TmapPair& tm, int64_t row, uint64_t pol) {
+    const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
+    uint64_t* vbar = vbar_of(slot);
+    mbar_arrive_expect_tx(vbar, KV_BYTES);
+#pragma unroll
+    for (int h = 0; h < 2 / BOX_HALVES; ++h) tma_load_3d(dst + KV_BYTES + h * 16384, &tm.v, 0, int(row), h, vbar, pol);
+  }
   __device__ __forceinline__ static void produce(unsigned char* dst, const DecodeArgs&, const TmapPair& tm, int64_t row,
                                                  int, uint64_t* bar, uint64_t pol) {
     // K on the ring's full barrier, V on the slot's own barrier: S^T, the softmax and P
@@ -1439,12 +1480,12 @@ struct SegInfo {
 // the ring and fewer fold rows per slot; the others get the neutral values.
 template <class E, class = void>
 struct EngX {
-  static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS;
+  static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS, VWIN = 1 << 20;
   static constexpr bool GF = false;  // fold buffers in global scratch (DecodeArgs::gfold)
 };
 template <class E>
 struct EngX<E, std::void_t<decltype(E::TMEM_COLS)>> {
-  static constexpr int TMEM = E::TMEM_COLS, EXTRA = E::EXTRA_BYTES, FW = E::FOLD_WPS;
+  static constexpr int TMEM = E::TMEM_COLS, EXTRA = E::EXTRA_BYTES, FW = E::FOLD_WPS, VWIN = E::VWIN;
   static constexpr bool GF = E::GLOBAL_FOLD;
 };
 
@@ -1893,6 +1934,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.v)) : "memory");
     }
     int j = 0, ks = 0;
+    const int win = a.win > 0 ? min(a.win, E::WIN) : E::WIN;  // stages in flight
 #ifdef LA_PROF
     long long prof_pwait = 0;  // producer cycles waiting for free slots -> trace field smid
 #endif
@@ -1997,12 +2039,25 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
           const long long c0 = clock64();
 #endif
           if (lane == 0 && j >= NST) mbar_wait(&empty[slot], ((j / NST) - 1) & 1);
+          // at most `win` stages in flight: stage j - win must be consumed first (its slot's next
+          // stage j - win + NST > j is not issued yet, so the phase cannot alias).  DESIGN §6: an
+          // SM with more bytes in flight than the memory system serves it at its fair share only
+          // adds queueing, and the CTAs' streaming rates then scatter (the kernel ends with the slowest)
+          if (win < NST && lane == 0 && j >= win) mbar_wait(&empty[(j - win) % NST], ((j - win) / NST) & 1);
 #ifdef LA_PROF
           if (lane == 0) prof_pwait += clock64() - c0;
 #endif
           const int ntok = min(a.stage_tokens, t1 - s0);
           if (!a.paged) {
-            if (lane == 0) E::produce(ring + slot * E::STAGE_BYTES, a, tm, row0 + s0, ntok, &full[slot], pol);
+            if constexpr (EngX<E>::VWIN < E::WIN) {  // (tcgen05) K now, V once stage j - VWIN is consumed
+              if (lane == 0) {
+                E::produce_k(ring + slot * E::STAGE_BYTES, tm, row0 + s0, &full[slot], pol);
+                if (j >= E::VWIN) mbar_wait(&empty[(j - E::VWIN) % NST], ((j - E::VWIN) / NST) & 1);
+                E::produce_v(ring + slot * E::STAGE_BYTES, tm, row0 + s0, pol);
+              }
+            } else {
+              if (lane == 0) E::produce(ring + slot * E::STAGE_BYTES, a, tm, row0 + s0, ntok, &full[slot], pol);
+            }
           } else {
             E::produce_paged(ring + slot * E::STAGE_BYTES, a, tm, pw, s0, ntok, &full[slot], pol, lane);
           }

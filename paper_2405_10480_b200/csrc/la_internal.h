@@ -151,6 +151,7 @@ struct DecodeArgs {
   size_t xflag_off;
   float* xpeer[8];    // every rank's buffer (xpeer[xr] = own), device-accessible addresses
   int* xerr;          // own buffer's error word: 1 after a wait timed out
+  int win;            // > 0: at most this many ring stages in flight (else the engine's default)
 };
 
 // DecodeArgs::counters
