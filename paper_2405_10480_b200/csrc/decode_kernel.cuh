@@ -122,7 +122,10 @@
 #endif
 #ifndef LA_MHA_WIN
 #define LA_MHA_WIN 0    // MHA engine: stages in flight (0: the whole ring; 4 measured within noise for
-                        // c2 stream-K, slower for the dynamic schedule and paged pools; 3: 630 us)
+                        // c2 stream-K, slower dynamic (582 -> 586 us) and paged (620 -> 649 us); 3: 630 us)
+#endif
+#ifndef LA_FP8_WIN
+#define LA_FP8_WIN 0    // FP8 engine: stages in flight (0: the whole ring; 4 measured slower: c2 304 -> 319 us)
 #endif
 #ifndef LA_GQA_WIN
 #define LA_GQA_WIN 0    // mma.sync GQA engine: stages in flight (0: the whole ring)
@@ -763,7 +766,7 @@ __device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t sel) {
 template <int D_, int NST_, int WPS_, int ROWS_>
 struct Fp8Engine {
   static constexpr int D = D_, NST = NST_, WPS = WPS_, NWG = NST, NCW = NWG * WPS;  // NWG: consumer warp sets
-  static constexpr int WIN = NST;                 // stages in flight: the whole ring
+  static constexpr int WIN = LA_FP8_WIN > 0 ? LA_FP8_WIN : NST;  // stages in flight
   static_assert(ROWS_ == 1 || ROWS_ == 8, "fold rows");
   static_assert(D == 128, "an E4M3 row of d = 128 is exactly one 128-B swizzle span");
   static constexpr int STAGE_TOK = 128;           // = TMA box rows (32 KiB of K+V per stage)
