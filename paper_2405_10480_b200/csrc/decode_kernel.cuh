@@ -1269,31 +1269,27 @@ struct Tc5Engine {
     TC5_CK(3);
     const uint32_t mcur = smem_u32(xs + MB_OFF) + 4 * HEADS * s.mpar, mnext = smem_u32(xs + MB_OFF) + 4 * HEADS * (s.mpar ^ 1);
     const uint32_t alp = smem_u32(xs + AL_OFF);
-    if (tid < HEADS) {  // row tid: m_new (Alg1§21) and alpha = e^{m - m_new} for every thread's O update
-      const uint32_t rl = smem_u32(red) + 4 * tid;
-      const float mo = lds_f32(mcur + 4 * tid);
-      const float mrow = fmaxf(mo, fmaxf(fmaxf(lds_f32(rl), lds_f32(rl + 4 * HEADS)),
-                                         fmaxf(lds_f32(rl + 8 * HEADS), lds_f32(rl + 12 * HEADS))));
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(mnext + 4 * tid), "f"(mrow) : "memory");
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(alp + 4 * tid), "f"(ex2_sub(mo, mrow)) : "memory");
-    }
-    // ---- P_f = exp(S_f - m_new) (Alg1§22), m_new 4 rows at a time (no per-row register array) --
-#pragma unroll
-    for (int h = 0; h < HEADS; h += 4) {
-      const uint32_t ra = smem_u32(red) + 4 * h;
-      const float4 w0 = lds_f32x4(ra), w1 = lds_f32x4(ra + 4 * HEADS), w2 = lds_f32x4(ra + 8 * HEADS),
-                   w3 = lds_f32x4(ra + 12 * HEADS), mo = lds_f32x4(mcur + 4 * h);
-      const float mo4[4] = {mo.x, mo.y, mo.z, mo.w};
-      const float mn4[4] = {fmaxf(mo.x, fmaxf(fmaxf(w0.x, w1.x), fmaxf(w2.x, w3.x))),
-                            fmaxf(mo.y, fmaxf(fmaxf(w0.y, w1.y), fmaxf(w2.y, w3.y))),
-                            fmaxf(mo.z, fmaxf(fmaxf(w0.z, w1.z), fmaxf(w2.z, w3.z))),
-                            fmaxf(mo.w, fmaxf(fmaxf(w0.w, w1.w), fmaxf(w2.w, w3.w)))};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float p = ex2_sub(sc[h + e], mn4[e]);
-        if constexpr (HEADS < 32) s.l[h + e] = fmaf(ex2_sub(mo4[e], mn4[e]), s.l[h + e], p);  // Alg1§23
-        sc[h + e] = p;
+    // lane r < HEADS of every warp: row r's m_new (Alg1§21) and alpha = e^{m - m_new}; every
+    // thread then takes them by shuffles (one lane's loads per row instead of every thread
+    // re-reading all rows' maxima); warp 0 also stores them for the O update and the next stage
+    float mrow_l = 0.f, al_l = 0.f;
+    if (lane < HEADS) {
+      const uint32_t rl = smem_u32(red) + 4 * lane;
+      const float mo = lds_f32(mcur + 4 * lane);
+      mrow_l = fmaxf(mo, fmaxf(fmaxf(lds_f32(rl), lds_f32(rl + 4 * HEADS)),
+                               fmaxf(lds_f32(rl + 8 * HEADS), lds_f32(rl + 12 * HEADS))));
+      al_l = ex2_sub(mo, mrow_l);
+      if (sub == 0) {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(mnext + 4 * lane), "f"(mrow_l) : "memory");
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(alp + 4 * lane), "f"(al_l) : "memory");
       }
+    }
+    // ---- P_f = exp(S_f - m_new) (Alg1§22) --------------------------------------------------
+#pragma unroll
+    for (int h = 0; h < HEADS; ++h) {
+      const float p = ex2_sub(sc[h], __shfl_sync(0xffffffffu, mrow_l, h));
+      if constexpr (HEADS < 32) s.l[h] = fmaf(__shfl_sync(0xffffffffu, al_l, h), s.l[h], p);  // Alg1§23
+      sc[h] = p;
     }
     // P^T MN-major: token t's 2 HEADS columns (P_hi rows, then P_lo rows) in one 128-B swizzled
     // line over the dead K tile -> 2 HEADS / 8 16-B stores per thread (the B-operand layout
@@ -1325,13 +1321,7 @@ struct Tc5Engine {
           sc[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
         }
       }
-      // m_new of row `lane` recomputed from red (complete since the first barrier; mnext is
-      // only complete after the second)
-      const uint32_t rl = smem_u32(red) + 4 * lane;
-      const float mo = lds_f32(mcur + 4 * lane);
-      const float mrow = fmaxf(mo, fmaxf(fmaxf(lds_f32(rl), lds_f32(rl + 4 * HEADS)),
-                                         fmaxf(lds_f32(rl + 8 * HEADS), lds_f32(rl + 12 * HEADS))));
-      s.l[0] = fmaf(ex2_sub(mo, mrow), s.l[0], sc[0]);
+      s.l[0] = fmaf(al_l, s.l[0], sc[0]);  // lane = row: its own alpha
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (+ zeroed V) -> tensor core
     tc5::fence_before();                                           // S loads done before reuse
