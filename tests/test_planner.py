@@ -37,6 +37,24 @@ def test_exports_every_declared_symbol(la):
     assert L.la_status_string(1) == b"LA_ERR_INVALID"
 
 
+def test_info_struct_and_trace_fields_match_the_header(la):
+    """la_plan_info's ctypes mirror lists the header's fields in order, la_plan_info_get on a
+    host-only plan fills the last one (sm_weighted), and the binding reads LA_TRACE_FIELDS
+    words per CTA."""
+    from paper_2405_10480_b200.leanattn import la_plan_info, Plan
+    header = open(os.path.join(ROOT, "include", "la.h")).read()
+    body = header[header.index("typedef struct {\n  int batch, heads_q"):header.index("} la_plan_info;")]
+    fields = []
+    for decl in re.findall(r"^\s*(?:int64_t|int|float|double)\s+([\w, ]+);", body, re.M):
+        fields += [f.strip() for f in decl.split(",")]
+    assert fields == [f for f, _ in la_plan_info._fields_]
+    assert int(re.search(r"#define LA_TRACE_FIELDS (\d+)", header).group(1)) == Plan.TRACE_FIELDS
+    p = la.Plan(1, 2, 2, 128, [5000], host_only=True, schedule="streamk")
+    assert p.info.sm_weighted == 0
+    p.set_weights([3] * p.info.grid)
+    assert p.info.sm_weighted == 1
+
+
 def test_plan_opts_struct_matches_the_header(la):
     """The ctypes mirror of la_plan_opts has the C layout: la_plan_opts_init memsets exactly
     sizeof(la_plan_opts) bytes, so it must touch the whole ctypes struct and nothing past it,
