@@ -276,7 +276,9 @@ la_status la_plan_set_weights(la_plan_t plan, const int32_t* weights, int n, voi
  * device buffer if the plan has none; the first sample is a warm-up): time_g =
  * t_stream_end - t_start of CTA g summed over the samples, then w_g <- w_g * (mean time /
  * time_g) (rate-proportional shares), so the CTAs finish streaming together.  out / lse receive the last launch's (correct) result.
- * Synchronises the device.  LA_SCHED_STREAMK plans only (LA_ERR_STATE otherwise);
+ * Synchronises the device.  LA_SCHED_STREAMK plans without a cross-GPU exchange only
+ * (LA_ERR_STATE otherwise: an exchange plan's launches wait for its peers' -- calibrate an
+ * exchange-free plan of the same shape and pass its weights to la_plan_set_weights);
  * launches, rounds >= 1.  Weights are a property of the GPU's SMs: calibrate once per plan
  * (la_plan_update keeps them).
  */

@@ -665,6 +665,8 @@ la_status la_plan_calibrate(la_plan_t plan, const void* q, const void* k_cache, 
   if (plan->host_only) return fail(LA_ERR_STATE, "host-only plan cannot decode");
   if (plan->prob.schedule != LA_SCHED_STREAMK) return fail(LA_ERR_STATE, "calibration applies to LA_SCHED_STREAMK plans");
   if (launches < 1 || rounds < 1) return fail(LA_ERR_INVALID, "launches and rounds must be >= 1");
+  if (plan->xw > 1)  // its launches would wait for the peers' exchange launches
+    return fail(LA_ERR_STATE, "la_plan_calibrate on a cross-GPU exchange plan: use la_plan_set_weights");
   const int GP = plan->sched.phys_grid;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned long long* own_trace = plan->d_trace;
