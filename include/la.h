@@ -278,7 +278,8 @@ la_status la_plan_set_weights(la_plan_t plan, const int32_t* weights, int n, voi
  * time_g) (rate-proportional shares), so the CTAs finish streaming together.  out / lse receive the last launch's (correct) result.
  * Synchronises the device.  LA_SCHED_STREAMK plans without a cross-GPU exchange only
  * (LA_ERR_STATE otherwise: an exchange plan's launches wait for its peers' -- calibrate an
- * exchange-free plan of the same shape and pass its weights to la_plan_set_weights);
+ * exchange-free plan of the same shape and pass its range lengths -- la_plan_export -- to
+ * la_plan_set_weights);
  * launches, rounds >= 1.  Weights are a property of the GPU's SMs: calibrate once per plan
  * (la_plan_update keeps them).
  */
