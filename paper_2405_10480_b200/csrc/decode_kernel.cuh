@@ -264,34 +264,41 @@ struct Chunk<float> {
 // row, refilled with 8 independent 16-byte loads (one L2 round trip per 32 pages).
 // =======================================================================================
 struct PageWin {
+  // A window of 64 consecutive block-table entries of the unit's request, held one per lane in
+  // two registers (entries base + lane and base + 32 + lane): a lookup is a shuffle, a stage
+  // (<= 8 pages) never straddles the window, and sliding by 32 entries reuses the upper half
+  // and issues ONE coalesced 128-B load for the next (consumed only at the slide after, so its
+  // latency is off the producer's path).  r01's per-lane local-memory table cost every stage
+  // dependent local-memory round trips and every 32 pages a 32-entry spill per lane.
   const int32_t* row;
-  int heads_kv, h, shift, base;
-  int32_t e[32];
+  int heads_kv, h, shift, base, n;
+  int32_t e0, e1;
+  __device__ __forceinline__ int32_t ld(int i) const { return i < n ? __ldg(row + i) : 0; }
   __device__ __forceinline__ void init(const DecodeArgs& a, int64_t unit_bh) {
     const int b = int(unit_bh / a.heads_kv);
     h = int(unit_bh % a.heads_kv);
     row = a.block_table + size_t(b) * a.pt_stride;
+    n = a.pt_stride;
     heads_kv = a.heads_kv;
     shift = a.page_shift;
     base = -1;
   }
-  __device__ __forceinline__ int64_t row_of(int t) {  // pool row of the unit's token t
-    const int pi = t >> shift;
-    if (base < 0 || pi < base || pi >= base + 32) {
-      base = pi & ~31;
-      const int4* src = reinterpret_cast<const int4*>(row + base);
-      int4 w[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) w[k] = __ldg(src + k);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        e[4 * k] = w[k].x;
-        e[4 * k + 1] = w[k].y;
-        e[4 * k + 2] = w[k].z;
-        e[4 * k + 3] = w[k].w;
-      }
+  // Whole warp (converged).  p0: the stage's first page (warp-uniform); t: this lane's token
+  // (any value for an idle lane: its result is garbage but harmless).  Pool row of token t.
+  __device__ __forceinline__ int64_t rows(int p0, int t, int lane) {
+    if (base < 0 || p0 < base || p0 >= base + 64) {  // (re)load both halves around p0
+      base = p0 & ~31;
+      e0 = ld(base + lane);
+      e1 = ld(base + 32 + lane);
+    } else if (p0 >= base + 32) {                    // slide by 32: the next half is prefetched
+      base += 32;
+      e0 = e1;
+      e1 = ld(base + 32 + lane);
     }
-    return (int64_t(e[pi - base]) * heads_kv + h) * (int64_t(1) << shift) + (t & ((1 << shift) - 1));
+    const int pi = (t >> shift) - base;              // in [0, 64) for the stage's tokens
+    const int32_t lo = __shfl_sync(0xffffffffu, e0, pi & 31), hi = __shfl_sync(0xffffffffu, e1, pi & 31);
+    const int32_t pg = pi < 32 ? lo : hi;
+    return (int64_t(pg) * heads_kv + h) * (int64_t(1) << shift) + (t & ((1 << shift) - 1));
   }
 };
 
@@ -341,9 +348,10 @@ struct MhaEngine {
     const int page = 1 << a.page_shift;
     const int first = s0 & ~(page - 1);
     const int t = lane == 0 ? s0 : first + lane * page;
+    const int64_t prow = pw.rows(s0 >> a.page_shift, t, lane);  // whole warp
     if (t < s0 + ntok) {
       const int run = min(first + (lane + 1) * page, s0 + ntok) - t;
-      const size_t goff = size_t(pw.row_of(t)) * ROWB;
+      const size_t goff = size_t(prow) * ROWB;
       const int doff = (t - s0) * ROWB;
       bulk_g2s(dst + doff, static_cast<const unsigned char*>(a.k) + goff, uint32_t(run) * ROWB, bar, pol);
       bulk_g2s(dst + STAGE_TOK * ROWB + doff, static_cast<const unsigned char*>(a.v) + goff, uint32_t(run) * ROWB,
@@ -572,14 +580,18 @@ struct GqaEngine {
     const int nb = (ntok + br - 1) / br;
     if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * NBOX * 2));
     __syncwarp();
-    for (int task = lane; task < nb * 2; task += 32) {
-      const int i = task >> 1, is_v = task & 1;
-      const int row = int(pw.row_of(s0 + i * br));
-      unsigned char* d = dst + (is_v ? KV_BYTES : 0) + i * br * 128 * NBOX;
-      if (NBOX == 1)
-        tma_load_2d(d, is_v ? &tm.v : &tm.k, 0, row, bar, pol);
-      else
-        tma_load_3d(d, is_v ? &tm.v : &tm.k, 0, row, 0, bar, pol);
+    {  // lane i: box i (<= 8), its K and V loads (one row coordinate for both)
+      const int i = lane;
+      const int row = int(pw.rows(s0 >> a.page_shift, s0 + i * br, lane));  // whole warp
+      if (i >= nb) return;
+      unsigned char* d = dst + i * br * 128 * NBOX;
+      if (NBOX == 1) {
+        tma_load_2d(d, &tm.k, 0, row, bar, pol);
+        tma_load_2d(d + KV_BYTES, &tm.v, 0, row, bar, pol);
+      } else {
+        tma_load_3d(d, &tm.k, 0, row, 0, bar, pol);
+        tma_load_3d(d + KV_BYTES, &tm.v, 0, row, 0, bar, pol);
+      }
     }
   }
 
@@ -802,10 +814,13 @@ struct Fp8Engine {
     const int nb = (ntok + br - 1) / br;
     if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * 2));
     __syncwarp();
-    for (int task = lane; task < nb * 2; task += 32) {
-      const int i = task >> 1, is_v = task & 1;
-      const int row = int(pw.row_of(s0 + i * br));
-      tma_load_2d(dst + (is_v ? KV_BYTES : 0) + i * br * 128, is_v ? &tm.v : &tm.k, 0, row, bar, pol);
+    {  // lane i: box i (<= 8), its K and V loads (one row coordinate for both)
+      const int i = lane;
+      const int row = int(pw.rows(s0 >> a.page_shift, s0 + i * br, lane));  // whole warp
+      if (i < nb) {
+        tma_load_2d(dst + i * br * 128, &tm.k, 0, row, bar, pol);
+        tma_load_2d(dst + KV_BYTES + i * br * 128, &tm.v, 0, row, bar, pol);
+      }
     }
   }
 
@@ -1134,11 +1149,15 @@ struct Tc5Engine {
       mbar_arrive_expect_tx(vbar, uint32_t(nb * br * 128 * 2));
     }
     __syncwarp();
-    for (int task = lane; task < nb * 4; task += 32) {
-      const int i = task >> 2, half = (task >> 1) & 1, is_v = task & 1;
-      const int row = int(pw.row_of(s0 + i * br));
-      tma_load_3d(dst + (is_v ? KV_BYTES : 0) + half * 16384 + i * br * 128, is_v ? &tm.v : &tm.k, 0, row, half,
-                  is_v ? vbar : bar, pol);
+    {  // lane i: box i (<= 8), both halves of its K and V (one row coordinate for all four)
+      const int i = lane;
+      const int row = int(pw.rows(s0 >> a.page_shift, s0 + i * br, lane));  // whole warp
+      if (i >= nb) return;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        tma_load_3d(dst + half * 16384 + i * br * 128, &tm.k, 0, row, half, bar, pol);
+        tma_load_3d(dst + KV_BYTES + half * 16384 + i * br * 128, &tm.v, 0, row, half, vbar, pol);
+      }
     }
   }
 
@@ -1559,7 +1578,9 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
     mbar_wait(&fold_full[b], (seg / kFB) & 1);
     const SegInfo si = seginfo[b];
     if (si.unit < 0) break;
+#ifndef LA_PROF
     if (tr && lane == 0) tr[TR_STREAM] = globaltimer();  // the consumers finished this segment
+#endif
     const float* fb = fold + b * FOLD_FLOATS;
     const DevUnit u = a.units[si.unit];
     const int v = si.v;
@@ -1930,6 +1951,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     const int win = a.win > 0 ? min(a.win, E::WIN) : E::WIN;  // stages in flight
 #ifdef LA_PROF
     long long prof_pwait = 0;  // producer cycles waiting for free slots -> trace field smid
+    long long prof_issue = 0;  // paged: cycles in produce_paged -> trace field t_stream_end
 #endif
     constexpr int QB = Smem<E>::QB;
     const int q_el = int(sizeof(typename E::QElem));
@@ -2052,7 +2074,14 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
               if (lane == 0) E::produce(ring + slot * E::STAGE_BYTES, a, tm, row0 + s0, ntok, &full[slot], pol);
             }
           } else {
+#ifdef LA_PROF
+            const long long ci = clock64();
+#endif
             E::produce_paged(ring + slot * E::STAGE_BYTES, a, tm, pw, s0, ntok, &full[slot], pol, lane);
+#ifdef LA_PROF
+            __syncwarp();
+            if (lane == 0) prof_issue += clock64() - ci;
+#endif
           }
           ++j;
         }
@@ -2084,7 +2113,10 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     // j - 1, the ring is idle (a dynamic last arriver may stage its fold there)
     if (lane == 0) *reinterpret_cast<volatile int*>(prod_j) = j;
 #ifdef LA_PROF
-    if (tr && lane == 0) tr[TR_SMID] = prof_pwait;
+    if (tr && lane == 0) {
+      tr[TR_SMID] = prof_pwait;
+      tr[TR_STREAM] = prof_issue;
+    }
 #endif
     return;
   }
@@ -2373,8 +2405,10 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
       const SegInfo si = seginfo[b];
       if (si.unit < 0) break;
       if (tr && lane == 0) {
+#ifndef LA_PROF
         tr[TR_STREAM] = globaltimer();                 // the consumers finished this segment
-        if (dynamic) tr[TR_PUBLISH] = tr[TR_STREAM];   // dynamic: the last segment taken
+#endif
+        if (dynamic) tr[TR_PUBLISH] = globaltimer();   // dynamic: the last segment taken
       }
       // ---- fold the consumer warps' partials of this segment ------------------------------
       const float* fb = fold + b * FOLD_FLOATS;
