@@ -94,3 +94,18 @@ def test_calibrate_full_size(cfg, engine):
         gate(O[b, 8 * h:8 * h + 8], L[b, 8 * h:8 * h + 8], O_ref, L_ref, what=f"{cfg} calibrated b{b} h{h}")
     plan.set_weights(None)
     assert plan.info.sm_weighted == 0 and plan.range_lengths().max() - plan.range_lengths().min() <= 1
+
+
+def test_calibrate_rejects_dynamic_and_exchange_plans():
+    import paper_2405_10480_b200 as la
+    p = synth.Problem(1, 4, 4, 128, [5000], dtype="bf16", dist="D1", seed=73)
+    q, k, v = cuda_inputs(p)
+    for kw in (dict(schedule="dynamic"), dict(schedule="streamk", xchg_world=2, xchg_rank=0)):
+        plan = la.Plan(1, 4, 4, 128, [5000], **kw)
+        with pytest.raises(la.LaError) as e:
+            plan.calibrate(q, k, v, launches=1, rounds=1)
+        assert e.value.status == la.LA_ERR_STATE, kw
+    plan = la.Plan(1, 4, 4, 128, [5000], schedule="streamk")
+    with pytest.raises(la.LaError) as e:
+        plan.calibrate(q, k, v, launches=0, rounds=1)
+    assert e.value.status == la.LA_ERR_INVALID
