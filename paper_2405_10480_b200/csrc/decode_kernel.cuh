@@ -124,6 +124,9 @@
 #define LA_MHA_WIN 0    // MHA engine: stages in flight (0: the whole ring; 4 measured within noise for
                         // c2 stream-K, slower dynamic (582 -> 586 us) and paged (620 -> 649 us); 3: 630 us)
 #endif
+#ifndef LA_PAGED_ELECT
+#define LA_PAGED_ELECT 1  // paged GQA / tcgen05 producers: loads issued by an elected lane of the converged warp
+#endif
 #ifndef LA_FP8_WIN
 #define LA_FP8_WIN 0    // FP8 engine: stages in flight (0: the whole ring; 4 measured slower: c2 304 -> 319 us)
 #endif
@@ -349,7 +352,19 @@ struct MhaEngine {
     const int first = s0 & ~(page - 1);
     const int t = lane == 0 ? s0 : first + lane * page;
     const int64_t prow = pw.rows(s0 >> a.page_shift, t, lane);  // whole warp
-    if (t < s0 + ntok) {
+    if constexpr (LA_PAGED_ELECT > 1) {  // (measured slower for 1-D bulk copies: c2 page 16 628 -> 672 us)
+      const int nrun = ((s0 + ntok - 1) >> a.page_shift) - (s0 >> a.page_shift) + 1;  // pages in the stage
+      #pragma unroll 1
+      for (int r = 0; r < nrun; ++r) {  // converged warp, one elected lane copies run r
+        const int tr = __shfl_sync(0xffffffffu, t, r);
+        const int64_t pr = __shfl_sync(0xffffffffu, prow, r);
+        const int run = min(first + (r + 1) * page, s0 + ntok) - tr;
+        const size_t goff = size_t(pr) * ROWB;
+        const int doff = (tr - s0) * ROWB;
+        bulk_g2s_kv_elect(dst + doff, dst + STAGE_TOK * ROWB + doff, static_cast<const unsigned char*>(a.k) + goff,
+                          static_cast<const unsigned char*>(a.v) + goff, uint32_t(run) * ROWB, bar, pol);
+      }
+    } else if (t < s0 + ntok) {
       const int run = min(first + (lane + 1) * page, s0 + ntok) - t;
       const size_t goff = size_t(prow) * ROWB;
       const int doff = (t - s0) * ROWB;
@@ -505,6 +520,33 @@ struct Mma<__half> {
   }
 };
 
+// Whole (converged) warp: one elected lane issues the 3-D box loads of K and V at the same
+// coordinates (paged producers: the operands are warp-uniform, so ptxas needs no per-lane
+// waterfall loop around the instructions)
+__device__ __forceinline__ void tma_load_3d_kv_elect(void* dk, void* dv, const CUtensorMap* tk, const CUtensorMap* tv,
+                                                     int c1, int c2, uint64_t* bk, uint64_t* bv, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+      "@pe cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%2, {0, %4, %5}], [%6], %8;\n\t"
+      "@pe cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%1], [%3, {0, %4, %5}], [%7], %8;\n\t}" ::"r"(smem_u32(dk)),
+      "r"(smem_u32(dv)), "l"(reinterpret_cast<uint64_t>(tk)), "l"(reinterpret_cast<uint64_t>(tv)), "r"(c1), "r"(c2),
+      "r"(smem_u32(bk)), "r"(smem_u32(bv)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_kv_elect(void* dk, void* dv, const CUtensorMap* tk, const CUtensorMap* tv,
+                                                     int c1, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+      "@pe cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%2, {0, %4}], [%5], %6;\n\t"
+      "@pe cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%1], [%3, {0, %4}], [%5], %6;\n\t}" ::"r"(smem_u32(dk)),
+      "r"(smem_u32(dv)), "l"(reinterpret_cast<uint64_t>(tk)), "l"(reinterpret_cast<uint64_t>(tv)), "r"(c1),
+      "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar,
                                             uint64_t policy) {
   asm volatile(
@@ -580,17 +622,21 @@ struct GqaEngine {
     const int nb = (ntok + br - 1) / br;
     if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * NBOX * 2));
     __syncwarp();
-    {  // lane i: box i (<= 8), its K and V loads (one row coordinate for both)
-      const int i = lane;
-      const int row = int(pw.rows(s0 >> a.page_shift, s0 + i * br, lane));  // whole warp
-      if (i >= nb) return;
-      unsigned char* d = dst + i * br * 128 * NBOX;
+    const int rowl = int(pw.rows(s0 >> a.page_shift, s0 + lane * br, lane));  // whole warp: lane i -> box i
+    if constexpr (NBOX == 2 && LA_PAGED_ELECT) {
+      #pragma unroll 1
+      for (int i = 0; i < nb; ++i) {  // converged warp, one elected lane issues (warp-uniform operands)
+        unsigned char* d = dst + i * br * 128 * NBOX;
+        tma_load_3d_kv_elect(d, d + KV_BYTES, &tm.k, &tm.v, __shfl_sync(0xffffffffu, rowl, i), 0, bar, bar, pol);
+      }
+    } else if (lane < nb) {  // lane i: box i (<= 8), its K and V loads (one row coordinate for both)
+      unsigned char* d = dst + lane * br * 128 * NBOX;
       if (NBOX == 1) {
-        tma_load_2d(d, &tm.k, 0, row, bar, pol);
-        tma_load_2d(d + KV_BYTES, &tm.v, 0, row, bar, pol);
+        tma_load_2d(d, &tm.k, 0, rowl, bar, pol);
+        tma_load_2d(d + KV_BYTES, &tm.v, 0, rowl, bar, pol);
       } else {
-        tma_load_3d(d, &tm.k, 0, row, 0, bar, pol);
-        tma_load_3d(d + KV_BYTES, &tm.v, 0, row, 0, bar, pol);
+        tma_load_3d(d, &tm.k, 0, rowl, 0, bar, pol);
+        tma_load_3d(d + KV_BYTES, &tm.v, 0, rowl, 0, bar, pol);
       }
     }
   }
@@ -814,13 +860,16 @@ struct Fp8Engine {
     const int nb = (ntok + br - 1) / br;
     if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(nb * br * 128 * 2));
     __syncwarp();
-    {  // lane i: box i (<= 8), its K and V loads (one row coordinate for both)
-      const int i = lane;
-      const int row = int(pw.rows(s0 >> a.page_shift, s0 + i * br, lane));  // whole warp
-      if (i < nb) {
-        tma_load_2d(dst + i * br * 128, &tm.k, 0, row, bar, pol);
-        tma_load_2d(dst + KV_BYTES + i * br * 128, &tm.v, 0, row, bar, pol);
+    const int rowl = int(pw.rows(s0 >> a.page_shift, s0 + lane * br, lane));  // whole warp: lane i -> box i
+    if constexpr (LA_PAGED_ELECT) {
+      #pragma unroll 1
+      for (int i = 0; i < nb; ++i) {  // converged warp, one elected lane issues (warp-uniform operands)
+        const int row = __shfl_sync(0xffffffffu, rowl, i);
+        tma_load_2d_kv_elect(dst + i * br * 128, dst + KV_BYTES + i * br * 128, &tm.k, &tm.v, row, bar, pol);
       }
+    } else if (lane < nb) {  // lane i: box i (<= 8), its K and V loads (one row coordinate for both)
+      tma_load_2d(dst + lane * br * 128, &tm.k, 0, rowl, bar, pol);
+      tma_load_2d(dst + KV_BYTES + lane * br * 128, &tm.v, 0, rowl, bar, pol);
     }
   }
 
@@ -1149,14 +1198,21 @@ struct Tc5Engine {
       mbar_arrive_expect_tx(vbar, uint32_t(nb * br * 128 * 2));
     }
     __syncwarp();
-    {  // lane i: box i (<= 8), both halves of its K and V (one row coordinate for all four)
-      const int i = lane;
-      const int row = int(pw.rows(s0 >> a.page_shift, s0 + i * br, lane));  // whole warp
-      if (i >= nb) return;
+    const int rowl = int(pw.rows(s0 >> a.page_shift, s0 + lane * br, lane));  // whole warp: lane i -> box i
+    if constexpr (LA_PAGED_ELECT) {
+      #pragma unroll 1
+      for (int i = 0; i < nb; ++i) {  // converged warp, one elected lane issues (warp-uniform operands)
+        const int row = __shfl_sync(0xffffffffu, rowl, i);
+#pragma unroll
+        for (int half = 0; half < 2; ++half)
+          tma_load_3d_kv_elect(dst + half * 16384 + i * br * 128, dst + KV_BYTES + half * 16384 + i * br * 128, &tm.k,
+                               &tm.v, row, half, bar, vbar, pol);
+      }
+    } else if (lane < nb) {  // lane i: box i (<= 8), both halves of its K and V
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        tma_load_3d(dst + half * 16384 + i * br * 128, &tm.k, 0, row, half, bar, pol);
-        tma_load_3d(dst + KV_BYTES + half * 16384 + i * br * 128, &tm.v, 0, row, half, vbar, pol);
+        tma_load_3d(dst + half * 16384 + lane * br * 128, &tm.k, 0, rowl, half, bar, pol);
+        tma_load_3d(dst + KV_BYTES + half * 16384 + lane * br * 128, &tm.v, 0, rowl, half, vbar, pol);
       }
     }
   }

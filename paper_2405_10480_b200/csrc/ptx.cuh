@@ -54,6 +54,19 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 }
 
 // 1-D TMA bulk copy global -> shared, completion counted in bytes on `bar`.
+// Whole (converged) warp: one elected lane copies the same byte range of K and V (paged
+// producers: warp-uniform operands, no per-lane waterfall loop around the copies)
+__device__ __forceinline__ void bulk_g2s_kv_elect(void* dk, void* dv, const void* sk, const void* sv, uint32_t bytes,
+                                                  uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+      "@pe cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%2], %4, [%5], %6;\n\t"
+      "@pe cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%1], [%3], %4, [%5], %6;\n\t}" ::"r"(smem_u32(dk)),
+      "r"(smem_u32(dv)), "l"(sk), "l"(sv), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
   asm volatile(
