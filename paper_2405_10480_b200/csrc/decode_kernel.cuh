@@ -124,6 +124,10 @@
 #define LA_MHA_WIN 0    // MHA engine: stages in flight (0: the whole ring; 4 measured within noise for
                         // c2 stream-K, slower dynamic (582 -> 586 us) and paged (620 -> 649 us); 3: 630 us)
 #endif
+#ifndef LA_ELECT_PRODUCE
+#define LA_ELECT_PRODUCE 1  // tcgen05 8-row tiles (BHSD / packed): stage loads issued by an elected lane of the
+                            // warp (measured equal to lane-0 issue: 305.0 vs 305.0 us; kept for one issue path)
+#endif
 #ifndef LA_PAGED_ELECT
 #define LA_PAGED_ELECT 1  // paged GQA / tcgen05 producers: loads issued by an elected lane of the converged warp
 #endif
@@ -533,6 +537,19 @@ __device__ __forceinline__ void tma_load_3d_kv_elect(void* dk, void* dv, const C
       " [%1], [%3, {0, %4, %5}], [%7], %8;\n\t}" ::"r"(smem_u32(dk)),
       "r"(smem_u32(dv)), "l"(reinterpret_cast<uint64_t>(tk)), "l"(reinterpret_cast<uint64_t>(tv)), "r"(c1), "r"(c2),
       "r"(smem_u32(bk)), "r"(smem_u32(bv)), "l"(policy)
+      : "memory");
+}
+// Whole (converged) warp: one elected lane loads both 128-B halves (coordinate 2 = 0, 1) of
+// one tensor's rows into dst and dst + 16 KiB
+__device__ __forceinline__ void tma_load_3d_halves_elect(void* dst, const CUtensorMap* tm, int c1, uint64_t* bar,
+                                                         uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+      "@pe cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%2, {0, %3, 0}], [%4], %5;\n\t"
+      "@pe cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%1], [%2, {0, %3, 1}], [%4], %5;\n\t}" ::"r"(smem_u32(dst)),
+      "r"(smem_u32(dst) + 16384u), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_kv_elect(void* dk, void* dv, const CUtensorMap* tk, const CUtensorMap* tv,
@@ -1157,6 +1174,21 @@ struct Tc5Engine {
     for (int s = 0; s < NST; ++s) mbar_init(vbar_of(s), 1);
   }
 
+  // Whole producer warp: K on the full barrier, then (after stage j - VWIN is consumed: vwait)
+  // V on the slot's barrier, each pair of half boxes issued by one elected lane.
+  __device__ __forceinline__ static void produce_w(unsigned char* dst, const TmapPair& tm, int64_t row, uint64_t* bar,
+                                                   uint64_t pol, int lane, uint64_t* vwait, uint32_t vpar) {
+    static_assert(BOX_HALVES == 1, "half boxes");
+    const int slot = int((dst - (extra() - NST * STAGE_BYTES)) / STAGE_BYTES);
+    uint64_t* vbar = vbar_of(slot);
+    if (lane == 0) mbar_arrive_expect_tx(bar, KV_BYTES);
+    __syncwarp();
+    tma_load_3d_halves_elect(dst, &tm.k, int(row), bar, pol);
+    if (vwait) mbar_wait(vwait, vpar);
+    if (lane == 0) mbar_arrive_expect_tx(vbar, KV_BYTES);
+    __syncwarp();
+    tma_load_3d_halves_elect(dst + KV_BYTES, &tm.v, int(row), vbar, pol);
+  }
   __device__ __forceinline__ static void produce_k(unsigned char* dst, const TmapPair& tm, int64_t row, uint64_t* bar,
                                                    uint64_t pol) {
     mbar_arrive_expect_tx(bar, KV_BYTES);
@@ -2120,7 +2152,11 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 #endif
           const int ntok = min(a.stage_tokens, t1 - s0);
           if (!a.paged) {
-            if constexpr (EngX<E>::VWIN < E::WIN) {  // (tcgen05) K now, V once stage j - VWIN is consumed
+            if constexpr (EngX<E>::VWIN < E::WIN && LA_ELECT_PRODUCE) {  // (tcgen05) K now, V after stage j - VWIN;
+              // the whole warp issues (one elected lane, warp-uniform operands)
+              E::produce_w(ring + slot * E::STAGE_BYTES, tm, row0 + s0, &full[slot], pol, lane,
+                           j >= E::VWIN ? &empty[(j - E::VWIN) % NST] : nullptr, ((j - E::VWIN) / NST) & 1);
+            } else if constexpr (EngX<E>::VWIN < E::WIN) {
               if (lane == 0) {
                 E::produce_k(ring + slot * E::STAGE_BYTES, tm, row0 + s0, &full[slot], pol);
                 if (j >= E::VWIN) mbar_wait(&empty[(j - E::VWIN) % NST], ((j - E::VWIN) / NST) & 1);
