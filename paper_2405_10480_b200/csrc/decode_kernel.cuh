@@ -124,6 +124,9 @@
 #define LA_MHA_WIN 0    // MHA engine: stages in flight (0: the whole ring; 4 measured within noise for
                         // c2 stream-K, slower dynamic (582 -> 586 us) and paged (620 -> 649 us); 3: 630 us)
 #endif
+#ifndef LA_TC5_LD32
+#define LA_TC5_LD32 1  // tcgen05 16/32-row tiles: 32-column TMEM loads (fewer load round trips)
+#endif
 #ifndef LA_ELECT_PRODUCE
 #define LA_ELECT_PRODUCE 1  // tcgen05 8-row tiles (BHSD / packed): stage loads issued by an elected lane of the
                             // warp (measured equal to lane-0 issue: 305.0 vs 305.0 us; kept for one issue path)
@@ -1337,6 +1340,9 @@ struct Tc5Engine {
     tc5::fence_after();
     TC5_CK(2);
     float sc[QR];
+    if constexpr (QR == 32 && SPLIT == 1 && LA_TC5_LD32) {  // one TMEM round trip for the 32 columns
+      tc5::ld32(tbase + tlane, sc);
+    } else
 #pragma unroll
     for (int c = 0; c < QR; c += 16) {
       float t16[16];
@@ -1488,6 +1494,33 @@ struct Tc5Engine {
     tc5::fence_after();
     // alpha from shared memory, 8 rows at a time (no registers held across the MMA)
     // O^T tile: column h = V^T P_hi row h, column HEADS + h = V^T P_lo row h (per chain)
+    if constexpr (HEADS >= 16 && SPLIT == 1 && LA_TC5_LD32) {  // 32-column loads: 1 (16 rows) / 2 (32 rows)
+      // TMEM round trips instead of 4 / 8; o[h] = alpha_h o[h] + (hi_h + lo_h) as below
+#pragma unroll
+      for (int c0 = 0; c0 < HEADS; c0 += 16) {
+        float hl[32];
+        if constexpr (HEADS == 16) {
+          tc5::ld32(tbase + tlane + OC, hl);  // hi 0-15, lo 16-31
+        } else {                            // rows c0 .. c0 + 15: hi columns c0.., lo columns 32 + c0..
+          float t16[16];
+          tc5::ld16(tbase + tlane + OC + c0, t16);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) hl[i] = t16[i];
+          tc5::ld16(tbase + tlane + OC + HEADS + c0, t16);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) hl[16 + i] = t16[i];
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+          const float4 a = lds_f32x4(alp + 4 * (c0 + q));
+          const float al[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) s.o[c0 + q + i] = fmaf(al[i], s.o[c0 + q + i], hl[q + i] + hl[16 + q + i]);
+        }
+      }
+      tc5::fence_before();
+      return;
+    }
 #pragma unroll
     for (int c0 = 0; c0 < HEADS; c0 += 8) {  // 8 rows at a time: hi columns c0.., lo columns HEADS + c0..
       float hv[8], lv[8];

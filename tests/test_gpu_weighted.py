@@ -109,3 +109,30 @@ def test_calibrate_rejects_dynamic_and_exchange_plans():
     with pytest.raises(la.LaError) as e:
         plan.calibrate(q, k, v, launches=0, rounds=1)
     assert e.value.status == la.LA_ERR_INVALID
+
+
+@pytest.mark.parametrize("layout,dtype", [("paged", "bf16"), ("bhsd", "fp8"), ("packed", "bf16")])
+def test_random_weights_other_layouts(layout, dtype):
+    """Weighted ranges on a paged pool (tcgen05 engine under AUTO), an FP8 cache and a packed
+    ragged cache: oracle-gated and bitwise reproducible."""
+    import paper_2405_10480_b200 as la
+    kw = dict(page_size=16) if layout == "paged" else {}
+    p = synth.Problem(3, 16, 2, 128, [3000, 517, 2048], dtype=dtype, dist="D2", seed=74, layout=layout, **kw)
+    O_ref, L_ref = run_oracle(p)
+    q, k, v = cuda_inputs(p)
+    extra = {}
+    if layout == "paged":
+        bt, num_pages = synth.paged_meta(p)
+        extra = dict(block_table=bt, page_size=16, num_pages=num_pages)
+    if dtype == "fp8":
+        extra.update(k_scale=p.k_scale, v_scale=p.v_scale)
+    rng = np.random.default_rng(11)
+    for grid, tile_n in ((0, 64), (9, 128)):
+        plan = _plan(la, p, grid=grid, tile_n=tile_n, **extra)
+        plan.set_weights(rng.integers(1, 1 << 20, size=plan.info.grid))
+        out, lse = plan.decode(q, k, v)
+        torch.cuda.synchronize()
+        plan.status()
+        gate(out.cpu().numpy(), lse.cpu().numpy(), O_ref, L_ref, what=f"weighted {layout}/{dtype} G{grid} T{tile_n}")
+        ref = out.clone()
+        assert torch.equal(plan.decode(q, k, v)[0], ref)
