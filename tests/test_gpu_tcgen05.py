@@ -212,3 +212,16 @@ def test_tcgen05_tiny_contexts(rows_per_head):
     O, L, plan = run_cuda(p2, causal=True, **TC5)
     assert plan.info.tile_rows == g
     gate(O, L, O_ref, L_ref, what=f"tc5 tiny Nq2 g{g // 2}")
+
+
+@pytest.mark.parametrize("q_len,n,grid,tile_n", [(4, 40000, 0, 128), (4, 40000, 37, 128), (2, 9000, 0, 32),
+                                                 (4, 2000, 148, 16)])
+def test_tcgen05_wide_tiles_many_peers(q_len, n, grid, tile_n):
+    """One 16 / 32-row unit spread over up to 148 CTAs: the host's peer partials exceed the idle
+    ring (147 peers x 32 rows), so its fold takes the per-row-group staging path, while units
+    spread over few CTAs stage every peer at once -- both against the oracle."""
+    p = synth.Problem(1, 8, 1, 128, [n], dtype="bf16", dist="D2", seed=75, q_len=q_len)
+    O_ref, L_ref = run_oracle(p)
+    O, L, plan = run_cuda(p, tile_n=tile_n, grid=grid, **TC5)
+    assert plan.info.tile_rows == 8 * q_len and plan.info.num_units == 1
+    gate(O, L, O_ref, L_ref, what=f"tc5 wide many peers Nq{q_len} n{n} G{plan.info.grid} T{tile_n}")
