@@ -124,6 +124,9 @@
 #define LA_MHA_WIN 0    // MHA engine: stages in flight (0: the whole ring; 4 measured within noise for
                         // c2 stream-K, slower dynamic (582 -> 586 us) and paged (620 -> 649 us); 3: 630 us)
 #endif
+#ifndef LA_TC5_QSTAGE8
+#define LA_TC5_QSTAGE8 1  // tcgen05 8-row tiles: Q rows staged per segment by the producer (2-deep queue)
+#endif
 #ifndef LA_TC5_LD32
 #define LA_TC5_LD32 1  // tcgen05 16/32-row tiles: 32-column TMEM loads (fewer load round trips)
 #endif
@@ -1121,7 +1124,11 @@ struct Tc5Engine {
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
   using QElem = T;
-  static constexpr bool QSTAGE = false;             // no smem left next to the 64 KiB ring slots: Q from global
+  // 8-row tiles: the producer stages each segment's Q rows in shared memory (2 KiB per queue
+  // entry, a 2-deep queue fits next to the ring) so a warpgroup's segment start reads no global
+  // memory; wider tiles read Q from global (no room next to their bigger per-warpgroup state)
+  static constexpr bool QSTAGE = HEADS == 8 && LA_TC5_QSTAGE8;
+  static constexpr int QD = QSTAGE ? 2 : 4;
   // accumulator chains per contraction (1 or 2).  LA_TC5_SPLIT = 2 applies to 8-row tiles only:
   // at 16 / 32 rows it fails a wide-tile parity test and measured slower (32 rows: 383 vs 368 us)
   static constexpr int SPLIT = HEADS == 8 ? LA_TC5_SPLIT : 1;
@@ -1592,7 +1599,8 @@ struct Tc5Engine {
 // =======================================================================================
 // The persistent decode kernel
 // =======================================================================================
-constexpr int kQD = 4;   // depth of the producer -> consumer virtual-CTA queue
+// depth of the producer -> consumer virtual-CTA queue: EngX<E>::QD (4; the tcgen05 8-row
+// engine stages its segments' Q rows in shared memory with a 2-deep queue)
 constexpr int kClaimAhead = 4;  // dynamic: LeanTiles before a piece's end at which the next claim is taken
 
 // One segment (one LeanTile() call, Alg2§11-18) handed from the producer to the consumer
@@ -1613,12 +1621,12 @@ struct SegInfo {
 // the ring and fewer fold rows per slot; the others get the neutral values.
 template <class E, class = void>
 struct EngX {
-  static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS, VWIN = 1 << 20;
+  static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS, VWIN = 1 << 20, QD = 4;
   static constexpr bool GF = false;  // fold buffers in global scratch (DecodeArgs::gfold)
 };
 template <class E>
 struct EngX<E, std::void_t<decltype(E::TMEM_COLS)>> {
-  static constexpr int TMEM = E::TMEM_COLS, EXTRA = E::EXTRA_BYTES, FW = E::FOLD_WPS, VWIN = E::VWIN;
+  static constexpr int TMEM = E::TMEM_COLS, EXTRA = E::EXTRA_BYTES, FW = E::FOLD_WPS, VWIN = E::VWIN, QD = E::QD;
   static constexpr bool GF = E::GLOBAL_FOLD;
 };
 
@@ -1628,6 +1636,7 @@ struct Smem {
   static constexpr int EXTRA = EngX<E>::EXTRA;  // engine state right after the ring
   static constexpr int kFB = E::FOLD_BUFS;  // consumer -> epilogue fold buffers
   static constexpr int FOLD = EngX<E>::GF ? 0 : kFB * E::FOLD_FLOATS * 4;
+  static constexpr int kQD = EngX<E>::QD;
   static constexpr int BARS = (2 * E::NST + 2 * kQD + 4 * kFB + 1) * 8;
   // segment queue, hand-off records, prod_j; then the segments' Q rows (TMA bulk copies)
   static constexpr int SQ_OFF = (RING + EXTRA + FOLD + BARS + 15) / 16 * 16;
@@ -1991,6 +2000,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   constexpr int FW = EngX<E>::FW;  // fold rows per ring slot (WPS, or 1 for a warpgroup engine)
   constexpr int FOLD_FLOATS = E::FOLD_FLOATS;
   constexpr int kFB = E::FOLD_BUFS;
+  constexpr int kQD = EngX<E>::QD;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* ring =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -2784,6 +2794,7 @@ KernelInfo info_of(bool tma) {
   KernelInfo k;
   k.supported = true;
   k.threads = (E::NCW + 2) * 32;
+  static_assert(Smem<E>::BYTES <= 232448, "dynamic shared memory exceeds 227 KiB per block");
   k.smem_bytes = Smem<E>::BYTES;
   k.stage_tokens_max = E::STAGE_TOK;
   k.uses_tma_tensor = tma;
