@@ -167,8 +167,8 @@ typedef enum {
                              with S^T and the per-stage O^T in TMEM (N up to 32 / 64), read back by
                              tcgen05.ld; query tiles of up to 32 rows (T_m)                 */
   LA_ENGINE_AUTO = 2      /* tcgen05 where g * N_q > 8 rows per KV head (one KV pass instead
-                             of two) or the cache is a paged pool, and it applies (bf16 / fp16,
-                             d = 128, static schedule); mma.sync otherwise                  */
+                             of two) and it applies (bf16 / fp16, d = 128, static schedule);
+                             mma.sync otherwise                                              */
 } la_engine;
 
 typedef struct la_plan_s* la_plan_t;

@@ -370,17 +370,17 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   p.q_len = uniform ? p.q_lens[0] : 0;
   // Engine for T_m > 1 tiles.  AUTO takes tcgen05 exactly where it wins (measured):
   // more than 8 rows per KV head (g * N_q > 8), which its N = 16 MMAs cover in one pass over
-  // the cache where mma.sync tiles need two, and paged pools; otherwise mma.sync (equal
-  // within box noise on a BHSD / packed cache, with a smaller run-to-run spread).
+  // the cache where mma.sync tiles need two; otherwise mma.sync (equal within box noise, with
+  // a smaller run-to-run spread).
   if (opts.engine != LA_ENGINE_MMA_SYNC && opts.engine != LA_ENGINE_TCGEN05 && opts.engine != LA_ENGINE_AUTO)
     return fail(LA_ERR_INVALID, "engine must be LA_ENGINE_AUTO, LA_ENGINE_MMA_SYNC or LA_ENGINE_TCGEN05");
   const bool tc5_ok = head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16);
   // AUTO resolves to stream-K for multi-row tiles (below), so it admits the wide tcgen05 tiles
   const bool static_sched = opts.schedule == LA_SCHED_STREAMK || opts.schedule == LA_SCHED_SEQUENTIAL ||
                             opts.schedule == LA_SCHED_AUTO;
-  // (r02: also on paged pools, where its elected-lane page-box loads keep the producer ahead --
-  // c3 page 16 / 64 / 256: 323 / 317 / 314 us vs mma.sync 331 / 321 / 315 us on one box)
-  const bool tc5_wins = max_rows > 8 || opts.layout == LA_KV_PAGED;
+  // (paged pools: box-dependent -- c3 page 16 tcgen05 323 vs mma.sync 331 us on one box, 338 vs
+  // 332 us on two others, page 64 equal -- so the rule stays the row count)
+  const bool tc5_wins = max_rows > 8;
   const int engine = opts.engine != LA_ENGINE_AUTO ? opts.engine
                      : (tc5_wins && tc5_ok && static_sched ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
   // T_m: 1 -> CUDA-core engine, else tensor-core tiles of <= 8 rows (mma.sync: N = 8), or
