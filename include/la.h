@@ -149,8 +149,8 @@ typedef struct {
   float v_scale;              /* V = code x v_scale (applied once, at finalize: O x v_scale)  */
   /* Tensor-core engine for T_m > 1 tiles (GQA groups / N_q > 1; MHA always runs on CUDA cores): */
   int engine;                 /* la_engine, default LA_ENGINE_AUTO.  LA_ENGINE_TCGEN05 needs
-                                 bf16 / fp16 and head_dim 128 when T_m > 1, and on an exchange
-                                 plan its 16/32-row tiles (g * N_q > 8) the static schedules, else
+                                 bf16 / fp16 and head_dim 128 when T_m > 1, and its 16-row
+                                 tiles (g * N_q > 8) the static schedules, else
                                  la_plan fails with LA_ERR_UNSUPPORTED; ignored for T_m = 1
                                  (MHA: a GEMV, CUDA cores) and FP8 caches                     */
   void* stream;               /* cudaStream_t for the plan's initial table upload: la_plan then
@@ -167,8 +167,7 @@ typedef enum {
                              with S^T and the per-stage O^T in TMEM (N up to 32 / 64), read back by
                              tcgen05.ld; query tiles of up to 32 rows (T_m)                 */
   LA_ENGINE_AUTO = 2      /* tcgen05 where g * N_q > 8 rows per KV head (one KV pass instead
-                             of two) and it applies (bf16 / fp16, d = 128; static schedules on
-                             an exchange plan);
+                             of two) and it applies (bf16 / fp16, d = 128, static schedule);
                              mma.sync otherwise                                              */
 } la_engine;
 

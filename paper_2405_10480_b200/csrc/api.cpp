@@ -382,7 +382,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
   // 332 us on two others, page 64 equal -- so the rule stays the row count)
   const bool tc5_wins = max_rows > 8;
   const int engine = opts.engine != LA_ENGINE_AUTO ? opts.engine
-                     : (tc5_wins && tc5_ok && (static_sched || !xw) ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
+                     : (tc5_wins && tc5_ok && static_sched ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
   // T_m: 1 -> CUDA-core engine, else tensor-core tiles of <= 8 rows (mma.sync: N = 8), or
   // <= 32 on the tcgen05 engine (N = 16 / 32 per MMA at no extra cost: one KV pass per 32 rows)
   const bool wide = engine == LA_ENGINE_TCGEN05 && tc5_ok;
@@ -455,9 +455,9 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     }
     plan->kinfo = la::decode_kernel_info(dtype, head_dim, p.rows(), p.rows() > 1 ? engine : 0);
     plan->engine = p.rows() > 1 && dtype != LA_FP8_E4M3 ? engine : -1;
-    if (plan->kinfo.global_fold_floats > 0 && xw && (p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT)) {
-      delete plan;  // their deferred last-arriver folds do not run the cross-GPU exchange
-      return fail(LA_ERR_UNSUPPORTED, "16/32-row tcgen05 tiles on an exchange plan run the static schedules");
+    if (plan->kinfo.global_fold_floats > 0 && (p.schedule == LA_SCHED_DYNAMIC || p.schedule == LA_SCHED_FIXED_SPLIT)) {
+      delete plan;  // their fold tree stages peers in the (shared-memory) fold buffer
+      return fail(LA_ERR_UNSUPPORTED, "16-row tcgen05 tiles run the static schedules (streamk, sequential)");
     }
     if (!plan->kinfo.supported) {
       delete plan;
@@ -535,11 +535,7 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     const size_t b_flags = align256(size_t(CAP) * sizeof(uint32_t));
     const size_t b_cnt = align256((la::kNumCounters + U) * sizeof(int));
     const size_t b_trace = opts.trace ? align256(size_t(GP) * LA_TRACE_FIELDS * sizeof(uint64_t)) : 0;
-    // per CTA: the engine's fold buffers + 2 x CAP ints of dynamic pending-fold ids (decode_kernel.cuh)
-    const size_t b_gf = plan->kinfo.global_fold_floats > 0
-                            ? align256(size_t(GP) * (plan->kinfo.global_fold_floats + ((2 * size_t(CAP) + 3) & ~size_t(3))) *
-                                       sizeof(float))
-                            : 0;
+    const size_t b_gf = align256(size_t(GP) * plan->kinfo.global_fold_floats * sizeof(float));
     const size_t o_po = plan->up_bytes, o_pml = o_po + b_po, o_flags = o_pml + b_pml, o_cnt = o_flags + b_flags;
     const size_t o_trace = o_cnt + b_cnt, o_gf = o_trace + b_trace, bytes = o_gf + b_gf;
     cudaError_t e = cudaMalloc(&plan->d_tables, bytes);

@@ -127,9 +127,6 @@
 #ifndef LA_TC5_QSTAGE8
 #define LA_TC5_QSTAGE8 1  // tcgen05 8-row tiles: Q rows staged per segment by the producer (2-deep queue)
 #endif
-#ifndef LA_TC5_FBW
-#define LA_TC5_FBW 1  // tcgen05 16/32-row tiles: consumer -> epilogue fold buffers (global scratch)
-#endif
 #ifndef LA_TC5_LD32
 #define LA_TC5_LD32 1  // tcgen05 16/32-row tiles: 32-column TMEM loads (fewer load round trips)
 #endif
@@ -1123,7 +1120,7 @@ struct Tc5Engine {
   static constexpr int NO = 2 * HEADS;              // O^T columns: P_hi rows, then P_lo rows
   static constexpr int FOLD_WPS = 1;                // one fold row set per slot (warpgroup)
   static constexpr int FOLD_FLOATS = NWG * HEADS * (D + 4);
-  static constexpr int FOLD_BUFS = HEADS > 8 ? LA_TC5_FBW : LA_TC5_FB8;  // wide tiles: global scratch
+  static constexpr int FOLD_BUFS = HEADS > 8 ? 1 : LA_TC5_FB8;
   static constexpr bool GLOBAL_FOLD = HEADS > 8;    // 16-row fold buffers (25 KB) do not fit next to the ring
   static constexpr bool ZERO_RING = false;          // tail V rows are zeroed per stage
   using QElem = T;
@@ -1697,7 +1694,7 @@ template <class E>
 __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPair&, unsigned char* ring, float* fold,
                                               uint64_t* fold_full, uint64_t* fold_empty, uint64_t* stage_bar,
                                               const SegInfo* seginfo, const int* prod_j, uint32_t epoch,
-                                              uint32_t xepoch, unsigned long long* tr, int lane, int* pend) {
+                                              uint32_t xepoch, unsigned long long* tr, int lane) {
   constexpr int NWG = E::NWG, D = E::D, H = E::HEADS, J = D / 32, RG = 8, RS = D + 4;
   constexpr int FW = EngX<E>::FW, kFB = E::FOLD_BUFS, FOLD_FLOATS = E::FOLD_FLOATS;
   static_assert(H % RG == 0, "row groups");
@@ -1705,107 +1702,6 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
   float o[RG][J], m[RG], l[RG];
   uint32_t stage_ph = 0;
   int nr = 0;
-  const int SS = a.slot_stride;
-  int npend = 0;  // dynamic: units this CTA arrived last for (their ids in pend[], global scratch)
-  // Fold partials p0 .. p0 + n - 1 (ascending; piece hv's partial lives in slot 1, SS + hv) into
-  // rows r0 .. r0 + 7 of (m, l, o): max-first weights by a butterfly over lanes = peers, O~ rows
-  // accumulated ascending.  staged: every partial's rows [0, nr) and (m, l) already sit in the
-  // ring (prow / pml, piece order); else each block's rows r0 .. r0 + 7 are staged into stg.
-  auto fold_peers = [&](int r0, int p0, int n, int hv, bool staged, const float* pml, const float* prow, float* stg) {
-    const bool stage_peers = staged;
-    auto slot_of = [&](int p) { return p + (p == hv ? SS : 0); };
-    #pragma unroll 1
-    for (int b0 = 0; b0 < n; b0 += 32) {  // (a 16 / 32-row unit spans few CTAs: one block)
-      const int bn = min(32, n - b0);
-      float2 ml[RG];
-      if (!stage_peers) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(bn) * RG * D * 4);
-        __syncwarp();
-        if (lane < bn)
-          bulk_g2s_plain(stg + lane * RG * D, a.part_o + (size_t(slot_of(p0 + b0 + lane)) * a.group + r0) * D, RG * D * 4,
-                         stage_bar);
-        const size_t mlrow = size_t(slot_of(p0 + b0 + min(lane, bn - 1))) * a.group + r0;
-#pragma unroll
-        for (int hh = 0; hh < RG; ++hh) ml[hh] = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (mlrow + hh) * 4));
-      } else {
-        const float* mls = pml + (size_t(b0 + min(lane, bn - 1)) * nr + r0) * 4;
-#pragma unroll
-        for (int hh = 0; hh < RG; ++hh)
-          ml[hh] = r0 + hh < nr ? *reinterpret_cast<const float2*>(mls + hh * 4) : make_float2(-INFINITY, 0.f);
-      }
-      float w[RG];
-#pragma unroll
-      for (int hh = 0; hh < RG; ++hh) {
-        float M = fmaxf(m[hh], lane < bn ? ml[hh].x : -INFINITY);
-#pragma unroll
-        for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-        w[hh] = lane < bn ? ex2_sub(ml[hh].x, M) : 0.f;
-        float lsum = w[hh] * (lane < bn ? ml[hh].y : 0.f);
-#pragma unroll
-        for (int off = 16; off; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
-        const float wa = ex2_sub(m[hh], M);
-        l[hh] = fmaf(wa, l[hh], lsum);
-        m[hh] = M;
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) o[hh][jj] *= wa;
-      }
-      if (!stage_peers) {
-        mbar_wait(stage_bar, stage_ph);
-        stage_ph ^= 1u;
-      }
-      #pragma unroll 1
-      for (int i = 0; i < bn; ++i) {  // ascending peers
-#pragma unroll
-        for (int hh = 0; hh < RG; ++hh) {
-          const float wk = __shfl_sync(0xffffffffu, w[hh], i);
-          float rv[J];
-          ldv<J>(stage_peers ? prow + ((size_t(b0 + i) * nr + r0 + hh) * D + J * lane)
-                             : stg + (i * RG + hh) * D + J * lane, rv);
-#pragma unroll
-          for (int jj = 0; jj < J; ++jj) o[hh][jj] = fmaf(wk, rv[jj], o[hh][jj]);
-        }
-      }
-      __syncwarp();
-    }
-  };
-  // O = diag(l)^-1 O, L = m + log(l) for rows r0 .. r0 + 7 of unit u (Alg2§38-39) -- or this
-  // rank's normalised shard partial pushed into every rank's exchange buffer (NEXT-2).  Lane hh
-  // computes row hh's 1 / l and log2 l (the same operations as a per-row loop, so the same
-  // bits): one division and one logarithm of latency instead of RG serial ones.
-  auto write_rows = [&](const DevUnit& u, int r0) {
-    float lsel = l[0], msel = m[0];
-#pragma unroll
-    for (int hh = 1; hh < RG; ++hh)
-      if (lane == hh) {
-        lsel = l[hh];
-        msel = m[hh];
-      }
-    const float inv_lane = a.out_scale / lsel, l2_lane = msel + log2f(lsel);
-    if (a.xw > 1) {
-      const int P = a.xw, par = int(xepoch & 1u);
-#pragma unroll
-      for (int hh = 0; hh < RG; ++hh) {
-        const float inv = __shfl_sync(0xffffffffu, inv_lane, hh), l2 = __shfl_sync(0xffffffffu, l2_lane, hh);
-        if (r0 + hh >= nr) continue;
-        #pragma unroll 1
-        for (int d = 0; d < P; ++d) {
-          float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + u.q_row + r0 + hh) * RS;
-          stv<J>(dst + J * lane, o[hh], inv);
-          if (lane == 0) dst[D] = l2;
-        }
-      }
-    } else {
-      float* dst = a.out + size_t(u.q_row + r0) * D + J * lane;
-#pragma unroll
-      for (int hh = 0; hh < RG; ++hh) {
-        const float inv = __shfl_sync(0xffffffffu, inv_lane, hh);
-        if (r0 + hh < nr) stv<J>(dst + hh * D, o[hh], inv);
-      }
-      if (a.lse && lane < RG && r0 + lane < nr) a.lse[u.q_row + r0 + lane] = l2_lane * kLn2;
-    }
-  };
   #pragma unroll 1
   for (int seg = 0;; ++seg) {
     const int b = seg % kFB;
@@ -1820,11 +1716,7 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
     const int v = si.v;
     nr = u.rows;
     const bool out = si.host && si.finishing;  // one CTA computed the whole unit (Alg2§38-39)
-    // dynamic schedule: every other piece publishes and counts in; the unit's last arriver folds
-    // all of its pieces -- here deferred to the end of this CTA's work, when the ring is idle
-    const bool dyn = a.dynamic != 0;
-    const bool host_wait = !dyn && si.host && !si.finishing;
-    const int pslot = dyn && si.host ? SS + v : v;  // a dynamic host piece's partial: slot 1
+    const bool host_wait = si.host && !si.finishing;
     // The CTA's last segment (its producer has issued every stage, all consumed): the ring is
     // idle, so the segment's warp partials (global fold buffer) and, for a waiting host, all
     // of its peers' partial rows and (m, l) are staged there by bulk copies -- ONE L2 round
@@ -1927,35 +1819,113 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
 #pragma unroll
         for (int hh = 0; hh < RG; ++hh) {
           if (r0 + hh >= nr) continue;
-          const size_t row = size_t(pslot) * a.group + r0 + hh;
+          const size_t row = size_t(v) * a.group + r0 + hh;
           stv<J>(a.part_o + row * D + J * lane, o[hh]);
           if (lane == 0) *reinterpret_cast<float2*>(a.part_ml + row * 4) = make_float2(m[hh], l[hh]);
         }
         continue;
       }
-      if (host_wait)
+      if (host_wait) {
         // ---- fold the peers v+1 .. last_cta (ascending, max-first, reading C22): all staged
         //      above (stage_peers), else their rows r0 .. r0 + 7 staged per group in the ring
         //      (past the staged fold buffer when it is there)
-        fold_peers(r0, v + 1, np, -1, stage_peers, pml, prow,
-                   idle ? fstg + FOLD_FLOATS : reinterpret_cast<float*>(ring));  // <= 33 + 128 KiB
+        const int p0 = v + 1, n = np;
+        float* stg = idle ? fstg + FOLD_FLOATS : reinterpret_cast<float*>(ring);  // <= 33 + 128 KiB
+        #pragma unroll 1
+        for (int b0 = 0; b0 < n; b0 += 32) {  // (a 16 / 32-row unit spans few CTAs: one block)
+          const int bn = min(32, n - b0);
+          float2 ml[RG];
+          if (!stage_peers) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(bn) * RG * D * 4);
+            __syncwarp();
+            if (lane < bn)
+              bulk_g2s_plain(stg + lane * RG * D, a.part_o + (size_t(p0 + b0 + lane) * a.group + r0) * D, RG * D * 4,
+                             stage_bar);
+            const size_t mlrow = size_t(p0 + b0 + min(lane, bn - 1)) * a.group + r0;
+#pragma unroll
+            for (int hh = 0; hh < RG; ++hh) ml[hh] = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (mlrow + hh) * 4));
+          } else {
+            const float* mls = pml + (size_t(b0 + min(lane, bn - 1)) * nr + r0) * 4;
+#pragma unroll
+            for (int hh = 0; hh < RG; ++hh)
+              ml[hh] = r0 + hh < nr ? *reinterpret_cast<const float2*>(mls + hh * 4) : make_float2(-INFINITY, 0.f);
+          }
+          float w[RG];
+#pragma unroll
+          for (int hh = 0; hh < RG; ++hh) {
+            float M = fmaxf(m[hh], lane < bn ? ml[hh].x : -INFINITY);
+#pragma unroll
+            for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            w[hh] = lane < bn ? ex2_sub(ml[hh].x, M) : 0.f;
+            float lsum = w[hh] * (lane < bn ? ml[hh].y : 0.f);
+#pragma unroll
+            for (int off = 16; off; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+            const float wa = ex2_sub(m[hh], M);
+            l[hh] = fmaf(wa, l[hh], lsum);
+            m[hh] = M;
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) o[hh][jj] *= wa;
+          }
+          if (!stage_peers) {
+            mbar_wait(stage_bar, stage_ph);
+            stage_ph ^= 1u;
+          }
+          #pragma unroll 1
+          for (int i = 0; i < bn; ++i) {  // ascending peers
+#pragma unroll
+            for (int hh = 0; hh < RG; ++hh) {
+              const float wk = __shfl_sync(0xffffffffu, w[hh], i);
+              float rv[J];
+              ldv<J>(stage_peers ? prow + ((size_t(b0 + i) * nr + r0 + hh) * D + J * lane)
+                                 : stg + (i * RG + hh) * D + J * lane, rv);
+#pragma unroll
+              for (int jj = 0; jj < J; ++jj) o[hh][jj] = fmaf(wk, rv[jj], o[hh][jj]);
+            }
+          }
+          __syncwarp();
+        }
+      }
 #ifdef LA_WIDE_PRINT
       if (r0 == 0) wt[6] = globaltimer();
 #endif
-      write_rows(u, r0);
-    }
-    if (!out && !host_wait && dyn) {  // count in; the last arriver queues the unit's fold
-      __threadfence();
-      __syncwarp();
-      int last = 0;
-      if (lane == 0 && atomicAdd(&a.unit_count[si.unit], 1) == u.last_cta - u.host_cta) {
-        __threadfence();
-        a.unit_count[si.unit] = 0;  // ready for the next launch
-        pend[npend] = si.unit;
-        last = 1;
+      // ---- O = diag(l)^-1 O, L = m + log(l) (Alg2§38-39) -- or this rank's normalised shard
+      //      partial pushed into every rank's exchange buffer (NEXT-2).  Lane hh computes row
+      //      hh's 1 / l and log2 l (the same operations as a per-row loop, so the same bits):
+      //      one division and one logarithm of latency instead of RG serial ones.
+      float lsel = l[0], msel = m[0];
+#pragma unroll
+      for (int hh = 1; hh < RG; ++hh)
+        if (lane == hh) {
+          lsel = l[hh];
+          msel = m[hh];
+        }
+      const float inv_lane = a.out_scale / lsel, l2_lane = msel + log2f(lsel);
+      if (a.xw > 1) {
+        const int P = a.xw, par = int(xepoch & 1u);
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh) {
+          const float inv = __shfl_sync(0xffffffffu, inv_lane, hh), l2 = __shfl_sync(0xffffffffu, l2_lane, hh);
+          if (r0 + hh >= nr) continue;
+          #pragma unroll 1
+          for (int d = 0; d < P; ++d) {
+            float* dst = a.xpeer[d] + ((size_t(par) * P + a.xr) * a.xrows + u.q_row + r0 + hh) * RS;
+            stv<J>(dst + J * lane, o[hh], inv);
+            if (lane == 0) dst[D] = l2;
+          }
+        }
+      } else {
+        float* dst = a.out + size_t(u.q_row + r0) * D + J * lane;
+#pragma unroll
+        for (int hh = 0; hh < RG; ++hh) {
+          const float inv = __shfl_sync(0xffffffffu, inv_lane, hh);
+          if (r0 + hh < nr) stv<J>(dst + hh * D, o[hh], inv);
+        }
+        if (a.lse && lane < RG && r0 + lane < nr) a.lse[u.q_row + r0 + lane] = l2_lane * kLn2;
       }
-      npend += __shfl_sync(0xffffffffu, last, 0);
-    } else if (!out && !host_wait) {  // Signal (Alg2§23)
+    }
+    if (!out && !host_wait) {  // Signal (Alg2§23)
       __threadfence();
       __syncwarp();
       if (lane == 0) {
@@ -2012,58 +1982,8 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
              wt[2] - wt[6]);
 #endif
   }
-  // ---- dynamic: the units this CTA arrived last for, folded now that its ring is idle (its
-  //      producer issued every stage and its consumers used them): every piece host_cta ..
-  //      last_cta ascending (fixed pieces, fixed order: bitwise deterministic), all staged at
-  //      once when they fit, else 8 rows at a time; then O = O~ / l, L (Alg2§27-39)
-  #pragma unroll 1
-  for (int i = 0; i < npend; ++i) {
-    const int unit = pend[i];
-    const DevUnit u = a.units[unit];
-    nr = u.rows;
-    const int hv = u.host_cta, n = u.last_cta - hv + 1;
-    float* pml = reinterpret_cast<float*>(ring);           // [n][nr][4]
-    float* prow = pml + size_t(n) * nr * 4;                 // [n][nr][D]
-    const bool staged = size_t(n) * nr * (D + 4) * 4 <= size_t(Smem<E>::RING);
-    asm volatile("fence.proxy.async.global;" ::: "memory");       // the pieces (acquired by the count) -> TMA
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the ring
-    __syncwarp();
-    if (staged) {
-      if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(n) * nr * (D + 4) * 4);
-      __syncwarp();
-      #pragma unroll 1
-      for (int k = lane; k < n; k += 32) {
-        const int p = hv + k;
-        const size_t row = size_t(p + (p == hv ? SS : 0)) * a.group;
-        bulk_g2s_plain(prow + size_t(k) * nr * D, a.part_o + row * D, uint32_t(nr) * D * 4, stage_bar);
-        bulk_g2s_plain(pml + size_t(k) * nr * 4, a.part_ml + row * 4, uint32_t(nr) * 16, stage_bar);
-      }
-      mbar_wait(stage_bar, stage_ph);
-      stage_ph ^= 1u;
-    }
-    #pragma unroll 1
-    for (int r0 = 0; r0 < nr; r0 += RG) {
-#pragma unroll
-      for (int hh = 0; hh < RG; ++hh) {
-        m[hh] = -INFINITY;
-        l[hh] = 0.f;
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) o[hh][jj] = 0.f;
-      }
-      fold_peers(r0, hv, n, hv, staged, pml, prow, reinterpret_cast<float*>(ring));
-      write_rows(u, r0);
-    }
-    __syncwarp();
-  }
   if (lane == 0) {
     if (tr) tr[TR_END] = globaltimer();
-    if (a.dynamic) {  // the last CTA out resets the claim counter for the next launch
-      __threadfence();
-      if (atomicAdd(&a.counters[CTR_DONE], 1) == int(gridDim.x) - 1) {
-        a.counters[CTR_CLAIM] = 0;
-        a.counters[CTR_DONE] = 0;
-      }
-    }
     __threadfence();  // every flag wait of this CTA is over: the last one out advances the epoch
     if (atomicAdd(&a.counters[CTR_EXITED], 1) == int(gridDim.x) - 1) {
       a.counters[CTR_EXITED] = 0;
@@ -2084,9 +2004,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   extern __shared__ unsigned char smem_raw[];
   unsigned char* ring =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // global fold scratch per CTA: kFB fold buffers, then (dynamic) the ids of the units it
-  // arrived last for -- 2 slot_stride entries (rounded to 16 B), twice the pieces any CTA can take
-  float* fold = EngX<E>::GF ? a.gfold + size_t(blockIdx.x) * (kFB * E::FOLD_FLOATS + ((2 * size_t(a.slot_stride) + 3) & ~size_t(3)))
+  float* fold = EngX<E>::GF ? a.gfold + size_t(blockIdx.x) * kFB * E::FOLD_FLOATS
                             : reinterpret_cast<float*>(ring + Smem<E>::RING + Smem<E>::EXTRA);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + Smem<E>::RING + Smem<E>::EXTRA + Smem<E>::FOLD);
   uint64_t* empty = full + NST;
@@ -2340,8 +2258,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
 
   if constexpr (H > 8) {
     if (warp == NCW) {
-      wide_epilogue<E>(a, tm, ring, fold, fold_full, fold_empty, stage_bar, seginfo, prod_j, epoch, xepoch, tr, lane,
-                       reinterpret_cast<int*>(fold + kFB * FOLD_FLOATS));
+      wide_epilogue<E>(a, tm, ring, fold, fold_full, fold_empty, stage_bar, seginfo, prod_j, epoch, xepoch, tr, lane);
       return;
     }
   }

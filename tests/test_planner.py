@@ -349,9 +349,7 @@ def test_heterogeneous_validation(la):
     assert p.info.tile_rows == 8 and p.info.num_units == 4
     p = la.Plan(1, 32, 2, 128, [1000], host_only=True)  # auto: tcgen05's 16-row tiles, one per KV head
     assert p.info.tile_rows == 16 and p.info.num_units == 2
-    p = la.Plan(1, 32, 2, 128, [1000], host_only=True, schedule="dynamic")  # auto, dynamic: tcgen05 tiles too
-    assert p.info.tile_rows == 16 and p.info.num_units == 2
-    p = la.Plan(1, 32, 2, 128, [1000], host_only=True, schedule="dynamic", xchg_world=2)  # exchange: mma.sync
+    p = la.Plan(1, 32, 2, 128, [1000], host_only=True, schedule="dynamic")  # auto, dynamic: mma.sync tiles
     assert p.info.tile_rows == 8 and p.info.num_units == 4
     p = la.Plan(1, 16, 2, 128, [1000], host_only=True)  # auto, g = 8: mma.sync
     assert p.info.tile_rows == 8 and p.info.num_units == 2
