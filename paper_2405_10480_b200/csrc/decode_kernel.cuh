@@ -112,10 +112,17 @@
                         // full ring scatters the CTAs' rates, 2 stages 311 -> 305 us, 3 with V at 2: 306 -> 304)
 #endif
 #ifndef LA_TC5_VWIN8
-#define LA_TC5_VWIN8 2  // tcgen05 engine, 8-row tiles: V of stage j after stage j - VWIN8 is consumed (0: off)
+#define LA_TC5_VWIN8 2  // tcgen05 engine, 8-row tiles: V of stage j after stage j - VWIN8 is consumed (0: off;
+                        // every tile size: K on the whole ring, V 2 stages ahead -- 32 rows 317.9 -> 317.2 us)
+#endif
+#ifndef LA_TC5_VWIN16
+#define LA_TC5_VWIN16 2  // ... 16-row tiles (0: off)
+#endif
+#ifndef LA_TC5_VWIN32
+#define LA_TC5_VWIN32 2  // ... 32-row tiles (0: off)
 #endif
 #ifndef LA_TC5_WIN16
-#define LA_TC5_WIN16 2  // ... 16-row tiles (measured: c3 N_q = 2 317 -> 313 us)
+#define LA_TC5_WIN16 0  // ... 16-row tiles (2 measured c3 N_q = 2 317 -> 313 us; V window 2 alone: 313.1 vs 313.7 us)
 #endif
 #ifndef LA_TC5_WIN32
 #define LA_TC5_WIN32 0  // ... 32-row tiles (compute-bound: 2 stages measured 314 -> 355 us)
@@ -1095,7 +1102,7 @@ struct Tc5Engine {
   static constexpr int WIN_ = HEADS_ == 8 ? LA_TC5_WIN8 : HEADS_ == 16 ? LA_TC5_WIN16 : LA_TC5_WIN32;
   static constexpr int WIN = WIN_ > 0 ? WIN_ : NST;  // stages in flight
   // V of stage j waits until stage j - VWIN is consumed (VWIN < WIN: ~WIN - 1/2 stages in flight)
-  static constexpr int VWIN_ = HEADS_ == 8 ? LA_TC5_VWIN8 : 0;
+  static constexpr int VWIN_ = HEADS_ == 8 ? LA_TC5_VWIN8 : HEADS_ == 16 ? LA_TC5_VWIN16 : LA_TC5_VWIN32;
   static constexpr int VWIN = VWIN_ > 0 ? VWIN_ : WIN;
   static_assert(NWG <= NST && NST <= 8, "ring");
   static constexpr int STAGE_TOK = 128;             // = TMA box rows = MMA M
