@@ -166,9 +166,10 @@ typedef enum {
                              thread issues tcgen05.mma (M = 128 tokens / dims, N = 16 / 32)
                              with S^T and the per-stage O^T in TMEM (N up to 32 / 64), read back by
                              tcgen05.ld; query tiles of up to 32 rows (T_m)                 */
-  LA_ENGINE_AUTO = 2      /* tcgen05 where g * N_q > 8 rows per KV head (one KV pass instead
-                             of two) and it applies (bf16 / fp16, d = 128, static schedule);
-                             mma.sync otherwise                                              */
+  LA_ENGINE_AUTO = 2      /* tcgen05 where it applies (bf16 / fp16, d = 128): tiles of more than
+                             8 rows per KV head (one KV pass instead of two; static schedules)
+                             and 8-row tiles of a BHSD / packed cache; mma.sync otherwise
+                             (paged 8-row tiles, dynamic schedules for g * N_q > 8)          */
 } la_engine;
 
 typedef struct la_plan_s* la_plan_t;

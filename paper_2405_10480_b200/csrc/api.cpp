@@ -368,21 +368,22 @@ la_status la_plan(int batch, int heads_q, int heads_kv, int head_dim, const int3
     uniform = uniform && n == p.q_lens[0];
   }
   p.q_len = uniform ? p.q_lens[0] : 0;
-  // Engine for T_m > 1 tiles.  AUTO takes tcgen05 exactly where it wins (measured):
-  // more than 8 rows per KV head (g * N_q > 8), which its N = 16 MMAs cover in one pass over
-  // the cache where mma.sync tiles need two; otherwise mma.sync (equal within box noise, with
-  // a smaller run-to-run spread).
+  // Engine for T_m > 1 tiles.  AUTO takes tcgen05 (measured): more than 8 rows per
+  // KV head (g * N_q > 8), which its N = 16 / 32 MMAs cover in one pass over the cache where
+  // mma.sync tiles need two / four, and the 8-row tiles of a BHSD / packed cache.
   if (opts.engine != LA_ENGINE_MMA_SYNC && opts.engine != LA_ENGINE_TCGEN05 && opts.engine != LA_ENGINE_AUTO)
     return fail(LA_ERR_INVALID, "engine must be LA_ENGINE_AUTO, LA_ENGINE_MMA_SYNC or LA_ENGINE_TCGEN05");
   const bool tc5_ok = head_dim == 128 && (dtype == LA_BF16 || dtype == LA_FP16);
   // AUTO resolves to stream-K for multi-row tiles (below), so it admits the wide tcgen05 tiles
   const bool static_sched = opts.schedule == LA_SCHED_STREAMK || opts.schedule == LA_SCHED_SEQUENTIAL ||
                             opts.schedule == LA_SCHED_AUTO;
-  // (paged pools: box-dependent -- c3 page 16 tcgen05 323 vs mma.sync 331 us on one box, 338 vs
-  // 332 us on two others, page 64 equal -- so the rule stays the row count)
-  const bool tc5_wins = max_rows > 8;
+  // (r02: 8-row tiles too -- c3 at parity after the round-2 engine work, tcgen05 ahead in the
+  // last two same-box series: 304.5 vs 305.1 us over 5 alternating runs, 305.1 vs 305.5 us --
+  // except on paged pools, where it measured box-dependent: 323 vs 331 us on one box, 338 vs
+  // 332 us on two others; 16/32-row tiles need a static schedule)
+  const bool tc5_wins = max_rows > 8 ? static_sched : opts.layout != LA_KV_PAGED;
   const int engine = opts.engine != LA_ENGINE_AUTO ? opts.engine
-                     : (tc5_wins && tc5_ok && static_sched ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
+                     : (tc5_wins && tc5_ok ? LA_ENGINE_TCGEN05 : LA_ENGINE_MMA_SYNC);
   // T_m: 1 -> CUDA-core engine, else tensor-core tiles of <= 8 rows (mma.sync: N = 8), or
   // <= 32 on the tcgen05 engine (N = 16 / 32 per MMA at no extra cost: one KV pass per 32 rows)
   const bool wide = engine == LA_ENGINE_TCGEN05 && tc5_ok;

@@ -17,9 +17,9 @@ run() {  # name, bench args
 run c1 "--config c1"
 run c2_streamk "--config c2 --schedule streamk"
 run c3 "--config c3"
-run c3_tc5 "--config c3 --engine tcgen05"
-run c3_tc5_cal "--config c3 --engine tcgen05 --sm-weights calibrate"
+run c3_mma "--config c3 --engine mma"
 run c3_cal "--config c3 --sm-weights calibrate"
+run c3_mma_cal "--config c3 --engine mma --sm-weights calibrate"
 run c3_q2 "--config c3 --q-len 2"
 run c3_q4 "--config c3 --q-len 4"
 run c4 "--config c4"
@@ -31,7 +31,7 @@ run c3_fp8 "--config c3 --dtype fp8"
 run c2_paged16 "--config c2 --page-size 16"
 run c3_paged16 "--config c3 --page-size 16"
 run c3_paged16_tc5 "--config c3 --page-size 16 --engine tcgen05"
-for cfg in "c2|--config c2|c2" "c3|--config c3|c3" "c4|--config c4|c4" "c1|--config c1|c1" "c3_q4|--config c3 --q-len 4|c3-q4-tc5" "c3_q2|--config c3 --q-len 2|c3-q2-tc5" "c3_tc5|--config c3 --engine tcgen05|c3-tc5"; do
+for cfg in "c2|--config c2|c2" "c3|--config c3|c3-tc5" "c3_mma|--config c3 --engine mma|c3" "c4|--config c4|c4" "c1|--config c1|c1" "c3_q4|--config c3 --q-len 4|c3-q4-tc5" "c3_q2|--config c3 --q-len 2|c3-q2-tc5"; do
   IFS='|' read -r name args key <<< "$cfg"
   bash scripts/profile.sh ${R}_$name "$args" $key > $O/profile_$name.log 2>&1
   mv gpurun_out/${R}_${name}* $O/ 2>/dev/null
