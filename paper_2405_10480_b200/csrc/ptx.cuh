@@ -2,6 +2,11 @@
 // gpu-scope release/acquire flags, timers).  Internal to libleanattn.so.
 #pragma once
 
+#ifndef LA_KV_L2_POLICY
+#define LA_KV_L2_POLICY 0  // K/V stream cache hint: 0 evict_first (default), 1 evict_normal, 2 evict_first 50%
+                           // (measured: c2 587.8 / 591.7 / 591.0 us, c3 306.0 / 310.5 us)
+#endif
+
 #include <cstdint>
 
 namespace la {
@@ -49,7 +54,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
+#if LA_KV_L2_POLICY == 1  // (experiment) evict_normal
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#elif LA_KV_L2_POLICY == 2  // (experiment) evict_first for half of the lines
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 0.5;" : "=l"(pol));
+#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
   return pol;
 }
 
