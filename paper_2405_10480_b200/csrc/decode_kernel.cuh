@@ -124,6 +124,12 @@
 #ifndef LA_TC5_WIN16
 #define LA_TC5_WIN16 0  // ... 16-row tiles (2 measured c3 N_q = 2 317 -> 313 us; V window 2 alone: 313.1 vs 313.7 us)
 #endif
+#ifndef LA_WIDE_NEP16
+#define LA_WIDE_NEP16 2  // 16-row tcgen05 tiles: epilogue warps (each folds / writes its own 8-row groups)
+#endif
+#ifndef LA_WIDE_NEP32
+#define LA_WIDE_NEP32 2  // 32-row tiles: epilogue warps (4 would cap the kernel at 152 registers)
+#endif
 #ifndef LA_TC5_WIN32
 #define LA_TC5_WIN32 0  // ... 32-row tiles (compute-bound: 2 stages measured 314 -> 355 us)
 #endif
@@ -1628,13 +1634,16 @@ struct SegInfo {
 // the ring and fewer fold rows per slot; the others get the neutral values.
 template <class E, class = void>
 struct EngX {
-  static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS, VWIN = 1 << 20, QD = 4;
+  static constexpr int TMEM = 0, EXTRA = 0, FW = E::WPS, VWIN = 1 << 20, QD = 4, NEP = 1;
   static constexpr bool GF = false;  // fold buffers in global scratch (DecodeArgs::gfold)
 };
 template <class E>
 struct EngX<E, std::void_t<decltype(E::TMEM_COLS)>> {
   static constexpr int TMEM = E::TMEM_COLS, EXTRA = E::EXTRA_BYTES, FW = E::FOLD_WPS, VWIN = E::VWIN, QD = E::QD;
   static constexpr bool GF = E::GLOBAL_FOLD;
+  // epilogue warps: one for 8-row tiles, else the 8-row groups split over NEP warps
+  static constexpr int NEP = E::HEADS == 8 ? 1 : E::HEADS == 16 ? LA_WIDE_NEP16 : LA_WIDE_NEP32;
+  static_assert(E::HEADS % (8 * NEP) == 0, "whole row groups per epilogue warp");
 };
 
 template <class E>
@@ -1700,12 +1709,20 @@ struct EpiAcc {
 template <class E>
 __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPair&, unsigned char* ring, float* fold,
                                               uint64_t* fold_full, uint64_t* fold_empty, uint64_t* stage_bar,
-                                              const SegInfo* seginfo, const int* prod_j, uint32_t epoch,
-                                              uint32_t xepoch, unsigned long long* tr, int lane) {
+                                              const SegInfo* seginfo, int* prod_j, uint32_t epoch,
+                                              uint32_t xepoch, unsigned long long* tr, int lane, int e) {
   constexpr int NWG = E::NWG, D = E::D, H = E::HEADS, J = D / 32, RG = 8, RS = D + 4;
   constexpr int FW = EngX<E>::FW, kFB = E::FOLD_BUFS, FOLD_FLOATS = E::FOLD_FLOATS;
-  static_assert(H % RG == 0, "row groups");
+  // NEP epilogue warps: warp e owns rows [e RW, e RW + RW) of every segment (whole 8-row
+  // groups, each folded in the same order as by one warp: the bits do not depend on NEP).
+  // Warp 0 alone stages, waits on the peers' flags, signals, exchanges and counts out.
+  constexpr int NEP = EngX<E>::NEP, RW = H / NEP;
+  static_assert(H % RG == 0 && RW % RG == 0, "row groups");
   static_assert((FOLD_FLOATS * 4) % 16 == 0, "fold buffer: whole 16-B units for one bulk copy");
+  auto epi_sync = [&]() {  // the NEP epilogue warps (named barrier 15; the consumers use 1 .. 2 + NST)
+    if constexpr (NEP > 1) asm volatile("bar.sync 15, %0;" ::"n"(NEP * 32) : "memory");
+  };
+  volatile int* epi_flags = prod_j + 1;  // warp 0 -> warps 1 .. NEP-1: this segment's idle / stage_peers
   float o[RG][J], m[RG], l[RG];
   uint32_t stage_ph = 0;
   int nr = 0;
@@ -1716,9 +1733,8 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
     const SegInfo si = seginfo[b];
     if (si.unit < 0) break;
 #ifndef LA_PROF
-    if (tr && lane == 0) tr[TR_STREAM] = globaltimer();  // the consumers finished this segment
+    if (e == 0 && tr && lane == 0) tr[TR_STREAM] = globaltimer();  // the consumers finished this segment
 #endif
-    const float* fb = fold + b * FOLD_FLOATS;
     const DevUnit u = a.units[si.unit];
     const int v = si.v;
     nr = u.rows;
@@ -1731,63 +1747,76 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
     // ~13 us that way, on the kernel's critical path).  The arithmetic is unchanged: only
     // where the operands are read from differs, so results stay bitwise identical.
     const int np = host_wait ? u.last_cta - v : 0;
-    const bool idle = *reinterpret_cast<volatile const int*>(prod_j) == si.jend;
-    const bool stage_peers = idle && host_wait &&
-                             FOLD_FLOATS * 4 + size_t(np) * nr * (D + 4) * 4 <= size_t(Smem<E>::RING);
     float* fstg = reinterpret_cast<float*>(ring);         // [FOLD_FLOATS]
     float* pml = fstg + FOLD_FLOATS;                       // [np][nr][4]  peers' (m, l, -, -)
     float* prow = pml + size_t(np) * nr * 4;               // [np][nr][D]  peers' O~ rows
-    if (idle) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");      // consumers' fold-buffer stores -> TMA
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring's last generic reads
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_expect_tx(stage_bar, uint32_t(FOLD_FLOATS) * 4);
-        bulk_g2s_plain(fstg, fb, uint32_t(FOLD_FLOATS) * 4, stage_bar);
-      }
-    }
-    if (host_wait) {  // Wait(flags[cta]) for cta = g+1 .. last_cta (Alg2§26-28, reading C9)
-      if (tr && lane == 0) tr[TR_WAIT0] = globaltimer();
-      #pragma unroll 1
-      for (int p = v + 1 + lane; p <= u.last_cta; p += 32) {
-        const unsigned long long t0 = globaltimer();
-        while (ld_acquire_gpu(&a.flags[p]) != epoch) {
-          __nanosleep(20);
-          if (globaltimer() - t0 > kWaitTimeoutNs || *reinterpret_cast<volatile int*>(&a.counters[CTR_ERROR])) {
-            atomicExch(&a.counters[CTR_ERROR], 1);
-            break;
-          }
+    bool idle = false, stage_peers = false;
+    if (e == 0) {
+      idle = *reinterpret_cast<volatile const int*>(prod_j) == si.jend;
+      stage_peers = idle && host_wait && FOLD_FLOATS * 4 + size_t(np) * nr * (D + 4) * 4 <= size_t(Smem<E>::RING);
+      if (idle) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");      // consumers' fold-buffer stores -> TMA
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the ring's last generic reads
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_expect_tx(stage_bar, uint32_t(FOLD_FLOATS) * 4);
+          bulk_g2s_plain(fstg, fold + b * FOLD_FLOATS, uint32_t(FOLD_FLOATS) * 4, stage_bar);
         }
       }
-      __syncwarp();
-      if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired partials -> TMA
-    }
-    if (idle) {  // the fold buffer has landed (issued before the peer wait)
-      mbar_wait(stage_bar, stage_ph);
-      stage_ph ^= 1u;
-      fb = fstg;
-    }
-    if (stage_peers) {  // every peer's rows [0, nr) and (m, l): contiguous runs of its slot
-      __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(np) * nr * (D + 4) * 4);
-      __syncwarp();
-      #pragma unroll 1
-      for (int i = lane; i < np; i += 32) {
-        const size_t row = size_t(v + 1 + i) * a.group;
-        bulk_g2s_plain(prow + size_t(i) * nr * D, a.part_o + row * D, uint32_t(nr) * D * 4, stage_bar);
-        bulk_g2s_plain(pml + size_t(i) * nr * 4, a.part_ml + row * 4, uint32_t(nr) * 16, stage_bar);
+      if (host_wait) {  // Wait(flags[cta]) for cta = g+1 .. last_cta (Alg2§26-28, reading C9)
+        if (tr && lane == 0) tr[TR_WAIT0] = globaltimer();
+        #pragma unroll 1
+        for (int p = v + 1 + lane; p <= u.last_cta; p += 32) {
+          const unsigned long long t0 = globaltimer();
+          while (ld_acquire_gpu(&a.flags[p]) != epoch) {
+            __nanosleep(20);
+            if (globaltimer() - t0 > kWaitTimeoutNs || *reinterpret_cast<volatile int*>(&a.counters[CTR_ERROR])) {
+              atomicExch(&a.counters[CTR_ERROR], 1);
+              break;
+            }
+          }
+        }
+        __syncwarp();
+        if (tr && lane == 0) tr[TR_WAIT1] = globaltimer();
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired partials -> TMA
       }
-      mbar_wait(stage_bar, stage_ph);
-      stage_ph ^= 1u;
+      if (idle) {  // the fold buffer has landed (issued before the peer wait)
+        mbar_wait(stage_bar, stage_ph);
+        stage_ph ^= 1u;
+      }
+      if (stage_peers) {  // every peer's rows [0, nr) and (m, l): contiguous runs of its slot
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(np) * nr * (D + 4) * 4);
+        __syncwarp();
+        #pragma unroll 1
+        for (int i = lane; i < np; i += 32) {
+          const size_t row = size_t(v + 1 + i) * a.group;
+          bulk_g2s_plain(prow + size_t(i) * nr * D, a.part_o + row * D, uint32_t(nr) * D * 4, stage_bar);
+          bulk_g2s_plain(pml + size_t(i) * nr * 4, a.part_ml + row * 4, uint32_t(nr) * 16, stage_bar);
+        }
+        mbar_wait(stage_bar, stage_ph);
+        stage_ph ^= 1u;
+      }
+      if (NEP > 1 && lane == 0) *epi_flags = int(idle) | int(stage_peers) << 1;
     }
+    if constexpr (NEP > 1) {
+      epi_sync();  // (A) staged operands, the acquired peers' partials and the flags word
+      if (e != 0) {
+        const int f = *epi_flags;
+        idle = f & 1;
+        stage_peers = f & 2;
+      }
+    }
+    const float* fb = idle ? fstg : fold + b * FOLD_FLOATS;
 #ifdef LA_WIDE_PRINT
     unsigned long long wt[8] = {globaltimer(), 0, 0, 0, 0, 0, 0, 0};
 #endif
+    const int rb = e * RW, re = min(nr, rb + RW);  // this warp's rows
+    if (rb >= re && lane == 0) mbar_arrive(&fold_empty[b]);
     #pragma unroll 1
-    for (int r0 = 0; r0 < nr; r0 += RG) {
+    for (int r0 = rb; r0 < re; r0 += RG) {
 #ifdef LA_WIDE_PRINT
-      if (r0 / RG < 6) wt[1 + r0 / RG] = globaltimer();
+      if ((r0 - rb) / RG < 4) wt[1 + (r0 - rb) / RG] = globaltimer();
 #endif
       // ---- rows r0 .. r0 + 7 of the NWG x FW warp partials (branch-free: loads issue together)
 #pragma unroll
@@ -1818,9 +1847,9 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
         l[hh] = ls;
       }
       __syncwarp();
-      if (r0 + RG >= nr && lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill it
+      if (r0 + RG >= re && lane == 0) mbar_arrive(&fold_empty[b]);  // consumers may refill it
 #ifdef LA_WIDE_PRINT
-      if (r0 == 0) wt[5] = globaltimer();
+      if (r0 == rb) wt[5] = globaltimer();
 #endif
       if (!out && !host_wait) {  // StorePartials (Alg2§20-22)
 #pragma unroll
@@ -1833,23 +1862,14 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
         continue;
       }
       if (host_wait) {
-        // ---- fold the peers v+1 .. last_cta (ascending, max-first, reading C22): all staged
-        //      above (stage_peers), else their rows r0 .. r0 + 7 staged per group in the ring
-        //      (past the staged fold buffer when it is there)
+        // ---- fold the peers v+1 .. last_cta (ascending, max-first, reading C22): staged above
+        //      (stage_peers), else read from L2 (acquired by warp 0 before barrier A)
         const int p0 = v + 1, n = np;
-        float* stg = idle ? fstg + FOLD_FLOATS : reinterpret_cast<float*>(ring);  // <= 33 + 128 KiB
         #pragma unroll 1
         for (int b0 = 0; b0 < n; b0 += 32) {  // (a 16 / 32-row unit spans few CTAs: one block)
           const int bn = min(32, n - b0);
           float2 ml[RG];
           if (!stage_peers) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(stage_bar, uint32_t(bn) * RG * D * 4);
-            __syncwarp();
-            if (lane < bn)
-              bulk_g2s_plain(stg + lane * RG * D, a.part_o + (size_t(p0 + b0 + lane) * a.group + r0) * D, RG * D * 4,
-                             stage_bar);
             const size_t mlrow = size_t(p0 + b0 + min(lane, bn - 1)) * a.group + r0;
 #pragma unroll
             for (int hh = 0; hh < RG; ++hh) ml[hh] = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (mlrow + hh) * 4));
@@ -1875,18 +1895,16 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
 #pragma unroll
             for (int jj = 0; jj < J; ++jj) o[hh][jj] *= wa;
           }
-          if (!stage_peers) {
-            mbar_wait(stage_bar, stage_ph);
-            stage_ph ^= 1u;
-          }
           #pragma unroll 1
           for (int i = 0; i < bn; ++i) {  // ascending peers
 #pragma unroll
             for (int hh = 0; hh < RG; ++hh) {
               const float wk = __shfl_sync(0xffffffffu, w[hh], i);
               float rv[J];
-              ldv<J>(stage_peers ? prow + ((size_t(b0 + i) * nr + r0 + hh) * D + J * lane)
-                                 : stg + (i * RG + hh) * D + J * lane, rv);
+              if (stage_peers)
+                ldv<J>(prow + ((size_t(b0 + i) * nr + r0 + hh) * D + J * lane), rv);
+              else
+                ldv_cg<J>(a.part_o + (size_t(p0 + b0 + i) * a.group + r0 + hh) * D + J * lane, rv);
 #pragma unroll
               for (int jj = 0; jj < J; ++jj) o[hh][jj] = fmaf(wk, rv[jj], o[hh][jj]);
             }
@@ -1895,7 +1913,7 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
         }
       }
 #ifdef LA_WIDE_PRINT
-      if (r0 == 0) wt[6] = globaltimer();
+      if (r0 == rb) wt[6] = globaltimer();
 #endif
       // ---- O = diag(l)^-1 O, L = m + log(l) (Alg2§38-39) -- or this rank's normalised shard
       //      partial pushed into every rank's exchange buffer (NEXT-2).  Lane hh computes row
@@ -1935,61 +1953,67 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
     if (!out && !host_wait) {  // Signal (Alg2§23)
       __threadfence();
       __syncwarp();
-      if (lane == 0) {
+      epi_sync();  // (B) every epilogue warp's partial rows are out
+      if (e == 0 && lane == 0) {
         st_release_gpu(&a.flags[v], epoch);
         if (tr && !tr[TR_PUBLISH]) tr[TR_PUBLISH] = globaltimer();
       }
     } else if (a.xw > 1) {  // NEXT-2: release, wait for the P ranks, fold their partials
-      const int P = a.xw, par = int(xepoch & 1u);
       __threadfence_system();
       __syncwarp();
-      if (lane < P) {
-        uint32_t* f = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(a.xpeer[lane]) + a.xflag_off);
-        st_release_sys(f + size_t(a.xr) * a.xunits + si.unit, xepoch);
-        const uint32_t* mine = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(a.xpeer[a.xr]) +
-                                                                 a.xflag_off) + size_t(lane) * a.xunits + si.unit;
-        const unsigned long long t0 = globaltimer();
-        while (int32_t(ld_acquire_sys(mine) - xepoch) < 0) {
-          if (*reinterpret_cast<volatile int*>(a.xerr) || globaltimer() - t0 > kXchgTimeoutNs) {
-            atomicExch(a.xerr, 1);
-            break;
+      epi_sync();  // (B) every epilogue warp's rows are in the exchange buffers
+      if (e == 0) {
+        const int P = a.xw, par = int(xepoch & 1u);
+        if (lane < P) {
+          uint32_t* f = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(a.xpeer[lane]) + a.xflag_off);
+          st_release_sys(f + size_t(a.xr) * a.xunits + si.unit, xepoch);
+          const uint32_t* mine = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(a.xpeer[a.xr]) +
+                                                                   a.xflag_off) + size_t(lane) * a.xunits + si.unit;
+          const unsigned long long t0 = globaltimer();
+          while (int32_t(ld_acquire_sys(mine) - xepoch) < 0) {
+            if (*reinterpret_cast<volatile int*>(a.xerr) || globaltimer() - t0 > kXchgTimeoutNs) {
+              atomicExch(a.xerr, 1);
+              break;
+            }
+            __nanosleep(64);
           }
-          __nanosleep(64);
+        }
+        __syncwarp();
+        const float* xb = a.xpeer[a.xr] + size_t(par) * P * a.xrows * RS;
+        #pragma unroll 1
+        for (int h = 0; h < nr; ++h) {
+          float M = -INFINITY, lsum = 0.f, acc[J];
+          #pragma unroll 1
+          for (int r = 0; r < P; ++r) M = fmaxf(M, ld_cg(xb + (size_t(r) * a.xrows + u.q_row + h) * RS + D));
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) acc[jj] = 0.f;
+          #pragma unroll 1
+          for (int r = 0; r < P; ++r) {
+            const float* src = xb + (size_t(r) * a.xrows + u.q_row + h) * RS;
+            const float w = ex2_sub(ld_cg(src + D), M);
+            lsum += w;
+            float rv[J];
+            ldv_cg<J>(src + J * lane, rv);
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) acc[jj] = fmaf(w, rv[jj], acc[jj]);
+          }
+          stv<J>(a.out + size_t(u.q_row + h) * D + J * lane, acc, 1.f / lsum);
+          if (lane == 0 && a.lse) a.lse[u.q_row + h] = (M + log2f(lsum)) * kLn2;
         }
       }
-      __syncwarp();
-      const float* xb = a.xpeer[a.xr] + size_t(par) * P * a.xrows * RS;
-      #pragma unroll 1
-      for (int h = 0; h < nr; ++h) {
-        float M = -INFINITY, lsum = 0.f, acc[J];
-        #pragma unroll 1
-        for (int r = 0; r < P; ++r) M = fmaxf(M, ld_cg(xb + (size_t(r) * a.xrows + u.q_row + h) * RS + D));
-#pragma unroll
-        for (int jj = 0; jj < J; ++jj) acc[jj] = 0.f;
-        #pragma unroll 1
-        for (int r = 0; r < P; ++r) {
-          const float* src = xb + (size_t(r) * a.xrows + u.q_row + h) * RS;
-          const float w = ex2_sub(ld_cg(src + D), M);
-          lsum += w;
-          float rv[J];
-          ldv_cg<J>(src + J * lane, rv);
-#pragma unroll
-          for (int jj = 0; jj < J; ++jj) acc[jj] = fmaf(w, rv[jj], acc[jj]);
-        }
-        stv<J>(a.out + size_t(u.q_row + h) * D + J * lane, acc, 1.f / lsum);
-        if (lane == 0 && a.lse) a.lse[u.q_row + h] = (M + log2f(lsum)) * kLn2;
-      }
+    } else {
+      epi_sync();  // (B) the staged operands are read: the next segment may restage the ring
     }
-    if (host_wait && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
+    if (e == 0 && host_wait && tr && lane == 0) tr[TR_PUBLISH] = globaltimer();  // host: fold done
 #ifdef LA_WIDE_PRINT
-    if (lane == 0 && host_wait && blockIdx.x % 16 == 0)
+    if (lane == 0 && e == 0 && host_wait && blockIdx.x % 16 == 0)
       printf("WIDE cta %d np %d nr %d idle %d sp %d: w1->loop %llu, rg %llu %llu %llu %llu, end %llu ns; rg0: cfold %llu peers %llu write %llu\n",
              int(blockIdx.x), np, nr, int(idle), int(stage_peers), wt[0] - (tr ? tr[TR_WAIT1] : wt[0]), wt[1] - wt[0],
              wt[2] - wt[1], wt[3] - wt[2], wt[4] - wt[3], globaltimer() - wt[0], wt[5] - wt[1], wt[6] - wt[5],
              wt[2] - wt[6]);
 #endif
   }
-  if (lane == 0) {
+  if (e == 0 && lane == 0) {
     if (tr) tr[TR_END] = globaltimer();
     __threadfence();  // every flag wait of this CTA is over: the last one out advances the epoch
     if (atomicAdd(&a.counters[CTR_EXITED], 1) == int(gridDim.x) - 1) {
@@ -2002,7 +2026,7 @@ __device__ __forceinline__ void wide_epilogue(const DecodeArgs& a, const TmapPai
 }
 
 template <class E>
-__global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeArgs a, const __grid_constant__ TmapPair tm) {
+__global__ void __launch_bounds__((E::NCW + 1 + EngX<E>::NEP) * 32, 1) la_decode(const DecodeArgs a, const __grid_constant__ TmapPair tm) {
   constexpr int NST = E::NST, NWG = E::NWG, WPS = E::WPS, NCW = E::NCW, D = E::D, H = E::HEADS, J = D / 32;
   constexpr int FW = EngX<E>::FW;  // fold rows per ring slot (WPS, or 1 for a warpgroup engine)
   constexpr int FOLD_FLOATS = E::FOLD_FLOATS;
@@ -2060,7 +2084,7 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
     }
     for (int b = 0; b < kFB; ++b) {
       mbar_init(&fold_full[b], NCW);
-      mbar_init(&fold_empty[b], 1);
+      mbar_init(&fold_empty[b], EngX<E>::NEP);
     }
     mbar_init(stage_bar, 1);
     *prod_j = -1;
@@ -2264,8 +2288,9 @@ __global__ void __launch_bounds__((E::NCW + 2) * 32, 1) la_decode(const DecodeAr
   }
 
   if constexpr (H > 8) {
-    if (warp == NCW) {
-      wide_epilogue<E>(a, tm, ring, fold, fold_full, fold_empty, stage_bar, seginfo, prod_j, epoch, xepoch, tr, lane);
+    if (warp == NCW || warp >= NCW + 2) {  // epilogue warps 0 .. NEP-1 (the producer is warp NCW + 1)
+      wide_epilogue<E>(a, tm, ring, fold, fold_full, fold_empty, stage_bar, seginfo, prod_j, epoch, xepoch, tr, lane,
+                       warp == NCW ? 0 : warp - NCW - 1);
       return;
     }
   }
@@ -2800,7 +2825,7 @@ template <class E>
 KernelInfo info_of(bool tma) {
   KernelInfo k;
   k.supported = true;
-  k.threads = (E::NCW + 2) * 32;
+  k.threads = (E::NCW + 1 + EngX<E>::NEP) * 32;  // consumers, producer, epilogue warp(s)
   static_assert(Smem<E>::BYTES <= 232448, "dynamic shared memory exceeds 227 KiB per block");
   k.smem_bytes = Smem<E>::BYTES;
   k.stage_tokens_max = E::STAGE_TOK;
