@@ -218,7 +218,7 @@ def test_tcgen05_tiny_contexts(rows_per_head):
                                                  (4, 2000, 148, 16)])
 def test_tcgen05_wide_tiles_many_peers(q_len, n, grid, tile_n):
     """One 16 / 32-row unit spread over up to 148 CTAs: the host's peer partials exceed the idle
-    ring (147 peers x 32 rows), so its fold takes the per-row-group staging path, while units
+    ring (147 peers x 32 rows), so its epilogue warps read the peers' rows from L2, while units
     spread over few CTAs stage every peer at once -- both against the oracle."""
     p = synth.Problem(1, 8, 1, 128, [n], dtype="bf16", dist="D2", seed=75, q_len=q_len)
     O_ref, L_ref = run_oracle(p)
